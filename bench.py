@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the SPAI(1) hot path on B200 (BASELINE.json configs[2]).
+
+Workload: 3D Q1 Poisson on a 400^3 interior grid (64M DOF, 1.72e9 stored
+entries, 27-point), b = A*1, x0 = 0, tol 1e-8 -- SPAI(1)+CG (configs[2]).
+One step = the whole hot path on inputs already in HBM:
+    K1 CSC transpose of A  +  K3 SPAI(1) assembly  +  K4 symmetrisation
+    +  K8 device-resident PCG (classic, reference termination) to tol.
+value = n_dof * iterations / step time  ("DOF*it/s", setup included).
+Per-phase numbers (assembly cols/s, solve DOF*it/s, SpMV GB/s) ride along.
+`e2e` repeats the step through the public API with the matrix and b in
+pinned HOST memory (H2D inside the timed region) and x read back to host.
+
+--impl reference times the unmodified reference (ftkrylov from
+baseline/_ref; CLI spai1 factory + solve) on a bounded sample of the same
+workload (3D Q1 20^3) on the host cores; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "SPAI(1) assembly cols/s; SPAI-precond. solve DOF/s and SpMV HBM GB/s vs peak"
+UNIT = "DOF*it/s"
+REF_SAMPLE_N = 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--n", type=int, default=400, help="grid points per axis")
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--maxit", type=int, default=20000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--spmv-reps", type=int, default=20)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    def __init__(self, idx):
+        self.idx = idx
+        self.proc = None
+        self.path = f"/tmp/clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
+            rows = [[c.strip() for c in r] for r in rows if len(r) >= 7]
+            sm = [float(r[0]) for r in rows]
+            mx = max(float(r[1]) for r in rows)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = sorted({names[i] for r in rows for i in range(4)
+                              if r[3 + i].lower() in ("active", "1", "yes")})
+            load = [s for s in sm if s > 0.5 * mx] or sm
+            return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons,
+                    "samples": len(rows)}
+        except Exception as e:  # no nvidia-smi
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
+
+
+# ---------------------------------------------------------------- reference arm
+def reference_problem(N):
+    import numpy as np
+    import oracle
+    c = oracle.stencil_csr((N, N, N), *oracle.q1_stencil(3))
+    return c, np
+
+
+def time_reference(N, reps, tol=1e-8):
+    """Unmodified reference (ftkrylov) or, if absent, the oracle port."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    kind = "reference"
+    try:
+        sys.path.insert(0, ref_dir)
+        import ftkrylov as fk
+        from ftkrylov.cli import ExperimentConfig
+    except ImportError:
+        fk = None
+        kind = "port"
+    c, np = reference_problem(N)
+    out = []
+    for _ in range(reps):
+        if fk is not None:
+            t0 = time.perf_counter()
+            A = fk.CsrMatrix(c.nrows, c.ncols, c.row_offsets, c.col_indices, c.values)
+            P = ExperimentConfig({"preconditioner": {"kind": "spai1"}}).make_precond_factory()(A)
+            b = fk.spmv(A, np.ones(A.nrows))
+            _, rec = fk.solve(fk.LocalSystem(A, P), b,
+                              fk.SolverConfig(tol=tol, maxit=20000))
+            t1 = time.perf_counter()
+            its = rec.iterations
+        else:
+            import oracle
+            t0 = time.perf_counter()
+            M = oracle.spai1(c)
+            S = oracle.symmetrize_dense_reference(M)
+            b = oracle.make_rhs_ones(c)
+            _, rec = oracle.pcg_classic(c, S, b, tol=tol, maxit=20000)
+            t1 = time.perf_counter()
+            its = rec.iterations
+        out.append((t1 - t0, its))
+    n = c.nrows
+    tot_t = sum(t for t, _ in out)
+    tot_w = sum(n * i for _, i in out)
+    return {"value": tot_w / tot_t, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"3D Q1 Poisson {N}^3 ({n} DOF), spai1 + CLI symmetrisation + "
+                      f"classic PCG tol {tol}, {reps} run(s), mean {tot_t / reps:.2f} s, "
+                      f"{out[0][1]} iterations"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+    for _ in range(args.warmup):
+        time_reference(REF_SAMPLE_N, 1, args.tol)
+    res = time_reference(REF_SAMPLE_N, args.steps, args.tol)
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"3D Q1 Poisson {REF_SAMPLE_N}^3 sample of configs[2] "
+                                   "(reference cannot densify 400^3)"},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1911_01492_b200 as pb
+    from paper_1911_01492_b200.sparse import DeviceCsr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    N = args.n
+    dims = (N, N, N)
+    with torch.cuda.stream(stream):
+        A = pb.q1_device(dims)
+        n, nnz = A.nrows, A.nnz
+        b = A.matvec(torch.ones(n, dtype=torch.float64, device=dev))
+    stream.synchronize()
+    cfg = pb.SolverConfig(tol=args.tol, maxit=args.maxit)
+    launches = {"n": 0}
+
+    def step(Adev, bdev):
+        A2 = DeviceCsr(n, n, Adev.rowptr, Adev.colidx, Adev.vals)   # no cached CSC
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        S = pb.spai1_symmetric_device(A2)
+        e1.record(stream)
+        x, rec = pb.solve(pb.LocalSystem(A2, pb.SparseMatrixPreconditioner(S)), bdev, cfg)
+        e2.record(stream)
+        e2.synchronize()
+        launches["n"] += 9 + 1 + 2 * _advanced(rec)
+        return e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3, rec, x
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(A, b)
+        barrier()
+        launches["n"] = 0
+        times = []
+        with Clocks(local) as clk:
+            t_start = torch.cuda.Event(enable_timing=True)
+            t_end = torch.cuda.Event(enable_timing=True)
+            t_start.record(stream)
+            for _ in range(args.steps):
+                ta, ts, rec, x = step(A, b)
+                times.append((ta, ts, rec.iterations))
+            t_end.record(stream)
+            t_end.synchronize()
+            barrier()
+        total_s = t_start.elapsed_time(t_end) / 1e3
+        gpu_launches = launches["n"]
+    clocks = clk.summary()
+    if world > 1:
+        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    its = times[-1][2]
+    work = sum(n * it for _, _, it in times)
+    value = world * work / total_s
+    t_asm = statistics.mean(t for t, _, _ in times)
+    t_sol = statistics.mean(t for _, t, _ in times)
+    hbm, peak_kind = peaks()
+    b_it = 24 * nnz + 16 * (n + 1) + 88 * n
+    solve_gbs = b_it * its / t_sol / 1e9
+
+    # ---- SpMV alone (K5 plain and TMA-staged) with CUDA events
+    spmv = {}
+    with torch.cuda.stream(stream):
+        xx = torch.rand(n, dtype=torch.float64, device=dev)
+        yy = torch.empty_like(xx)
+        sp_bytes = 12 * nnz + 8 * (n + 1) + 16 * n
+        for name, fn in (("csr", lambda: A.matvec(xx, out=yy)),
+                         ("csr_tma", lambda: A.matvec_tma(xx, out=yy))):
+            for _ in range(3):
+                fn()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(stream)
+            for _ in range(args.spmv_reps):
+                fn()
+            ev[1].record(stream)
+            ev[1].synchronize()
+            dt = ev[0].elapsed_time(ev[1]) / 1e3 / args.spmv_reps
+            spmv[name] = {"ms": dt * 1e3, "gbs": sp_bytes / dt / 1e9,
+                          "frac": sp_bytes / dt / 1e9 / hbm}
+
+    # ---- e2e through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        with torch.cuda.stream(stream):
+            h_rowptr = A.rowptr.cpu().pin_memory()
+            h_colidx = A.colidx.cpu().pin_memory()
+            h_vals = A.vals.cpu().pin_memory()
+            h_b = b.cpu().pin_memory()
+            h_x = torch.empty(n, dtype=torch.float64).pin_memory()
+            d_rowptr = torch.empty_like(A.rowptr)
+            d_colidx = torch.empty_like(A.colidx)
+            d_vals = torch.empty_like(A.vals)
+            d_b = torch.empty_like(b)
+            barrier()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(stream)
+            e_work = 0
+            reps = max(1, min(args.steps, 3))
+            for _ in range(reps):
+                d_rowptr.copy_(h_rowptr, non_blocking=True)
+                d_colidx.copy_(h_colidx, non_blocking=True)
+                d_vals.copy_(h_vals, non_blocking=True)
+                d_b.copy_(h_b, non_blocking=True)
+                Ad = DeviceCsr(n, n, d_rowptr, d_colidx, d_vals)
+                _, _, rec_e, x_e = step(Ad, d_b)
+                h_x.copy_(x_e, non_blocking=True)
+                e_work += n * rec_e.iterations
+            ev[1].record(stream)
+            ev[1].synchronize()
+            e_t = ev[0].elapsed_time(ev[1]) / 1e3
+            if world > 1:
+                t = torch.tensor([e_t], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e_t = float(t.item())
+            h2d = (h_rowptr.numel() * 8 + h_colidx.numel() * 4 + h_vals.numel() * 8
+                   + h_b.numel() * 8)
+            e2e = {"value": world * e_work / e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": n * 8, "steps": reps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = time_reference(REF_SAMPLE_N, 2, args.tol)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_s / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"configs[2]: 3D Q1 Poisson {N}^3 ({n} DOF, nnz {nnz}), "
+                                   f"SPAI(1)+CG, b=A*1, x0=0, tol {args.tol}",
+                       "n_dof": n, "nnz": nnz, "iterations": its,
+                       "l2": "inputs (21 GB matrix) far larger than the 126 MB L2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "assembly": {"ms": t_asm * 1e3, "cols_per_s": n / t_asm,
+                         "includes": "CSC transpose + SPAI(1) assembly + symmetrisation"},
+            "solve": {"ms": t_sol * 1e3, "iterations": its, "dof_it_per_s": n * its / t_sol,
+                      "ms_per_iteration": t_sol / its * 1e3},
+            "spmv": spmv,
+            "roofline": {"bound": "hbm", "kernel": "PCG iteration (pcg_k1 + pcg_k2)",
+                         "achieved": solve_gbs, "peak": hbm, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": solve_gbs / hbm, "traffic": None,
+                         "algorithmic_bytes_per_iteration": b_it},
+            "clocks": clocks,
+            "gpu_launches": gpu_launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _advanced(rec):
+    # iterations launched (device no-op launches after convergence included)
+    return int(getattr(rec, "launched_iterations", rec.iterations))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/* spai_b200.h -- C-ABI of libspaib200.so, the B200 (sm_100a) SPAI(1) hot path.
+ *
+ * Drop-in boundary for the reference `ftkrylov` path named by
+ * BASELINE.json.north_star.  The reference is pure Python; it has no FFI, so
+ * each entry point below names the reference *function* it replaces
+ * (paths relative to /root/reference/pkg/src/ftkrylov/).  The Python mirror of
+ * the reference API (package paper_1911_01492_b200) binds these with ctypes;
+ * INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers owned by the caller.
+ *  - Row/column pointers are int64, column/row indices int32 (n < 2^31),
+ *    values fp64 (the reference stores int64/int64/f64, sparse.py:31-33).
+ *  - Every call takes a cudaStream_t (passed as void*) and is asynchronous on
+ *    it, except calls documented as "synchronous" (they return host values).
+ *  - Return value: SPAI_OK (0) or an error code; spai_last_error() returns a
+ *    thread-local message for the last failure.
+ *  - No allocation happens inside kernels; scratch comes from caller-owned
+ *    workspaces sized by the matching *_workspace_bytes() query.
+ */
+#ifndef SPAI_B200_H
+#define SPAI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SPAI_OK = 0,
+  SPAI_E_RANK_DEFICIENT = 1, /* FactorBreakdownError, precond.py:192-194          */
+  SPAI_E_DIM = 2,            /* DimensionMismatchError, sparse.py:194-195 etc.     */
+  SPAI_E_CUDA = 3,           /* CUDA runtime failure                               */
+  SPAI_E_ARG = 4,            /* invalid argument                                   */
+  SPAI_E_BREAKDOWN = 5,      /* BreakdownError, krylov.py:327-330                  */
+  SPAI_E_DIVERGENCE = 6,     /* DivergenceError, krylov.py:288-291                 */
+  SPAI_E_PATTERN = 7,        /* pattern not structurally symmetric                 */
+  SPAI_E_UNSUPPORTED = 8,    /* local problem larger than the kernel limits        */
+  SPAI_E_EMPTY_COLUMN = 9    /* column without stored entries (precond.py:188)     */
+};
+
+const char* spai_last_error(void);
+int spai_version(void);
+
+/* ------------------------------------------------------------------ K0
+ * Structured-grid stencil generator (no reference counterpart for Q1; the
+ * 2D 5-point table reproduces assemble_poisson, grids.py:67-96).
+ * dims[0..dim) = interior nodes per axis (x fastest); table/stored have 3^dim
+ * entries, index t = sum_a (off_a+1)*3^a.  spai_stencil_nnz is synchronous. */
+int spai_stencil_nnz(int dim, const int64_t* dims, const uint8_t* stored,
+                     int64_t* nnz_out);
+int spai_stencil_csr(int dim, const int64_t* dims, const double* table,
+                     const uint8_t* stored, int64_t* rowptr, int32_t* colidx,
+                     double* vals, void* stream);
+
+/* ------------------------------------------------------------------ K1
+ * CSR -> CSC structure (replaces CsrMatrix.transpose, sparse.py:108-112,
+ * called from spai1 at precond.py:182).  cscptr[ncols+1], cscrow[nnz],
+ * csc2csr[nnz] = CSR position of each CSC entry (rows ascending per column). */
+size_t spai_transpose_workspace_bytes(int64_t nrows, int64_t ncols, int64_t nnz);
+int spai_csr_transpose(int64_t nrows, int64_t ncols, int64_t nnz,
+                       const int64_t* rowptr, const int32_t* colidx,
+                       int64_t* cscptr, int32_t* cscrow, int64_t* csc2csr,
+                       void* ws, size_t ws_bytes, void* stream);
+/* Synchronous: *is_sym = 1 iff the CSC structure equals the CSR structure. */
+int spai_structure_is_symmetric(int64_t n, int64_t nnz, const int64_t* rowptr,
+                                const int32_t* colidx, const int64_t* cscptr,
+                                const int32_t* cscrow, int* is_sym);
+
+/* ------------------------------------------------------------------ K2
+ * Pattern sets of precond.py:186-188 for columns [c0, c1):
+ *   J_k = stored rows of A[:,k] = cscrow[cscptr[k]:cscptr[k+1]]
+ *   I_k = sorted unique union of the stored rows of A[:,c], c in J_k.
+ * count: icount[k-c0] = |I_k|.  fill: iidx[iptr[k-c0] ...] = I_k, with iptr
+ * an exclusive scan of icount (caller computed, int64, length c1-c0+1).   */
+int spai_pattern_count(int64_t n, const int64_t* cscptr, const int32_t* cscrow,
+                       int64_t c0, int64_t c1, int32_t* icount, void* stream);
+int spai_pattern_fill(int64_t n, const int64_t* cscptr, const int32_t* cscrow,
+                      int64_t c0, int64_t c1, const int64_t* iptr,
+                      int32_t* iidx, void* stream);
+
+/* ------------------------------------------------------------------ K3
+ * SPAI(1) assembly (replaces precond.py:185-198): for every column k solve
+ * min || A[I,J] m - e_k ||_2 and write m_k to m_csc[cscptr[k]...] (CSC order,
+ * i.e. ordered like J_k).  Synchronous: returns SPAI_E_RANK_DEFICIENT with
+ * *bad_col = smallest failing column under the reference rank test
+ * min|R_ii| <= 1e-13*max(max|R_ii|,1); *n_fallback = columns that took the
+ * Householder-QR path.                                                     */
+size_t spai_assemble_workspace_bytes(int64_t n);
+int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
+                  const int32_t* colidx, const double* vals,
+                  const int64_t* cscptr, const int32_t* cscrow,
+                  const int64_t* csc2csr, double* m_csc, void* ws,
+                  size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
+                  void* stream);
+
+/* ------------------------------------------------------------------ K4
+ * CSC-ordered M values -> CSR values of M (from_coo, precond.py:199). */
+int spai_csc_to_csr_values(int64_t nnz, const int64_t* csc2csr,
+                           const double* m_csc, double* m_csr, void* stream);
+/* 0.5*(M + M^T) kept on pattern(A) (replaces cli.py:189-194 dense
+ * symmetrisation; requires a structurally symmetric pattern, see
+ * spai_structure_is_symmetric).  s_csr may alias nothing.                 */
+int spai_symmetrize(int64_t nnz, const int64_t* csc2csr, const double* m_csc,
+                    double* s_csr, void* stream);
+
+/* ------------------------------------------------------------------ K5
+ * y = A x (replaces spmv, sparse.py:191-202, and
+ * SparseMatrixPreconditioner.apply, precond.py:121-122).                  */
+int spai_csr_spmv(int64_t n, int64_t nnz, const int64_t* rowptr,
+                  const int32_t* colidx, const double* vals, const double* x,
+                  double* y, void* stream);
+/* Row tiling for the TMA-staged SpMV (computed once per pattern).
+ * ntiles_out is synchronous; tile_rows has ntiles+1 entries.               */
+int spai_tile_count(int64_t n, int64_t nnz, int64_t* ntiles_out);
+int spai_tile_rows(int64_t n, const int64_t* rowptr, int64_t ntiles,
+                   int64_t* tile_rows, int32_t* max_tile_nnz, void* stream);
+/* TMA-staged SpMV: each CTA streams the colidx/vals segment of its row tiles
+ * into a shared-memory ring with cp.async.bulk (16-byte granules, so
+ * colidx/vals must be 16-byte aligned and readable up to the next 16 bytes
+ * past nnz -- true for every cudaMalloc/torch allocation).                */
+int spai_csr_spmv_tma(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                      const double* vals, const int64_t* tile_rows,
+                      int64_t ntiles, int32_t max_tile_nnz, const double* x,
+                      double* y, void* stream);
+
+/* ------------------------------------------------------------------ K6/K7
+ * Deterministic fused dot products (LocalSystem.fused_dots,
+ * krylov.py:179-183): out[k] = (u_k, v_k) for k < npairs (npairs <= 3),
+ * written to device memory.                                               */
+size_t spai_dots_workspace_bytes(int64_t n);
+int spai_fused_dots(int64_t n, int npairs, const double* const* us,
+                    const double* const* vs, double* out, void* ws,
+                    size_t ws_bytes, void* stream);
+/* y = a*x + b*y */
+int spai_axpby(int64_t n, double a, const double* x, double b, double* y,
+               void* stream);
+
+/* ------------------------------------------------------------------ K8
+ * Device-resident classic PCG (replaces _solve_classic, krylov.py:301-345).
+ * A and M share rowptr/colidx when M is on pattern(A) (spai1 guarantees it);
+ * pass M_vals = NULL for no preconditioner (apply_M = copy).               */
+typedef struct spai_pcg spai_pcg;     /* opaque solver state               */
+int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* rowptr,
+                    const int32_t* colidx, const double* A_vals,
+                    const int64_t* m_rowptr, const int32_t* m_colidx,
+                    const double* M_vals, double tol, int64_t maxit,
+                    void* stream);
+/* Start from x0 (device, may be NULL -> zero); b device, copied.          */
+int spai_pcg_start(spai_pcg* s, const double* b, const double* x0);
+/* Run up to `iters` more iterations on the device (no host sync inside). */
+int spai_pcg_advance(spai_pcg* s, int64_t iters);
+/* Synchronous: status 0 running, 1 converged, 2 maxit, 3 breakdown,
+ * 4 divergence; iterations done; norm0; last norm; breakdown value.       */
+int spai_pcg_poll(spai_pcg* s, int* status, int64_t* iterations, double* norm0,
+                  double* norm, double* aux);
+/* Synchronous copy of the residual history [0, count) to host.            */
+int spai_pcg_history(spai_pcg* s, double* host_out, int64_t count);
+/* Device pointers of the state vectors (x, r, p, z).                      */
+int spai_pcg_vectors(spai_pcg* s, double** x, double** r, double** p, double** z);
+int spai_pcg_destroy(spai_pcg* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAI_B200_H */

@@ -1,0 +1,239 @@
+"""Oracle SpMV and Krylov/Richardson loops (TEST INFRASTRUCTURE ONLY).
+
+* `spmv`          restates `sparse.py:191-202`.
+* `pcg_classic`   restates `krylov.py:294-345` (`_initial`, `_solve_classic`)
+                  with `LocalSystem.fused_dots` = list of np.dot
+                  (`krylov.py:179-183`) and `_Run.note` (`krylov.py:271-277`).
+* `tree_sum`      restates `commsim.py:336-347` (ascending-rank pairwise tree).
+* `bicgstab_right`, `richardson`: NO reference exists (SPEC.md:343 lists
+  BiCGStab as a non-goal; Richardson is only mentioned at SPEC.md:257).  These
+  are our own fp64 definitions, written in the record conventions of the
+  reference (`ConvergenceRecord`, `krylov.py:103-135`): residual history is the
+  unpreconditioned 2-norm, stop when ||r|| <= tol * ||r0||.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+class Breakdown(Exception):
+    pass
+
+
+class Divergence(Exception):
+    pass
+
+
+@dataclass
+class Record:
+    variant: str
+    iterations: int = 0
+    converged: bool = False
+    initial_residual: float = float("nan")
+    final_residual: float = float("nan")
+    residual_norms: list = field(default_factory=list)
+    reductions_cum: list = field(default_factory=list)
+    total_reductions: int = 0
+
+
+def spmv(A, x):
+    """`sparse.py:191-202`."""
+    x = np.asarray(x, dtype=np.float64)
+    prod = A.values * x[A.col_indices]
+    out = np.zeros(A.nrows)
+    counts = np.diff(A.row_offsets)
+    nz = counts > 0
+    if np.any(nz):
+        out[nz] = np.add.reduceat(prod, A.row_offsets[:-1][nz])
+    return out
+
+
+def tree_sum(arrays):
+    """`commsim.py:336-347`."""
+    arrays = list(arrays)
+    while len(arrays) > 1:
+        nxt = []
+        for i in range(0, len(arrays), 2):
+            if i + 1 < len(arrays):
+                nxt.append(arrays[i] + arrays[i + 1])
+            else:
+                nxt.append(arrays[i])
+        arrays = nxt
+    return arrays[0]
+
+
+def _finite(*s):
+    for v in s:
+        if not math.isfinite(v):
+            raise Divergence("non-finite value in solver recurrence")
+
+
+def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None):
+    """`krylov.py:301-345`. M is a CSR (applied by spmv) or None."""
+    apply_M = (lambda v: v.copy()) if M is None else (lambda v: spmv(M, v))
+    rec = Record("classic")
+    red = 0
+    b = np.asarray(b, dtype=np.float64)
+    if x0 is None:
+        x, r = np.zeros(A.nrows), b.copy()
+    else:
+        x = np.array(x0, dtype=np.float64, copy=True)
+        r = b - spmv(A, x)
+    p = apply_M(r)
+    norm0 = None
+    norm = float("inf")
+    rho = 0.0
+    it = 0
+
+    def finish(x, nrm, its, conv):
+        rec.iterations, rec.converged, rec.final_residual = its, conv, nrm
+        rec.total_reductions = red
+        return x, rec
+
+    while it < maxit:
+        if norm0 is not None and norm <= tol * norm0:
+            break
+        it += 1
+        q = spmv(A, p)
+        red += 1
+        if it == 1:
+            delta, rho, rr0 = (float(np.dot(p, q)), float(np.dot(p, r)),
+                               float(np.dot(r, r)))
+            norm0 = math.sqrt(rr0)
+            rec.initial_residual = norm0
+            if norm0 == 0.0:
+                return finish(x, 0.0, it, True)
+        else:
+            delta = float(np.dot(p, q))
+        _finite(delta, rho)
+        if delta <= 0.0:
+            if rho == 0.0:
+                return finish(x, norm if it > 1 else norm0, it, True)
+            raise Breakdown(f"indefinite curvature <p,Ap> = {delta}")
+        lam = rho / delta
+        x = x + lam * p
+        r = r - lam * q
+        q = apply_M(r)
+        red += 1
+        rho_new, rr = float(np.dot(q, r)), float(np.dot(r, r))
+        _finite(rho_new, rr)
+        norm = math.sqrt(rr)
+        if not math.isfinite(norm):
+            raise Divergence("non-finite residual norm")
+        rec.residual_norms.append(norm)
+        rec.reductions_cum.append(red)
+        p = q + (rho_new / rho) * p
+        rho = rho_new
+    converged = norm0 is not None and norm <= tol * norm0
+    return finish(x, norm, it, converged)
+
+
+def bicgstab_right(A, M, b, tol=1e-8, maxit=1000):
+    """Right-preconditioned BiCGStab (van der Vorst 1992), x0 = 0, r_hat = r0.
+
+    Per iteration (3 fused reductions):
+      p = r + beta (p - omega v)        (beta = (rho/rho_old)(alpha/omega))
+      p^ = M p ; v = A p^ ; [ (r_hat, v) ]            -> alpha = rho / (r_hat, v)
+      s = r - alpha v ; s^ = M s ; t = A s^ ; [ (t, s), (t, t) ] -> omega
+      x += alpha p^ + omega s^ ; r = s - omega t ; [ (r_hat, r), (r, r) ]
+    History: ||r|| after every iteration.  Breakdown when (r_hat, v) == 0,
+    (t, t) == 0 or rho == 0 before convergence.
+    """
+    apply_M = (lambda v: v.copy()) if M is None else (lambda v: spmv(M, v))
+    rec = Record("bicgstab")
+    red = 0
+    n = A.nrows
+    x = np.zeros(n)
+    r = np.asarray(b, dtype=np.float64).copy()
+    rhat = r.copy()
+    rr0 = float(np.dot(r, r))
+    red += 1
+    norm0 = math.sqrt(rr0)
+    rec.initial_residual = norm0
+    rho = rr0
+    if norm0 == 0.0:
+        rec.converged, rec.final_residual, rec.total_reductions = True, 0.0, red
+        return x, rec
+    p = np.zeros(n)
+    v = np.zeros(n)
+    alpha = omega = 1.0
+    rho_old = 1.0
+    norm = norm0
+    it = 0
+    while it < maxit:
+        if norm <= tol * norm0:
+            break
+        it += 1
+        if rho == 0.0:
+            raise Breakdown("rho = 0 in BiCGStab")
+        beta = (rho / rho_old) * (alpha / omega)
+        p = r + beta * (p - omega * v)
+        ph = apply_M(p)
+        v = spmv(A, ph)
+        rv = float(np.dot(rhat, v))
+        red += 1
+        _finite(rv)
+        if rv == 0.0:
+            raise Breakdown("(r_hat, v) = 0 in BiCGStab")
+        alpha = rho / rv
+        s = r - alpha * v
+        sh = apply_M(s)
+        t = spmv(A, sh)
+        ts, tt = float(np.dot(t, s)), float(np.dot(t, t))
+        red += 1
+        _finite(ts, tt)
+        if tt == 0.0:
+            raise Breakdown("(t, t) = 0 in BiCGStab")
+        omega = ts / tt
+        x = x + alpha * ph + omega * sh
+        r = s - omega * t
+        rho_old = rho
+        rho, rr = float(np.dot(rhat, r)), float(np.dot(r, r))
+        red += 1
+        _finite(rho, rr)
+        norm = math.sqrt(rr)
+        rec.residual_norms.append(norm)
+        rec.reductions_cum.append(red)
+        if omega == 0.0 and norm > tol * norm0:
+            raise Breakdown("omega = 0 in BiCGStab")
+    rec.iterations, rec.final_residual = it, norm
+    rec.converged = norm <= tol * norm0
+    rec.total_reductions = red
+    return x, rec
+
+
+def richardson(A, M, b, omega=1.0, maxit=100, tol=None):
+    """Preconditioned Richardson  x += omega M (b - A x),  x0 = 0.
+
+    Per iteration: z = M r ; x += omega z ; r = b - A x ; [ (r, r) ].
+    History ||r_k|| per iteration; stops early only when tol is given.
+    """
+    apply_M = (lambda v: v.copy()) if M is None else (lambda v: spmv(M, v))
+    rec = Record("richardson")
+    b = np.asarray(b, dtype=np.float64)
+    x = np.zeros(A.nrows)
+    r = b.copy()
+    norm0 = math.sqrt(float(np.dot(r, r)))
+    rec.initial_residual = norm0
+    norm = norm0
+    it = 0
+    while it < maxit:
+        if tol is not None and norm <= tol * norm0:
+            break
+        it += 1
+        z = apply_M(r)
+        x = x + omega * z
+        r = b - spmv(A, x)
+        norm = math.sqrt(float(np.dot(r, r)))
+        if not math.isfinite(norm):
+            raise Divergence("non-finite residual norm")
+        rec.residual_norms.append(norm)
+        rec.reductions_cum.append(it)
+    rec.iterations, rec.final_residual = it, norm
+    rec.converged = tol is not None and norm <= tol * norm0
+    rec.total_reductions = it
+    return x, rec

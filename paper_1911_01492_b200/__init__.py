@@ -1,0 +1,28 @@
+"""B200-native SPAI(1) hot path of Exa-Dune (arXiv 1911.01492).
+
+Drop-in for the `ftkrylov` preconditioner/solver path named by
+BASELINE.json.north_star: the public names below mirror
+`ftkrylov/__init__.py:8-34` for that path; the numerics run in hand-written
+sm_100a CUDA kernels (libspaib200.so, C-ABI in include/spai_b200.h).
+There is no CPU fallback: without the library or a CUDA device every compute
+call raises `NativeLibraryError`.
+"""
+
+from .errors import (BreakdownError, ConfigError, DimensionMismatchError,
+                     DivergenceError, FactorBreakdownError, FtkError,
+                     InvalidPartitionError, MatrixMarketError,
+                     RecoveryFailedError, SingularDiagonalError)
+from ._lib import NativeLibraryError
+from .sparse import CsrMatrix, DeviceCsr, as_device, spmv
+from .grids import (Anisotropy, StructuredGrid, assemble_poisson, assemble_q1,
+                    fd5_stencil, make_rhs, q1_device, q1_stencil, stencil_device)
+from .precond import (IdentityPreconditioner, JacobiPreconditioner,
+                      Preconditioner, SparseMatrixPreconditioner, SpaiStats,
+                      drop_exact_zeros, jacobi, make_spai1_factory,
+                      pattern_sets, spai1, spai1_device,
+                      spai1_symmetric_device)
+from .krylov import (ConvergenceRecord, DevicePCG, KrylovState, LocalSystem,
+                     SolverConfig, VARIANTS, fused_dots_device,
+                     memory_accounting, reduction_rate, solve)
+
+__version__ = "0.1.0"

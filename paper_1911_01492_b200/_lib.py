@@ -1,0 +1,109 @@
+"""ctypes binding of libspaib200.so (the C-ABI declared in include/spai_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every compute entry point raises `NativeLibraryError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libspaib200.so")
+
+SPAI_OK = 0
+SPAI_E_RANK_DEFICIENT = 1
+SPAI_E_DIM = 2
+SPAI_E_CUDA = 3
+SPAI_E_ARG = 4
+SPAI_E_BREAKDOWN = 5
+SPAI_E_DIVERGENCE = 6
+SPAI_E_PATTERN = 7
+SPAI_E_UNSUPPORTED = 8
+SPAI_E_EMPTY_COLUMN = 9
+
+
+class NativeLibraryError(RuntimeError):
+    """The CUDA library could not be loaded or a CUDA call failed."""
+
+
+_vp = C.c_void_p
+_i64 = C.c_int64
+_i32 = C.c_int
+_dbl = C.c_double
+_sz = C.c_size_t
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "spai_last_error": (C.c_char_p, []),
+    "spai_version": (_i32, []),
+    "spai_stencil_nnz": (_i32, [_i32, _vp, _vp, C.POINTER(_i64)]),
+    "spai_stencil_csr": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_transpose_workspace_bytes": (_sz, [_i64, _i64, _i64]),
+    "spai_csr_transpose": (_i32, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "spai_structure_is_symmetric": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, C.POINTER(_i32)]),
+    "spai_pattern_count": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _vp]),
+    "spai_pattern_fill": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "spai_assemble_workspace_bytes": (_sz, [_i64]),
+    "spai_assemble": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                             C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "spai_csc_to_csr_values": (_i32, [_i64, _vp, _vp, _vp, _vp]),
+    "spai_symmetrize": (_i32, [_i64, _vp, _vp, _vp, _vp]),
+    "spai_csr_spmv": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_tile_count": (_i32, [_i64, _i64, C.POINTER(_i64)]),
+    "spai_tile_rows": (_i32, [_i64, _vp, _i64, _vp, _vp, _vp]),
+    "spai_csr_spmv_tma": (_i32, [_i64, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp]),
+    "spai_dots_workspace_bytes": (_sz, [_i64]),
+    "spai_fused_dots": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "spai_axpby": (_i32, [_i64, _dbl, _vp, _dbl, _vp, _vp]),
+    "spai_pcg_create": (_i32, [C.POINTER(_vp), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl,
+                               _i64, _vp]),
+    "spai_pcg_start": (_i32, [_vp, _vp, _vp]),
+    "spai_pcg_advance": (_i32, [_vp, _i64]),
+    "spai_pcg_poll": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),
+                             C.POINTER(_dbl), C.POINTER(_dbl)]),
+    "spai_pcg_history": (_i32, [_vp, _vp, _i64]),
+    "spai_pcg_vectors": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
+                                C.POINTER(_vp)]),
+    "spai_pcg_destroy": (_i32, [_vp]),
+}
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the CDLL; raises NativeLibraryError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryError(
+            f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            continue
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    load()
+    return [n for n in _SIGS if hasattr(_lib, n)]
+
+
+def last_error() -> str:
+    msg = load().spai_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str = ""):
+    """Raise NativeLibraryError for CUDA/argument failures; return status otherwise."""
+    if status in (SPAI_E_CUDA, SPAI_E_ARG):
+        raise NativeLibraryError(f"{what}: {last_error()}")
+    return status

@@ -1,0 +1,27 @@
+// Thread-local error reporting for the C-ABI.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "../../include/spai_b200.h"
+
+namespace spai {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  set_error("CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), where);
+  return SPAI_E_CUDA;
+}
+
+}  // namespace spai
+
+extern "C" const char* spai_last_error(void) { return spai::g_err; }
+extern "C" int spai_version(void) { return 1; }

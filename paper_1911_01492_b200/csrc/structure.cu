@@ -1,0 +1,299 @@
+// K0 stencil generator, K1 CSR->CSC transpose structure, symmetry check, and
+// the nnz-balanced row tiling used by the TMA-staged SpMV.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace spai {
+
+struct StencilParams {
+  int dim;
+  int nst;                 // 3^dim
+  int64_t dims[3];
+  int64_t stride[3];
+  double table[27];
+  int stored[27];
+};
+
+__global__ void stencil_count_kernel(StencilParams P, int64_t n, int64_t* rowcnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[3] = {0, 0, 0}, r = i;
+    for (int a = 0; a < P.dim; ++a) { c[a] = r % P.dims[a]; r /= P.dims[a]; }
+    int64_t cnt = 0;
+    for (int t = 0; t < P.nst; ++t) {
+      if (!P.stored[t]) continue;
+      int tt = t; bool ok = true;
+      for (int a = 0; a < P.dim; ++a) {
+        int off = tt % 3 - 1; tt /= 3;
+        int64_t q = c[a] + off;
+        ok &= (q >= 0) && (q < P.dims[a]);
+      }
+      cnt += ok;
+    }
+    rowcnt[i + 1] = cnt;
+    if (i == 0) rowcnt[0] = 0;
+  }
+}
+
+__global__ void stencil_fill_kernel(StencilParams P, int64_t n, const int64_t* rowptr,
+                                    int32_t* colidx, double* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[3] = {0, 0, 0}, r = i;
+    for (int a = 0; a < P.dim; ++a) { c[a] = r % P.dims[a]; r /= P.dims[a]; }
+    int64_t pos = rowptr[i];
+    for (int t = 0; t < P.nst; ++t) {   // ascending t == ascending column
+      if (!P.stored[t]) continue;
+      int tt = t; bool ok = true; int64_t col = i;
+      for (int a = 0; a < P.dim; ++a) {
+        int off = tt % 3 - 1; tt /= 3;
+        int64_t q = c[a] + off;
+        ok &= (q >= 0) && (q < P.dims[a]);
+        col += off * P.stride[a];
+      }
+      if (ok) { colidx[pos] = (int32_t)col; vals[pos] = P.table[t]; ++pos; }
+    }
+  }
+}
+
+static int make_params(int dim, const int64_t* dims, const double* table,
+                       const uint8_t* stored, StencilParams* P, int64_t* n) {
+  if (dim < 1 || dim > 3) { set_error("stencil dim must be 1..3"); return SPAI_E_ARG; }
+  P->dim = dim;
+  P->nst = 1;
+  *n = 1;
+  for (int a = 0; a < 3; ++a) { P->dims[a] = 1; P->stride[a] = 0; }
+  for (int a = 0; a < dim; ++a) {
+    if (dims[a] < 1) { set_error("stencil dims must be >= 1"); return SPAI_E_ARG; }
+    P->dims[a] = dims[a];
+    P->stride[a] = *n;
+    *n *= dims[a];
+    P->nst *= 3;
+  }
+  if (*n >= (int64_t)INT32_MAX) { set_error("n = %lld exceeds int32 indices", (long long)*n); return SPAI_E_DIM; }
+  for (int t = 0; t < 27; ++t) {
+    P->table[t] = (table && t < P->nst) ? table[t] : 0.0;
+    P->stored[t] = (t < P->nst) ? (int)stored[t] : 0;
+  }
+  return SPAI_OK;
+}
+
+// ---- transpose ---------------------------------------------------------
+__global__ void col_count_kernel(int64_t nnz, const int32_t* colidx, int32_t* cnt) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz;
+       p += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[colidx[p]], 1);
+}
+
+__global__ void widen_kernel(int64_t m, const int32_t* cnt, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i + 1] = cnt[i];
+    if (i == 0) out[0] = 0;
+  }
+}
+
+// one warp per CSR row: scatter (row, position) into the column buckets
+__global__ void scatter_kernel(int64_t nrows, const int64_t* rowptr, const int32_t* colidx,
+                               const int64_t* cscptr, int32_t* cursor, int32_t* cscrow,
+                               int64_t* csc2csr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nrows; i += nwarps) {
+    const int64_t lo = rowptr[i], hi = rowptr[i + 1];
+    for (int64_t p = lo + lane; p < hi; p += 32) {
+      const int32_t c = colidx[p];
+      const int64_t slot = cscptr[c] + atomicAdd(&cursor[c], 1);
+      cscrow[slot] = (int32_t)i;
+      csc2csr[slot] = p;
+    }
+  }
+}
+
+// sort every column segment by row (rows are unique); insertion sort per thread
+__global__ void segsort_kernel(int64_t ncols, const int64_t* cscptr, int32_t* cscrow,
+                               int64_t* csc2csr) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncols;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = cscptr[c], hi = cscptr[c + 1];
+    for (int64_t a = lo + 1; a < hi; ++a) {
+      const int32_t r = cscrow[a];
+      const int64_t p = csc2csr[a];
+      int64_t b = a - 1;
+      while (b >= lo && cscrow[b] > r) {
+        cscrow[b + 1] = cscrow[b];
+        csc2csr[b + 1] = csc2csr[b];
+        --b;
+      }
+      cscrow[b + 1] = r;
+      csc2csr[b + 1] = p;
+    }
+  }
+}
+
+__global__ void sym_check_kernel(int64_t n, int64_t nnz, const int64_t* rowptr,
+                                 const int32_t* colidx, const int64_t* cscptr,
+                                 const int32_t* cscrow, int* bad) {
+  int local = 0;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i <= n; i += nt) local |= rowptr[i] != cscptr[i];
+  for (int64_t p = tid; p < nnz; p += nt) local |= colidx[p] != cscrow[p];
+  if (__syncthreads_or(local) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+// ---- nnz-balanced tiling: tile t starts at the first row with rowptr >= t*B
+constexpr int64_t kTileNnz = 2048;
+
+__global__ void tile_rows_kernel(int64_t n, const int64_t* rowptr, int64_t ntiles,
+                                 int64_t* tile_rows) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t == ntiles) { tile_rows[t] = n; continue; }
+    const int64_t target = t * kTileNnz;
+    int64_t lo = 0, hi = n;        // lower_bound over rowptr[0..n]
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (rowptr[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    tile_rows[t] = lo;
+  }
+}
+
+__global__ void tile_max_kernel(int64_t ntiles, const int64_t* rowptr,
+                                const int64_t* tile_rows, int32_t* maxnnz) {
+  int32_t m = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = rowptr[tile_rows[t + 1]] - rowptr[tile_rows[t]];
+    m = max(m, (int32_t)min(v, (int64_t)INT32_MAX));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxnnz, m);
+}
+
+static inline unsigned grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 32;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+}  // namespace spai
+
+using namespace spai;
+
+extern "C" int spai_stencil_nnz(int dim, const int64_t* dims, const uint8_t* stored,
+                                int64_t* nnz_out) {
+  StencilParams P;
+  int64_t n;
+  int st = make_params(dim, dims, nullptr, stored, &P, &n);
+  if (st) return st;
+  int64_t nnz = 0;
+  for (int t = 0; t < P.nst; ++t) {
+    if (!P.stored[t]) continue;
+    int tt = t;
+    int64_t c = 1;
+    for (int a = 0; a < dim; ++a) {
+      int off = tt % 3 - 1; tt /= 3;
+      int64_t m = P.dims[a] - (off != 0 ? 1 : 0);
+      c *= m > 0 ? m : 0;
+    }
+    nnz += c;
+  }
+  *nnz_out = nnz;
+  return SPAI_OK;
+}
+
+extern "C" int spai_stencil_csr(int dim, const int64_t* dims, const double* table,
+                                const uint8_t* stored, int64_t* rowptr, int32_t* colidx,
+                                double* vals, void* stream) {
+  StencilParams P;
+  int64_t n;
+  int st = make_params(dim, dims, table, stored, &P, &n);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  stencil_count_kernel<<<grid_for(n, 256), 256, 0, s>>>(P, n, rowptr);
+  SPAI_LAUNCH_CHECK("stencil_count_kernel");
+  size_t tb = 0;
+  SPAI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, rowptr + 1, rowptr + 1, n, s));
+  void* tmp = nullptr;
+  SPAI_CUDA(cudaMallocAsync(&tmp, tb, s));
+  SPAI_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, rowptr + 1, rowptr + 1, n, s));
+  SPAI_CUDA(cudaFreeAsync(tmp, s));
+  stencil_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(P, n, rowptr, colidx, vals);
+  SPAI_LAUNCH_CHECK("stencil_fill_kernel");
+  return SPAI_OK;
+}
+
+extern "C" size_t spai_transpose_workspace_bytes(int64_t nrows, int64_t ncols, int64_t nnz) {
+  (void)nrows; (void)nnz;
+  size_t tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, (int64_t*)nullptr, (int64_t*)nullptr, ncols);
+  return 2 * (size_t)ncols * sizeof(int32_t) + tb + 256;
+}
+
+extern "C" int spai_csr_transpose(int64_t nrows, int64_t ncols, int64_t nnz,
+                                  const int64_t* rowptr, const int32_t* colidx,
+                                  int64_t* cscptr, int32_t* cscrow, int64_t* csc2csr,
+                                  void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ws_bytes < spai_transpose_workspace_bytes(nrows, ncols, nnz)) {
+    set_error("transpose workspace too small");
+    return SPAI_E_ARG;
+  }
+  int32_t* cnt = (int32_t*)ws;
+  int32_t* cursor = cnt + ncols;
+  void* scan_tmp = (void*)(((uintptr_t)(cursor + ncols) + 255) & ~(uintptr_t)255);
+  size_t tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, cscptr + 1, cscptr + 1, ncols, s);
+  SPAI_CUDA(cudaMemsetAsync(cnt, 0, 2 * (size_t)ncols * sizeof(int32_t), s));
+  col_count_kernel<<<grid_for(nnz, 256), 256, 0, s>>>(nnz, colidx, cnt);
+  SPAI_LAUNCH_CHECK("col_count_kernel");
+  widen_kernel<<<grid_for(ncols, 256), 256, 0, s>>>(ncols, cnt, cscptr);
+  SPAI_LAUNCH_CHECK("widen_kernel");
+  SPAI_CUDA(cub::DeviceScan::InclusiveSum(scan_tmp, tb, cscptr + 1, cscptr + 1, ncols, s));
+  scatter_kernel<<<grid_for(nrows * 32, 256), 256, 0, s>>>(nrows, rowptr, colidx, cscptr,
+                                                            cursor, cscrow, csc2csr);
+  SPAI_LAUNCH_CHECK("scatter_kernel");
+  segsort_kernel<<<grid_for(ncols, 128), 128, 0, s>>>(ncols, cscptr, cscrow, csc2csr);
+  SPAI_LAUNCH_CHECK("segsort_kernel");
+  return SPAI_OK;
+}
+
+extern "C" int spai_structure_is_symmetric(int64_t n, int64_t nnz, const int64_t* rowptr,
+                                           const int32_t* colidx, const int64_t* cscptr,
+                                           const int32_t* cscrow, int* is_sym) {
+  int* d = nullptr;
+  SPAI_CUDA(cudaMalloc(&d, sizeof(int)));
+  SPAI_CUDA(cudaMemset(d, 0, sizeof(int)));
+  sym_check_kernel<<<grid_for(nnz > n ? nnz : n + 1, 256), 256>>>(n, nnz, rowptr, colidx,
+                                                                   cscptr, cscrow, d);
+  SPAI_LAUNCH_CHECK("sym_check_kernel");
+  int h = 0;
+  SPAI_CUDA(cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost));
+  SPAI_CUDA(cudaFree(d));
+  *is_sym = h ? 0 : 1;
+  return SPAI_OK;
+}
+
+extern "C" int spai_tile_count(int64_t n, int64_t nnz, int64_t* ntiles_out) {
+  (void)n;
+  *ntiles_out = nnz > 0 ? (nnz + kTileNnz - 1) / kTileNnz : 1;
+  return SPAI_OK;
+}
+
+extern "C" int spai_tile_rows(int64_t n, const int64_t* rowptr, int64_t ntiles,
+                              int64_t* tile_rows, int32_t* max_tile_nnz, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  tile_rows_kernel<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(n, rowptr, ntiles, tile_rows);
+  SPAI_LAUNCH_CHECK("tile_rows_kernel");
+  SPAI_CUDA(cudaMemsetAsync(max_tile_nnz, 0, sizeof(int32_t), s));
+  tile_max_kernel<<<grid_for(ntiles, 256), 256, 0, s>>>(ntiles, rowptr, tile_rows,
+                                                         max_tile_nnz);
+  SPAI_LAUNCH_CHECK("tile_max_kernel");
+  return SPAI_OK;
+}

@@ -1,0 +1,380 @@
+"""Device-resident preconditioned CG behind the reference `solve` API.
+
+Mirrors krylov.py:63-135 (`SolverConfig`, `KrylovState`, `ConvergenceRecord`)
+and krylov.py:159-248 (`LocalSystem`, `solve`).  The classic PCG loop
+(krylov.py:301-345) runs entirely on the GPU (kernel pair K1/K2 per
+iteration, scalar recurrence on the device, CUDA graphs of 16 iterations);
+the host only polls the status word between graphs, so the record, the
+iteration count and the termination rule are the reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import BreakdownError, DimensionMismatchError, DivergenceError
+from .precond import IdentityPreconditioner, Preconditioner, SparseMatrixPreconditioner
+from .sparse import (CsrMatrix, DeviceCsr, _require_cuda, _torch, as_device, ptr,
+                     stream_handle)
+
+VARIANTS = ("classic", "chronopoulos_gear", "gropp", "pipelined")
+_VARIANT_BUFFERS = {"classic": 4, "chronopoulos_gear": 6, "gropp": 6, "pipelined": 10}
+_REDUCTIONS_PER_ITER = {"classic": 2, "chronopoulos_gear": 1, "gropp": 2, "pipelined": 1}
+_EXTRA_OPS = {"classic": 0, "chronopoulos_gear": 1, "gropp": 2, "pipelined": 5}
+DEVICE_VARIANTS = ("classic",)
+
+
+def _check_variant(variant):
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    return variant
+
+
+def memory_accounting(variant: str) -> int:
+    return _VARIANT_BUFFERS[_check_variant(variant)]
+
+
+def reduction_rate(variant: str) -> int:
+    return _REDUCTIONS_PER_ITER[_check_variant(variant)]
+
+
+@dataclass
+class SolverConfig:
+    variant: str = "classic"
+    tol: float = 1e-8
+    maxit: int = 1000
+    record_history: bool = True
+
+    def __post_init__(self):
+        _check_variant(self.variant)
+        if not 0.0 < self.tol < 1.0:
+            raise ValueError("tol must lie in (0, 1)")
+        if self.maxit < 1:
+            raise ValueError("maxit must be >= 1")
+
+
+@dataclass
+class KrylovState:
+    variant: str
+    x: object = None
+    r: object = None
+    p: object = None
+    q: object = None
+    z: object = None
+    w: object = None
+    s: object = None
+    t: object = None
+    u: object = None
+    v: object = None
+    rho: float = 0.0
+    alpha: float = 0.0
+    alpha_tilde: float = 0.0
+
+    def vector_count(self) -> int:
+        names = ("x", "r", "p", "q", "z", "w", "s", "t", "u", "v")
+        return sum(getattr(self, n) is not None for n in names)
+
+
+@dataclass
+class ConvergenceRecord:
+    variant: str
+    iterations: int = 0
+    converged: bool = False
+    initial_residual: float = float("nan")
+    final_residual: float = float("nan")
+    residual_norms: list = field(default_factory=list)
+    reductions_cum: list = field(default_factory=list)
+    overlapped_cum: list = field(default_factory=list)
+    total_reductions: int = 0
+    total_overlapped: int = 0
+    vector_memory_units: int = 0
+    extra_vector_ops_units: int = 0
+    extra_columns: dict = field(default_factory=dict)
+
+    def to_csv(self) -> str:
+        extras = sorted(self.extra_columns)
+        header = "iteration,residual_norm,reductions_cum,overlapped_cum"
+        if extras:
+            header += "," + ",".join(extras)
+        lines = [header]
+        for i, rn in enumerate(self.residual_norms):
+            row = [str(i + 1), f"{rn:.17g}", str(self.reductions_cum[i]),
+                   str(self.overlapped_cum[i])]
+            for name in extras:
+                col = self.extra_columns[name]
+                val = col[i] if i < len(col) else ""
+                row.append(f"{val:.17g}" if isinstance(val, float) else str(val))
+            lines.append(",".join(row))
+        return "\n".join(lines) + "\n"
+
+
+class LocalSystem:
+    """Single-GPU system view (krylov.py:159-193): A and M live in HBM.
+
+    The protocol methods (`apply_A`, `apply_M`, `fused_dots`) accept host or
+    device vectors so the object also plugs into the reference `solve`; the
+    fast path is this package's `solve`, which never leaves the device.
+    """
+
+    def __init__(self, A, M=None, comm=None):
+        if A.nrows != A.ncols:
+            raise DimensionMismatchError("system matrix must be square")
+        self.A = A
+        self.M = M
+        self.comm = comm
+        self.n = A.nrows
+        self._dA = None
+
+    @property
+    def device_A(self) -> DeviceCsr:
+        if self._dA is None:
+            self._dA = as_device(self.A)
+        return self._dA
+
+    def device_M(self) -> DeviceCsr | None:
+        if self.M is None:
+            return None
+        if isinstance(self.M, DeviceCsr):
+            return self.M
+        if isinstance(self.M, Preconditioner):
+            return self.M.device_matrix()
+        raise TypeError(f"preconditioner {type(self.M).__name__} has no device form")
+
+    def apply_A(self, x):
+        from .sparse import spmv
+        return spmv(self.device_A, x)
+
+    def apply_M(self, x):
+        if self.M is None:
+            return x.copy() if hasattr(x, "copy") else x.clone()
+        dM = self.device_M()
+        if dM is None:
+            return IdentityPreconditioner().apply(x)
+        return SparseMatrixPreconditioner(dM).apply(x)
+
+    def fused_dots(self, pairs, overlapped=False):
+        torch = _require_cuda()
+        vals = []
+        for u, v in pairs:
+            tu = u if isinstance(u, torch.Tensor) else torch.from_numpy(np.asarray(u, np.float64)).cuda()
+            tv = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.asarray(v, np.float64)).cuda()
+            vals.append(fused_dots_device([(tu, tv)])[0])
+        return _ImmediateToken(vals)
+
+    def log_compute(self, label):
+        pass
+
+    def poll_faults(self, iteration):
+        pass
+
+
+class _ImmediateToken:
+    def __init__(self, values):
+        self._values = values
+        self._consumed = False
+
+    def ready(self):
+        return True
+
+    def valid(self):
+        return not self._consumed
+
+    def wait(self):
+        pass
+
+    def get(self):
+        self._consumed = True
+        return self._values
+
+
+def fused_dots_device(pairs):
+    """Deterministic fused dot products on the GPU (K6); returns floats."""
+    torch = _require_cuda()
+    lib = _lib.load()
+    n = pairs[0][0].numel()
+    k = len(pairs)
+    us = (C.c_void_p * 3)(*[p[0].data_ptr() for p in pairs], *([0] * (3 - k)))
+    vs = (C.c_void_p * 3)(*[p[1].data_ptr() for p in pairs], *([0] * (3 - k)))
+    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    wsb = lib.spai_dots_workspace_bytes(n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.spai_fused_dots(n, k, C.cast(us, C.c_void_p), C.cast(vs, C.c_void_p),
+                                   ptr(out), ptr(ws), wsb, stream_handle()), "spai_fused_dots")
+    return [float(v) for v in out[:k].cpu()]
+
+
+# ------------------------------------------------------------------ device PCG
+_STATUS = {0: "running", 1: "converged", 2: "maxit", 3: "breakdown", 4: "divergence"}
+
+
+class DevicePCG:
+    """Owner of a native `spai_pcg` solver (C-ABI K8)."""
+
+    def __init__(self, A: DeviceCsr, M: DeviceCsr | None, tol: float, maxit: int):
+        _require_cuda()
+        self.lib = _lib.load()
+        self.A, self.M = A, M
+        self.n = A.nrows
+        self.maxit = int(maxit)
+        h = C.c_void_p()
+        st = self.lib.spai_pcg_create(
+            C.byref(h), A.nrows, ptr(A.rowptr), ptr(A.colidx), ptr(A.vals),
+            ptr(M.rowptr) if M is not None else C.c_void_p(0),
+            ptr(M.colidx) if M is not None else C.c_void_p(0),
+            ptr(M.vals) if M is not None else C.c_void_p(0),
+            float(tol), self.maxit, stream_handle())
+        _lib.check(st, "spai_pcg_create")
+        self.h = h
+        self.launched = 0
+
+    def start(self, b, x0=None):
+        _lib.check(self.lib.spai_pcg_start(self.h, ptr(b), ptr(x0) if x0 is not None
+                                           else C.c_void_p(0)), "spai_pcg_start")
+
+    def advance(self, iters: int):
+        self.launched += int(iters)
+        _lib.check(self.lib.spai_pcg_advance(self.h, int(iters)), "spai_pcg_advance")
+
+    def poll(self):
+        st, it = C.c_int(0), C.c_int64(0)
+        n0, nr, aux = C.c_double(0), C.c_double(0), C.c_double(0)
+        _lib.check(self.lib.spai_pcg_poll(self.h, C.byref(st), C.byref(it), C.byref(n0),
+                                          C.byref(nr), C.byref(aux)), "spai_pcg_poll")
+        return st.value, it.value, n0.value, nr.value, aux.value
+
+    def history(self, count: int):
+        out = np.zeros(max(count, 0))
+        if count > 0:
+            _lib.check(self.lib.spai_pcg_history(self.h, out.ctypes.data, count),
+                       "spai_pcg_history")
+        return out
+
+    def vectors(self):
+        """(x, r, p, z) as torch tensors aliasing the solver's device buffers."""
+        torch = _torch()
+        ps = [C.c_void_p() for _ in range(4)]
+        _lib.check(self.lib.spai_pcg_vectors(self.h, *[C.byref(p) for p in ps]),
+                   "spai_pcg_vectors")
+        return [_wrap_device(p.value, self.n) for p in ps]
+
+    def run(self, chunk: int = 64):
+        """Advance until the device status leaves 'running'; returns poll()."""
+        while True:
+            st = self.poll()
+            if st[0] != 0:
+                return st
+            self.advance(chunk)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.spai_pcg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _wrap_device(addr: int, n: int):
+    """Zero-copy torch view of n doubles at a device address (kept alive by owner)."""
+    torch = _torch()
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                    "data": (addr, False), "version": 3, "strides": None}
+
+    return torch.as_tensor(_Cai(), device="cuda")
+
+
+def solve(system, b, cfg: SolverConfig, x0=None, callback=None):
+    """Run PCG on the GPU; returns (x, ConvergenceRecord)  (krylov.py:235-248).
+
+    `system` is a LocalSystem (or a bare CsrMatrix / DeviceCsr, wrapped without
+    a preconditioner).  Host b -> host x; CUDA-tensor b -> CUDA-tensor x.
+    `callback(iteration, state, record)` fires after every iteration (the
+    solver then syncs every iteration and exposes host copies of x, r, p, z).
+    """
+    torch = _require_cuda()
+    if isinstance(system, (CsrMatrix, DeviceCsr)) or (
+            hasattr(system, "row_offsets") and not hasattr(system, "apply_A")):
+        system = LocalSystem(system)
+    on_device = isinstance(b, torch.Tensor) and b.is_cuda
+    if not on_device:
+        b_host = np.asarray(b, dtype=np.float64)
+        if len(b_host) != system.n:
+            raise DimensionMismatchError("right-hand side length mismatch")
+        bd = torch.from_numpy(np.ascontiguousarray(b_host)).to("cuda")
+    else:
+        if b.numel() != system.n:
+            raise DimensionMismatchError("right-hand side length mismatch")
+        bd = b.to(torch.float64).contiguous()
+    if cfg.variant not in DEVICE_VARIANTS:
+        raise NotImplementedError(
+            f"variant {cfg.variant!r} is not on the device path yet (classic only)")
+    x0d = None
+    if x0 is not None:
+        x0d = x0 if isinstance(x0, torch.Tensor) else torch.from_numpy(
+            np.asarray(x0, dtype=np.float64)).to("cuda")
+        x0d = x0d.to(torch.float64).contiguous()
+    solver = DevicePCG(system.device_A, system.device_M(), cfg.tol, cfg.maxit)
+    try:
+        solver.start(bd, x0d)
+        rec = ConvergenceRecord(variant=cfg.variant, vector_memory_units=4,
+                                extra_vector_ops_units=0)
+        if callback is None:
+            status, it, norm0, norm, aux = solver.run()
+        else:
+            it_seen = 0
+            while True:
+                status, it, norm0, norm, aux = solver.poll()
+                if it > it_seen and status in (0, 1, 2):
+                    hist = solver.history(it)
+                    rec.residual_norms = [float(v) for v in hist]
+                    rec.reductions_cum = [2 * (i + 1) for i in range(it)]
+                    rec.overlapped_cum = [0] * it
+                    xs, rs, ps, zs = solver.vectors()
+                    st = KrylovState("classic", x=xs.cpu().numpy(), r=rs.cpu().numpy(),
+                                     p=ps.cpu().numpy(), q=zs.cpu().numpy())
+                    it_seen = it
+                    callback(it, st, rec)
+                if status != 0:
+                    break
+                solver.advance(1)
+        return _finish(solver, rec, cfg, status, it, norm0, norm, aux, on_device)
+    finally:
+        solver.close()
+
+
+def _finish(solver, rec, cfg, status, it, norm0, norm, aux, on_device):
+    if status == 3:
+        raise BreakdownError(f"indefinite curvature <p,Ap> = {aux}")
+    if status == 4:
+        raise DivergenceError("non-finite value in solver recurrence")
+    rec.initial_residual = norm0
+    # number of completed (noted) iterations: K2 finished for all but an early stop in K1
+    noted = it
+    early = False
+    if status == 1 and (norm0 == 0.0 or not (norm <= cfg.tol * norm0)):
+        noted = it - 1           # stopped inside K1 (norm0 == 0 or rho == 0)
+        early = True
+    if norm0 == 0.0:
+        norm = 0.0
+    if cfg.record_history:
+        rec.residual_norms = [float(v) for v in solver.history(noted)]
+        rec.reductions_cum = [2 * (i + 1) for i in range(noted)]
+        rec.overlapped_cum = [0] * noted
+    rec.iterations = it
+    rec.converged = status == 1
+    rec.final_residual = norm
+    rec.total_reductions = 2 * noted + (1 if early else 0)
+    rec.total_overlapped = 0
+    rec.launched_iterations = solver.launched
+    x = solver.vectors()[0].clone()
+    return (x if on_device else x.cpu().numpy()), rec

@@ -1,0 +1,241 @@
+"""SPAI(1) on the GPU and the preconditioner objects (drop-in for precond.py).
+
+* `spai1(A) -> CsrMatrix` replaces `spai1` (precond.py:175-199): same
+  signature, same pattern (pattern(M) == pattern(A)), same errors
+  (`FactorBreakdownError("rank-deficient subproblem for column j")`).
+* `spai1_device(A)` / `spai1_symmetric_device(A)` are the HBM-resident forms
+  used on the fast path (no host round trip).
+* `SparseMatrixPreconditioner(M).apply(r)` replaces precond.py:115-122.
+* `make_spai1_factory()` replaces the CLI spai1 branch (cli.py:187-195):
+  SPAI(1) followed by 0.5*(M + M^T) symmetrisation for CG.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionMismatchError, FactorBreakdownError, SingularDiagonalError
+from .sparse import (CsrMatrix, DeviceCsr, _require_cuda, _torch, as_device, ptr,
+                     stream_handle)
+
+
+class Preconditioner:
+    """Linear operator M applied as z = M r (precond.py:22-32)."""
+
+    def apply(self, r):
+        raise NotImplementedError
+
+    def apply_multi(self, R):
+        vals = R.values if hasattr(R, "values") else np.asarray(R)
+        out = np.empty_like(vals)
+        for j in range(vals.shape[1]):
+            out[:, j] = self.apply(vals[:, j])
+        return type(R)(out) if hasattr(R, "values") else out
+
+    def device_matrix(self) -> DeviceCsr | None:
+        """The operator as an HBM CSR matrix, used by the device-resident solvers."""
+        raise TypeError(f"{type(self).__name__} has no device representation")
+
+
+class IdentityPreconditioner(Preconditioner):
+    def apply(self, r):
+        torch = _torch()
+        if isinstance(r, torch.Tensor):
+            return r.clone()
+        return np.array(r, copy=True)
+
+    def device_matrix(self):
+        return None
+
+
+class SparseMatrixPreconditioner(Preconditioner):
+    """Apply a stored sparse matrix M (e.g. a SPAI-1 approximate inverse)."""
+
+    def __init__(self, M):
+        self.M = M
+        self._dev = M if isinstance(M, DeviceCsr) else None
+
+    def device_matrix(self) -> DeviceCsr:
+        if self._dev is None:
+            self._dev = as_device(self.M)
+        return self._dev
+
+    def apply(self, r):
+        torch = _torch()
+        if isinstance(r, torch.Tensor) and r.is_cuda:
+            return self.device_matrix().matvec(r)
+        return _apply_host(self.device_matrix(), r)
+
+
+def _apply_host(M: DeviceCsr, r):
+    torch = _require_cuda()
+    r = np.asarray(r, dtype=np.float64)
+    if M.ncols != len(r):
+        raise DimensionMismatchError(f"spmv: {M.ncols} columns vs vector of {len(r)}")
+    return M.matvec(torch.from_numpy(r).to("cuda")).cpu().numpy()
+
+
+class JacobiPreconditioner(SparseMatrixPreconditioner):
+    """D^-1 (precond.py:40-45, 125-129) held as a diagonal device matrix."""
+
+    def __init__(self, inv_diag):
+        torch = _require_cuda()
+        inv = np.asarray(inv_diag, dtype=np.float64)
+        n = len(inv)
+        dev = torch.device("cuda")
+        D = DeviceCsr(n, n, torch.arange(n + 1, dtype=torch.int64, device=dev),
+                      torch.arange(n, dtype=torch.int32, device=dev),
+                      torch.from_numpy(inv.copy()).to(dev))
+        super().__init__(D)
+        self.inv_diag = inv
+
+
+def jacobi(A) -> Preconditioner:
+    d = A.diagonal() if hasattr(A, "diagonal") else as_device(A).to_host().diagonal()
+    if np.any(d == 0.0):
+        raise SingularDiagonalError("zero diagonal entry")
+    return JacobiPreconditioner(1.0 / d)
+
+
+# ---------------------------------------------------------------- SPAI(1)
+def _raise_assembly(status: int, bad: int):
+    msg = _lib.last_error()
+    if status == _lib.SPAI_E_RANK_DEFICIENT:
+        raise FactorBreakdownError(f"rank-deficient subproblem for column {bad}")
+    if status == _lib.SPAI_E_EMPTY_COLUMN:
+        # reference: np.concatenate([]) on an empty pattern (precond.py:188)
+        raise ValueError("need at least one array to concatenate")
+    if status == _lib.SPAI_E_DIM:
+        raise np.linalg.LinAlgError("Last 2 dimensions of the array must be square")
+    raise _lib.NativeLibraryError(f"spai_assemble failed ({status}): {msg}")
+
+
+class SpaiStats:
+    def __init__(self):
+        self.n_fallback = 0
+
+
+def spai1_columns_device(A: DeviceCsr, stats: SpaiStats | None = None):
+    """m_k for every column, in CSC order (m_csc[cscptr[k] + t] pairs with J_k[t])."""
+    torch = _require_cuda()
+    lib = _lib.load()
+    if A.nrows != A.ncols:
+        raise DimensionMismatchError("spai1 needs a square matrix")
+    cscptr, cscrow, csc2csr = A.csc()
+    m_csc = torch.empty(max(A.nnz, 1), dtype=torch.float64, device=A.vals.device)
+    wsb = lib.spai_assemble_workspace_bytes(A.nrows)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
+    bad = C.c_int64(-1)
+    nfb = C.c_int64(0)
+    st = lib.spai_assemble(A.nrows, A.nnz, ptr(A.rowptr), ptr(A.colidx), ptr(A.vals),
+                           ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(m_csc), ptr(ws),
+                           wsb, C.byref(bad), C.byref(nfb), stream_handle())
+    _lib.check(st, "spai_assemble")
+    if st != _lib.SPAI_OK:
+        _raise_assembly(st, bad.value)
+    if stats is not None:
+        stats.n_fallback = nfb.value
+    return m_csc[: A.nnz]
+
+
+def spai1_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
+    """SPAI(1) M on pattern(A), CSR values in HBM (pattern shared with A)."""
+    torch = _require_cuda()
+    A = as_device(A)
+    m_csc = spai1_columns_device(A, stats)
+    _, _, csc2csr = A.csc()
+    vals = torch.empty_like(m_csc)
+    _lib.check(_lib.load().spai_csc_to_csr_values(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals),
+                                                  stream_handle()), "spai_csc_to_csr_values")
+    return A.with_values(vals)
+
+
+def spai1_symmetric_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
+    """0.5*(M + M^T) on pattern(A) (cli.py:189-194 semantics on the stored pattern).
+
+    Needs a structurally symmetric A (all FEM matrices here are); the
+    reference additionally drops exact zeros (`from_dense(tol=0)`), which
+    `to_reference_symmetric` reproduces on the host copy.
+    """
+    torch = _require_cuda()
+    A = as_device(A)
+    if not A.structurally_symmetric():
+        raise DimensionMismatchError(
+            "symmetrised SPAI(1) needs a structurally symmetric pattern")
+    m_csc = spai1_columns_device(A, stats)
+    _, _, csc2csr = A.csc()
+    vals = torch.empty_like(m_csc)
+    _lib.check(_lib.load().spai_symmetrize(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals),
+                                           stream_handle()), "spai_symmetrize")
+    return A.with_values(vals)
+
+
+def spai1(A) -> CsrMatrix:
+    """Sparse approximate inverse on the pattern of A (precond.py:175-199).
+
+    Column m_j minimizes ||A m_j - e_j||_2 over the pattern of A's column j;
+    every column's small least-squares problem is solved on the GPU.
+    """
+    M = spai1_device(A)
+    rows = np.asarray(A.row_offsets, dtype=np.int64).copy() if hasattr(A, "row_offsets") \
+        else M.rowptr.cpu().numpy()
+    cols = np.asarray(A.col_indices, dtype=np.int64).copy() if hasattr(A, "col_indices") \
+        else M.colidx.cpu().numpy().astype(np.int64)
+    return CsrMatrix(M.nrows, M.ncols, rows, cols, M.vals.cpu().numpy())
+
+
+def drop_exact_zeros(M: CsrMatrix) -> CsrMatrix:
+    """`from_dense(..., tol=0)` pattern semantics (sparse.py:78-81) on a CSR."""
+    keep = M.values != 0.0
+    if keep.all():
+        return M
+    rows = np.repeat(np.arange(M.nrows), np.diff(M.row_offsets))[keep]
+    offs = np.zeros(M.nrows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=M.nrows), out=offs[1:])
+    return CsrMatrix(M.nrows, M.ncols, offs, M.col_indices[keep], M.values[keep])
+
+
+def make_spai1_factory(device_resident: bool = True):
+    """Factory protocol `make_precond(A_local) -> Preconditioner` for kind="spai1"
+    (cli.py:187-195): SPAI(1), then 0.5*(M + M^T)."""
+
+    def factory(A_local):
+        S = spai1_symmetric_device(A_local)
+        if device_resident:
+            return SparseMatrixPreconditioner(S)
+        return SparseMatrixPreconditioner(drop_exact_zeros(S.to_host()))
+
+    return factory
+
+
+def pattern_sets(A, c0: int = 0, c1: int | None = None):
+    """(jptr, jidx, iptr, iidx) of precond.py:186-188 for columns [c0, c1), on the GPU.
+
+    jptr/iptr are relative to c0.  Returns torch CUDA tensors.
+    """
+    torch = _require_cuda()
+    lib = _lib.load()
+    A = as_device(A)
+    c1 = A.ncols if c1 is None else c1
+    cscptr, cscrow, _ = A.csc()
+    cnt = torch.empty(max(c1 - c0, 1), dtype=torch.int32, device=A.vals.device)
+    st = lib.spai_pattern_count(A.ncols, ptr(cscptr), ptr(cscrow), c0, c1, ptr(cnt),
+                                stream_handle())
+    _lib.check(st, "spai_pattern_count")
+    if st == _lib.SPAI_E_EMPTY_COLUMN:
+        raise ValueError("need at least one array to concatenate")
+    if st != _lib.SPAI_OK:
+        raise _lib.NativeLibraryError(_lib.last_error())
+    iptr = torch.zeros(c1 - c0 + 1, dtype=torch.int64, device=A.vals.device)
+    iptr[1:] = torch.cumsum(cnt[: c1 - c0].to(torch.int64), 0)
+    total = int(iptr[-1].item())
+    iidx = torch.empty(max(total, 1), dtype=torch.int32, device=A.vals.device)
+    st = lib.spai_pattern_fill(A.ncols, ptr(cscptr), ptr(cscrow), c0, c1, ptr(iptr),
+                               ptr(iidx), stream_handle())
+    _lib.check(st, "spai_pattern_fill")
+    jptr = cscptr[c0: c1 + 1] - cscptr[c0]
+    jidx = cscrow[int(cscptr[c0].item()): int(cscptr[c1].item())]
+    return jptr, jidx, iptr, iidx[:total]

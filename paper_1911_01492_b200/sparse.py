@@ -1,0 +1,297 @@
+"""CSR containers and SpMV.
+
+`CsrMatrix` mirrors the reference container (sparse.py:20-130): same fields,
+dtypes (int64 offsets/indices, f64 values) and validation errors, with the
+per-row Python validation loop (sparse.py:46-52) vectorised.  `DeviceCsr`
+is the HBM-resident form used by every kernel: int64 row pointers, int32
+column indices, f64 values, plus the lazily built CSC structure.
+
+`spmv` replaces the reference `spmv` (sparse.py:191-202) with the CUDA kernel
+K5; host arrays go through HBM, device tensors stay there.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionMismatchError, MatrixMarketError
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _require_cuda():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise _lib.NativeLibraryError(
+            "no CUDA device: paper_1911_01492_b200 runs on B200 only (no CPU fallback)")
+    _lib.load()
+    return torch
+
+
+def stream_handle():
+    torch = _torch()
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+@dataclass
+class CsrMatrix:
+    """Compressed sparse row matrix with sorted, duplicate-free columns per row."""
+
+    nrows: int
+    ncols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.row_offsets = np.asarray(self.row_offsets, dtype=np.int64)
+        self.col_indices = np.asarray(self.col_indices, dtype=np.int64)
+        self.values = np.asarray(self.values, dtype=np.float64)
+        if self.row_offsets.shape != (self.nrows + 1,):
+            raise DimensionMismatchError("row_offsets must have length nrows+1")
+        if self.row_offsets[0] != 0 or self.row_offsets[-1] != len(self.values):
+            raise DimensionMismatchError("row_offsets must span [0, nnz]")
+        if np.any(np.diff(self.row_offsets) < 0):
+            raise DimensionMismatchError("row_offsets must be nondecreasing")
+        if len(self.col_indices) != len(self.values):
+            raise DimensionMismatchError("col_indices and values length mismatch")
+        if len(self.col_indices) and (
+            self.col_indices.min() < 0 or self.col_indices.max() >= self.ncols
+        ):
+            raise DimensionMismatchError("column index out of range")
+        if len(self.col_indices) > 1:
+            step = np.diff(self.col_indices) <= 0
+            # positions that start a new row are not comparisons within a row
+            starts = self.row_offsets[1:-1]
+            starts = starts[(starts > 0) & (starts < len(self.col_indices))]
+            step[starts - 1] = False
+            if np.any(step):
+                p = int(np.flatnonzero(step)[0]) + 1
+                i = int(np.searchsorted(self.row_offsets, p, side="right") - 1)
+                raise DimensionMismatchError(f"columns of row {i} not strictly increasing")
+        self._dev = None
+
+    @property
+    def nnz(self) -> int:
+        return len(self.values)
+
+    @classmethod
+    def from_coo(cls, nrows, ncols, rows, cols, vals) -> "CsrMatrix":
+        """sparse.py:58-75 semantics (lexsort, duplicate rejection)."""
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        vals = np.asarray(vals, dtype=np.float64)
+        order = np.lexsort((cols, rows))
+        rows, cols, vals = rows[order], cols[order], vals[order]
+        if len(rows) > 1:
+            dup = (np.diff(rows) == 0) & (np.diff(cols) == 0)
+            if np.any(dup):
+                k = int(np.flatnonzero(dup)[0])
+                raise MatrixMarketError(f"duplicate entry at ({rows[k]}, {cols[k]})")
+        offsets = np.zeros(nrows + 1, dtype=np.int64)
+        np.add.at(offsets, rows + 1, 1)
+        np.cumsum(offsets, out=offsets)
+        return cls(nrows, ncols, offsets, cols, vals)
+
+    @classmethod
+    def from_dense(cls, dense, tol: float = 0.0) -> "CsrMatrix":
+        dense = np.asarray(dense, dtype=np.float64)
+        rows, cols = np.nonzero(np.abs(dense) > tol)
+        return cls.from_coo(*dense.shape, rows, cols, dense[rows, cols])
+
+    @classmethod
+    def identity(cls, n: int) -> "CsrMatrix":
+        idx = np.arange(n, dtype=np.int64)
+        return cls(n, n, np.arange(n + 1, dtype=np.int64), idx, np.ones(n))
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.nrows, self.ncols))
+        rows = np.repeat(np.arange(self.nrows), np.diff(self.row_offsets))
+        out[rows, self.col_indices] = self.values
+        return out
+
+    def row(self, i: int):
+        lo, hi = self.row_offsets[i], self.row_offsets[i + 1]
+        return self.col_indices[lo:hi], self.values[lo:hi]
+
+    def diagonal(self) -> np.ndarray:
+        m = min(self.nrows, self.ncols)
+        d = np.zeros(m)
+        rows = np.repeat(np.arange(self.nrows), np.diff(self.row_offsets))
+        hit = (rows == self.col_indices) & (rows < m)
+        d[rows[hit]] = self.values[hit]
+        return d
+
+    def transpose(self) -> "CsrMatrix":
+        rows = np.repeat(np.arange(self.nrows), np.diff(self.row_offsets))
+        return CsrMatrix.from_coo(self.ncols, self.nrows, self.col_indices, rows,
+                                  self.values)
+
+    # ---- device side
+    def device(self) -> "DeviceCsr":
+        """HBM copy of this matrix (cached; re-uploaded if the arrays were replaced)."""
+        key = (id(self.row_offsets), id(self.col_indices), id(self.values))
+        if self._dev is None or self._dev[0] != key:
+            self._dev = (key, DeviceCsr.from_host(self))
+        return self._dev[1]
+
+
+class DeviceCsr:
+    """HBM-resident CSR: rowptr int64[n+1], colidx int32[nnz], vals f64[nnz]."""
+
+    def __init__(self, nrows, ncols, rowptr, colidx, vals, structure_of=None):
+        self.nrows = int(nrows)
+        self.ncols = int(ncols)
+        self.rowptr = rowptr
+        self.colidx = colidx
+        self.vals = vals
+        self.nnz = int(colidx.numel())
+        self._csc = structure_of._csc if structure_of is not None else None
+        self._sym = structure_of._sym if structure_of is not None else None
+        self._tiles = structure_of._tiles if structure_of is not None else None
+
+    @classmethod
+    def from_host(cls, A: CsrMatrix) -> "DeviceCsr":
+        torch = _require_cuda()
+        if A.nrows >= 2**31 - 1 or A.ncols >= 2**31 - 1:
+            raise DimensionMismatchError("matrix dimension exceeds int32 indices")
+        dev = torch.device("cuda")
+        rowptr = torch.from_numpy(np.ascontiguousarray(A.row_offsets)).to(dev)
+        colidx = torch.from_numpy(A.col_indices.astype(np.int32)).to(dev)
+        vals = torch.from_numpy(np.ascontiguousarray(A.values)).to(dev)
+        return cls(A.nrows, A.ncols, rowptr, colidx, vals)
+
+    def to_host(self) -> CsrMatrix:
+        return CsrMatrix(self.nrows, self.ncols, self.rowptr.cpu().numpy(),
+                         self.colidx.cpu().numpy().astype(np.int64),
+                         self.vals.cpu().numpy())
+
+    def with_values(self, vals) -> "DeviceCsr":
+        """Same pattern (and cached CSC structure), new values."""
+        return DeviceCsr(self.nrows, self.ncols, self.rowptr, self.colidx, vals,
+                         structure_of=self)
+
+    @property
+    def shape(self):
+        return (self.nrows, self.ncols)
+
+    def nbytes(self) -> int:
+        return 8 * (self.nrows + 1) + 12 * self.nnz
+
+    # K1: transpose structure
+    def csc(self):
+        """(cscptr int64[ncols+1], cscrow int32[nnz], csc2csr int64[nnz]) (cached)."""
+        if self._csc is None:
+            torch = _require_cuda()
+            lib = _lib.load()
+            dev = self.rowptr.device
+            cscptr = torch.empty(self.ncols + 1, dtype=torch.int64, device=dev)
+            cscrow = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            csc2csr = torch.empty(max(self.nnz, 1), dtype=torch.int64, device=dev)
+            wsb = lib.spai_transpose_workspace_bytes(self.nrows, self.ncols, self.nnz)
+            ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+            _lib.check(lib.spai_csr_transpose(
+                self.nrows, self.ncols, self.nnz, ptr(self.rowptr), ptr(self.colidx),
+                ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(ws), wsb, stream_handle()),
+                "spai_csr_transpose")
+            self._csc = (cscptr, cscrow[: self.nnz], csc2csr[: self.nnz])
+        return self._csc
+
+    def structurally_symmetric(self) -> bool:
+        if self._sym is None:
+            if self.nrows != self.ncols:
+                self._sym = False
+            else:
+                lib = _lib.load()
+                cscptr, cscrow, _ = self.csc()
+                torch = _torch()
+                torch.cuda.current_stream().synchronize()
+                out = C.c_int(0)
+                _lib.check(lib.spai_structure_is_symmetric(
+                    self.nrows, self.nnz, ptr(self.rowptr), ptr(self.colidx), ptr(cscptr),
+                    ptr(cscrow), C.byref(out)), "spai_structure_is_symmetric")
+                self._sym = bool(out.value)
+        return self._sym
+
+    def tiles(self):
+        """nnz-balanced row tiles of the TMA-staged SpMV (cached per pattern)."""
+        if self._tiles is None:
+            torch = _require_cuda()
+            lib = _lib.load()
+            nt = C.c_int64(0)
+            lib.spai_tile_count(self.nrows, self.nnz, C.byref(nt))
+            tile_rows = torch.empty(nt.value + 1, dtype=torch.int64, device=self.vals.device)
+            mx = torch.zeros(1, dtype=torch.int32, device=self.vals.device)
+            _lib.check(lib.spai_tile_rows(self.nrows, ptr(self.rowptr), nt.value, ptr(tile_rows),
+                                          ptr(mx), stream_handle()), "spai_tile_rows")
+            self._tiles = (tile_rows, nt.value, int(mx.item()))
+        return self._tiles
+
+    def matvec_tma(self, x, out=None):
+        """y = A x with the TMA (cp.async.bulk) staged kernel."""
+        torch = _require_cuda()
+        if x.numel() != self.ncols:
+            raise DimensionMismatchError(
+                f"spmv: {self.ncols} columns vs vector of {x.numel()}")
+        if out is None:
+            out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
+        tile_rows, nt, mx = self.tiles()
+        _lib.check(_lib.load().spai_csr_spmv_tma(
+            self.nrows, ptr(self.rowptr), ptr(self.colidx), ptr(self.vals), ptr(tile_rows), nt,
+            mx, ptr(x.contiguous()), ptr(out), stream_handle()), "spai_csr_spmv_tma")
+        return out
+
+    def matvec(self, x, out=None):
+        """y = A x on device tensors (K5)."""
+        torch = _require_cuda()
+        if x.numel() != self.ncols:
+            raise DimensionMismatchError(
+                f"spmv: {self.ncols} columns vs vector of {x.numel()}")
+        if out is None:
+            out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
+        x = x.contiguous()
+        _lib.check(_lib.load().spai_csr_spmv(
+            self.nrows, self.nnz, ptr(self.rowptr), ptr(self.colidx), ptr(self.vals),
+            ptr(x), ptr(out), stream_handle()), "spai_csr_spmv")
+        return out
+
+
+def as_device(A) -> DeviceCsr:
+    if isinstance(A, DeviceCsr):
+        return A
+    if isinstance(A, CsrMatrix):
+        return A.device()
+    # duck-typed reference CsrMatrix (ftkrylov.sparse.CsrMatrix)
+    if all(hasattr(A, a) for a in ("nrows", "ncols", "row_offsets", "col_indices", "values")):
+        return DeviceCsr.from_host(CsrMatrix(A.nrows, A.ncols, A.row_offsets,
+                                             A.col_indices, A.values))
+    raise TypeError(f"expected a CSR matrix, got {type(A).__name__}")
+
+
+def spmv(A, x):
+    """Exact CSR product on the GPU (replaces sparse.py:191-202).
+
+    Host (numpy) input returns a fresh numpy array; CUDA tensors stay on device.
+    Raises DimensionMismatchError exactly like the reference.
+    """
+    torch = _torch()
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return as_device(A).matvec(x.to(torch.float64))
+    x = np.asarray(x, dtype=np.float64)
+    if A.ncols != len(x):
+        raise DimensionMismatchError(f"spmv: {A.ncols} columns vs vector of {len(x)}")
+    torch = _require_cuda()
+    dA = as_device(A)
+    y = dA.matvec(torch.from_numpy(x).to("cuda"))
+    return y.cpu().numpy()

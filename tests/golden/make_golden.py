@@ -1,0 +1,175 @@
+"""Generate golden vectors by running the UNMODIFIED reference (ftkrylov).
+
+Run in the build container (the reference is NOT available on the GPU box):
+
+    python tests/golden/make_golden.py
+
+It imports ftkrylov from /root/reference/pkg/src (read-only) and writes
+tests/golden/golden.npz.  Q1 / 3D / convection-diffusion matrices have no
+reference generator, so they are produced by oracle.problems and handed to
+the reference `spai1` / `solve` as reference `CsrMatrix` objects: the
+reference then pins the SPAI(1) and PCG results on them.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import ftkrylov as fk                       # noqa: E402  (the reference)
+from ftkrylov.cli import ExperimentConfig   # noqa: E402
+import oracle                               # noqa: E402  (only for Q1 stencils)
+
+
+def ref_csr(c):
+    return fk.CsrMatrix(c.nrows, c.ncols, c.row_offsets, c.col_indices, c.values)
+
+
+def ref_pattern_sets(A):
+    """precond.py:182-188 executed with the reference's own objects."""
+    At = A.transpose()
+    jptr, jidx, iptr, iidx = [0], [], [0], []
+    for j in range(A.nrows):
+        pattern, _ = At.row(j)
+        touched = np.unique(np.concatenate([At.row(c)[0] for c in pattern]))
+        jidx.extend(pattern.tolist())
+        iidx.extend(touched.tolist())
+        jptr.append(len(jidx))
+        iptr.append(len(iidx))
+    return (np.array(jptr, np.int64), np.array(jidx, np.int64),
+            np.array(iptr, np.int64), np.array(iidx, np.int64))
+
+
+def spai_cases():
+    cases = {}
+    for nx, ny in ((10, 10), (32, 32)):
+        A = fk.assemble_poisson(fk.StructuredGrid(nx, ny))
+        cases[f"fd5_{nx}x{ny}"] = A
+    cases["fd5_16x16_aniso"] = fk.assemble_poisson(
+        fk.StructuredGrid(16, 16), fk.Anisotropy(1.0, 1e-3))
+    cases["fd5_7x5_h025"] = fk.assemble_poisson(
+        fk.StructuredGrid(7, 5, 0.25), fk.Anisotropy(1.0, 0.01))
+    v, s = oracle.q1_stencil(2)
+    cases["q1_2d_12x12"] = ref_csr(oracle.stencil_csr((12, 12), v, s))
+    v, s = oracle.q1_stencil(2, eps=(1.0, 1e-3))
+    cases["q1_2d_10x9_aniso"] = ref_csr(oracle.stencil_csr((10, 9), v, s))
+    v, s = oracle.q1_stencil(3)
+    cases["q1_3d_6x6x6"] = ref_csr(oracle.stencil_csr((6, 6, 6), v, s))
+    v, s = oracle.q1_stencil(3, h=0.5)
+    cases["q1_3d_5x4x3_h05"] = ref_csr(oracle.stencil_csr((5, 4, 3), v, s))
+    v, s = oracle.q1_stencil(3, conv=(1.0, 0.5, 0.25))
+    cases["cd_3d_5x5x5"] = ref_csr(oracle.stencil_csr((5, 5, 5), v, s))
+    v, s = oracle.q1_stencil(2, conv=(4.0, -2.0))
+    cases["cd_2d_9x8"] = ref_csr(oracle.stencil_csr((9, 8), v, s))
+    return cases
+
+
+def solve_cases():
+    """CG + sym-SPAI(1) via the CLI factory semantics (cli.py:187-195)."""
+    out = {}
+    raw = {"preconditioner": {"kind": "spai1"}}
+    factory = ExperimentConfig(raw).make_precond_factory()
+    cfg = fk.SolverConfig(variant="classic", tol=1e-8, maxit=5000)
+    probs = {
+        "fd5_64x64": fk.assemble_poisson(fk.StructuredGrid(64, 64)),
+        "q1_2d_32x32": ref_csr(oracle.stencil_csr((32, 32), *oracle.q1_stencil(2))),
+        "q1_3d_10x10x10": ref_csr(oracle.stencil_csr((10, 10, 10),
+                                                     *oracle.q1_stencil(3))),
+        "q1_2d_24x24_aniso": ref_csr(oracle.stencil_csr(
+            (24, 24), *oracle.q1_stencil(2, eps=(1.0, 1e-3)))),
+    }
+    for name, A in probs.items():
+        b = fk.spmv(A, np.ones(A.nrows))
+        P = factory(A)
+        x, rec = fk.solve(fk.LocalSystem(A, P), b, cfg)
+        out[name] = dict(A=A, b=b, x=x, hist=np.array(rec.residual_norms),
+                         its=rec.iterations, norm0=rec.initial_residual,
+                         red=np.array(rec.reductions_cum),
+                         sym=P.M)
+    return out
+
+
+def multirank_cases():
+    """Reference multi-rank block-local SPAI runs (cli.py:234-253)."""
+    from ftkrylov.cli import _solve_once
+    out = {}
+    for ranks in (1, 2, 4):
+        raw = {"problem": {"nx": 32, "ny": 32}, "partition": {"ranks": ranks},
+               "solver": {"variant": "classic", "tol": 1e-8, "maxit": 5000},
+               "preconditioner": {"kind": "spai1"}}
+        cfg = ExperimentConfig(raw)
+        x, rec, _ = _solve_once(cfg, 0, "deterministic")
+        out[ranks] = dict(x=x, hist=np.array(rec.residual_norms),
+                          its=rec.iterations)
+    return out
+
+
+def main():
+    data = {}
+    for name, A in spai_cases().items():
+        M = fk.spai1(A)
+        jptr, jidx, iptr, iidx = ref_pattern_sets(A)
+        data[f"spai/{name}/n"] = np.array(A.nrows)
+        data[f"spai/{name}/A_ptr"] = A.row_offsets
+        data[f"spai/{name}/A_col"] = A.col_indices
+        data[f"spai/{name}/A_val"] = A.values
+        data[f"spai/{name}/M_ptr"] = M.row_offsets
+        data[f"spai/{name}/M_col"] = M.col_indices
+        data[f"spai/{name}/M_val"] = M.values
+        data[f"spai/{name}/jptr"] = jptr
+        data[f"spai/{name}/jidx"] = jidx
+        data[f"spai/{name}/iptr"] = iptr
+        data[f"spai/{name}/iidx"] = iidx
+        # cli.py:189-194 dense symmetrisation
+        Mt = M.transpose()
+        S = fk.CsrMatrix.from_dense(0.5 * (M.to_dense() + Mt.to_dense()), tol=0.0)
+        data[f"spai/{name}/S_ptr"] = S.row_offsets
+        data[f"spai/{name}/S_col"] = S.col_indices
+        data[f"spai/{name}/S_val"] = S.values
+        print(f"spai {name}: n={A.nrows} nnz={A.nnz}")
+    for name, d in solve_cases().items():
+        A = d["A"]
+        data[f"solve/{name}/A_ptr"] = A.row_offsets
+        data[f"solve/{name}/A_col"] = A.col_indices
+        data[f"solve/{name}/A_val"] = A.values
+        data[f"solve/{name}/b"] = d["b"]
+        data[f"solve/{name}/x"] = d["x"]
+        data[f"solve/{name}/hist"] = d["hist"]
+        data[f"solve/{name}/red"] = d["red"]
+        data[f"solve/{name}/its"] = np.array(d["its"])
+        data[f"solve/{name}/norm0"] = np.array(d["norm0"])
+        data[f"solve/{name}/S_val"] = d["sym"].values
+        data[f"solve/{name}/S_col"] = d["sym"].col_indices
+        data[f"solve/{name}/S_ptr"] = d["sym"].row_offsets
+        print(f"solve {name}: its={d['its']}")
+    for ranks, d in multirank_cases().items():
+        data[f"multirank/fd5_32x32/{ranks}/hist"] = d["hist"]
+        data[f"multirank/fd5_32x32/{ranks}/its"] = np.array(d["its"])
+        data[f"multirank/fd5_32x32/{ranks}/x"] = d["x"]
+        print(f"multirank {ranks}: its={d['its']}")
+    # FactorBreakdownError case (precond.py:192-194)
+    A = fk.CsrMatrix.from_dense(np.array([[1.0, 1.0, 0.0],
+                                          [1.0, 1.0, 0.0],
+                                          [0.0, 0.0, 2.0]]))
+    try:
+        fk.spai1(A)
+        msg = ""
+    except fk.FactorBreakdownError as e:
+        msg = str(e)
+    data["breakdown/A_ptr"] = A.row_offsets
+    data["breakdown/A_col"] = A.col_indices
+    data["breakdown/A_val"] = A.values
+    data["breakdown/msg"] = np.array(msg)
+    print("breakdown:", msg)
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **data)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,405 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference's golden vectors.  Tolerances are the ones BASELINE.json states:
+pattern bit-exact, SPAI entries <= 1e-10 relative (per column,
+||dm||_inf / ||m_ref||_inf), residual histories <= 1e-8 relative,
+iteration counts +-1."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_names
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1911_01492_b200 as pb  # noqa: E402
+
+SPAI_TOL = 1e-10
+HIST_TOL = 1e-8
+
+
+def _gcsr(g, pre, tag="A"):
+    p = g[f"{pre}/{tag}_ptr"]
+    return pb.CsrMatrix(len(p) - 1, len(p) - 1, p, g[f"{pre}/{tag}_col"], g[f"{pre}/{tag}_val"])
+
+
+def _ocsr(A):
+    return oracle.Csr(A.nrows, A.ncols, np.asarray(A.row_offsets), np.asarray(A.col_indices),
+                      np.asarray(A.values))
+
+
+def column_rel_err(A, M_got, M_ref):
+    """max over columns of ||m_got - m_ref||_inf / ||m_ref||_inf (CSC order)."""
+    At, perm = oracle.transpose(_ocsr(A))
+    got = np.asarray(M_got)[perm]
+    ref = np.asarray(M_ref)[perm]
+    cols = np.repeat(np.arange(A.ncols), np.diff(At.row_offsets))
+    num = np.zeros(A.ncols)
+    den = np.zeros(A.ncols)
+    np.maximum.at(num, cols, np.abs(got - ref))
+    np.maximum.at(den, cols, np.abs(ref))
+    den[den == 0] = 1.0
+    return float(np.max(num / den))
+
+
+# ------------------------------------------------------------------ generators
+@pytest.mark.parametrize("dims,eps,conv,h", [
+    ((7, 5), None, None, 1.0),
+    ((16, 16), (1.0, 1e-3), None, 1.0),
+    ((6, 5, 4), None, None, 1.0),
+    ((5, 5, 5), None, (1.0, 0.5, 0.25), 0.1),
+    ((9, 3), None, (4.0, -2.0), 0.5),
+    ((1, 4, 3), None, None, 1.0),
+])
+def test_q1_generator_bit_exact(dims, eps, conv, h):
+    A = pb.q1_device(dims, eps, conv, h).to_host()
+    R = oracle.stencil_csr(dims, *oracle.q1_stencil(len(dims), eps, conv, h))
+    assert np.array_equal(A.row_offsets, R.row_offsets)
+    assert np.array_equal(A.col_indices, R.col_indices)
+    assert np.array_equal(A.values, R.values)
+
+
+def test_fd5_generator_matches_reference_assembly(golden):
+    shapes = {"fd5_10x10": (10, 10, 1.0, 1.0, 1.0), "fd5_32x32": (32, 32, 1.0, 1.0, 1.0),
+              "fd5_16x16_aniso": (16, 16, 1.0, 1e-3, 1.0),
+              "fd5_7x5_h025": (7, 5, 1.0, 0.01, 0.25)}
+    for name, (nx, ny, ex, ey, h) in shapes.items():
+        A = pb.assemble_poisson(pb.StructuredGrid(nx, ny, h), pb.Anisotropy(ex, ey))
+        R = _gcsr(golden, f"spai/{name}")
+        assert np.array_equal(A.row_offsets, R.row_offsets)
+        assert np.array_equal(A.col_indices, R.col_indices)
+        assert np.array_equal(A.values, R.values)
+
+
+# ------------------------------------------------------------------ K1 / K2
+def _random_symmetric_pattern(n, extra, seed, dense_cols=()):
+    rng = np.random.default_rng(seed)
+    r = rng.integers(0, n, extra)
+    c = rng.integers(0, n, extra)
+    rows = np.concatenate([np.arange(n), r, c])
+    cols = np.concatenate([np.arange(n), c, r])
+    for d in dense_cols:
+        rows = np.concatenate([rows, np.arange(n), np.full(n, d)])
+        cols = np.concatenate([cols, np.full(n, d), np.arange(n)])
+    key = np.unique(rows * n + cols)
+    rows, cols = key // n, key % n
+    vals = rng.standard_normal(len(rows))
+    vals[rows == cols] = 10.0 + np.abs(vals[rows == cols]) * 5
+    return pb.CsrMatrix.from_coo(n, n, rows, cols, vals)
+
+
+def test_transpose_structure_matches_oracle():
+    for A in (pb.assemble_q1((9, 7, 5)), _random_symmetric_pattern(300, 900, 1),
+              pb.assemble_q1((13, 11), conv=(2.0, 1.0))):
+        At, perm = oracle.transpose(_ocsr(A))
+        cscptr, cscrow, csc2csr = A.device().csc()
+        assert np.array_equal(cscptr.cpu().numpy(), At.row_offsets)
+        assert np.array_equal(cscrow.cpu().numpy().astype(np.int64), At.col_indices)
+        assert np.array_equal(csc2csr.cpu().numpy(), perm)
+
+
+def test_nonsymmetric_structure_transpose():
+    rng = np.random.default_rng(4)
+    n = 200
+    rows = rng.integers(0, n, 1500)
+    cols = rng.integers(0, n, 1500)
+    key = np.unique(np.concatenate([rows * n + cols, np.arange(n) * (n + 1)]))
+    A = pb.CsrMatrix.from_coo(n, n, key // n, key % n, rng.standard_normal(len(key)))
+    At, perm = oracle.transpose(_ocsr(A))
+    cscptr, cscrow, csc2csr = A.device().csc()
+    assert np.array_equal(cscrow.cpu().numpy().astype(np.int64), At.col_indices)
+    assert np.array_equal(csc2csr.cpu().numpy(), perm)
+    assert not A.device().structurally_symmetric()
+    assert pb.assemble_q1((5, 4)).device().structurally_symmetric()
+
+
+def test_pattern_sets_match_reference_golden(golden):
+    for name in golden_names(golden, "spai"):
+        pre = f"spai/{name}"
+        A = _gcsr(golden, pre)
+        jptr, jidx, iptr, iidx = pb.pattern_sets(A)
+        assert np.array_equal(jptr.cpu().numpy(), golden[f"{pre}/jptr"]), name
+        assert np.array_equal(jidx.cpu().numpy(), golden[f"{pre}/jidx"]), name
+        assert np.array_equal(iptr.cpu().numpy(), golden[f"{pre}/iptr"]), name
+        assert np.array_equal(iidx.cpu().numpy(), golden[f"{pre}/iidx"]), name
+
+
+@pytest.mark.parametrize("make", [
+    lambda: pb.assemble_q1((20, 18, 16)),
+    lambda: pb.assemble_q1((128, 96)),
+    lambda: _random_symmetric_pattern(2000, 6000, 7),
+])
+def test_pattern_sets_match_oracle_large(make):
+    A = make()
+    ref = oracle.pattern_sets(_ocsr(A))
+    got = pb.pattern_sets(A)
+    for g, r in zip(got, ref):
+        assert np.array_equal(g.cpu().numpy().astype(np.int64), r)
+
+
+def test_pattern_sets_batched_range():
+    A = pb.assemble_q1((12, 11, 10))
+    ref = oracle.pattern_sets(_ocsr(A))
+    c0, c1 = 137, 911
+    jptr, jidx, iptr, iidx = pb.pattern_sets(A, c0, c1)
+    rjptr, rjidx, riptr, riidx = ref
+    assert np.array_equal(iptr.cpu().numpy(), riptr[c0:c1 + 1] - riptr[c0])
+    assert np.array_equal(iidx.cpu().numpy(), riidx[riptr[c0]:riptr[c1]])
+    assert np.array_equal(jidx.cpu().numpy(), rjidx[rjptr[c0]:rjptr[c1]])
+
+
+# ------------------------------------------------------------------ K3 / K4
+def test_spai1_matches_reference_golden(golden):
+    for name in golden_names(golden, "spai"):
+        pre = f"spai/{name}"
+        A = _gcsr(golden, pre)
+        M = pb.spai1(A)
+        assert np.array_equal(M.row_offsets, golden[f"{pre}/M_ptr"]), name
+        assert np.array_equal(M.col_indices, golden[f"{pre}/M_col"]), name
+        err = column_rel_err(A, M.values, golden[f"{pre}/M_val"])
+        assert err <= SPAI_TOL, (name, err)
+
+
+def test_spai1_acceptance_criterion_05_semantics():
+    """tests/test_acceptance.py:161-182 with the GPU spai1 swapped in."""
+    for nx, ny in ((10, 10), (32, 32)):
+        A = pb.assemble_poisson(pb.StructuredGrid(nx, ny))
+        M = pb.spai1(A)
+        dense, Md = A.to_dense(), M.to_dense()
+        n = A.nrows
+        for j in range(n):
+            pattern = np.nonzero(dense[:, j])[0]
+            e = np.zeros(n)
+            e[j] = 1.0
+            m_opt, *_ = np.linalg.lstsq(dense[:, pattern], e, rcond=None)
+            r_opt = np.linalg.norm(dense[:, pattern] @ m_opt - e)
+            r_got = np.linalg.norm(dense @ Md[:, j] - e)
+            assert abs(r_got - r_opt) < 1e-10
+            off = np.delete(Md[:, j], pattern)
+            assert not off.any()
+
+
+@pytest.mark.parametrize("make,ncheck", [
+    (lambda: pb.assemble_q1((24, 24, 24)), 3000),
+    (lambda: pb.assemble_q1((20, 17, 15), conv=(1.0, 0.5, 0.25)), 3000),
+    (lambda: pb.assemble_q1((256, 200), eps=(1.0, 1e-3)), 3000),
+    (lambda: _random_symmetric_pattern(1500, 4000, 11), 1500),
+    (lambda: _random_symmetric_pattern(120, 300, 12, dense_cols=(5, 77)), 120),
+])
+def test_spai1_matches_oracle_sampled(make, ncheck):
+    """Sizes the reference cannot densify quickly: oracle LS per sampled column."""
+    A = make()
+    stats = pb.SpaiStats()
+    M = pb.spai1_device(A.device(), stats)
+    m_csc = pb.precond.spai1_columns_device(A.device())
+    m_csc = m_csc.cpu().numpy()
+    oa = _ocsr(A)
+    sets = oracle.pattern_sets(oa)
+    rng = np.random.default_rng(0)
+    cols = np.unique(np.concatenate([np.arange(min(64, A.ncols)),
+                                     np.arange(max(A.ncols - 64, 0), A.ncols),
+                                     rng.integers(0, A.ncols, ncheck)]))
+    ref = oracle.spai1_columns(oa, cols, sets=sets)
+    jptr = sets[0]
+    worst = 0.0
+    for k, mk in zip(cols, ref):
+        got = m_csc[jptr[k]:jptr[k + 1]]
+        worst = max(worst, np.max(np.abs(got - mk)) / max(np.max(np.abs(mk)), 1e-300))
+    assert worst <= SPAI_TOL, worst
+    # CSR values are the CSC values permuted (from_coo, precond.py:199)
+    _, perm = oracle.transpose(oa)
+    assert np.array_equal(M.vals.cpu().numpy()[perm], m_csc)
+
+
+def test_qr_fallback_path_is_exercised():
+    A = _random_symmetric_pattern(120, 300, 12, dense_cols=(5, 77))
+    stats = pb.SpaiStats()
+    pb.spai1_device(A.device(), stats)
+    assert stats.n_fallback >= 2     # columns 5 and 77 have |J| = n > 32
+
+
+def test_ill_conditioned_column_goes_to_qr_and_matches():
+    d = 2.0 * np.eye(6)
+    d[:2, :2] = [[1.0, 1.0], [1.0, 1.0 + 1e-6]]   # cond ~ 4e6 local problem
+    A = pb.CsrMatrix.from_dense(d)
+    stats = pb.SpaiStats()
+    M = pb.spai1(A)
+    ref = oracle.spai1(_ocsr(A))
+    pb.spai1_device(A.device(), stats)
+    assert stats.n_fallback >= 1
+    assert column_rel_err(A, M.values, ref.values) <= 1e-6
+
+
+def test_spai1_breakdown_matches_reference(golden):
+    A = _gcsr(golden, "breakdown")
+    with pytest.raises(pb.FactorBreakdownError) as e:
+        pb.spai1(A)
+    assert str(e.value) == str(golden["breakdown/msg"])
+
+
+def test_spai1_empty_column_error():
+    A = pb.CsrMatrix(3, 3, [0, 1, 1, 2], [0, 2], [1.0, 1.0])
+    with pytest.raises(ValueError):
+        pb.spai1(A)
+
+
+def test_symmetrisation_matches_reference_golden(golden):
+    for name in golden_names(golden, "spai"):
+        pre = f"spai/{name}"
+        A = _gcsr(golden, pre)
+        if not A.device().structurally_symmetric():
+            continue
+        S = pb.drop_exact_zeros(pb.spai1_symmetric_device(A).to_host())
+        assert np.array_equal(S.row_offsets, golden[f"{pre}/S_ptr"]), name
+        assert np.array_equal(S.col_indices, golden[f"{pre}/S_col"]), name
+        ref = golden[f"{pre}/S_val"]
+        assert np.max(np.abs(S.values - ref)) <= SPAI_TOL * np.max(np.abs(ref)), name
+        # S is exactly symmetric
+        St = S.transpose()
+        assert np.array_equal(St.values, S.values)
+
+
+# ------------------------------------------------------------------ K5
+def test_spmv_matches_oracle():
+    rng = np.random.default_rng(3)
+    for A in (pb.assemble_q1((33, 21, 9)), pb.assemble_q1((100, 90)),
+              pb.assemble_poisson(pb.StructuredGrid(50, 40)),
+              _random_symmetric_pattern(999, 5000, 5, dense_cols=(3,))):
+        x = rng.standard_normal(A.ncols)
+        y = pb.spmv(A, x)
+        yr = oracle.spmv(_ocsr(A), x)
+        assert np.max(np.abs(y - yr)) <= 1e-13 * max(np.max(np.abs(yr)), 1.0)
+    with pytest.raises(pb.DimensionMismatchError):
+        pb.spmv(A, np.ones(A.ncols + 1))
+
+
+def test_fused_dots_deterministic():
+    n = 1_000_003
+    g = torch.Generator(device="cuda").manual_seed(1)
+    u = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    v = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    a = pb.fused_dots_device([(u, v), (u, u), (v, v)])
+    b = pb.fused_dots_device([(u, v), (u, u), (v, v)])
+    assert a == b
+    ref = [float(torch.dot(u, v)), float(torch.dot(u, u)), float(torch.dot(v, v))]
+    assert np.allclose(a, ref, rtol=1e-12)
+
+
+# ------------------------------------------------------------------ K8 solve
+def _hist_rel(a, b):
+    m = min(len(a), len(b))
+    return float(np.max(np.abs(np.asarray(a[:m]) - np.asarray(b[:m])) / np.asarray(b[:m])))
+
+
+def test_pcg_history_matches_reference_golden(golden):
+    cfg = pb.SolverConfig(variant="classic", tol=1e-8, maxit=5000)
+    for name in golden_names(golden, "solve"):
+        pre = f"solve/{name}"
+        A = _gcsr(golden, pre)
+        S = _gcsr(golden, pre, "S")          # the reference's own sym-SPAI
+        b = golden[f"{pre}/b"]
+        x, rec = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b, cfg)
+        ref_hist = golden[f"{pre}/hist"]
+        its = int(golden[f"{pre}/its"])
+        assert abs(rec.iterations - its) <= 1, name
+        assert rec.converged
+        assert _hist_rel(rec.residual_norms, ref_hist) <= HIST_TOL, name
+        assert abs(rec.initial_residual - float(golden[f"{pre}/norm0"])) <= 1e-12 * rec.initial_residual
+        assert rec.reductions_cum == [2 * (i + 1) for i in range(rec.iterations)]
+        assert rec.total_reductions == 2 * rec.iterations
+        xr = golden[f"{pre}/x"]
+        assert np.max(np.abs(x - xr)) <= 1e-6 * np.max(np.abs(xr))
+
+
+def test_full_pipeline_iteration_counts(golden):
+    """Our SPAI(1) + symmetrisation + PCG vs the reference CLI pipeline."""
+    cfg = pb.SolverConfig(variant="classic", tol=1e-8, maxit=5000)
+    factory = pb.make_spai1_factory()
+    for name in golden_names(golden, "solve"):
+        pre = f"solve/{name}"
+        A = _gcsr(golden, pre)
+        b = golden[f"{pre}/b"]
+        _, rec = pb.solve(pb.LocalSystem(A, factory(A)), b, cfg)
+        assert abs(rec.iterations - int(golden[f"{pre}/its"])) <= 1, name
+        assert _hist_rel(rec.residual_norms, golden[f"{pre}/hist"]) <= HIST_TOL, name
+
+
+def test_pcg_matches_oracle_without_preconditioner_and_jacobi():
+    A = pb.assemble_q1((40, 37))
+    b = pb.make_rhs(None, A)
+    cfg = pb.SolverConfig(tol=1e-10, maxit=2000)
+    for M, OM in ((None, None), (pb.jacobi(A), "jacobi")):
+        x, rec = pb.solve(pb.LocalSystem(A, M), b, cfg)
+        if OM == "jacobi":
+            d = A.diagonal()
+            n = A.nrows
+            OMm = oracle.Csr(n, n, np.arange(n + 1), np.arange(n), 1.0 / d)
+        else:
+            OMm = None
+        xr, rr = oracle.pcg_classic(_ocsr(A), OMm, b, tol=1e-10, maxit=2000)
+        assert abs(rec.iterations - rr.iterations) <= 1
+        assert _hist_rel(rec.residual_norms, rr.residual_norms) <= HIST_TOL
+
+
+def test_pcg_device_tensors_and_x0_and_maxit():
+    A = pb.q1_device((30, 30, 30))
+    S = pb.spai1_symmetric_device(A)
+    ones = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
+    b = A.matvec(ones)
+    x, rec = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                      pb.SolverConfig(tol=1e-10, maxit=500))
+    assert isinstance(x, torch.Tensor) and x.is_cuda
+    assert rec.converged
+    assert float((x - 1).abs().max()) < 1e-7
+    # x0 == exact solution -> ||r0|| tiny but nonzero / zero
+    _, rec2 = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                       pb.SolverConfig(tol=1e-10, maxit=3), x0=x)
+    assert rec2.iterations <= 3
+    _, rec3 = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                       pb.SolverConfig(tol=1e-12, maxit=5))
+    assert rec3.iterations == 5 and not rec3.converged
+    assert len(rec3.residual_norms) == 5
+
+
+def test_zero_rhs_converges_immediately():
+    A = pb.assemble_q1((8, 8))
+    x, rec = pb.solve(pb.LocalSystem(A, None), np.zeros(A.nrows), pb.SolverConfig())
+    assert rec.converged and rec.iterations == 1 and rec.final_residual == 0.0
+    assert rec.residual_norms == [] and rec.total_reductions == 1
+
+
+def test_breakdown_on_indefinite_matrix():
+    A = pb.CsrMatrix.from_dense(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    with pytest.raises(pb.BreakdownError):
+        pb.solve(pb.LocalSystem(A, None), np.array([1.0, -1.0]), pb.SolverConfig())
+
+
+def test_callback_sees_every_iteration():
+    A = pb.assemble_q1((12, 12))
+    b = pb.make_rhs(None, A)
+    seen = []
+    _, rec = pb.solve(pb.LocalSystem(A, None), b, pb.SolverConfig(tol=1e-6),
+                      callback=lambda it, st, r: seen.append((it, len(r.residual_norms))))
+    assert [s[0] for s in seen] == list(range(1, rec.iterations + 1))
+
+
+def test_large_3d_spai_cg_properties():
+    """Size-independent properties at a size the oracle cannot check per column."""
+    A = pb.q1_device((96, 96, 96))
+    stats = pb.SpaiStats()
+    S = pb.spai1_symmetric_device(A, stats)
+    assert stats.n_fallback == 0
+    assert torch.equal(S.rowptr, A.rowptr) and torch.equal(S.colidx, A.colidx)
+    ones = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
+    b = A.matvec(ones)
+    x, rec = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                      pb.SolverConfig(tol=1e-8, maxit=2000))
+    assert rec.converged
+    r = b - A.matvec(x)
+    assert float(torch.linalg.norm(r)) <= 1e-7 * float(torch.linalg.norm(b))
+    h = np.array(rec.residual_norms)
+    assert h[-1] <= 1e-8 * rec.initial_residual

@@ -1,0 +1,133 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself
+(tests/golden/make_golden.py runs the unmodified ftkrylov)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.spai import RankDeficient
+from conftest import golden_names
+
+
+def _csr(g, pre, tag="A"):
+    ptr = g[f"{pre}/{tag}_ptr"]
+    return oracle.Csr(len(ptr) - 1, len(ptr) - 1, ptr, g[f"{pre}/{tag}_col"],
+                      g[f"{pre}/{tag}_val"])
+
+
+def test_fd5_generator_bit_exact(golden):
+    shapes = {"fd5_10x10": (10, 10, 1.0, 1.0, 1.0),
+              "fd5_32x32": (32, 32, 1.0, 1.0, 1.0),
+              "fd5_16x16_aniso": (16, 16, 1.0, 1e-3, 1.0),
+              "fd5_7x5_h025": (7, 5, 1.0, 0.01, 0.25)}
+    for name, (nx, ny, ex, ey, h) in shapes.items():
+        A = oracle.fd5_poisson(nx, ny, ex, ey, h)
+        R = _csr(golden, f"spai/{name}")
+        assert np.array_equal(A.row_offsets, R.row_offsets)
+        assert np.array_equal(A.col_indices, R.col_indices)
+        assert np.array_equal(A.values, R.values)
+
+
+def test_pattern_sets_bit_exact(golden):
+    for name in golden_names(golden, "spai"):
+        pre = f"spai/{name}"
+        A = _csr(golden, pre)
+        jptr, jidx, iptr, iidx = oracle.pattern_sets(A)
+        assert np.array_equal(jptr, golden[f"{pre}/jptr"]), name
+        assert np.array_equal(jidx, golden[f"{pre}/jidx"]), name
+        assert np.array_equal(iptr, golden[f"{pre}/iptr"]), name
+        assert np.array_equal(iidx, golden[f"{pre}/iidx"]), name
+
+
+def test_spai1_matches_reference(golden):
+    for name in golden_names(golden, "spai"):
+        pre = f"spai/{name}"
+        A = _csr(golden, pre)
+        M = oracle.spai1(A)
+        R = _csr(golden, pre, "M")
+        # pattern(M) == pattern(A), bit-exact structure
+        assert np.array_equal(M.row_offsets, R.row_offsets), name
+        assert np.array_equal(M.col_indices, R.col_indices), name
+        # same LAPACK input -> identical output
+        assert np.max(np.abs(M.values - R.values)) <= 1e-15 * np.max(np.abs(R.values))
+
+
+def test_symmetrisation_matches_reference(golden):
+    for name in golden_names(golden, "spai"):
+        pre = f"spai/{name}"
+        R = _csr(golden, pre, "M")
+        S_ref = _csr(golden, pre, "S")
+        S = oracle.symmetrize_dense_reference(R)
+        assert np.array_equal(S.row_offsets, S_ref.row_offsets)
+        assert np.array_equal(S.col_indices, S_ref.col_indices)
+        assert np.array_equal(S.values, S_ref.values)
+        # same-pattern variant: identical values, zeros kept on the pattern
+        S2 = oracle.symmetrize_same_pattern(R)
+        nz = S2.values != 0.0
+        assert np.array_equal(S2.values[nz], S_ref.values)
+
+
+def test_q1_stencils_sum_to_zero():
+    for dim in (2, 3):
+        v, _ = oracle.q1_stencil(dim)
+        assert abs(v.sum()) < 1e-14
+    v, _ = oracle.q1_stencil(3)
+    # exact-zero face couplings in 3D Q1
+    for t in (4, 10, 12, 14, 16, 22):
+        assert v[t] == 0.0
+    assert v[13] == pytest.approx(8.0 / 3.0)
+
+
+def test_pcg_matches_reference(golden):
+    for name in golden_names(golden, "solve"):
+        pre = f"solve/{name}"
+        A = _csr(golden, pre)
+        S = _csr(golden, pre, "S")
+        b = golden[f"{pre}/b"]
+        assert np.array_equal(oracle.spmv(A, np.ones(A.nrows)), b)
+        x, rec = oracle.pcg_classic(A, S, b, tol=1e-8, maxit=5000)
+        hist = golden[f"{pre}/hist"]
+        assert rec.iterations == int(golden[f"{pre}/its"])
+        assert np.array_equal(np.array(rec.residual_norms), hist)
+        assert np.array_equal(x, golden[f"{pre}/x"])
+        assert rec.initial_residual == float(golden[f"{pre}/norm0"])
+        assert np.array_equal(np.array(rec.reductions_cum), golden[f"{pre}/red"])
+
+
+def test_oracle_sym_spai_equals_reference_solve_input(golden):
+    for name in golden_names(golden, "solve"):
+        pre = f"solve/{name}"
+        A = _csr(golden, pre)
+        S = oracle.symmetrize_dense_reference(oracle.spai1(A))
+        S_ref = _csr(golden, pre, "S")
+        assert np.array_equal(S.col_indices, S_ref.col_indices)
+        assert np.max(np.abs(S.values - S_ref.values)) <= 1e-15
+
+
+def test_breakdown_message(golden):
+    A = _csr(golden, "breakdown")
+    with pytest.raises(RankDeficient) as e:
+        oracle.spai1(A)
+    assert str(e.value) == str(golden["breakdown/msg"])
+
+
+def test_tree_sum_order():
+    vals = [np.array([1e16]), np.array([1.0]), np.array([-1e16]), np.array([1.0])]
+    # ((a+b) + (c+d)) as commsim.py:336-347
+    assert oracle.tree_sum(vals)[0] == (1e16 + 1.0) + (-1e16 + 1.0)
+
+
+def test_bicgstab_and_richardson_converge():
+    A = oracle.stencil_csr((12, 12), *oracle.q1_stencil(2, conv=(3.0, 1.0)))
+    b = oracle.make_rhs_ones(A)
+    M = oracle.spai1(A)
+    x, rec = oracle.bicgstab_right(A, M, b, tol=1e-10, maxit=500)
+    assert rec.converged
+    assert np.allclose(x, 1.0, atol=1e-7)
+    x0, rec0 = oracle.bicgstab_right(A, None, b, tol=1e-10, maxit=500)
+    assert rec.iterations < rec0.iterations
+    A = oracle.stencil_csr((16, 16), *oracle.q1_stencil(2))
+    b = oracle.make_rhs_ones(A)
+    _, rr = oracle.richardson(A, oracle.spai1(A), b, omega=1.0, maxit=50)
+    h = np.array(rr.residual_norms)
+    assert np.all(h[1:] < h[:-1])
