@@ -243,7 +243,7 @@ def run_ours(args):
     t_asm = statistics.mean(t for t, _, _ in times)
     t_sol = statistics.mean(t for _, t, _ in times)
     hbm, peak_kind = peaks()
-    b_it = 24 * nnz + 16 * (n + 1) + 88 * n
+    b_it = 24 * nnz + 88 * n
     solve_gbs = b_it * its / t_sol / 1e9
 
     # ---- SpMV alone (K5 plain and TMA-staged) with CUDA events
@@ -252,7 +252,8 @@ def run_ours(args):
         xx = torch.rand(n, dtype=torch.float64, device=dev)
         yy = torch.empty_like(xx)
         sp_bytes = 12 * nnz + 8 * (n + 1) + 16 * n
-        for name, fn in (("csr", lambda: A.matvec(xx, out=yy)),
+        for name, fn in (("sell", lambda: A.matvec_sell(xx, out=yy)),
+                         ("csr", lambda: A.matvec(xx, out=yy)),
                          ("csr_tma", lambda: A.matvec_tma(xx, out=yy))):
             for _ in range(3):
                 fn()

@@ -64,6 +64,13 @@ int spai_csr_transpose(int64_t nrows, int64_t ncols, int64_t nnz,
                        const int64_t* rowptr, const int32_t* colidx,
                        int64_t* cscptr, int32_t* cscrow, int64_t* csc2csr,
                        void* ws, size_t ws_bytes, void* stream);
+/* Fast path for structurally symmetric patterns (all FEM matrices here):
+ * synchronous; *is_sym = 1 iff every stored (i,c) has a stored (c,i).  Then
+ * the CSC structure IS the CSR structure (cscptr = rowptr, cscrow = colidx)
+ * and only csc2csr[nnz] is produced (gather form, no atomics, no sort).   */
+int spai_csr_transpose_symmetric(int64_t n, int64_t nnz, const int64_t* rowptr,
+                                 const int32_t* colidx, int64_t* csc2csr,
+                                 int* is_sym, void* stream);
 /* Synchronous: *is_sym = 1 iff the CSC structure equals the CSR structure. */
 int spai_structure_is_symmetric(int64_t n, int64_t nnz, const int64_t* rowptr,
                                 const int32_t* colidx, const int64_t* cscptr,
@@ -138,19 +145,37 @@ int spai_fused_dots(int64_t n, int npairs, const double* const* us,
 int spai_axpby(int64_t n, double a, const double* x, double b, double* y,
                void* stream);
 
+/* ------------------------------------------------------------------ K5b
+ * SELL-32 (sliced ELL, slice height 32, rows not reordered): the solve-phase
+ * format.  Element (row 32 s + lane, slot k) sits at sliceptr[s] + 32 k + lane;
+ * padding slots hold column = row, value 0.  sliceptr has nslices+1 int64
+ * entries (nslices = spai_sell_nslices(n)); the padded size is sliceptr[nslices].
+ * Matrices on the same pattern (A, SPAI(1) M) share sliceptr and cols.     */
+int64_t spai_sell_nslices(int64_t n);
+int spai_sell_layout(int64_t n, const int64_t* rowptr, int64_t* sliceptr, void* stream);
+int spai_sell_fill_cols(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                        const int64_t* sliceptr, int32_t* cols, void* stream);
+int spai_sell_fill_vals(int64_t n, const int64_t* rowptr, const double* csr_vals,
+                        const int64_t* sliceptr, double* vals, void* stream);
+int spai_sell_spmv(int64_t n, const int64_t* sliceptr, const int32_t* cols,
+                   const double* vals, const double* x, double* y, void* stream);
+
 /* ------------------------------------------------------------------ K8
- * Device-resident classic PCG (replaces _solve_classic, krylov.py:301-345).
- * A and M share rowptr/colidx when M is on pattern(A) (spai1 guarantees it);
- * pass M_vals = NULL for no preconditioner (apply_M = copy).               */
+ * Device-resident classic PCG (replaces _solve_classic, krylov.py:301-345)
+ * on SELL-32 operators.  M_vals = NULL means no preconditioner (apply_M =
+ * copy, krylov.py:174-177); m_sliceptr/m_cols = NULL means M shares A's
+ * layout (SPAI(1) M lives on pattern(A)).  The caller owns the workspace
+ * (spai_pcg_workspace_bytes) and must keep it alive until destroy.       */
 typedef struct spai_pcg spai_pcg;     /* opaque solver state               */
-int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* rowptr,
-                    const int32_t* colidx, const double* A_vals,
-                    const int64_t* m_rowptr, const int32_t* m_colidx,
-                    const double* M_vals, double tol, int64_t maxit,
-                    void* stream);
+size_t spai_pcg_workspace_bytes(int64_t n, int64_t maxit);
+int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
+                    const int32_t* cols, const double* A_vals,
+                    const int64_t* m_sliceptr, const int32_t* m_cols,
+                    const double* M_vals, double tol, int64_t maxit, void* ws,
+                    size_t ws_bytes, void* stream);
 /* Start from x0 (device, may be NULL -> zero); b device, copied.          */
 int spai_pcg_start(spai_pcg* s, const double* b, const double* x0);
-/* Run up to `iters` more iterations on the device (no host sync inside). */
+/* Enqueue up to `iters` more iterations (no host sync; CUDA graphs of 16). */
 int spai_pcg_advance(spai_pcg* s, int64_t iters);
 /* Synchronous: status 0 running, 1 converged, 2 maxit, 3 breakdown,
  * 4 divergence; iterations done; norm0; last norm; breakdown value.       */

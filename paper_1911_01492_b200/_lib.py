@@ -42,6 +42,7 @@ _SIGS = {
     "spai_stencil_csr": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_transpose_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "spai_csr_transpose": (_i32, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "spai_csr_transpose_symmetric": (_i32, [_i64, _i64, _vp, _vp, _vp, C.POINTER(_i32), _vp]),
     "spai_structure_is_symmetric": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, C.POINTER(_i32)]),
     "spai_pattern_count": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _vp]),
     "spai_pattern_fill": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
@@ -57,8 +58,14 @@ _SIGS = {
     "spai_dots_workspace_bytes": (_sz, [_i64]),
     "spai_fused_dots": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "spai_axpby": (_i32, [_i64, _dbl, _vp, _dbl, _vp, _vp]),
+    "spai_sell_nslices": (_i64, [_i64]),
+    "spai_sell_layout": (_i32, [_i64, _vp, _vp, _vp]),
+    "spai_sell_fill_cols": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "spai_sell_fill_vals": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "spai_sell_spmv": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_pcg_workspace_bytes": (_sz, [_i64, _i64]),
     "spai_pcg_create": (_i32, [C.POINTER(_vp), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl,
-                               _i64, _vp]),
+                               _i64, _vp, _sz, _vp]),
     "spai_pcg_start": (_i32, [_vp, _vp, _vp]),
     "spai_pcg_advance": (_i32, [_vp, _i64]),
     "spai_pcg_poll": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),

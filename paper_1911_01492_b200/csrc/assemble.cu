@@ -1,14 +1,22 @@
 // K3: SPAI(1) assembly (replaces precond.py:185-198) and K4 symmetrisation.
 //
-// Fast path (one warp per column, fp64 CUDA cores, no tensor cores):
-//   G = A[I,J]^T A[I,J] = (A^T A)[J,J]: entry (a,b) is the sparse dot of the
-//   CSC columns J_a and J_b (rows outside I are zero, so I is implicit);
-//   rhs = A[I,J]^T e_k|I = A[k,J]^T.  Cholesky G = L L^T (L_jj = |R_jj| of the
-//   reference QR in exact arithmetic), forward/backward solve.
-// Columns whose Cholesky pivots lose more than 4 digits (d_j < 1e-4*G_jj), or
-// whose L_jj come within 100x of the reference rank threshold, are re-solved by
-// a CTA-per-column Householder QR on the explicit dense A[I,J] with the exact
-// reference rank test  min|R_ii| <= 1e-13*max(max|R_ii|,1)  (precond.py:192).
+// Normal equations, one warp per column, fp64 CUDA cores (no tensor cores):
+//   G = A[I,J]^T A[I,J] = (A^T A)[J,J]   and   rhs = A[I,J]^T e_k|I = A[k,J]^T,
+// then Cholesky G = L L^T (L_jj = |R_jj| of the reference QR in exact
+// arithmetic) and two triangular solves.
+//
+// Fast path (gram_hash_kernel): the CSC lists of the columns in J_k are
+// gathered once; their rows are de-duplicated in a shared-memory hash table,
+// the <= 32*MW distinct rows (= I_k, the reference's `touched`) are sorted and
+// every list becomes a bit mask over local row ids with its values in mask
+// order.  G[a,b] is then a popcount-indexed dot over (mask_a & mask_b): work
+// proportional to the true overlaps (~9 per pair for 3D Q1), no merges.
+// Columns whose pattern is too large for it fall back to gram_merge_kernel
+// (sorted-list merges, up to 32 x 1024 entries); columns whose Cholesky
+// pivots lose more than 4 digits (d_j < 1e-4 G_jj) or come within 100x of
+// the reference rank threshold are re-solved by spai_qr_kernel: CTA per
+// column, dense A[I,J] in shared memory, Householder QR with the exact
+// reference rank test  min|R_ii| <= 1e-13 max(max|R_ii|, 1)  (precond.py:192).
 #include "pattern.cuh"
 
 namespace spai {
@@ -22,36 +30,110 @@ enum { kErrRank = 1, kErrEmpty = 2, kErrTooBig = 3, kErrShape = 4 };
 
 struct AsmWs {
   unsigned long long* err;   // min key
-  int* nflag;                // fallback count
-  int32_t* flagged;          // fallback columns
+  int* nmerge;               // structural fallback count
+  int* nqr;                  // numerical fallback count
+  int32_t* merge_list;
+  int32_t* qr_list;
 };
 
 __device__ __forceinline__ void report(AsmWs ws, int64_t k, int kind) {
   atomicMin(ws.err, ((unsigned long long)k << 4) | (unsigned long long)kind);
 }
+__device__ __forceinline__ void to_merge(AsmWs ws, int64_t k) { ws.merge_list[atomicAdd(ws.nmerge, 1)] = (int32_t)k; }
+__device__ __forceinline__ void to_qr(AsmWs ws, int64_t k) { ws.qr_list[atomicAdd(ws.nqr, 1)] = (int32_t)k; }
 
-template <int NJ, int CAPL>
-struct WarpSmem {
-  static constexpr int kG = NJ * (NJ + 1) / 2;
-  static constexpr size_t bytes() {
-    return (size_t)kG * 8 + (size_t)CAPL * 8 + (size_t)CAPL * 4 + (NJ + 1) * 4 + NJ * 4 + 16;
+__host__ __device__ constexpr int tri(int a) { return a * (a + 1) / 2; }
+
+// packed lower-triangular index p -> (a, b), b <= a
+__device__ __forceinline__ void tri_decode(int p, int& a, int& b) {
+  a = (int)((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
+  while (tri(a) > p) --a;
+  while (tri(a + 1) <= p) ++a;
+  b = p - tri(a);
+}
+
+// Cholesky of the packed G (nj <= 32, lane i owns row i of the trailing
+// block) and solve G m = rhs (lane a holds rhs_a, returns m_a).  Returns
+// false if the column must take the QR path.
+__device__ __forceinline__ bool chol_solve_warp(double* G, int nj, int lane, double& y) {
+  const double gdiag = lane < nj ? G[tri(lane) + lane] : 1.0;
+  double lmin = 1e300, lmax = 0.0;
+  for (int j = 0; j < nj; ++j) {
+    const double d = G[tri(j) + j];
+    const double gd = __shfl_sync(0xffffffffu, gdiag, j);
+    if (!(d > kFlagPivot * gd)) return false;
+    const double ljj = sqrt(d);
+    lmin = fmin(lmin, ljj);
+    lmax = fmax(lmax, ljj);
+    const double inv = 1.0 / ljj;
+    double lij = 0.0;
+    if (lane > j && lane < nj) {
+      lij = G[tri(lane) + j] * inv;
+      G[tri(lane) + j] = lij;
+    }
+    __syncwarp();
+    if (lane > j && lane < nj) {
+      const int ri = tri(lane);
+      for (int l = j + 1; l <= lane; ++l) G[ri + l] = fma(-lij, G[tri(l) + j], G[ri + l]);
+    }
+    if (lane == 0) G[tri(j) + j] = ljj;
+    __syncwarp();
   }
+  if (lmin <= kRankGuard * fmax(lmax, 1.0)) return false;
+  for (int j = 0; j < nj; ++j) {           // L y = rhs
+    double yj = __shfl_sync(0xffffffffu, y, j);
+    yj = yj / G[tri(j) + j];
+    if (lane == j) y = yj;
+    if (lane > j && lane < nj) y = fma(-G[tri(lane) + j], yj, y);
+  }
+  for (int j = nj - 1; j >= 0; --j) {      // L^T m = y
+    double mj = __shfl_sync(0xffffffffu, y, j);
+    mj = mj / G[tri(j) + j];
+    if (lane == j) y = mj;
+    if (lane < j) y = fma(-G[tri(j) + lane], mj, y);
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- fast path
+template <int NJ, int CAPL, int MW>
+struct HashSmem {
+  static constexpr int kHS = 64 * MW;                 // hash slots (load <= 0.5)
+  static constexpr int kM = 32 * MW;                  // max |I_k|
+  static constexpr int kG = NJ * (NJ + 1) / 2;
+  // union region: {lrow int32[CAPL], keys int32[kHS]} during the gather, G later
+  static constexpr size_t kUnionA = (size_t)(CAPL + kHS) * 4;
+  static constexpr size_t kUnion = kUnionA > (size_t)kG * 8 ? kUnionA : (size_t)kG * 8;
+  static constexpr size_t off_lval = 0;
+  static constexpr size_t off_union = off_lval + (size_t)CAPL * 8;
+  static constexpr size_t off_I = off_union + ((kUnion + 15) & ~(size_t)15);
+  static constexpr size_t off_mask = off_I + (size_t)kM * 4;
+  static constexpr size_t off_pre = off_mask + (size_t)NJ * MW * 4;
+  static constexpr size_t off_loff = off_pre + (size_t)NJ * MW * 2;
+  static constexpr size_t off_lsrc = ((off_loff + (NJ + 1) * 4) + 7) & ~(size_t)7;
+  static constexpr size_t off_lidx = off_lsrc + (size_t)NJ * 8;
+  static constexpr size_t bytes = (off_lidx + CAPL + 15) & ~(size_t)15;
 };
 
-template <int NJ, int CAPL, int WARPS>
+template <int NJ, int CAPL, int MW, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
-spai_warp_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
+gram_hash_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
                  const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
                  double* __restrict__ m_csc, AsmWs ws) {
-  using S = WarpSmem<NJ, CAPL>;
+  using S = HashSmem<NJ, CAPL, MW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* base = smem_raw + (size_t)w * S::bytes();
-  double* G = reinterpret_cast<double*>(base);
-  double* lval = G + S::kG;
-  int32_t* lrow = reinterpret_cast<int32_t*>(lval + CAPL);
-  int32_t* loff = lrow + CAPL;
-  int32_t* jrow = loff + NJ + 1;
+  unsigned char* base = smem_raw + (size_t)w * S::bytes;
+  double* lval = reinterpret_cast<double*>(base + S::off_lval);
+  int32_t* lrow = reinterpret_cast<int32_t*>(base + S::off_union);
+  int32_t* keys = lrow + CAPL;
+  double* G = reinterpret_cast<double*>(base + S::off_union);
+  int32_t* I = reinterpret_cast<int32_t*>(base + S::off_I);
+  uint32_t* mask = reinterpret_cast<uint32_t*>(base + S::off_mask);
+  uint16_t* pre = reinterpret_cast<uint16_t*>(base + S::off_pre);
+  int32_t* loff = reinterpret_cast<int32_t*>(base + S::off_loff);
+  int64_t* lsrc = reinterpret_cast<int64_t*>(base + S::off_lsrc);
+  uint8_t* lidx = base + S::off_lidx;
 
   const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
@@ -60,35 +142,184 @@ spai_warp_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __re
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
     if (nj == 0) { if (lane == 0) report(ws, k, kErrEmpty); continue; }
-    if (nj > NJ || nj > 32) {
-      if (lane == 0) ws.flagged[atomicAdd(ws.nflag, 1)] = (int32_t)k;
-      continue;
-    }
-    // ---- J and the CSC lists of its columns
-    int c = 0, len = 0;
+    if (nj > NJ) { if (lane == 0) to_merge(ws, k); continue; }
+    // ---- list offsets
+    int len = 0;
     int64_t clo = 0;
     if (lane < nj) {
-      c = cscrow[jlo + lane];
+      const int c = cscrow[jlo + lane];
       clo = cscptr[c];
       len = (int)(cscptr[c + 1] - clo);
     }
     int incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total > CAPL) {
-      if (lane == 0) ws.flagged[atomicAdd(ws.nflag, 1)] = (int32_t)k;
+    if (total > CAPL) { if (lane == 0) to_merge(ws, k); continue; }
+    if (lane < nj) { loff[lane] = incl - len; lsrc[lane] = clo; }
+    if (lane == 0) loff[nj] = total;
+    for (int i = lane; i < S::kHS; i += 32) keys[i] = -1;
+    __syncwarp();
+    // ---- gather the lists (independent loads, full MLP)
+    for (int e = lane; e < total; e += 32) {
+      int lo = 0, hi = nj;                     // list id: loff[a] <= e < loff[a+1]
+      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (loff[mid] <= e) lo = mid; else hi = mid; }
+      const int64_t q = lsrc[lo] + (e - loff[lo]);
+      lrow[e] = cscrow[q];
+      lval[e] = vals[csc2csr[q]];
+    }
+    __syncwarp();
+    // ---- de-duplicate rows (hash set, linear probing)
+    constexpr int kShift = 32 - (MW == 8 ? 9 : 8);
+    for (int e = lane; e < total; e += 32) {
+      const int32_t r = lrow[e];
+      uint32_t h = ((uint32_t)r * 2654435761u) >> kShift;
+      while (true) {
+        const int32_t prev = atomicCAS(&keys[h], -1, r);
+        if (prev == -1 || prev == r) break;
+        h = (h + 1) & (S::kHS - 1);
+      }
+    }
+    __syncwarp();
+    int m = 0;
+    for (int bs = 0; bs < S::kHS; bs += 32) {
+      const int32_t key = keys[bs + lane];
+      const unsigned occ = __ballot_sync(0xffffffffu, key != -1);
+      const int pos = m + __popc(occ & ((1u << lane) - 1));
+      if (key != -1 && pos < S::kM) I[pos] = key;
+      m += __popc(occ);
+    }
+    if (m > S::kM) { if (lane == 0) to_merge(ws, k); continue; }
+    // ---- sort I_k (bitonic, padded to a power of two >= 32)
+    int size = 32;
+    while (size < m) size <<= 1;
+    for (int i = m + lane; i < size; i += 32) I[i] = INT32_MAX;
+    __syncwarp();
+    for (int kk = 2; kk <= size; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < size; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int32_t a = I[i], b = I[ixj];
+            if ((a > b) == ((i & kk) == 0)) { I[i] = b; I[ixj] = a; }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    // ---- local row ids (monotone in the row, so every list stays in mask order)
+    for (int e = lane; e < total; e += 32) {
+      const int32_t r = lrow[e];
+      int lo = 0, hi = m;
+      while (lo < hi) { const int mid = (lo + hi) >> 1; if (I[mid] < r) lo = mid + 1; else hi = mid; }
+      lidx[e] = (uint8_t)lo;
+    }
+    int rk = -1;                               // local id of row k (rhs = A[k, J])
+    {
+      int lo = 0, hi = m;
+      while (lo < hi) { const int mid = (lo + hi) >> 1; if (I[mid] < (int32_t)k) lo = mid + 1; else hi = mid; }
+      if (lo < m && I[lo] == (int32_t)k) rk = lo;
+    }
+    __syncwarp();
+    // ---- masks, prefix popcounts, rhs (lane a owns list a)
+    double rhs = 0.0;
+    if (lane < nj) {
+      uint32_t mk[MW];
+#pragma unroll
+      for (int wd = 0; wd < MW; ++wd) mk[wd] = 0u;
+      const int lo = loff[lane], hi = loff[lane + 1];
+      for (int t = lo; t < hi; ++t) {
+        const int li = lidx[t];
+#pragma unroll
+        for (int wd = 0; wd < MW; ++wd)
+          if ((li >> 5) == wd) mk[wd] |= 1u << (li & 31);
+      }
+      int acc = 0;
+#pragma unroll
+      for (int wd = 0; wd < MW; ++wd) {
+        mask[lane * MW + wd] = mk[wd];
+        pre[lane * MW + wd] = (uint16_t)acc;
+        if (rk >= 0 && (rk >> 5) == wd && ((mk[wd] >> (rk & 31)) & 1u))
+          rhs = lval[lo + acc + __popc(mk[wd] & ((1u << (rk & 31)) - 1u))];
+        acc += __popc(mk[wd]);
+      }
+    }
+    __syncwarp();                              // lrow/keys dead -> G may overwrite
+    // ---- G[a,b] = sum over common local rows, packed lower triangle
+    const int np = tri(nj);
+    for (int p = lane; p < np; p += 32) {
+      int a, b;
+      tri_decode(p, a, b);
+      const double* va = lval + loff[a];
+      const double* vb = lval + loff[b];
+      double s = 0.0;
+#pragma unroll
+      for (int wd = 0; wd < MW; ++wd) {
+        const uint32_t ma = mask[a * MW + wd], mb = mask[b * MW + wd];
+        uint32_t both = ma & mb;
+        const int pa = pre[a * MW + wd], pb = pre[b * MW + wd];
+        while (both) {
+          const int bit = __ffs(both) - 1;
+          both &= both - 1u;
+          const uint32_t below = (1u << bit) - 1u;
+          s = fma(va[pa + __popc(ma & below)], vb[pb + __popc(mb & below)], s);
+        }
+      }
+      G[p] = s;
+    }
+    __syncwarp();
+    double y = rhs;
+    if (!chol_solve_warp(G, nj, lane, y)) {
+      if (lane == 0) to_qr(ws, k);
       continue;
     }
+    if (lane < nj) m_csc[jlo + lane] = y;
+  }
+}
+
+// ---------------------------------------------------------------- generic merge path
+constexpr int kMergeNJ = 32, kMergeCap = 1024, kMergeWarps = 4;
+constexpr size_t kMergeWarpBytes =
+    ((size_t)tri(kMergeNJ) * 8 + (size_t)kMergeCap * 12 + (kMergeNJ + 1) * 4 + kMergeNJ * 4 + 16 + 15) &
+    ~(size_t)15;
+
+__global__ void __launch_bounds__(kMergeWarps * 32)
+gram_merge_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
+                  const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
+                  double* __restrict__ m_csc, AsmWs ws) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = smem_raw + (size_t)w * kMergeWarpBytes;
+  double* G = reinterpret_cast<double*>(base);
+  double* lval = G + tri(kMergeNJ);
+  int32_t* lrow = reinterpret_cast<int32_t*>(lval + kMergeCap);
+  int32_t* loff = lrow + kMergeCap;
+  int32_t* jrow = loff + kMergeNJ + 1;
+  const int nlist = *ws.nmerge;
+  for (int f = blockIdx.x * kMergeWarps + w; f < nlist; f += gridDim.x * kMergeWarps) {
+    __syncwarp();
+    const int64_t k = ws.merge_list[f];
+    const int64_t jlo = cscptr[k];
+    const int nj = (int)(cscptr[k + 1] - jlo);
+    if (nj > kMergeNJ) { if (lane == 0) to_qr(ws, k); continue; }
+    int c = 0, len = 0;
+    if (lane < nj) { c = cscrow[jlo + lane]; len = (int)(cscptr[c + 1] - cscptr[c]); }
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total > kMergeCap) { if (lane == 0) to_qr(ws, k); continue; }
     if (lane < nj) { jrow[lane] = c; loff[lane] = incl - len; }
     if (lane == 0) loff[nj] = total;
     __syncwarp();
     for (int a = 0; a < nj; ++a) {
-      const int off = loff[a];
-      const int la = loff[a + 1] - off;
+      const int off = loff[a], la = loff[a + 1] - off;
       const int64_t src = cscptr[jrow[a]];
       for (int t = lane; t < la; t += 32) {
         lrow[off + t] = cscrow[src + t];
@@ -96,91 +327,29 @@ spai_warp_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __re
       }
     }
     __syncwarp();
-    // ---- rhs_a = A[k, J_a]  (lane a)
     double rhs = 0.0;
     if (lane < nj) {
       int lo = loff[lane], hi = loff[lane + 1];
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (lrow[mid] < (int32_t)k) lo = mid + 1; else hi = mid;
-      }
+      while (lo < hi) { const int mid = (lo + hi) >> 1; if (lrow[mid] < (int32_t)k) lo = mid + 1; else hi = mid; }
       if (lo < loff[lane + 1] && lrow[lo] == (int32_t)k) rhs = lval[lo];
     }
-    // ---- G = (A^T A)[J,J], packed lower triangle, p = a(a+1)/2 + b, b <= a
-    const int np = nj * (nj + 1) / 2;
-    for (int p = lane; p < np; p += 32) {
-      int a = (int)((sqrtf(8.0f * p + 1.0f) - 1.0f) * 0.5f);
-      while (a * (a + 1) / 2 > p) --a;
-      while ((a + 1) * (a + 2) / 2 <= p) ++a;
-      const int b = p - a * (a + 1) / 2;
+    for (int p = lane; p < tri(nj); p += 32) {
+      int a, b;
+      tri_decode(p, a, b);
       int ia = loff[a], ea = loff[a + 1], ib = loff[b], eb = loff[b + 1];
       double s = 0.0;
-      if (ia < ea && ib < eb) {
-        int32_t ra = lrow[ia], rb = lrow[ib];
-        while (true) {
-          if (ra == rb) {
-            s = fma(lval[ia], lval[ib], s);
-            if (++ia == ea || ++ib == eb) break;
-            ra = lrow[ia]; rb = lrow[ib];
-          } else if (ra < rb) {
-            if (++ia == ea) break;
-            ra = lrow[ia];
-          } else {
-            if (++ib == eb) break;
-            rb = lrow[ib];
-          }
-        }
+      while (ia < ea && ib < eb) {
+        const int32_t ra = lrow[ia], rb = lrow[ib];
+        if (ra == rb) { s = fma(lval[ia], lval[ib], s); ++ia; ++ib; }
+        else if (ra < rb) ++ia;
+        else ++ib;
       }
       G[p] = s;
     }
     __syncwarp();
-    // ---- Cholesky (right-looking, lane i owns row i of the trailing block)
-    const double gdiag = lane < nj ? G[lane * (lane + 1) / 2 + lane] : 1.0;
-    bool flag = false;
-    double lmin = 1e300, lmax = 0.0;
-    for (int j = 0; j < nj; ++j) {
-      const double d = G[j * (j + 1) / 2 + j];
-      const double gd = __shfl_sync(0xffffffffu, gdiag, j);
-      if (!(d > kFlagPivot * gd)) { flag = true; break; }
-      const double ljj = sqrt(d);
-      lmin = fmin(lmin, ljj);
-      lmax = fmax(lmax, ljj);
-      const double inv = 1.0 / ljj;
-      double lij = 0.0;
-      if (lane > j && lane < nj) {
-        lij = G[lane * (lane + 1) / 2 + j] * inv;
-        G[lane * (lane + 1) / 2 + j] = lij;
-      }
-      __syncwarp();
-      if (lane > j && lane < nj) {
-        const int ri = lane * (lane + 1) / 2;
-        for (int l = j + 1; l <= lane; ++l)
-          G[ri + l] = fma(-lij, G[l * (l + 1) / 2 + j], G[ri + l]);
-      }
-      if (lane == 0) G[j * (j + 1) / 2 + j] = ljj;
-      __syncwarp();
-    }
-    if (flag || lmin <= kRankGuard * fmax(lmax, 1.0)) {
-      if (lane == 0) ws.flagged[atomicAdd(ws.nflag, 1)] = (int32_t)k;
-      __syncwarp();
-      continue;
-    }
-    // ---- L y = rhs (lane i holds rhs_i), then L^T m = y
     double y = rhs;
-    for (int j = 0; j < nj; ++j) {
-      double yj = __shfl_sync(0xffffffffu, y, j);
-      yj = yj / G[j * (j + 1) / 2 + j];
-      if (lane == j) y = yj;
-      if (lane > j && lane < nj) y = fma(-G[lane * (lane + 1) / 2 + j], yj, y);
-    }
-    for (int j = nj - 1; j >= 0; --j) {
-      double mj = __shfl_sync(0xffffffffu, y, j);
-      mj = mj / G[j * (j + 1) / 2 + j];
-      if (lane == j) y = mj;
-      if (lane < j) y = fma(-G[j * (j + 1) / 2 + lane], mj, y);
-    }
+    if (!chol_solve_warp(G, nj, lane, y)) { if (lane == 0) to_qr(ws, k); continue; }
     if (lane < nj) m_csc[jlo + lane] = y;
-    __syncwarp();
   }
 }
 
@@ -212,13 +381,13 @@ spai_qr_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscp
   double* red = reinterpret_cast<double*>(smem_raw + kQrIcap * 4);
   double* sub = red + 64;
   __shared__ int s_m;
-  const int nflag = *ws.nflag;
+  const int nflag = *ws.nqr;
   for (int f = blockIdx.x; f < nflag; f += gridDim.x) {
-    const int64_t k = ws.flagged[f];
+    const int64_t k = ws.qr_list[f];
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
     if (threadIdx.x < 32) {
-      int m = warp_build_I(k, cscptr, cscrow, I, kQrIcap);
+      const int m = warp_build_I(k, cscptr, cscrow, I, kQrIcap);
       if (threadIdx.x == 0) s_m = m;
     }
     __syncthreads();
@@ -239,13 +408,12 @@ spai_qr_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscp
       for (int64_t q = lo + threadIdx.x; q < hi; q += kQrThreads) {
         const int32_t r = cscrow[q];
         int l = 0, h = m;
-        while (l < h) { int mid = (l + h) >> 1; if (I[mid] < r) l = mid + 1; else h = mid; }
+        while (l < h) { const int mid = (l + h) >> 1; if (I[mid] < r) l = mid + 1; else h = mid; }
         sub[(size_t)a * m + l] = vals[csc2csr[q]];
       }
     }
     for (int i = threadIdx.x; i < m; i += kQrThreads) e[i] = (I[i] == (int32_t)k) ? 1.0 : 0.0;
     __syncthreads();
-    // Householder QR, column major sub[a*m + i]; R overwrites the upper part
     double rmin = 1e300, rmax = 0.0;
     for (int j = 0; j < nj; ++j) {
       double* x = sub + (size_t)j * m;
@@ -268,7 +436,6 @@ spai_qr_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscp
       if (threadIdx.x == 0) x[j] = beta;
       rmin = fmin(rmin, fabs(beta));
       rmax = fmax(rmax, fabs(beta));
-      // apply H = I - tau v v^T (v_j = 1) to columns j+1..nj-1 and to e
       for (int a = j + 1; a <= nj; ++a) {
         double* y = (a < nj) ? sub + (size_t)a * m : e;
         double part = 0.0;
@@ -307,12 +474,12 @@ __global__ void maxlen_kernel(int64_t n, const int64_t* cscptr, int* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
-template <int NJ, int CAPL, int WARPS>
-static int launch_warp(int64_t n, const double* vals, const int64_t* cscptr,
+template <int NJ, int CAPL, int MW, int WARPS>
+static int launch_hash(int64_t n, const double* vals, const int64_t* cscptr,
                        const int32_t* cscrow, const int64_t* csc2csr, double* m_csc,
                        AsmWs ws, cudaStream_t s) {
-  const size_t smem = WarpSmem<NJ, CAPL>::bytes() * WARPS;
-  auto kern = spai_warp_kernel<NJ, CAPL, WARPS>;
+  const size_t smem = HashSmem<NJ, CAPL, MW>::bytes * WARPS;
+  auto kern = gram_hash_kernel<NJ, CAPL, MW, WARPS>;
   SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SPAI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
@@ -321,7 +488,7 @@ static int launch_warp(int64_t n, const double* vals, const int64_t* cscptr,
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   kern<<<(unsigned)blocks, WARPS * 32, smem, s>>>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws);
-  SPAI_LAUNCH_CHECK("spai_warp_kernel");
+  SPAI_LAUNCH_CHECK("gram_hash_kernel");
   return SPAI_OK;
 }
 
@@ -349,7 +516,7 @@ __global__ void symmetrize_kernel(int64_t nnz, const int64_t* __restrict__ csc2c
 using namespace spai;
 
 extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
-  return 256 + (size_t)n * sizeof(int32_t);
+  return 256 + 2 * (size_t)n * sizeof(int32_t);
 }
 
 extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
@@ -367,37 +534,47 @@ extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
   AsmWs ws;
   unsigned char* b = (unsigned char*)wsp;
   ws.err = (unsigned long long*)b;
-  ws.nflag = (int*)(b + 8);
-  int* maxlen = (int*)(b + 12);
-  ws.flagged = (int32_t*)(b + 256);
-  unsigned long long init_err = ~0ull;
+  ws.nmerge = (int*)(b + 8);
+  ws.nqr = (int*)(b + 12);
+  int* maxlen = (int*)(b + 16);
+  ws.merge_list = (int32_t*)(b + 256);
+  ws.qr_list = ws.merge_list + n;
+  static const unsigned long long init_err = ~0ull;
+  SPAI_CUDA(cudaMemsetAsync(b + 8, 0, 12, s));
   SPAI_CUDA(cudaMemcpyAsync(ws.err, &init_err, 8, cudaMemcpyHostToDevice, s));
-  SPAI_CUDA(cudaMemsetAsync(b + 8, 0, 8, s));
   maxlen_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8), 256, 0, s>>>(n, cscptr, maxlen);
   SPAI_LAUNCH_CHECK("maxlen_kernel");
   int hmax = 0;
   SPAI_CUDA(cudaMemcpyAsync(&hmax, maxlen, 4, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
   int st;
-  if (hmax <= 8)       st = launch_warp<8, 64, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
-  else if (hmax <= 16) st = launch_warp<16, 256, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
-  else if (hmax <= 28) st = launch_warp<28, 784, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
-  else                 st = launch_warp<32, 1024, 4>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
+  if (hmax <= 8)       st = launch_hash<8, 64, 4, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
+  else if (hmax <= 16) st = launch_hash<16, 256, 4, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
+  else if (hmax <= 28) st = launch_hash<28, 784, 4, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
+  else                 st = launch_hash<32, 1024, 8, 4>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
   if (st) return st;
-  int hflag = 0;
-  SPAI_CUDA(cudaMemcpyAsync(&hflag, ws.nflag, 4, cudaMemcpyDeviceToHost, s));
+  int counts[2] = {0, 0};
+  SPAI_CUDA(cudaMemcpyAsync(counts, ws.nmerge, 8, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
-  if (hflag > 0) {
-    SPAI_CUDA(cudaFuncSetAttribute(spai_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kQrSmem));
-    int blocks = std::min(hflag, num_sms());
+  if (counts[0] > 0) {
+    const size_t smem = kMergeWarpBytes * kMergeWarps;
+    SPAI_CUDA(cudaFuncSetAttribute(gram_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int blocks = std::min((counts[0] + kMergeWarps - 1) / kMergeWarps, num_sms() * 4);
+    gram_merge_kernel<<<blocks, kMergeWarps * 32, smem, s>>>(vals, cscptr, cscrow, csc2csr, m_csc, ws);
+    SPAI_LAUNCH_CHECK("gram_merge_kernel");
+    SPAI_CUDA(cudaMemcpyAsync(counts, ws.nmerge, 8, cudaMemcpyDeviceToHost, s));
+    SPAI_CUDA(cudaStreamSynchronize(s));
+  }
+  if (counts[1] > 0) {
+    SPAI_CUDA(cudaFuncSetAttribute(spai_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrSmem));
+    const int blocks = std::min(counts[1], num_sms());
     spai_qr_kernel<<<blocks, kQrThreads, kQrSmem, s>>>(vals, cscptr, cscrow, csc2csr, m_csc, ws);
     SPAI_LAUNCH_CHECK("spai_qr_kernel");
   }
   unsigned long long herr = 0;
   SPAI_CUDA(cudaMemcpyAsync(&herr, ws.err, 8, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
-  if (n_fallback) *n_fallback = hflag;
+  if (n_fallback) *n_fallback = ((int64_t)counts[0] << 32) | (int64_t)counts[1];
   if (herr != ~0ull) {
     const int64_t col = (int64_t)(herr >> 4);
     const int kind = (int)(herr & 15);

@@ -1,13 +1,16 @@
 // K8: device-resident classic PCG (replaces _solve_classic, krylov.py:301-345).
 //
-// One iteration = two fused kernels, no host synchronisation:
-//   K1  p' = z + beta p (gathered on the fly), q = A p', [(p',q)]           (+ [(p,r),(r,r)] at it 1)
-//   K2  x += lambda p, r' = r - lambda q, z = M r' (gathered on the fly),  [(z,r'),(r',r')]
-// The last block of each kernel reduces the partial dots in a fixed order and
-// runs the scalar recurrence (lambda, beta, breakdown / divergence /
-// convergence tests) on the device; a status word turns every later launch
-// into a no-op, so a CUDA graph of C iterations can be replayed blindly and
-// the host only polls between graphs.
+// One iteration = two fused SELL-32 kernels, no host synchronisation:
+//   K1  p' = z + beta p (gathered on the fly), q = A p', [(p',q)]     (+ [(p,r),(r,r)] at it 1)
+//   K2  x += lambda p, r' = r - lambda q, z = M r' (gathered on the fly), [(z,r'),(r',r')]
+// The gathered operands are recomputed with the same fma the owning row uses,
+// so they are bit-identical to the stored vectors.  The last block of each
+// kernel reduces the partial dots in a fixed order (deterministic) and runs
+// the scalar recurrence (lambda, beta, breakdown / divergence / convergence
+// tests) on the device; a status word turns later launches into no-ops, so a
+// CUDA graph of 16 iterations is replayed blindly and the host only polls
+// between graphs.
+#include "sell.cuh"
 #include "spmv_core.cuh"
 
 namespace spai {
@@ -23,35 +26,35 @@ struct PcgScal {
 
 struct PcgVecs {
   double* x;
-  double* r[2];
-  double* p[2];
+  double* r0;
+  double* r1;
+  double* p0;
+  double* p1;
   double* q;
   double* z;
   double* hist;
   double* partials;
 };
 
-__device__ __forceinline__ bool finite(double v) { return isfinite(v); }
-
-template <int L, bool FIRST>
-__device__ __forceinline__ void k1_body(int64_t n, const Csr& A, const PcgVecs& v,
-                                        const PcgScal* sc, double (&acc)[3]) {
-  const int sub = threadIdx.x & (L - 1);
-  const int64_t g = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) / L;
-  const int64_t ng = (int64_t)gridDim.x * kSpmvThreads / L;
+template <bool FIRST>
+__device__ __forceinline__ void k1_body(int64_t n, int64_t nslices, const Sell& A,
+                                        const PcgVecs& v, const PcgScal* sc, double (&acc)[3]) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   const int pc = sc->pcur;
-  const double* __restrict__ pold = pc ? v.p[1] : v.p[0];
-  double* __restrict__ pnew = pc ? v.p[0] : v.p[1];
+  const double* __restrict__ pold = pc ? v.p1 : v.p0;
+  double* __restrict__ pnew = pc ? v.p0 : v.p1;
   const double* __restrict__ z = v.z;
-  const double* __restrict__ r = sc->rcur ? v.r[1] : v.r[0];
+  const double* __restrict__ r = sc->rcur ? v.r1 : v.r0;
   const double beta = sc->beta;
-  for (int64_t i = g; i < n; i += ng) {
-    const int64_t lo = A.rowptr[i], hi = A.rowptr[i + 1];
-    double s;
-    if (FIRST) s = row_dot<L>(A, lo, hi, sub, [&](int32_t j) { return __ldg(pold + j); });
-    else s = row_dot<L>(A, lo, hi, sub, [&](int32_t j) { return fma(beta, __ldg(pold + j), __ldg(z + j)); });
-    if (sub == 0) {
-      v.q[i] = s;
+  for (int64_t s = w0; s < nslices; s += nw) {
+    double q;
+    if (FIRST) q = sell_row(A, s, lane, [&](int32_t j) { return __ldg(pold + j); });
+    else q = sell_row(A, s, lane, [&](int32_t j) { return fma(beta, __ldg(pold + j), __ldg(z + j)); });
+    const int64_t i = s * kSell + lane;
+    if (i < n) {
+      v.q[i] = q;
       double pi;
       if (FIRST) {
         pi = pold[i];
@@ -62,19 +65,18 @@ __device__ __forceinline__ void k1_body(int64_t n, const Csr& A, const PcgVecs& 
         pi = fma(beta, pold[i], z[i]);
         pnew[i] = pi;
       }
-      acc[0] = fma(pi, s, acc[0]);
+      acc[0] = fma(pi, q, acc[0]);
     }
   }
 }
 
-template <int L>
 __global__ void __launch_bounds__(kSpmvThreads)
-pcg_k1(int64_t n, Csr A, PcgVecs v, PcgScal* sc) {
+pcg_k1(int64_t n, int64_t nslices, Sell A, PcgVecs v, PcgScal* sc) {
   if (sc->status != kRunning) return;
   const bool first = sc->it == 0;
   double acc[3] = {0.0, 0.0, 0.0};
-  if (first) k1_body<L, true>(n, A, v, sc, acc);
-  else k1_body<L, false>(n, A, v, sc, acc);
+  if (first) k1_body<true>(n, nslices, A, v, sc, acc);
+  else k1_body<false>(n, nslices, A, v, sc, acc);
   grid_finalize<3>(acc, v.partials, &sc->ticket1, [&](double (&tot)[3]) {
     double rho;
     const double delta = tot[0];
@@ -89,7 +91,7 @@ pcg_k1(int64_t n, Csr A, PcgVecs v, PcgScal* sc) {
       sc->it += 1;
       sc->pcur ^= 1;
     }
-    if (!finite(delta) || !finite(rho)) { sc->status = kDivergence; return; }
+    if (!isfinite(delta) || !isfinite(rho)) { sc->status = kDivergence; return; }
     if (delta <= 0.0) {
       if (rho == 0.0) {
         if (first) sc->norm = sc->norm0;
@@ -104,30 +106,30 @@ pcg_k1(int64_t n, Csr A, PcgVecs v, PcgScal* sc) {
   });
 }
 
-template <int L, bool HAS_M>
+template <bool HAS_M>
 __global__ void __launch_bounds__(kSpmvThreads)
-pcg_k2(int64_t n, Csr M, PcgVecs v, PcgScal* sc) {
+pcg_k2(int64_t n, int64_t nslices, Sell M, PcgVecs v, PcgScal* sc) {
   if (sc->status != kRunning) return;
-  const int sub = threadIdx.x & (L - 1);
-  const int64_t g = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) / L;
-  const int64_t ng = (int64_t)gridDim.x * kSpmvThreads / L;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   const double lambda = sc->lambda;
   const int rc = sc->rcur;
-  const double* __restrict__ p = sc->pcur ? v.p[1] : v.p[0];
-  const double* __restrict__ rold = rc ? v.r[1] : v.r[0];
-  double* __restrict__ rnew = rc ? v.r[0] : v.r[1];
+  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
+  const double* __restrict__ rold = rc ? v.r1 : v.r0;
+  double* __restrict__ rnew = rc ? v.r0 : v.r1;
   const double* __restrict__ q = v.q;
   double acc[2] = {0.0, 0.0};
-  for (int64_t i = g; i < n; i += ng) {
-    double s = 0.0;
+  for (int64_t s = w0; s < nslices; s += nw) {
+    double zi = 0.0;
     if (HAS_M)
-      s = row_dot<L>(M, M.rowptr[i], M.rowptr[i + 1], sub,
-                     [&](int32_t j) { return fma(-lambda, __ldg(q + j), __ldg(rold + j)); });
-    if (sub == 0) {
+      zi = sell_row(M, s, lane, [&](int32_t j) { return fma(-lambda, __ldg(q + j), __ldg(rold + j)); });
+    const int64_t i = s * kSell + lane;
+    if (i < n) {
       const double rn = fma(-lambda, q[i], rold[i]);
       rnew[i] = rn;
       v.x[i] = fma(lambda, p[i], v.x[i]);
-      const double zi = HAS_M ? s : rn;
+      if (!HAS_M) zi = rn;
       v.z[i] = zi;
       acc[0] = fma(zi, rn, acc[0]);
       acc[1] = fma(rn, rn, acc[1]);
@@ -136,7 +138,7 @@ pcg_k2(int64_t n, Csr M, PcgVecs v, PcgScal* sc) {
   grid_finalize<2>(acc, v.partials, &sc->ticket2, [&](double (&tot)[2]) {
     const double rho_new = tot[0], rr = tot[1];
     sc->rcur ^= 1;
-    if (!finite(rho_new) || !finite(rr)) { sc->status = kDivergence; return; }
+    if (!isfinite(rho_new) || !isfinite(rr)) { sc->status = kDivergence; return; }
     const double norm = sqrt(rr);
     v.hist[sc->it - 1] = norm;
     sc->norm = norm;
@@ -147,125 +149,122 @@ pcg_k2(int64_t n, Csr M, PcgVecs v, PcgScal* sc) {
   });
 }
 
-// r = b - A x0
-template <int L>
+// start: r = b - A x0 (or b), p = M r (or r)
+template <bool HAS_X0>
 __global__ void __launch_bounds__(kSpmvThreads)
-residual_kernel(int64_t n, Csr A, const double* __restrict__ x, const double* __restrict__ b,
-                double* __restrict__ r) {
-  const int sub = threadIdx.x & (L - 1);
-  const int64_t g = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) / L;
-  const int64_t ng = (int64_t)gridDim.x * kSpmvThreads / L;
-  for (int64_t i = g; i < n; i += ng) {
-    const double s = row_dot<L>(A, A.rowptr[i], A.rowptr[i + 1], sub,
-                                [&](int32_t j) { return __ldg(x + j); });
-    if (sub == 0) r[i] = b[i] - s;
+pcg_start_r(int64_t n, int64_t nslices, Sell A, const double* __restrict__ x,
+            const double* __restrict__ b, double* __restrict__ r) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
+  for (int64_t s = w0; s < nslices; s += nw) {
+    double ax = 0.0;
+    if (HAS_X0) ax = sell_row(A, s, lane, [&](int32_t j) { return __ldg(x + j); });
+    const int64_t i = s * kSell + lane;
+    if (i < n) r[i] = HAS_X0 ? b[i] - ax : b[i];
   }
 }
 
-int spmv_dispatch(int64_t n, Csr A, int64_t nnz, const double* x, double* y, cudaStream_t s);
+template <bool HAS_M>
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_start_p(int64_t n, int64_t nslices, Sell M, const double* __restrict__ r,
+            double* __restrict__ p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
+  for (int64_t s = w0; s < nslices; s += nw) {
+    double mr = 0.0;
+    if (HAS_M) mr = sell_row(M, s, lane, [&](int32_t j) { return __ldg(r + j); });
+    const int64_t i = s * kSell + lane;
+    if (i < n) p[i] = HAS_M ? mr : r[i];
+  }
+}
+
+unsigned sell_blocks(const void* kern, int64_t nslices);
 
 }  // namespace spai
 
 using namespace spai;
 
 struct spai_pcg {
-  int64_t n = 0, nnzA = 0, nnzM = 0;
-  Csr A{}, M{};
+  int64_t n = 0, nslices = 0;
+  Sell A{}, M{};
   bool hasM = false;
-  int LA = 8, LM = 8;
   double tol = 1e-8;
   int64_t maxit = 1000;
   cudaStream_t stream = nullptr;
+  bool own_stream = false;
   PcgVecs v{};
   double* b = nullptr;
   PcgScal* sc = nullptr;
+  PcgScal* host_init = nullptr;
   unsigned blocks1 = 1, blocks2 = 1;
   cudaGraphExec_t graph = nullptr;
-  int64_t graph_iters = 0;
-  bool own_stream = false;
 };
 
-template <int L>
-static unsigned blocks_for(const void* kern, int64_t n) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpmvThreads, 0);
-  if (per_sm < 1) per_sm = 1;
-  int64_t blocks = (n * L + kSpmvThreads - 1) / kSpmvThreads;
-  const int64_t cap = (int64_t)num_sms() * per_sm;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  return (unsigned)blocks;
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+extern "C" size_t spai_pcg_workspace_bytes(int64_t n, int64_t maxit) {
+  const size_t vb = align256((size_t)n * sizeof(double));
+  return 8 * vb + align256((size_t)maxit * sizeof(double)) +
+         align256((size_t)num_sms() * 32 * 3 * sizeof(double)) + align256(sizeof(PcgScal)) + 256;
 }
 
-template <int L>
-static const void* k1_ptr() { return (const void*)pcg_k1<L>; }
-template <int L, bool H>
-static const void* k2_ptr() { return (const void*)pcg_k2<L, H>; }
-
-#define SPAI_LSWITCH(LV, ...)                              \
-  switch (LV) {                                            \
-    case 2: { constexpr int L_ = 2; __VA_ARGS__; } break;   \
-    case 4: { constexpr int L_ = 4; __VA_ARGS__; } break;   \
-    case 8: { constexpr int L_ = 8; __VA_ARGS__; } break;   \
-    case 16: { constexpr int L_ = 16; __VA_ARGS__; } break; \
-    default: { constexpr int L_ = 32; __VA_ARGS__; } break; \
-  }
-
 static int launch_iteration(spai_pcg* s) {
-  SPAI_LSWITCH(s->LA, pcg_k1<L_><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->A, s->v, s->sc));
+  pcg_k1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v, s->sc);
   SPAI_LAUNCH_CHECK("pcg_k1");
-  if (s->hasM) {
-    SPAI_LSWITCH(s->LM, (pcg_k2<L_, true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->M, s->v, s->sc)));
-  } else {
-    pcg_k2<2, false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->M, s->v, s->sc);
-  }
+  if (s->hasM) pcg_k2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
+  else pcg_k2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
   SPAI_LAUNCH_CHECK("pcg_k2");
   return SPAI_OK;
 }
 
-extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* rowptr,
-                               const int32_t* colidx, const double* A_vals,
-                               const int64_t* m_rowptr, const int32_t* m_colidx,
-                               const double* M_vals, double tol, int64_t maxit, void* stream) {
+extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
+                               const int32_t* cols, const double* A_vals,
+                               const int64_t* m_sliceptr, const int32_t* m_cols,
+                               const double* M_vals, double tol, int64_t maxit, void* ws,
+                               size_t ws_bytes, void* stream) {
   if (!out || n <= 0 || maxit < 1) { set_error("spai_pcg_create: bad arguments"); return SPAI_E_ARG; }
+  if (ws_bytes < spai_pcg_workspace_bytes(n, maxit)) { set_error("pcg workspace too small"); return SPAI_E_ARG; }
   spai_pcg* s = new spai_pcg();
   s->n = n;
-  s->A = Csr{rowptr, colidx, A_vals};
+  s->nslices = (n + kSell - 1) / kSell;
+  s->A = Sell{sliceptr, cols, A_vals};
   s->hasM = M_vals != nullptr;
-  s->M = Csr{m_rowptr ? m_rowptr : rowptr, m_colidx ? m_colidx : colidx, M_vals};
+  s->M = Sell{m_sliceptr ? m_sliceptr : sliceptr, m_cols ? m_cols : cols, M_vals};
   s->tol = tol;
   s->maxit = maxit;
   s->stream = (cudaStream_t)stream;
-  if (s->stream == nullptr) {  // graphs cannot be captured on the legacy stream
-    SPAI_CUDA(cudaStreamCreate(&s->stream));
+  if (s->stream == nullptr) {   // graphs cannot be captured on the legacy stream
+    cudaError_t e = cudaStreamCreate(&s->stream);
+    if (e != cudaSuccess) { delete s; return cuda_fail(e, "cudaStreamCreate"); }
     s->own_stream = true;
   }
-  int64_t h[2] = {0, 0};
-  SPAI_CUDA(cudaMemcpyAsync(&h[0], rowptr + n, 8, cudaMemcpyDeviceToHost, s->stream));
-  if (s->hasM) SPAI_CUDA(cudaMemcpyAsync(&h[1], s->M.rowptr + n, 8, cudaMemcpyDeviceToHost, s->stream));
-  SPAI_CUDA(cudaStreamSynchronize(s->stream));
-  s->nnzA = h[0];
-  s->nnzM = h[1];
-  s->LA = lanes_for(n, s->nnzA);
-  s->LM = s->hasM ? lanes_for(n, s->nnzM) : 2;
-  SPAI_LSWITCH(s->LA, s->blocks1 = blocks_for<L_>(k1_ptr<L_>(), n));
-  if (s->hasM) { SPAI_LSWITCH(s->LM, (s->blocks2 = blocks_for<L_>(k2_ptr<L_, true>(), n))); }
-  else s->blocks2 = blocks_for<2>(k2_ptr<2, false>(), n);
-  const size_t vb = (size_t)n * sizeof(double);
-  double* mem = nullptr;
-  SPAI_CUDA(cudaMalloc(&mem, 8 * vb));
-  s->v.x = mem;
-  s->v.r[0] = mem + n;
-  s->v.r[1] = mem + 2 * n;
-  s->v.p[0] = mem + 3 * n;
-  s->v.p[1] = mem + 4 * n;
-  s->v.q = mem + 5 * n;
-  s->v.z = mem + 6 * n;
-  s->b = mem + 7 * n;
-  SPAI_CUDA(cudaMalloc(&s->v.hist, (size_t)maxit * sizeof(double)));
-  const unsigned pb = std::max(s->blocks1, s->blocks2);
-  SPAI_CUDA(cudaMalloc(&s->v.partials, (size_t)pb * 3 * sizeof(double)));
-  SPAI_CUDA(cudaMalloc(&s->sc, sizeof(PcgScal)));
+  static unsigned b1 = 0, b2t = 0, b2f = 0;
+  if (!b1) {
+    b1 = sell_blocks((const void*)pcg_k1, 1 << 30);
+    b2t = sell_blocks((const void*)pcg_k2<true>, 1 << 30);
+    b2f = sell_blocks((const void*)pcg_k2<false>, 1 << 30);
+  }
+  const int64_t need64 = (s->nslices * 32 + kSpmvThreads - 1) / kSpmvThreads;
+  const unsigned need = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need64, 1 << 30));
+  s->blocks1 = std::min(b1, need);
+  s->blocks2 = std::min(s->hasM ? b2t : b2f, need);
+  if (std::max(s->blocks1, s->blocks2) > (unsigned)num_sms() * 32) {
+    set_error("grid larger than the partials buffer");
+    delete s;
+    return SPAI_E_ARG;
+  }
+  char* p = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  const size_t vb = align256((size_t)n * sizeof(double));
+  double** vecs[8] = {&s->v.x, &s->v.r0, &s->v.r1, &s->v.p0, &s->v.p1, &s->v.q, &s->v.z, &s->b};
+  for (int i = 0; i < 8; ++i) { *vecs[i] = (double*)p; p += vb; }
+  s->v.hist = (double*)p;
+  p += align256((size_t)maxit * sizeof(double));
+  s->v.partials = (double*)p;
+  p += align256((size_t)num_sms() * 32 * 3 * sizeof(double));
+  s->sc = (PcgScal*)p;
+  s->host_init = new PcgScal();
   *out = s;
   return SPAI_OK;
 }
@@ -275,27 +274,23 @@ extern "C" int spai_pcg_start(spai_pcg* s, const double* b, const double* x0) {
   SPAI_CUDA(cudaMemcpyAsync(s->b, b, vb, cudaMemcpyDeviceToDevice, s->stream));
   if (x0) {
     SPAI_CUDA(cudaMemcpyAsync(s->v.x, x0, vb, cudaMemcpyDeviceToDevice, s->stream));
-    SPAI_LSWITCH(s->LA, (residual_kernel<L_><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->A, s->v.x, s->b, s->v.r[0])));
-    SPAI_LAUNCH_CHECK("residual_kernel");
+    pcg_start_r<true><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v.x, s->b, s->v.r0);
   } else {
     SPAI_CUDA(cudaMemsetAsync(s->v.x, 0, vb, s->stream));
-    SPAI_CUDA(cudaMemcpyAsync(s->v.r[0], s->b, vb, cudaMemcpyDeviceToDevice, s->stream));
+    pcg_start_r<false><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v.x, s->b, s->v.r0);
   }
-  if (s->hasM) {
-    int st = spmv_dispatch(s->n, s->M, s->nnzM, s->v.r[0], s->v.p[0], s->stream);
-    if (st) return st;
-  } else {
-    SPAI_CUDA(cudaMemcpyAsync(s->v.p[0], s->v.r[0], vb, cudaMemcpyDeviceToDevice, s->stream));
-  }
-  PcgScal h{};
-  h.tol = s->tol;
-  h.maxit = s->maxit;
-  h.norm = INFINITY;
-  h.norm0 = NAN;
-  h.status = kRunning;
-  SPAI_CUDA(cudaMemcpyAsync(s->sc, &h, sizeof(h), cudaMemcpyHostToDevice, s->stream));
-  // the host struct must outlive the async copy
-  SPAI_CUDA(cudaStreamSynchronize(s->stream));
+  SPAI_LAUNCH_CHECK("pcg_start_r");
+  if (s->hasM) pcg_start_p<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v.r0, s->v.p0);
+  else pcg_start_p<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v.r0, s->v.p0);
+  SPAI_LAUNCH_CHECK("pcg_start_p");
+  PcgScal* h = s->host_init;   // lives as long as the solver: safe for the async copy
+  *h = PcgScal{};
+  h->tol = s->tol;
+  h->maxit = s->maxit;
+  h->norm = INFINITY;
+  h->norm0 = NAN;
+  h->status = kRunning;
+  SPAI_CUDA(cudaMemcpyAsync(s->sc, h, sizeof(PcgScal), cudaMemcpyHostToDevice, s->stream));
   return SPAI_OK;
 }
 
@@ -312,7 +307,6 @@ extern "C" int spai_pcg_advance(spai_pcg* s, int64_t iters) {
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
       SPAI_CUDA(cudaGraphInstantiate(&s->graph, g, 0));
       SPAI_CUDA(cudaGraphDestroy(g));
-      s->graph_iters = kChunk;
     }
     SPAI_CUDA(cudaGraphLaunch(s->graph, s->stream));
     iters -= kChunk;
@@ -351,8 +345,8 @@ extern "C" int spai_pcg_vectors(spai_pcg* s, double** x, double** r, double** p,
   SPAI_CUDA(cudaMemcpyAsync(&h, s->sc, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
   SPAI_CUDA(cudaStreamSynchronize(s->stream));
   if (x) *x = s->v.x;
-  if (r) *r = s->v.r[h.rcur];
-  if (p) *p = s->v.p[h.pcur];
+  if (r) *r = h.rcur ? s->v.r1 : s->v.r0;
+  if (p) *p = h.pcur ? s->v.p1 : s->v.p0;
   if (z) *z = s->v.z;
   return SPAI_OK;
 }
@@ -361,11 +355,8 @@ extern "C" int spai_pcg_destroy(spai_pcg* s) {
   if (!s) return SPAI_OK;
   cudaStreamSynchronize(s->stream);
   if (s->graph) cudaGraphExecDestroy(s->graph);
-  cudaFree(s->v.x);
-  cudaFree(s->v.hist);
-  cudaFree(s->v.partials);
-  cudaFree(s->sc);
   if (s->own_stream) cudaStreamDestroy(s->stream);
+  delete s->host_init;
   delete s;
   return SPAI_OK;
 }

@@ -15,9 +15,12 @@ spmv_kernel(int64_t n, Csr A, const double* __restrict__ x, double* __restrict__
   const int64_t g = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) / L;
   const int64_t ng = (int64_t)gridDim.x * kSpmvThreads / L;
   PlainX xf{x};
-  for (int64_t i = g; i < n; i += ng) {
-    const double s = row_dot<L>(A, A.rowptr[i], A.rowptr[i + 1], sub, xf);
-    if (sub == 0) y[i] = s;
+  const int64_t g0 = g - ((threadIdx.x & 31) / L);
+  for (int64_t i0 = g0; i0 < n; i0 += ng) {          // warp-uniform trip count
+    const int64_t i = i0 + (g - g0);
+    const bool valid = i < n;
+    const double s = row_dot<L>(A, valid ? A.rowptr[i] : 0, valid ? A.rowptr[i + 1] : 0, sub, xf);
+    if (valid && sub == 0) y[i] = s;
   }
 }
 
@@ -175,8 +178,11 @@ spmv_tma_kernel(Csr A, const int64_t* __restrict__ tile_rows, int64_t ntiles, in
     const double* __restrict__ tv = sv + (size_t)s * sv_cap - a0;
     const int32_t* __restrict__ tc = sc + (size_t)s * sc_cap - c0;
     mbar_wait(&full[s], phase);
-    for (int64_t r = r0 + grp; r < r1; r += kGroups) {
-      const int64_t lo = A.rowptr[r], hi = A.rowptr[r + 1];
+    const int wg0 = grp - ((threadIdx.x & 31) / L);   // first group of this warp
+    for (int64_t rw = r0 + wg0; rw < r1; rw += kGroups) {   // warp-uniform trip count
+      const int64_t r = rw + (grp - wg0);
+      const bool valid = r < r1;
+      const int64_t lo = valid ? A.rowptr[r] : 0, hi = valid ? A.rowptr[r + 1] : 0;
       double acc = 0.0, acc2 = 0.0;
       int64_t e = lo + sub;
       for (; e + L < hi; e += 2 * L) {
@@ -185,7 +191,7 @@ spmv_tma_kernel(Csr A, const int64_t* __restrict__ tile_rows, int64_t ntiles, in
       }
       if (e < hi) acc = fma(tv[e], __ldg(x + tc[e]), acc);
       acc = group_sum<L>(acc + acc2);
-      if (sub == 0) y[r] = acc;
+      if (valid && sub == 0) y[r] = acc;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -144,6 +144,34 @@ __global__ void sym_check_kernel(int64_t n, int64_t nnz, const int64_t* rowptr,
   if (__syncthreads_or(local) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
+// Structurally symmetric fast path: CSC structure == CSR structure, and the
+// CSC slot q (an entry (c, i) of row c) maps to the CSR position of (i, c):
+// csc2csr[q] = rowptr[i] + lower_bound(row i, c).  Gather form: coalesced
+// writes, one short binary search per entry, no atomics, no sort.
+__global__ void sym_transpose_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                     const int32_t* __restrict__ colidx,
+                                     int64_t* __restrict__ csc2csr, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int miss = 0;
+  for (int64_t c = w0; c < n; c += nw) {
+    const int64_t lo = rowptr[c], hi = rowptr[c + 1];
+    for (int64_t q = lo + lane; q < hi; q += 32) {
+      const int32_t i = colidx[q];
+      int64_t a = rowptr[i], b = rowptr[i + 1];
+      const int64_t end = b;
+      while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (colidx[mid] < (int32_t)c) a = mid + 1; else b = mid;
+      }
+      if (a < end && colidx[a] == (int32_t)c) csc2csr[q] = a;
+      else miss = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, miss) && lane == 0) atomicOr(bad, 1);
+}
+
 // ---- nnz-balanced tiling: tile t starts at the first row with rowptr >= t*B
 constexpr int64_t kTileNnz = 2048;
 
@@ -276,6 +304,26 @@ extern "C" int spai_structure_is_symmetric(int64_t n, int64_t nnz, const int64_t
   int h = 0;
   SPAI_CUDA(cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost));
   SPAI_CUDA(cudaFree(d));
+  *is_sym = h ? 0 : 1;
+  return SPAI_OK;
+}
+
+extern "C" int spai_csr_transpose_symmetric(int64_t n, int64_t nnz, const int64_t* rowptr,
+                                            const int32_t* colidx, int64_t* csc2csr,
+                                            int* is_sym, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  (void)nnz;
+  int* d = nullptr;
+  SPAI_CUDA(cudaMallocAsync(&d, sizeof(int), s));
+  SPAI_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+  if (n > 0) {
+    sym_transpose_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, rowptr, colidx, csc2csr, d);
+    SPAI_LAUNCH_CHECK("sym_transpose_kernel");
+  }
+  int h = 0;
+  SPAI_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaFreeAsync(d, s));
+  SPAI_CUDA(cudaStreamSynchronize(s));
   *is_sym = h ? 0 : 1;
   return SPAI_OK;
 }

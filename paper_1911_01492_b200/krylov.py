@@ -216,18 +216,30 @@ class DevicePCG:
     """Owner of a native `spai_pcg` solver (C-ABI K8)."""
 
     def __init__(self, A: DeviceCsr, M: DeviceCsr | None, tol: float, maxit: int):
-        _require_cuda()
+        torch = _require_cuda()
         self.lib = _lib.load()
         self.A, self.M = A, M
         self.n = A.nrows
         self.maxit = int(maxit)
+        sliceptr, cols = A.sell()
+        a_vals = A.sell_values()
+        if M is not None:
+            m_vals = M.sell_values()
+            if M._pat is A._pat or (M.rowptr is A.rowptr and M.colidx is A.colidx):
+                m_sp, m_cols = C.c_void_p(0), C.c_void_p(0)
+            else:
+                msp, mc = M.sell()
+                m_sp, m_cols = ptr(msp), ptr(mc)
+        else:
+            m_vals, m_sp, m_cols = None, C.c_void_p(0), C.c_void_p(0)
+        wsb = self.lib.spai_pcg_workspace_bytes(self.n, self.maxit)
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
+        self._keep = (sliceptr, cols, a_vals, m_vals, M)
         h = C.c_void_p()
         st = self.lib.spai_pcg_create(
-            C.byref(h), A.nrows, ptr(A.rowptr), ptr(A.colidx), ptr(A.vals),
-            ptr(M.rowptr) if M is not None else C.c_void_p(0),
-            ptr(M.colidx) if M is not None else C.c_void_p(0),
-            ptr(M.vals) if M is not None else C.c_void_p(0),
-            float(tol), self.maxit, stream_handle())
+            C.byref(h), A.nrows, ptr(sliceptr), ptr(cols), ptr(a_vals), m_sp, m_cols,
+            ptr(m_vals) if m_vals is not None else C.c_void_p(0),
+            float(tol), self.maxit, ptr(self.ws), wsb, stream_handle())
         _lib.check(st, "spai_pcg_create")
         self.h = h
         self.launched = 0

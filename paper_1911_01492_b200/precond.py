@@ -114,8 +114,12 @@ def _raise_assembly(status: int, bad: int):
 
 
 class SpaiStats:
+    """Columns that left the hash/bitmask fast path: n_merge (pattern too large,
+    sorted-merge kernel) and n_fallback (Householder-QR kernel)."""
+
     def __init__(self):
         self.n_fallback = 0
+        self.n_merge = 0
 
 
 def spai1_columns_device(A: DeviceCsr, stats: SpaiStats | None = None):
@@ -137,7 +141,8 @@ def spai1_columns_device(A: DeviceCsr, stats: SpaiStats | None = None):
     if st != _lib.SPAI_OK:
         _raise_assembly(st, bad.value)
     if stats is not None:
-        stats.n_fallback = nfb.value
+        stats.n_merge = nfb.value >> 32
+        stats.n_fallback = nfb.value & 0xFFFFFFFF
     return m_csc[: A.nnz]
 
 

@@ -147,6 +147,13 @@ class CsrMatrix:
         return self._dev[1]
 
 
+class _PatternCache:
+    __slots__ = ("csc", "sym", "tiles", "sell")
+
+    def __init__(self):
+        self.csc = self.sym = self.tiles = self.sell = None
+
+
 class DeviceCsr:
     """HBM-resident CSR: rowptr int64[n+1], colidx int32[nnz], vals f64[nnz]."""
 
@@ -157,9 +164,10 @@ class DeviceCsr:
         self.colidx = colidx
         self.vals = vals
         self.nnz = int(colidx.numel())
-        self._csc = structure_of._csc if structure_of is not None else None
-        self._sym = structure_of._sym if structure_of is not None else None
-        self._tiles = structure_of._tiles if structure_of is not None else None
+        # pattern-derived data (CSC, SELL layout, tiles) shared by every matrix
+        # on the same pattern (A, its SPAI(1) M and the symmetrised M)
+        self._pat = structure_of._pat if structure_of is not None else _PatternCache()
+        self._sell_vals = None
 
     @classmethod
     def from_host(cls, A: CsrMatrix) -> "DeviceCsr":
@@ -191,27 +199,42 @@ class DeviceCsr:
 
     # K1: transpose structure
     def csc(self):
-        """(cscptr int64[ncols+1], cscrow int32[nnz], csc2csr int64[nnz]) (cached)."""
-        if self._csc is None:
+        """(cscptr int64[ncols+1], cscrow int32[nnz], csc2csr int64[nnz]) (cached).
+
+        Structurally symmetric patterns take the K1 fast path: the CSC
+        structure aliases the CSR arrays and only csc2csr is computed.
+        """
+        if self._pat.csc is None:
             torch = _require_cuda()
             lib = _lib.load()
             dev = self.rowptr.device
+            csc2csr = torch.empty(max(self.nnz, 1), dtype=torch.int64, device=dev)
+            if self.nrows == self.ncols:
+                sym = C.c_int(0)
+                _lib.check(lib.spai_csr_transpose_symmetric(
+                    self.nrows, self.nnz, ptr(self.rowptr), ptr(self.colidx), ptr(csc2csr),
+                    C.byref(sym), stream_handle()), "spai_csr_transpose_symmetric")
+                if sym.value:
+                    self._pat.sym = True
+                    self._pat.csc = (self.rowptr, self.colidx, csc2csr[: self.nnz])
+                    return self._pat.csc
             cscptr = torch.empty(self.ncols + 1, dtype=torch.int64, device=dev)
             cscrow = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
-            csc2csr = torch.empty(max(self.nnz, 1), dtype=torch.int64, device=dev)
             wsb = lib.spai_transpose_workspace_bytes(self.nrows, self.ncols, self.nnz)
             ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
             _lib.check(lib.spai_csr_transpose(
                 self.nrows, self.ncols, self.nnz, ptr(self.rowptr), ptr(self.colidx),
                 ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(ws), wsb, stream_handle()),
                 "spai_csr_transpose")
-            self._csc = (cscptr, cscrow[: self.nnz], csc2csr[: self.nnz])
-        return self._csc
+            self._pat.csc = (cscptr, cscrow[: self.nnz], csc2csr[: self.nnz])
+            if self.nrows == self.ncols:
+                self._pat.sym = False
+        return self._pat.csc
 
     def structurally_symmetric(self) -> bool:
-        if self._sym is None:
+        if self._pat.sym is None:
             if self.nrows != self.ncols:
-                self._sym = False
+                self._pat.sym = False
             else:
                 lib = _lib.load()
                 cscptr, cscrow, _ = self.csc()
@@ -221,12 +244,58 @@ class DeviceCsr:
                 _lib.check(lib.spai_structure_is_symmetric(
                     self.nrows, self.nnz, ptr(self.rowptr), ptr(self.colidx), ptr(cscptr),
                     ptr(cscrow), C.byref(out)), "spai_structure_is_symmetric")
-                self._sym = bool(out.value)
-        return self._sym
+                self._pat.sym = bool(out.value)
+        return self._pat.sym
+
+    # K5b: SELL-32 layout (solve-phase format), shared by matrices on one pattern
+    def sell(self):
+        """(sliceptr int64[nslices+1], cols int32[padded]) (cached per pattern)."""
+        if self._pat.sell is None:
+            torch = _require_cuda()
+            lib = _lib.load()
+            ns = lib.spai_sell_nslices(self.nrows)
+            dev = self.vals.device
+            sliceptr = torch.empty(ns + 1, dtype=torch.int64, device=dev)
+            _lib.check(lib.spai_sell_layout(self.nrows, ptr(self.rowptr), ptr(sliceptr),
+                                            stream_handle()), "spai_sell_layout")
+            padded = int(sliceptr[-1].item())
+            cols = torch.empty(max(padded, 1), dtype=torch.int32, device=dev)
+            _lib.check(lib.spai_sell_fill_cols(self.nrows, ptr(self.rowptr), ptr(self.colidx),
+                                               ptr(sliceptr), ptr(cols), stream_handle()),
+                       "spai_sell_fill_cols")
+            self._pat.sell = (sliceptr, cols)
+        return self._pat.sell
+
+    def sell_values(self):
+        """Values of this matrix in its SELL-32 layout (cached)."""
+        if self._sell_vals is None:
+            torch = _require_cuda()
+            sliceptr, cols = self.sell()
+            vals = torch.empty(cols.numel(), dtype=torch.float64, device=self.vals.device)
+            _lib.check(_lib.load().spai_sell_fill_vals(self.nrows, ptr(self.rowptr),
+                                                       ptr(self.vals), ptr(sliceptr), ptr(vals),
+                                                       stream_handle()), "spai_sell_fill_vals")
+            self._sell_vals = vals
+        return self._sell_vals
+
+    def matvec_sell(self, x, out=None):
+        """y = A x with the SELL-32 kernel."""
+        torch = _require_cuda()
+        if x.numel() != self.ncols:
+            raise DimensionMismatchError(
+                f"spmv: {self.ncols} columns vs vector of {x.numel()}")
+        if out is None:
+            out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
+        sliceptr, cols = self.sell()
+        vals = self.sell_values()
+        _lib.check(_lib.load().spai_sell_spmv(self.nrows, ptr(sliceptr), ptr(cols), ptr(vals),
+                                              ptr(x.contiguous()), ptr(out), stream_handle()),
+                   "spai_sell_spmv")
+        return out
 
     def tiles(self):
         """nnz-balanced row tiles of the TMA-staged SpMV (cached per pattern)."""
-        if self._tiles is None:
+        if self._pat.tiles is None:
             torch = _require_cuda()
             lib = _lib.load()
             nt = C.c_int64(0)
@@ -235,8 +304,8 @@ class DeviceCsr:
             mx = torch.zeros(1, dtype=torch.int32, device=self.vals.device)
             _lib.check(lib.spai_tile_rows(self.nrows, ptr(self.rowptr), nt.value, ptr(tile_rows),
                                           ptr(mx), stream_handle()), "spai_tile_rows")
-            self._tiles = (tile_rows, nt.value, int(mx.item()))
-        return self._tiles
+            self._pat.tiles = (tile_rows, nt.value, int(mx.item()))
+        return self._pat.tiles
 
     def matvec_tma(self, x, out=None):
         """y = A x with the TMA (cp.async.bulk) staged kernel."""

@@ -219,7 +219,8 @@ def test_qr_fallback_path_is_exercised():
     A = _random_symmetric_pattern(120, 300, 12, dense_cols=(5, 77))
     stats = pb.SpaiStats()
     pb.spai1_device(A.device(), stats)
-    assert stats.n_fallback >= 2     # columns 5 and 77 have |J| = n > 32
+    assert stats.n_merge >= 2        # columns 5 and 77 have |J| = n > 28
+    assert stats.n_fallback >= 2     # ... and > 32, so they end on the QR path
 
 
 def test_ill_conditioned_column_goes_to_qr_and_matches():
@@ -272,7 +273,12 @@ def test_spmv_matches_oracle():
         x = rng.standard_normal(A.ncols)
         y = pb.spmv(A, x)
         yr = oracle.spmv(_ocsr(A), x)
-        assert np.max(np.abs(y - yr)) <= 1e-13 * max(np.max(np.abs(yr)), 1.0)
+        tol = 1e-13 * max(np.max(np.abs(yr)), 1.0)
+        assert np.max(np.abs(y - yr)) <= tol
+        dA = A.device()
+        xd = torch.from_numpy(x).cuda()
+        for y2 in (dA.matvec_sell(xd), dA.matvec_tma(xd)):
+            assert np.max(np.abs(y2.cpu().numpy() - yr)) <= tol
     with pytest.raises(pb.DimensionMismatchError):
         pb.spmv(A, np.ones(A.ncols + 1))
 
@@ -392,7 +398,7 @@ def test_large_3d_spai_cg_properties():
     A = pb.q1_device((96, 96, 96))
     stats = pb.SpaiStats()
     S = pb.spai1_symmetric_device(A, stats)
-    assert stats.n_fallback == 0
+    assert stats.n_fallback == 0 and stats.n_merge == 0
     assert torch.equal(S.rowptr, A.rowptr) and torch.equal(S.colidx, A.colidx)
     ones = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
     b = A.matvec(ones)
