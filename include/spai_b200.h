@@ -103,6 +103,10 @@ int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
                   size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
                   void* stream);
 
+/* Toggle the symbolic-plan replay (default on; env SPAI_NO_PLANS=1 disables):
+ * columns with identical relative structure share one precomputed plan.   */
+int spai_set_assembly_plans(int enable);
+
 /* ------------------------------------------------------------------ K4
  * CSC-ordered M values -> CSR values of M (from_coo, precond.py:199). */
 int spai_csc_to_csr_values(int64_t nnz, const int64_t* csc2csr,

@@ -19,7 +19,7 @@ from .grids import (Anisotropy, StructuredGrid, assemble_poisson, assemble_q1,
 from .precond import (IdentityPreconditioner, JacobiPreconditioner,
                       Preconditioner, SparseMatrixPreconditioner, SpaiStats,
                       drop_exact_zeros, jacobi, make_spai1_factory,
-                      pattern_sets, spai1, spai1_device,
+                      pattern_sets, set_assembly_plans, spai1, spai1_device,
                       spai1_symmetric_device)
 from .krylov import (ConvergenceRecord, DevicePCG, KrylovState, LocalSystem,
                      SolverConfig, VARIANTS, fused_dots_device,

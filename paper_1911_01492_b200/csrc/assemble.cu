@@ -18,6 +18,7 @@
 // column, dense A[I,J] in shared memory, Householder QR with the exact
 // reference rank test  min|R_ii| <= 1e-13 max(max|R_ii|, 1)  (precond.py:192).
 #include "pattern.cuh"
+#include "plan.cuh"
 
 namespace spai {
 
@@ -119,7 +120,8 @@ template <int NJ, int CAPL, int MW, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 gram_hash_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
                  const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
-                 double* __restrict__ m_csc, AsmWs ws) {
+                 double* __restrict__ m_csc, AsmWs ws, const int32_t* __restrict__ list,
+                 const int* __restrict__ nlist) {
   using S = HashSmem<NJ, CAPL, MW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -137,8 +139,10 @@ gram_hash_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __re
 
   const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
-  for (int64_t k = gw; k < n; k += nw) {
+  const int64_t count = list ? (int64_t)*nlist : n;
+  for (int64_t f = gw; f < count; f += nw) {
     __syncwarp();
+    const int64_t k = list ? (int64_t)list[f] : f;
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
     if (nj == 0) { if (lane == 0) report(ws, k, kErrEmpty); continue; }
@@ -465,6 +469,420 @@ spai_qr_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscp
   }
 }
 
+// ---------------------------------------------------------------- plan path
+// Register Cholesky: lane i holds row i of G (g[l] = G[i][l], l <= i) in
+// registers; the pivot and the column of L are broadcast with shuffles.
+template <int NJ>
+__device__ __forceinline__ bool chol_solve_regs(double (&g)[NJ], double gdiag, int nj, int lane,
+                                                double& y) {
+  double myinv = 0.0, lmin = 1e300, lmax = 0.0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    if (j < nj) {
+      const double d = __shfl_sync(0xffffffffu, g[j], j);
+      const double gd = __shfl_sync(0xffffffffu, gdiag, j);
+      if (!(d > kFlagPivot * gd)) return false;
+      const double inv = rsqrt(d);
+      const double ljj = d * inv;
+      lmin = fmin(lmin, ljj);
+      lmax = fmax(lmax, ljj);
+      double lij = 0.0;
+      if (lane > j) { lij = g[j] * inv; g[j] = lij; }
+      if (lane == j) { g[j] = ljj; myinv = inv; }
+#pragma unroll
+      for (int l = j + 1; l < NJ; ++l) {
+        if (l < nj) {
+          const double llj = __shfl_sync(0xffffffffu, lij, l);
+          if (lane >= l) g[l] = fma(-lij, llj, g[l]);
+        }
+      }
+    }
+  }
+  if (lmin <= kRankGuard * fmax(lmax, 1.0)) return false;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {           // L y = rhs
+    if (j < nj) {
+      const double yj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
+      if (lane == j) y = yj;
+      if (lane > j) y = fma(-g[j], yj, y);
+    }
+  }
+  double m = 0.0;
+#pragma unroll
+  for (int j = NJ - 1; j >= 0; --j) {      // L^T m = y (column sums over lanes > j)
+    if (j < nj) {
+      double c = (lane > j && lane < nj) ? g[j] * m : 0.0;
+      c = warp_sum(c);
+      if (lane == j) m = (y - c) * myinv;
+    }
+  }
+  y = m;
+  return true;
+}
+
+// (A) signature of every column: hash of (nj, list lengths, relative rows)
+__global__ void __launch_bounds__(256)
+plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __restrict__ cscrow,
+                PlanWs pw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = w0; k < n; k += nw) {
+    const int64_t jlo = cscptr[k];
+    const int nj = (int)(cscptr[k + 1] - jlo);
+    if (nj == 0 || nj > kPlanNJ) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
+    int len = 0, c = 0;
+    int64_t clo = 0;
+    if (lane < nj) { c = cscrow[jlo + lane]; clo = cscptr[c]; len = (int)(cscptr[c + 1] - clo); }
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total > kPlanCap) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
+    uint64_t h = 0;
+    if (lane < nj) h += mix64(((uint64_t)(0x10000 + lane) << 32) ^ (uint32_t)len);
+    for (int a = 0; a < nj; ++a) {
+      const int la = __shfl_sync(0xffffffffu, len, a);
+      const int64_t src = __shfl_sync(0xffffffffu, clo, a);
+      const int off = __shfl_sync(0xffffffffu, incl, a) - la;
+      for (int t = lane; t < la; t += 32)
+        h += mix64(((uint64_t)(off + t) << 32) ^ (uint32_t)(cscrow[src + t] - (int32_t)k));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    h = mix64(h ^ (uint64_t)nj);
+    if (h == 0) h = 1;
+    if (lane == 0) {
+      int slot = (int)(h & (kPlanTable - 1));
+      int found = -1;
+      for (int probe = 0; probe < kPlanTable; ++probe) {
+        const unsigned long long prev = atomicCAS(pw.keys + slot, 0ull, (unsigned long long)h);
+        if (prev == 0ull) { pw.rep[slot] = (int32_t)k; atomicAdd(pw.nplans, 1); found = slot; break; }
+        if (prev == h) { found = slot; break; }
+        slot = (slot + 1) & (kPlanTable - 1);
+      }
+      pw.plan_slot[k] = found;
+    }
+  }
+}
+
+// (B) build one plan per distinct signature from its representative column
+constexpr int kBuildWarps = 4;
+struct BuildSmem {
+  int32_t lrow[kPlanCap];
+  int32_t keys[512];
+  int32_t I[256];
+  uint8_t lidx[kPlanCap];
+  uint32_t mask[kPlanNJ * 8];
+  uint16_t pre[kPlanNJ * 8];
+  int16_t cnt[tri(kPlanNJ)];
+  uint8_t assign[tri(kPlanNJ)];
+  int32_t loff[kPlanNJ + 1];
+  int32_t loads[32];
+  int64_t lsrc[kPlanNJ];
+};
+
+__global__ void __launch_bounds__(kBuildWarps * 32)
+plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict__ cscrow,
+                  PlanWs pw) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  BuildSmem& S = reinterpret_cast<BuildSmem*>(smem_raw)[w];
+  for (int slot = blockIdx.x * kBuildWarps + w; slot < kPlanTable; slot += gridDim.x * kBuildWarps) {
+    __syncwarp();
+    if (pw.keys[slot] == 0ull) continue;
+    int pi = 0;
+    if (lane == 0) pi = atomicAdd(pw.nbuilt, 1);
+    pi = __shfl_sync(0xffffffffu, pi, 0);
+    if (pi >= kMaxPlans) { if (lane == 0) pw.slot_plan[slot] = -1; continue; }
+    uint32_t* P = pw.plans + (size_t)pi * kPlanWords;
+    const int64_t k0 = pw.rep[slot];
+    const int64_t jlo = cscptr[k0];
+    const int nj = (int)(cscptr[k0 + 1] - jlo);
+    int len = 0;
+    int64_t clo = 0;
+    if (lane < nj) { const int c = cscrow[jlo + lane]; clo = cscptr[c]; len = (int)(cscptr[c + 1] - clo); }
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane < nj) { S.loff[lane] = incl - len; S.lsrc[lane] = clo; }
+    if (lane == 0) S.loff[nj] = total;
+    for (int i = lane; i < 512; i += 32) S.keys[i] = -1;
+    __syncwarp();
+    for (int a = 0; a < nj; ++a)
+      for (int t = lane; t < S.loff[a + 1] - S.loff[a]; t += 32) {
+        S.lrow[S.loff[a] + t] = cscrow[S.lsrc[a] + t];
+        reinterpret_cast<uint8_t*>(P + kPO_listid)[S.loff[a] + t] = (uint8_t)a;
+      }
+    __syncwarp();
+    for (int e = lane; e < total; e += 32) {
+      const int32_t r = S.lrow[e];
+      P[kPO_relofs + e] = (uint32_t)(r - (int32_t)k0);
+      uint32_t h = ((uint32_t)r * 2654435761u) >> 23;
+      while (true) {
+        const int32_t prev = atomicCAS(&S.keys[h], -1, r);
+        if (prev == -1 || prev == r) break;
+        h = (h + 1) & 511;
+      }
+    }
+    __syncwarp();
+    int m = 0;
+    for (int bs = 0; bs < 512; bs += 32) {
+      const int32_t key = S.keys[bs + lane];
+      const unsigned occ = __ballot_sync(0xffffffffu, key != -1);
+      const int pos = m + __popc(occ & ((1u << lane) - 1));
+      if (key != -1 && pos < 256) S.I[pos] = key;
+      m += __popc(occ);
+    }
+    bool ok = m <= 256;
+    if (ok) {
+      int size = 32;
+      while (size < m) size <<= 1;
+      for (int i = m + lane; i < size; i += 32) S.I[i] = INT32_MAX;
+      __syncwarp();
+      for (int kk = 2; kk <= size; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          for (int i = lane; i < size; i += 32) {
+            const int ixj = i ^ j;
+            if (ixj > i) {
+              const int32_t a = S.I[i], b = S.I[ixj];
+              if ((a > b) == ((i & kk) == 0)) { S.I[i] = b; S.I[ixj] = a; }
+            }
+          }
+          __syncwarp();
+        }
+      for (int e = lane; e < total; e += 32) {
+        const int32_t r = S.lrow[e];
+        int lo = 0, hi = m;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (S.I[mid] < r) lo = mid + 1; else hi = mid; }
+        S.lidx[e] = (uint8_t)lo;
+      }
+      int rk = -1;
+      {
+        int lo = 0, hi = m;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (S.I[mid] < (int32_t)k0) lo = mid + 1; else hi = mid; }
+        if (lo < m && S.I[lo] == (int32_t)k0) rk = lo;
+      }
+      __syncwarp();
+      if (lane < nj) {
+        uint32_t mk[8];
+#pragma unroll
+        for (int wd = 0; wd < 8; ++wd) mk[wd] = 0u;
+        for (int t = S.loff[lane]; t < S.loff[lane + 1]; ++t) {
+          const int li = S.lidx[t];
+#pragma unroll
+          for (int wd = 0; wd < 8; ++wd)
+            if ((li >> 5) == wd) mk[wd] |= 1u << (li & 31);
+        }
+        int acc = 0, ridx = -1;
+#pragma unroll
+        for (int wd = 0; wd < 8; ++wd) {
+          S.mask[lane * 8 + wd] = mk[wd];
+          S.pre[lane * 8 + wd] = (uint16_t)acc;
+          if (rk >= 0 && (rk >> 5) == wd && ((mk[wd] >> (rk & 31)) & 1u))
+            ridx = S.loff[lane] + acc + __popc(mk[wd] & ((1u << (rk & 31)) - 1u));
+          acc += __popc(mk[wd]);
+        }
+        P[kPO_rhs + lane] = (uint32_t)ridx;
+      }
+      if (lane <= nj) P[kPO_loff + lane] = (uint32_t)S.loff[lane];
+      if (lane == 0) P[kPO_loff + nj] = (uint32_t)total;
+      __syncwarp();
+      // overlap count per pair, then longest-processing-time lane assignment
+      const int np = tri(nj);
+      int maxc = 0;
+      for (int p = lane; p < np; p += 32) {
+        int a, b;
+        tri_decode(p, a, b);
+        int c = 0;
+#pragma unroll
+        for (int wd = 0; wd < 8; ++wd) c += __popc(S.mask[a * 8 + wd] & S.mask[b * 8 + wd]);
+        S.cnt[p] = (int16_t)c;
+        maxc = max(maxc, c);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, o));
+      __syncwarp();
+      if (lane == 0) {
+        for (int l = 0; l < 32; ++l) S.loads[l] = 0;
+        for (int p = 0; p < np; ++p) S.assign[p] = 255;
+        for (int c = maxc; c >= 1; --c)
+          for (int p = 0; p < np; ++p)
+            if (S.cnt[p] == c) {
+              int best = 0;
+              for (int l = 1; l < 32; ++l) if (S.loads[l] < S.loads[best]) best = l;
+              S.assign[p] = (uint8_t)best;
+              S.loads[best] += c;
+            }
+      }
+      __syncwarp();
+      // emit the product program of this lane
+      int step = 0;
+      uint32_t* ops = P + kPO_ops;
+      for (int p = 0; p < np; ++p) {
+        if (S.assign[p] != lane) continue;
+        int a, b;
+        tri_decode(p, a, b);
+        int remaining = S.cnt[p];
+#pragma unroll
+        for (int wd = 0; wd < 8; ++wd) {
+          const uint32_t ma = S.mask[a * 8 + wd], mb = S.mask[b * 8 + wd];
+          uint32_t both = ma & mb;
+          while (both) {
+            const int bit = __ffs(both) - 1;
+            both &= both - 1u;
+            const uint32_t below = (1u << bit) - 1u;
+            const int ea = S.loff[a] + S.pre[a * 8 + wd] + __popc(ma & below);
+            const int eb = S.loff[b] + S.pre[b * 8 + wd] + __popc(mb & below);
+            --remaining;
+            if (step < kPlanSteps) ops[step * 32 + lane] = op_pack(ea, eb, p, remaining == 0);
+            ++step;
+          }
+        }
+      }
+      int nsteps = step;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsteps = max(nsteps, __shfl_xor_sync(0xffffffffu, nsteps, o));
+      ok = nsteps <= kPlanSteps;
+      if (ok)
+        for (int t = step; t < nsteps; ++t) ops[t * 32 + lane] = kNop;
+      if (lane == 0) P[kPH_nsteps] = ok ? (uint32_t)nsteps : 0xFFFFFFFFu;
+    } else if (lane == 0) {
+      P[kPH_nsteps] = 0xFFFFFFFFu;
+    }
+    if (lane == 0) {
+      P[kPH_nj] = (uint32_t)nj;
+      P[kPH_total] = (uint32_t)total;
+    }
+    __threadfence();
+    if (lane == 0) pw.slot_plan[slot] = pi;
+  }
+}
+
+// (C) numeric replay: gather values, verify the relative pattern, run the
+// product program, register Cholesky, solve.  Mismatches -> direct list.
+template <int NJ, int CAPL>
+struct ReplaySmem {
+  static constexpr size_t off_lval = 0;
+  static constexpr size_t off_G = (size_t)CAPL * 8;
+  static constexpr size_t off_lsrc = off_G + (size_t)tri(NJ) * 8;
+  static constexpr size_t bytes = (off_lsrc + (size_t)NJ * 8 + 15) & ~(size_t)15;
+};
+
+template <int NJ, int CAPL, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
+                   const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
+                   const double* __restrict__ cscval, double* __restrict__ m_csc, AsmWs ws,
+                   PlanWs pw, int32_t* __restrict__ direct, int* __restrict__ ndirect) {
+  using S = ReplaySmem<NJ, CAPL>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = smem_raw + (size_t)w * S::bytes;
+  double* lval = reinterpret_cast<double*>(base + S::off_lval);
+  double* G = reinterpret_cast<double*>(base + S::off_G);
+  int64_t* lsrc = reinterpret_cast<int64_t*>(base + S::off_lsrc);
+  const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  for (int64_t k = gw; k < n; k += nw) {
+    __syncwarp();
+    const int slot = pw.plan_slot[k];
+    const int pi = slot >= 0 ? pw.slot_plan[slot] : -1;
+    const uint32_t* P = pi >= 0 ? pw.plans + (size_t)pi * kPlanWords : nullptr;
+    const int nsteps = P ? (int)P[kPH_nsteps] : -1;
+    const int64_t jlo = cscptr[k];
+    const int nj = (int)(cscptr[k + 1] - jlo);
+    if (nsteps < 0 || nj > NJ || (int)P[kPH_nj] != nj) {
+      if (lane == 0) direct[atomicAdd(ndirect, 1)] = (int32_t)k;
+      continue;
+    }
+    const int total = (int)P[kPH_total];
+    int len = 0;
+    int64_t clo = 0;
+    if (lane < nj) { const int c = cscrow[jlo + lane]; clo = cscptr[c]; len = (int)(cscptr[c + 1] - clo); }
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    bool bad = lane < nj && (incl - len) != (int)P[kPO_loff + lane];
+    if (lane == 31) bad |= incl != total;
+    if (total > CAPL || __any_sync(0xffffffffu, bad)) {
+      if (lane == 0) direct[atomicAdd(ndirect, 1)] = (int32_t)k;
+      continue;
+    }
+    if (lane < nj) lsrc[lane] = clo - (incl - len);      // entry e of list a sits at lsrc[a] + e
+    __syncwarp();
+    const uint8_t* listid = reinterpret_cast<const uint8_t*>(P + kPO_listid);
+    const uint32_t* relofs = P + kPO_relofs;
+    for (int e = lane; e < total; e += 32) {
+      const int64_t q = lsrc[listid[e]] + e;
+      const int32_t r = cscrow[q];
+      bad |= (uint32_t)(r - (int32_t)k) != relofs[e];
+      lval[e] = cscval ? cscval[q] : vals[csc2csr[q]];
+    }
+    for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) direct[atomicAdd(ndirect, 1)] = (int32_t)k;
+      continue;
+    }
+    __syncwarp();
+    const uint32_t* ops = P + kPO_ops + lane;
+    double s = 0.0;
+#pragma unroll 4
+    for (int t = 0; t < nsteps; ++t) {
+      const uint32_t op = ops[t * 32];
+      if (op != kNop) {
+        s = fma(lval[op & 1023u], lval[(op >> 10) & 1023u], s);
+        if (op >> 31) { G[(op >> 20) & 1023u] = s; s = 0.0; }
+      }
+    }
+    __syncwarp();
+    double g[NJ];
+#pragma unroll
+    for (int l = 0; l < NJ; ++l) g[l] = (l <= lane && lane < nj) ? G[tri(lane) + l] : 0.0;
+    const double gdiag = lane < nj ? G[tri(lane) + lane] : 1.0;
+    double y = 0.0;
+    if (lane < nj) {
+      const int ridx = (int)P[kPO_rhs + lane];
+      if (ridx >= 0) y = lval[ridx];
+    }
+    if (!chol_solve_regs<NJ>(g, gdiag, nj, lane, y)) {
+      if (lane == 0) to_qr(ws, k);
+      continue;
+    }
+    if (lane < nj) m_csc[jlo + lane] = y;
+  }
+}
+
+template <int NJ, int CAPL, int WARPS>
+static int launch_replay(int64_t n, const double* vals, const int64_t* cscptr,
+                         const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
+                         double* m_csc, AsmWs ws, PlanWs pw, int32_t* direct, int* ndirect,
+                         cudaStream_t s) {
+  const size_t smem = ReplaySmem<NJ, CAPL>::bytes * WARPS;
+  auto kern = plan_replay_kernel<NJ, CAPL, WARPS>;
+  SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SPAI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t blocks = (n + WARPS - 1) / WARPS;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, WARPS * 32, smem, s>>>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc,
+                                                  ws, pw, direct, ndirect);
+  SPAI_LAUNCH_CHECK("plan_replay_kernel");
+  return SPAI_OK;
+}
+
 __global__ void maxlen_kernel(int64_t n, const int64_t* cscptr, int* out) {
   int m = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
@@ -477,17 +895,20 @@ __global__ void maxlen_kernel(int64_t n, const int64_t* cscptr, int* out) {
 template <int NJ, int CAPL, int MW, int WARPS>
 static int launch_hash(int64_t n, const double* vals, const int64_t* cscptr,
                        const int32_t* cscrow, const int64_t* csc2csr, double* m_csc,
-                       AsmWs ws, cudaStream_t s) {
+                       AsmWs ws, const int32_t* list, const int* nlist, int64_t count,
+                       cudaStream_t s) {
   const size_t smem = HashSmem<NJ, CAPL, MW>::bytes * WARPS;
   auto kern = gram_hash_kernel<NJ, CAPL, MW, WARPS>;
   SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SPAI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
   if (per_sm < 1) per_sm = 1;
-  int64_t blocks = (n + WARPS - 1) / WARPS;
+  int64_t blocks = (count + WARPS - 1) / WARPS;
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
-  kern<<<(unsigned)blocks, WARPS * 32, smem, s>>>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws);
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, WARPS * 32, smem, s>>>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws,
+                                                  list, nlist);
   SPAI_LAUNCH_CHECK("gram_hash_kernel");
   return SPAI_OK;
 }
@@ -511,12 +932,57 @@ __global__ void symmetrize_kernel(int64_t nnz, const int64_t* __restrict__ csc2c
   }
 }
 
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
+  return 1024 + 4 * align256((size_t)n * sizeof(int32_t)) +
+         align256((size_t)kPlanTable * 16) +
+         align256((size_t)kMaxPlans * kPlanWords * sizeof(uint32_t));
+}
+
+template <int NJ, int CAPL, int MW, int WARPS>
+static int assemble_all(int64_t n, const double* vals, const int64_t* cscptr,
+                        const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
+                        double* m_csc, AsmWs ws, PlanWs pw, int32_t* direct, int* ndirect,
+                        bool use_plans, cudaStream_t s) {
+  int nd = 0;
+  if (use_plans) {
+    SPAI_CUDA(cudaMemsetAsync(pw.keys, 0, (size_t)kPlanTable * 8, s));
+    plan_sig_kernel<<<(unsigned)std::min<int64_t>((n * 32 + 255) / 256, num_sms() * 8), 256, 0, s>>>(
+        n, cscptr, cscrow, pw);
+    SPAI_LAUNCH_CHECK("plan_sig_kernel");
+    int np = 0;
+    SPAI_CUDA(cudaMemcpyAsync(&np, pw.nplans, 4, cudaMemcpyDeviceToHost, s));
+    SPAI_CUDA(cudaStreamSynchronize(s));
+    if (np > 0 && np <= kMaxPlans && (int64_t)np * 4 <= n) {
+      const size_t bsm = sizeof(BuildSmem) * kBuildWarps;
+      SPAI_CUDA(cudaFuncSetAttribute(plan_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      plan_build_kernel<<<kPlanTable / kBuildWarps / 8, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw);
+      SPAI_LAUNCH_CHECK("plan_build_kernel");
+      constexpr int RNJ = NJ <= 16 ? 16 : 32;   // register Cholesky fully unrolls at 16/32
+      int st = launch_replay<RNJ, CAPL, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
+                                          direct, ndirect, s);
+      if (st) return st;
+      SPAI_CUDA(cudaMemcpyAsync(&nd, ndirect, 4, cudaMemcpyDeviceToHost, s));
+      SPAI_CUDA(cudaStreamSynchronize(s));
+      if (nd == 0) return SPAI_OK;
+      return launch_hash<NJ, CAPL, MW, WARPS>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, direct,
+                                              ndirect, nd, s);
+    }
+  }
+  return launch_hash<NJ, CAPL, MW, WARPS>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, nullptr,
+                                          nullptr, n, s);
+}
+
 }  // namespace spai
 
 using namespace spai;
 
-extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
-  return 256 + 2 * (size_t)n * sizeof(int32_t);
+static int g_use_plans = -1;
+
+extern "C" int spai_set_assembly_plans(int enable) {
+  g_use_plans = enable ? 1 : 0;
+  return SPAI_OK;
 }
 
 extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
@@ -531,27 +997,46 @@ extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
   if (bad_col) *bad_col = -1;
   if (n_fallback) *n_fallback = 0;
   if (n == 0) return SPAI_OK;
+  if (g_use_plans < 0) {
+    const char* e = getenv("SPAI_NO_PLANS");
+    g_use_plans = (e && *e && *e != '0') ? 0 : 1;
+  }
   AsmWs ws;
-  unsigned char* b = (unsigned char*)wsp;
+  PlanWs pw;
+  unsigned char* b = (unsigned char*)(((uintptr_t)wsp + 255) & ~(uintptr_t)255);
   ws.err = (unsigned long long*)b;
   ws.nmerge = (int*)(b + 8);
   ws.nqr = (int*)(b + 12);
   int* maxlen = (int*)(b + 16);
-  ws.merge_list = (int32_t*)(b + 256);
-  ws.qr_list = ws.merge_list + n;
+  int* ndirect = (int*)(b + 20);
+  pw.nplans = (int*)(b + 24);
+  pw.nbuilt = (int*)(b + 28);
+  unsigned char* p = b + 256;
+  const size_t lb = align256((size_t)n * sizeof(int32_t));
+  ws.merge_list = (int32_t*)p; p += lb;
+  ws.qr_list = (int32_t*)p; p += lb;
+  int32_t* direct = (int32_t*)p; p += lb;
+  pw.plan_slot = (int32_t*)p; p += lb;
+  pw.keys = (unsigned long long*)p;
+  pw.rep = (int32_t*)(p + (size_t)kPlanTable * 8);
+  pw.slot_plan = (int32_t*)(p + (size_t)kPlanTable * 12);
+  p += align256((size_t)kPlanTable * 16);
+  pw.plans = (uint32_t*)p;
   static const unsigned long long init_err = ~0ull;
-  SPAI_CUDA(cudaMemsetAsync(b + 8, 0, 12, s));
+  SPAI_CUDA(cudaMemsetAsync(b + 8, 0, 24, s));
   SPAI_CUDA(cudaMemcpyAsync(ws.err, &init_err, 8, cudaMemcpyHostToDevice, s));
   maxlen_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8), 256, 0, s>>>(n, cscptr, maxlen);
   SPAI_LAUNCH_CHECK("maxlen_kernel");
   int hmax = 0;
   SPAI_CUDA(cudaMemcpyAsync(&hmax, maxlen, 4, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
+  const double* cscval = nullptr;   // values gathered through csc2csr
+  const bool plans = g_use_plans == 1;
   int st;
-  if (hmax <= 8)       st = launch_hash<8, 64, 4, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
-  else if (hmax <= 16) st = launch_hash<16, 256, 4, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
-  else if (hmax <= 28) st = launch_hash<28, 784, 4, 8>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
-  else                 st = launch_hash<32, 1024, 8, 4>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, s);
+  if (hmax <= 8)       st = assemble_all<8, 64, 4, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
+  else if (hmax <= 16) st = assemble_all<16, 256, 4, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
+  else if (hmax <= 28) st = assemble_all<28, 784, 4, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
+  else                 st = assemble_all<32, 1024, 8, 4>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
   if (st) return st;
   int counts[2] = {0, 0};
   SPAI_CUDA(cudaMemcpyAsync(counts, ws.nmerge, 8, cudaMemcpyDeviceToHost, s));

@@ -1,0 +1,59 @@
+// Symbolic plans for SPAI(1) assembly.
+//
+// The local least-squares problem of column k depends on the pattern only
+// through the *relative* row offsets of the gathered CSC lists (rows - k).
+// Columns with identical relative structure (every interior column of a
+// structured FEM matrix, and each of the boundary classes) therefore share
+// all index work: I_k, local ranks, the sparse overlap structure of
+// G = (A^T A)[J,J] and the position of e_k.  A plan stores that once:
+//   - loff[nj+1], listid[e], relofs[e]   (verifies a column matches exactly)
+//   - rhsidx[a]                          (entry holding A[k, J_a], or -1)
+//   - ops[t*32 + lane]                   (lane-balanced product program:
+//                                          G[p] += lval[ea] * lval[eb])
+// The numeric kernel then only gathers values, replays the product program
+// and factors G -- no hashing, sorting or searching per column.  Exact
+// verification of relofs keeps the result bit-identical in pattern semantics
+// to a from-scratch column (a mismatch sends the column to the direct path).
+#pragma once
+#include "common.cuh"
+
+namespace spai {
+
+constexpr int kPlanNJ = 32;          // max |J_k| on the plan path
+constexpr int kPlanCap = 1024;       // max gathered entries per column
+constexpr int kPlanSteps = 192;      // max product-program length per lane
+constexpr int kPlanTable = 8192;     // signature hash-table slots (power of 2)
+constexpr int kMaxPlans = 2048;
+constexpr uint32_t kNop = 0xFFFFFFFFu;
+
+// plan layout in 32-bit words
+constexpr int kPH_nj = 0, kPH_total = 1, kPH_nsteps = 2;
+constexpr int kPO_loff = 4;
+constexpr int kPO_rhs = kPO_loff + kPlanNJ + 1;
+constexpr int kPO_listid = kPO_rhs + kPlanNJ;                 // uint8, packed
+constexpr int kPO_relofs = kPO_listid + kPlanCap / 4;
+constexpr int kPO_ops = kPO_relofs + kPlanCap;
+constexpr int kPlanWords = ((kPO_ops + 32 * kPlanSteps) + 31) & ~31;
+
+__device__ __forceinline__ uint32_t op_pack(int ea, int eb, int p, bool last) {
+  return (uint32_t)ea | ((uint32_t)eb << 10) | ((uint32_t)p << 20) | (last ? 0x80000000u : 0u);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+struct PlanWs {
+  unsigned long long* keys;   // [kPlanTable]  0 = empty
+  int32_t* rep;               // [kPlanTable]  representative column
+  int32_t* slot_plan;         // [kPlanTable]  plan index of a slot (-1 invalid)
+  int32_t* plan_slot;         // [n]           table slot of each column (-1 = direct)
+  int* nplans;                // distinct signatures
+  int* nbuilt;                // plans built
+  uint32_t* plans;            // [kMaxPlans * kPlanWords]
+};
+
+}  // namespace spai

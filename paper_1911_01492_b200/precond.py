@@ -113,6 +113,12 @@ def _raise_assembly(status: int, bad: int):
     raise _lib.NativeLibraryError(f"spai_assemble failed ({status}): {msg}")
 
 
+def set_assembly_plans(enable: bool) -> None:
+    """Enable/disable symbolic-plan replay in the assembly (K3); both paths give
+    the same pattern and agree to rounding."""
+    _lib.load().spai_set_assembly_plans(1 if enable else 0)
+
+
 class SpaiStats:
     """Columns that left the hash/bitmask fast path: n_merge (pattern too large,
     sorted-merge kernel) and n_fallback (Householder-QR kernel)."""

@@ -37,6 +37,9 @@ with torch.cuda.stream(s):
     out["transpose_ms"] = timed(lambda: DeviceCsr(n, n, A.rowptr, A.colidx, A.vals).csc())
     A.csc()
     out["assemble_ms"] = timed(lambda: pb.precond.spai1_columns_device(A))
+    pb.set_assembly_plans(False)
+    out["assemble_direct_ms"] = timed(lambda: pb.precond.spai1_columns_device(A), 2)
+    pb.set_assembly_plans(True)
     st = pb.SpaiStats()
     pb.precond.spai1_columns_device(A, st)
     out["fallback"] = (st.n_merge, st.n_fallback)

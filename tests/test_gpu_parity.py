@@ -215,6 +215,26 @@ def test_spai1_matches_oracle_sampled(make, ncheck):
     assert np.array_equal(M.vals.cpu().numpy()[perm], m_csc)
 
 
+@pytest.mark.parametrize("plans", [True, False])
+def test_plan_and_direct_paths_agree_with_oracle(plans):
+    A = pb.assemble_q1((14, 13, 12), conv=(1.0, 0.5, 0.25))
+    pb.set_assembly_plans(plans)
+    try:
+        m = pb.precond.spai1_columns_device(A.device()).cpu().numpy()
+    finally:
+        pb.set_assembly_plans(True)
+    oa = _ocsr(A)
+    sets = oracle.pattern_sets(oa)
+    ref = np.concatenate(oracle.spai1_columns(oa, sets=sets))
+    At, perm = oracle.transpose(oa)
+    cols = np.repeat(np.arange(A.ncols), np.diff(At.row_offsets))
+    num = np.zeros(A.ncols)
+    den = np.zeros(A.ncols)
+    np.maximum.at(num, cols, np.abs(m - ref))
+    np.maximum.at(den, cols, np.abs(ref))
+    assert np.max(num / den) <= SPAI_TOL
+
+
 def test_qr_fallback_path_is_exercised():
     A = _random_symmetric_pattern(120, 300, 12, dense_cols=(5, 77))
     stats = pb.SpaiStats()
