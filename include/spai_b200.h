@@ -96,10 +96,15 @@ int spai_pattern_fill(int64_t n, const int64_t* cscptr, const int32_t* cscrow,
  * min|R_ii| <= 1e-13*max(max|R_ii|,1); *n_fallback = columns that took the
  * Householder-QR path.                                                     */
 size_t spai_assemble_workspace_bytes(int64_t n);
+/* cscval (optional, may be NULL) = A's values in CSC order; spai_csc_values
+ * builds it (synchronous) and reports whether it equals vals entry for entry
+ * (numerically symmetric A: then pass vals itself and skip the copy).      */
+int spai_csc_values(int64_t nnz, const int64_t* csc2csr, const double* vals,
+                    double* cscval, int* identical, void* stream);
 int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
                   const int32_t* colidx, const double* vals,
                   const int64_t* cscptr, const int32_t* cscrow,
-                  const int64_t* csc2csr, double* m_csc, void* ws,
+                  const int64_t* csc2csr, const double* cscval, double* m_csc, void* ws,
                   size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
                   void* stream);
 

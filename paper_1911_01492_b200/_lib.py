@@ -47,8 +47,9 @@ _SIGS = {
     "spai_pattern_count": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _vp]),
     "spai_pattern_fill": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "spai_assemble_workspace_bytes": (_sz, [_i64]),
-    "spai_assemble": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+    "spai_assemble": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
                              C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "spai_csc_values": (_i32, [_i64, _vp, _vp, _vp, C.POINTER(_i32), _vp]),
     "spai_set_assembly_plans": (_i32, [_i32]),
     "spai_csc_to_csr_values": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_symmetrize": (_i32, [_i64, _vp, _vp, _vp, _vp]),

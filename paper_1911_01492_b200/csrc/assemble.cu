@@ -470,53 +470,72 @@ spai_qr_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscp
 }
 
 // ---------------------------------------------------------------- plan path
-// Register Cholesky: lane i holds row i of G (g[l] = G[i][l], l <= i) in
-// registers; the pivot and the column of L are broadcast with shuffles.
+// Register Cholesky of the packed G in smem, padded to NJ with identity rows
+// (no per-element predicates): lane i keeps row i of the lower factor in
+// registers; column j of L is broadcast through a 32-entry smem buffer
+// (one broadcast LDS per FMA).  The factor is written back to G for the
+// backward solve.  Returns false if the column must take the QR path.
 template <int NJ>
-__device__ __forceinline__ bool chol_solve_regs(double (&g)[NJ], double gdiag, int nj, int lane,
-                                                double& y) {
-  double myinv = 0.0, lmin = 1e300, lmax = 0.0;
+__device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int nj, int lane,
+                                                  double& y) {
+  const int ti = tri(lane);
+  double g[NJ];
+#pragma unroll
+  for (int l = 0; l < NJ; ++l)
+    g[l] = lane < nj ? (l <= lane ? G[ti + l] : 0.0) : (l == lane ? 1.0 : 0.0);
+  const double gdiag = lane < nj ? G[ti + lane] : 1.0;
+  if (lane >= nj) y = 0.0;
+  double myinv = 0.0, myd = 1.0;
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
-    if (j < nj) {
-      const double d = __shfl_sync(0xffffffffu, g[j], j);
-      const double gd = __shfl_sync(0xffffffffu, gdiag, j);
-      if (!(d > kFlagPivot * gd)) return false;
-      const double inv = rsqrt(d);
-      const double ljj = d * inv;
-      lmin = fmin(lmin, ljj);
-      lmax = fmax(lmax, ljj);
-      double lij = 0.0;
-      if (lane > j) { lij = g[j] * inv; g[j] = lij; }
-      if (lane == j) { g[j] = ljj; myinv = inv; }
+    const double d = __shfl_sync(0xffffffffu, g[j], j);
+    const double inv = rsqrt(d);
+    const double lij = lane > j ? g[j] * inv : 0.0;
+    colbuf[lane] = lij;
+    __syncwarp();
+    if (lane == j) { g[j] = d * inv; myinv = inv; myd = d; }
+    else if (lane > j) g[j] = lij;
+    if ((j + 1) & 1) {                 // odd start: one scalar, then aligned pairs
+      if (j + 1 < NJ) g[j + 1] = fma(-lij, colbuf[j + 1], g[j + 1]);
+    }
 #pragma unroll
-      for (int l = j + 1; l < NJ; ++l) {
-        if (l < nj) {
-          const double llj = __shfl_sync(0xffffffffu, lij, l);
-          if (lane >= l) g[l] = fma(-lij, llj, g[l]);
-        }
+    for (int l = (j + 2) & ~1; l < NJ; l += 2) {
+      if (l + 1 < NJ) {
+        const double2 c2 = *reinterpret_cast<const double2*>(colbuf + l);
+        g[l] = fma(-lij, c2.x, g[l]);
+        g[l + 1] = fma(-lij, c2.y, g[l + 1]);
+      } else {
+        g[l] = fma(-lij, colbuf[l], g[l]);
       }
     }
+    __syncwarp();
   }
-  if (lmin <= kRankGuard * fmax(lmax, 1.0)) return false;
+  // pivot tests after the fact: d_j > 1e-4 G_jj and the rank guard on L_jj = sqrt(d_j)
+  const bool bad = lane < nj && !(myd > kFlagPivot * gdiag);
+  double dmin = lane < nj ? myd : 1e300, dmax = lane < nj ? myd : 0.0;
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {           // L y = rhs
-    if (j < nj) {
-      const double yj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
-      if (lane == j) y = yj;
-      if (lane > j) y = fma(-g[j], yj, y);
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   }
-  double m = 0.0;
+  if (__any_sync(0xffffffffu, bad) || !(sqrt(dmin) > kRankGuard * fmax(sqrt(dmax), 1.0))) return false;
+  // forward: L y = rhs
 #pragma unroll
-  for (int j = NJ - 1; j >= 0; --j) {      // L^T m = y (column sums over lanes > j)
-    if (j < nj) {
-      double c = (lane > j && lane < nj) ? g[j] * m : 0.0;
-      c = warp_sum(c);
-      if (lane == j) m = (y - c) * myinv;
-    }
+  for (int j = 0; j < NJ; ++j) {
+    const double yj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
+    y = lane == j ? yj : (lane > j ? fma(-g[j], yj, y) : y);
   }
-  y = m;
+  // store L (row i by lane i) for the backward solve L^T m = y
+  if (lane < nj) {
+#pragma unroll
+    for (int l = 0; l < NJ; ++l) if (l <= lane) G[ti + l] = g[l];
+  }
+  __syncwarp();
+  for (int j = nj - 1; j >= 0; --j) {
+    const double mj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
+    if (lane == j) y = mj;
+    else if (lane < j) y = fma(-G[tri(j) + lane], mj, y);
+  }
   return true;
 }
 
@@ -541,7 +560,7 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
       if (lane >= o) incl += t;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total > kPlanCap) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
+    if (total > kPadIdx) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
     uint64_t h = 0;
     if (lane < nj) h += mix64(((uint64_t)(0x10000 + lane) << 32) ^ (uint32_t)len);
     for (int a = 0; a < nj; ++a) {
@@ -770,14 +789,15 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
 // product program, register Cholesky, solve.  Mismatches -> direct list.
 template <int NJ, int CAPL>
 struct ReplaySmem {
-  static constexpr size_t off_lval = 0;
-  static constexpr size_t off_G = (size_t)CAPL * 8;
-  static constexpr size_t off_lsrc = off_G + (size_t)tri(NJ) * 8;
+  static constexpr size_t off_lval = 0;                          // values + zero slot 1023
+  static constexpr size_t off_G = (size_t)(kPadIdx + 1) * 8;
+  static constexpr size_t off_col = (off_G + (size_t)tri(NJ) * 8 + 15) & ~(size_t)15;
+  static constexpr size_t off_lsrc = off_col + 32 * 8;
   static constexpr size_t bytes = (off_lsrc + (size_t)NJ * 8 + 15) & ~(size_t)15;
 };
 
 template <int NJ, int CAPL, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 2)
 plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
                    const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
                    const double* __restrict__ cscval, double* __restrict__ m_csc, AsmWs ws,
@@ -788,7 +808,9 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
   unsigned char* base = smem_raw + (size_t)w * S::bytes;
   double* lval = reinterpret_cast<double*>(base + S::off_lval);
   double* G = reinterpret_cast<double*>(base + S::off_G);
+  double* colbuf = reinterpret_cast<double*>(base + S::off_col);
   int64_t* lsrc = reinterpret_cast<int64_t*>(base + S::off_lsrc);
+  if (lane == 0) lval[kPadIdx] = 0.0;   // target of padding ops
   const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   for (int64_t k = gw; k < n; k += nw) {
@@ -835,27 +857,22 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
       continue;
     }
     __syncwarp();
+    // product program; padding ops multiply the zero slot and never store
     const uint32_t* ops = P + kPO_ops + lane;
     double s = 0.0;
 #pragma unroll 4
     for (int t = 0; t < nsteps; ++t) {
       const uint32_t op = ops[t * 32];
-      if (op != kNop) {
-        s = fma(lval[op & 1023u], lval[(op >> 10) & 1023u], s);
-        if (op >> 31) { G[(op >> 20) & 1023u] = s; s = 0.0; }
-      }
+      s = fma(lval[op & 1023u], lval[(op >> 10) & 1023u], s);
+      if (op >> 31) { G[(op >> 20) & 1023u] = s; s = 0.0; }
     }
     __syncwarp();
-    double g[NJ];
-#pragma unroll
-    for (int l = 0; l < NJ; ++l) g[l] = (l <= lane && lane < nj) ? G[tri(lane) + l] : 0.0;
-    const double gdiag = lane < nj ? G[tri(lane) + lane] : 1.0;
     double y = 0.0;
     if (lane < nj) {
       const int ridx = (int)P[kPO_rhs + lane];
       if (ridx >= 0) y = lval[ridx];
     }
-    if (!chol_solve_regs<NJ>(g, gdiag, nj, lane, y)) {
+    if (!chol_solve_padded<NJ>(G, colbuf, nj, lane, y)) {
       if (lane == 0) to_qr(ws, k);
       continue;
     }
@@ -913,6 +930,19 @@ static int launch_hash(int64_t n, const double* vals, const int64_t* cscptr,
   return SPAI_OK;
 }
 
+__global__ void csc_values_kernel(int64_t nnz, const int64_t* __restrict__ csc2csr,
+                                  const double* __restrict__ vals, double* __restrict__ out,
+                                  int* differ) {
+  int d = 0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double v = vals[csc2csr[q]];
+    out[q] = v;
+    d |= v != vals[q];
+  }
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(differ, 1);
+}
+
 __global__ void csc_to_csr_kernel(int64_t nnz, const int64_t* __restrict__ csc2csr,
                                   const double* __restrict__ m_csc, double* __restrict__ m_csr) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
@@ -959,7 +989,7 @@ static int assemble_all(int64_t n, const double* vals, const int64_t* cscptr,
       SPAI_CUDA(cudaFuncSetAttribute(plan_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
       plan_build_kernel<<<kPlanTable / kBuildWarps / 8, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw);
       SPAI_LAUNCH_CHECK("plan_build_kernel");
-      constexpr int RNJ = NJ <= 16 ? 16 : 32;   // register Cholesky fully unrolls at 16/32
+      constexpr int RNJ = NJ;
       int st = launch_replay<RNJ, CAPL, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
                                           direct, ndirect, s);
       if (st) return st;
@@ -988,7 +1018,7 @@ extern "C" int spai_set_assembly_plans(int enable) {
 extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
                              const int32_t* colidx, const double* vals,
                              const int64_t* cscptr, const int32_t* cscrow,
-                             const int64_t* csc2csr, double* m_csc, void* wsp,
+                             const int64_t* csc2csr, const double* cscval_in, double* m_csc, void* wsp,
                              size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
                              void* stream) {
   (void)rowptr; (void)colidx; (void)nnz;
@@ -1030,7 +1060,7 @@ extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
   int hmax = 0;
   SPAI_CUDA(cudaMemcpyAsync(&hmax, maxlen, 4, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
-  const double* cscval = nullptr;   // values gathered through csc2csr
+  const double* cscval = cscval_in;   // NULL: values gathered through csc2csr
   const bool plans = g_use_plans == 1;
   int st;
   if (hmax <= 8)       st = assemble_all<8, 64, 4, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
@@ -1070,6 +1100,25 @@ extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
     set_error("column %lld: local least-squares problem exceeds kernel limits", (long long)col);
     return SPAI_E_UNSUPPORTED;
   }
+  return SPAI_OK;
+}
+
+extern "C" int spai_csc_values(int64_t nnz, const int64_t* csc2csr, const double* vals,
+                               double* cscval, int* identical, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int* d = nullptr;
+  SPAI_CUDA(cudaMallocAsync(&d, sizeof(int), s));
+  SPAI_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+  if (nnz > 0) {
+    int64_t blocks = std::min<int64_t>((nnz + 255) / 256, (int64_t)num_sms() * 16);
+    csc_values_kernel<<<(unsigned)blocks, 256, 0, s>>>(nnz, csc2csr, vals, cscval, d);
+    SPAI_LAUNCH_CHECK("csc_values_kernel");
+  }
+  int h = 0;
+  SPAI_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaFreeAsync(d, s));
+  SPAI_CUDA(cudaStreamSynchronize(s));
+  *identical = h ? 0 : 1;
   return SPAI_OK;
 }
 

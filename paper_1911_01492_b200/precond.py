@@ -135,13 +135,14 @@ def spai1_columns_device(A: DeviceCsr, stats: SpaiStats | None = None):
     if A.nrows != A.ncols:
         raise DimensionMismatchError("spai1 needs a square matrix")
     cscptr, cscrow, csc2csr = A.csc()
+    cscval = A.csc_values()
     m_csc = torch.empty(max(A.nnz, 1), dtype=torch.float64, device=A.vals.device)
     wsb = lib.spai_assemble_workspace_bytes(A.nrows)
     ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
     bad = C.c_int64(-1)
     nfb = C.c_int64(0)
     st = lib.spai_assemble(A.nrows, A.nnz, ptr(A.rowptr), ptr(A.colidx), ptr(A.vals),
-                           ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(m_csc), ptr(ws),
+                           ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(cscval), ptr(m_csc), ptr(ws),
                            wsb, C.byref(bad), C.byref(nfb), stream_handle())
     _lib.check(st, "spai_assemble")
     if st != _lib.SPAI_OK:

@@ -168,6 +168,7 @@ class DeviceCsr:
         # on the same pattern (A, its SPAI(1) M and the symmetrised M)
         self._pat = structure_of._pat if structure_of is not None else _PatternCache()
         self._sell_vals = None
+        self._cscval = None
 
     @classmethod
     def from_host(cls, A: CsrMatrix) -> "DeviceCsr":
@@ -230,6 +231,21 @@ class DeviceCsr:
             if self.nrows == self.ncols:
                 self._pat.sym = False
         return self._pat.csc
+
+    def csc_values(self):
+        """A's values in CSC order (cached); aliases `vals` when A is
+        numerically symmetric on a symmetric pattern (no copy kept)."""
+        if self._cscval is None:
+            torch = _require_cuda()
+            _, _, csc2csr = self.csc()
+            out = torch.empty(max(self.nnz, 1), dtype=torch.float64, device=self.vals.device)
+            same = C.c_int(0)
+            _lib.check(_lib.load().spai_csc_values(self.nnz, ptr(csc2csr), ptr(self.vals),
+                                                   ptr(out), C.byref(same), stream_handle()),
+                       "spai_csc_values")
+            sym_pattern = self._pat.csc[0] is self.rowptr
+            self._cscval = self.vals if (same.value and sym_pattern) else out[: self.nnz]
+        return self._cscval
 
     def structurally_symmetric(self) -> bool:
         if self._pat.sym is None:
