@@ -327,7 +327,7 @@ def run_ours(args):
             "solve": {"ms": t_sol * 1e3, "iterations": its, "dof_it_per_s": n * its / t_sol,
                       "ms_per_iteration": t_sol / its * 1e3},
             "spmv": spmv,
-            "roofline": {"bound": "hbm", "kernel": "PCG iteration (pcg_k1 + pcg_k2)",
+            "roofline": {"bound": "hbm", "kernel": "PCG iteration (pcg_v1 + pcg_u1 + pcg_v2 + pcg_u2)",
                          "achieved": solve_gbs, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": solve_gbs / hbm, "traffic": None,
                          "algorithmic_bytes_per_iteration": b_it},

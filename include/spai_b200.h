@@ -182,6 +182,10 @@ int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
                     const int64_t* m_sliceptr, const int32_t* m_cols,
                     const double* M_vals, double tol, int64_t maxit, void* ws,
                     size_t ws_bytes, void* stream);
+/* 0 (default): 4 kernels per iteration (vector updates in their own
+ * kernels, one gather per stored entry); 1: 2 kernels (vector updates
+ * recomputed inside the SpMV gathers).  Same arithmetic, same results.    */
+int spai_pcg_set_fused(spai_pcg* s, int fused);
 /* Start from x0 (device, may be NULL -> zero); b device, copied.          */
 int spai_pcg_start(spai_pcg* s, const double* b, const double* x0);
 /* Enqueue up to `iters` more iterations (no host sync; CUDA graphs of 16). */

@@ -149,6 +149,124 @@ pcg_k2(int64_t n, int64_t nslices, Sell M, PcgVecs v, PcgScal* sc) {
   });
 }
 
+// ---- unfused variant: vector updates in their own kernels, one gather per nnz
+// V1: p' = z + beta p (it >= 2)          U1: q = A p', [(p',q)] (+ [(p,r),(r,r)] at it 1)
+// V2: x += lambda p, r' = r - lambda q    U2: z = M r', [(z,r'),(r',r')]
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_v1(int64_t n, PcgVecs v, const PcgScal* sc) {
+  if (sc->status != kRunning || sc->it == 0) return;
+  const double beta = sc->beta;
+  const double* __restrict__ pold = sc->pcur ? v.p1 : v.p0;
+  double* __restrict__ pnew = sc->pcur ? v.p0 : v.p1;
+  for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kSpmvThreads)
+    pnew[i] = fma(beta, pold[i], v.z[i]);
+}
+
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_u1(int64_t n, int64_t nslices, Sell A, PcgVecs v, PcgScal* sc) {
+  if (sc->status != kRunning) return;
+  const bool first = sc->it == 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
+  // current p: at it 1 the start vector p0, later the buffer V1 just wrote
+  const int pc = first ? sc->pcur : (sc->pcur ^ 1);
+  const double* __restrict__ p = pc ? v.p1 : v.p0;
+  const double* __restrict__ r = sc->rcur ? v.r1 : v.r0;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t s = w0; s < nslices; s += nw) {
+    const double q = sell_row(A, s, lane, [&](int32_t j) { return __ldg(p + j); });
+    const int64_t i = s * kSell + lane;
+    if (i < n) {
+      v.q[i] = q;
+      const double pi = p[i];
+      acc[0] = fma(pi, q, acc[0]);
+      if (first) {
+        const double ri = r[i];
+        acc[1] = fma(pi, ri, acc[1]);
+        acc[2] = fma(ri, ri, acc[2]);
+      }
+    }
+  }
+  grid_finalize<3>(acc, v.partials, &sc->ticket1, [&](double (&tot)[3]) {
+    double rho;
+    const double delta = tot[0];
+    if (first) {
+      rho = tot[1];
+      sc->rho = rho;
+      sc->norm0 = sqrt(tot[2]);
+      sc->it = 1;
+      if (sc->norm0 == 0.0) { sc->norm = 0.0; sc->status = kConverged; return; }
+    } else {
+      rho = sc->rho;
+      sc->it += 1;
+      sc->pcur ^= 1;
+    }
+    if (!isfinite(delta) || !isfinite(rho)) { sc->status = kDivergence; return; }
+    if (delta <= 0.0) {
+      if (rho == 0.0) {
+        if (first) sc->norm = sc->norm0;
+        sc->status = kConverged;
+      } else {
+        sc->aux = delta;
+        sc->status = kBreakdown;
+      }
+      return;
+    }
+    sc->lambda = rho / delta;
+  });
+}
+
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_v2(int64_t n, PcgVecs v, const PcgScal* sc) {
+  if (sc->status != kRunning) return;
+  const double lambda = sc->lambda;
+  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
+  const double* __restrict__ rold = sc->rcur ? v.r1 : v.r0;
+  double* __restrict__ rnew = sc->rcur ? v.r0 : v.r1;
+  for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kSpmvThreads) {
+    rnew[i] = fma(-lambda, v.q[i], rold[i]);
+    v.x[i] = fma(lambda, p[i], v.x[i]);
+  }
+}
+
+template <bool HAS_M>
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_u2(int64_t n, int64_t nslices, Sell M, PcgVecs v, PcgScal* sc) {
+  if (sc->status != kRunning) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
+  const double* __restrict__ rnew = sc->rcur ? v.r0 : v.r1;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t s = w0; s < nslices; s += nw) {
+    double zi = 0.0;
+    if (HAS_M) zi = sell_row(M, s, lane, [&](int32_t j) { return __ldg(rnew + j); });
+    const int64_t i = s * kSell + lane;
+    if (i < n) {
+      const double rn = rnew[i];
+      if (!HAS_M) zi = rn;
+      v.z[i] = zi;
+      acc[0] = fma(zi, rn, acc[0]);
+      acc[1] = fma(rn, rn, acc[1]);
+    }
+  }
+  grid_finalize<2>(acc, v.partials, &sc->ticket2, [&](double (&tot)[2]) {
+    const double rho_new = tot[0], rr = tot[1];
+    sc->rcur ^= 1;
+    if (!isfinite(rho_new) || !isfinite(rr)) { sc->status = kDivergence; return; }
+    const double norm = sqrt(rr);
+    v.hist[sc->it - 1] = norm;
+    sc->norm = norm;
+    sc->beta = rho_new / sc->rho;
+    sc->rho = rho_new;
+    if (norm <= sc->tol * sc->norm0) sc->status = kConverged;
+    else if (sc->it >= sc->maxit) sc->status = kMaxit;
+  });
+}
+
 // start: r = b - A x0 (or b), p = M r (or r)
 template <bool HAS_X0>
 __global__ void __launch_bounds__(kSpmvThreads)
@@ -198,7 +316,8 @@ struct spai_pcg {
   double* b = nullptr;
   PcgScal* sc = nullptr;
   PcgScal* host_init = nullptr;
-  unsigned blocks1 = 1, blocks2 = 1;
+  unsigned blocks1 = 1, blocks2 = 1, vblocks = 1;
+  bool fused = false;   // measured on B200: 4 single-gather kernels beat 2 double-gather ones
   cudaGraphExec_t graph = nullptr;
 };
 
@@ -211,6 +330,15 @@ extern "C" size_t spai_pcg_workspace_bytes(int64_t n, int64_t maxit) {
 }
 
 static int launch_iteration(spai_pcg* s) {
+  if (!s->fused) {
+    pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+    pcg_u1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v, s->sc);
+    pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+    if (s->hasM) pcg_u2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
+    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
+    SPAI_LAUNCH_CHECK("pcg unfused iteration");
+    return SPAI_OK;
+  }
   pcg_k1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v, s->sc);
   SPAI_LAUNCH_CHECK("pcg_k1");
   if (s->hasM) pcg_k2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
@@ -250,6 +378,12 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
   const unsigned need = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need64, 1 << 30));
   s->blocks1 = std::min(b1, need);
   s->blocks2 = std::min(s->hasM ? b2t : b2f, need);
+  s->vblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kSpmvThreads - 1) / kSpmvThreads,
+                                                                (int64_t)num_sms() * 8));
+  {
+    const char* e = getenv("SPAI_PCG_FUSED");
+    if (e && *e) s->fused = *e != '0';
+  }
   if (std::max(s->blocks1, s->blocks2) > (unsigned)num_sms() * 32) {
     set_error("grid larger than the partials buffer");
     delete s;
@@ -266,6 +400,12 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
   s->sc = (PcgScal*)p;
   s->host_init = new PcgScal();
   *out = s;
+  return SPAI_OK;
+}
+
+extern "C" int spai_pcg_set_fused(spai_pcg* s, int fused) {
+  if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
+  s->fused = fused != 0;
   return SPAI_OK;
 }
 

@@ -244,6 +244,9 @@ class DevicePCG:
         self.h = h
         self.launched = 0
 
+    def set_fused(self, fused: bool):
+        _lib.check(self.lib.spai_pcg_set_fused(self.h, 1 if fused else 0), "spai_pcg_set_fused")
+
     def start(self, b, x0=None):
         _lib.check(self.lib.spai_pcg_start(self.h, ptr(b), ptr(x0) if x0 is not None
                                            else C.c_void_p(0)), "spai_pcg_start")

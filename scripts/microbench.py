@@ -53,6 +53,7 @@ with torch.cuda.stream(s):
     t = timed(lambda: A.matvec_tma(x, out=y), 20)
     out["spmv_tma_ms"], out["spmv_tma_gbs"] = t, sp / t / 1e6
     out["sell_layout_ms"] = timed(lambda: DeviceCsr(n, n, A.rowptr, A.colidx, A.vals).sell_values(), 2)
+    out["csc_values_ms"] = timed(lambda: DeviceCsr(n, n, A.rowptr, A.colidx, A.vals, structure_of=A).csc_values(), 2)
     A.sell_values()
     t = timed(lambda: A.matvec_sell(x, out=y), 20)
     out["spmv_sell_ms"], out["spmv_sell_gbs"] = t, sp / t / 1e6
@@ -67,6 +68,18 @@ with torch.cuda.stream(s):
     e1.record(s)
     e1.synchronize()
     t = e0.elapsed_time(e1) / 256
+    for fused in (False, True):
+        pu = DevicePCG(A, S, 1e-30, 100000)
+        pu.set_fused(fused)
+        pu.start(b)
+        pu.advance(64)
+        torch.cuda.synchronize()
+        e0.record(s)
+        pu.advance(128)
+        e1.record(s)
+        e1.synchronize()
+        out[f"pcg_iter_ms_fused{int(fused)}"] = e0.elapsed_time(e1) / 128
+        pu.close()
     st = pcg.poll()
     b_it = 24 * nnz + 16 * (n + 1) + 88 * n
     out["pcg_iter_ms"], out["pcg_gbs"], out["pcg_status"] = t, b_it / t / 1e6, st[:2]
