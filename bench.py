@@ -243,7 +243,9 @@ def run_ours(args):
     t_asm = statistics.mean(t for t, _, _ in times)
     t_sol = statistics.mean(t for _, t, _ in times)
     hbm, peak_kind = peaks()
-    b_it = 24 * nnz + 88 * n
+    # algorithmic bytes of one reference PCG iteration (krylov.py:315-339):
+    # A.p and M.r (12 B/stored entry + x gather 8 + y write 8 each) + vector updates
+    b_it = 24 * nnz + 104 * n
     solve_gbs = b_it * its / t_sol / 1e9
 
     # ---- SpMV alone (K5 plain and TMA-staged) with CUDA events
