@@ -168,6 +168,12 @@ int spai_sell_fill_vals(int64_t n, const int64_t* rowptr, const double* csr_vals
                         const int64_t* sliceptr, double* vals, void* stream);
 int spai_sell_spmv(int64_t n, const int64_t* sliceptr, const int32_t* cols,
                    const double* vals, const double* x, double* y, void* stream);
+/* TMA-staged SELL-32 SpMV: one persistent CTA of 8 warps per SM, each warp
+ * streams its slices with cp.async.bulk into a 2-stage shared-memory ring.
+ * wmax = widest slice (in slots); needs 8*2*wmax*384 B <= 200 KB.          */
+int spai_sell_spmv_tma(int64_t n, const int64_t* sliceptr, const int32_t* cols,
+                       const double* vals, int wmax, const double* x, double* y,
+                       void* stream);
 
 /* ------------------------------------------------------------------ K8
  * Device-resident classic PCG (replaces _solve_classic, krylov.py:301-345)
@@ -186,6 +192,8 @@ int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
  * kernels, one gather per stored entry); 1: 2 kernels (vector updates
  * recomputed inside the SpMV gathers).  Same arithmetic, same results.    */
 int spai_pcg_set_fused(spai_pcg* s, int fused);
+/* 1 (default when the widest slice fits): U1/U2 stream SELL slices with TMA. */
+int spai_pcg_set_tma(spai_pcg* s, int tma);
 /* Start from x0 (device, may be NULL -> zero); b device, copied.          */
 int spai_pcg_start(spai_pcg* s, const double* b, const double* x0);
 /* Enqueue up to `iters` more iterations (no host sync; CUDA graphs of 16). */

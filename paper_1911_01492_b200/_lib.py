@@ -65,10 +65,12 @@ _SIGS = {
     "spai_sell_fill_cols": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "spai_sell_fill_vals": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "spai_sell_spmv": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_sell_spmv_tma": (_i32, [_i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "spai_pcg_workspace_bytes": (_sz, [_i64, _i64]),
     "spai_pcg_create": (_i32, [C.POINTER(_vp), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl,
                                _i64, _vp, _sz, _vp]),
     "spai_pcg_set_fused": (_i32, [_vp, _i32]),
+    "spai_pcg_set_tma": (_i32, [_vp, _i32]),
     "spai_pcg_start": (_i32, [_vp, _vp, _vp]),
     "spai_pcg_advance": (_i32, [_vp, _i64]),
     "spai_pcg_poll": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),

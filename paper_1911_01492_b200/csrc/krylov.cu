@@ -267,6 +267,102 @@ pcg_u2(int64_t n, int64_t nslices, Sell M, PcgVecs v, PcgScal* sc) {
   });
 }
 
+// ---- TMA-staged versions of U1 / U2 (persistent: one CTA of 8 warps per SM)
+__global__ void __launch_bounds__(kTmaWarps * 32)
+pcg_u1_tma(int64_t n, int64_t nslices, Sell A, int wmax, PcgVecs v, PcgScal* sc) {
+  if (sc->status != kRunning) return;
+  extern __shared__ __align__(128) unsigned char tsm[];
+  const bool first = sc->it == 0;
+  const int lane = threadIdx.x & 31;
+  const int pc = first ? sc->pcur : (sc->pcur ^ 1);
+  const double* __restrict__ p = pc ? v.p1 : v.p0;
+  const double* __restrict__ r = sc->rcur ? v.r1 : v.r0;
+  double acc[3] = {0.0, 0.0, 0.0};
+  sell_tma_loop(nslices, A, wmax, tsm + (threadIdx.x >> 5) * SellTmaSmem::warp_bytes(wmax),
+                [&](int32_t j) { return __ldg(p + j); },
+                [&](int64_t s, double q) {
+                  const int64_t i = s * kSell + lane;
+                  if (i < n) {
+                    v.q[i] = q;
+                    const double pi = p[i];
+                    acc[0] = fma(pi, q, acc[0]);
+                    if (first) {
+                      const double ri = r[i];
+                      acc[1] = fma(pi, ri, acc[1]);
+                      acc[2] = fma(ri, ri, acc[2]);
+                    }
+                  }
+                });
+  grid_finalize<3>(acc, v.partials, &sc->ticket1, [&](double (&tot)[3]) {
+    double rho;
+    const double delta = tot[0];
+    if (first) {
+      rho = tot[1];
+      sc->rho = rho;
+      sc->norm0 = sqrt(tot[2]);
+      sc->it = 1;
+      if (sc->norm0 == 0.0) { sc->norm = 0.0; sc->status = kConverged; return; }
+    } else {
+      rho = sc->rho;
+      sc->it += 1;
+      sc->pcur ^= 1;
+    }
+    if (!isfinite(delta) || !isfinite(rho)) { sc->status = kDivergence; return; }
+    if (delta <= 0.0) {
+      if (rho == 0.0) {
+        if (first) sc->norm = sc->norm0;
+        sc->status = kConverged;
+      } else {
+        sc->aux = delta;
+        sc->status = kBreakdown;
+      }
+      return;
+    }
+    sc->lambda = rho / delta;
+  });
+}
+
+__global__ void __launch_bounds__(kTmaWarps * 32)
+pcg_u2_tma(int64_t n, int64_t nslices, Sell M, int wmax, PcgVecs v, PcgScal* sc) {
+  if (sc->status != kRunning) return;
+  extern __shared__ __align__(128) unsigned char tsm[];
+  const int lane = threadIdx.x & 31;
+  const double* __restrict__ rnew = sc->rcur ? v.r0 : v.r1;
+  double acc[2] = {0.0, 0.0};
+  sell_tma_loop(nslices, M, wmax, tsm + (threadIdx.x >> 5) * SellTmaSmem::warp_bytes(wmax),
+                [&](int32_t j) { return __ldg(rnew + j); },
+                [&](int64_t s, double zi) {
+                  const int64_t i = s * kSell + lane;
+                  if (i < n) {
+                    const double rn = rnew[i];
+                    v.z[i] = zi;
+                    acc[0] = fma(zi, rn, acc[0]);
+                    acc[1] = fma(rn, rn, acc[1]);
+                  }
+                });
+  grid_finalize<2>(acc, v.partials, &sc->ticket2, [&](double (&tot)[2]) {
+    const double rho_new = tot[0], rr = tot[1];
+    sc->rcur ^= 1;
+    if (!isfinite(rho_new) || !isfinite(rr)) { sc->status = kDivergence; return; }
+    const double norm = sqrt(rr);
+    v.hist[sc->it - 1] = norm;
+    sc->norm = norm;
+    sc->beta = rho_new / sc->rho;
+    sc->rho = rho_new;
+    if (norm <= sc->tol * sc->norm0) sc->status = kConverged;
+    else if (sc->it >= sc->maxit) sc->status = kMaxit;
+  });
+}
+
+__global__ void width_max_kernel(int64_t nslices, const int64_t* sliceptr, int* out) {
+  int m = 0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices;
+       s += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (int)((sliceptr[s + 1] - sliceptr[s]) >> 5));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // start: r = b - A x0 (or b), p = M r (or r)
 template <bool HAS_X0>
 __global__ void __launch_bounds__(kSpmvThreads)
@@ -318,6 +414,9 @@ struct spai_pcg {
   PcgScal* host_init = nullptr;
   unsigned blocks1 = 1, blocks2 = 1, vblocks = 1;
   bool fused = false;   // measured on B200: 4 single-gather kernels beat 2 double-gather ones
+  bool tma = false;     // TMA-staged SELL slices (set when the stage fits in smem)
+  int wmaxA = 0, wmaxM = 0;
+  size_t smemA = 0, smemM = 0;
   cudaGraphExec_t graph = nullptr;
 };
 
@@ -330,6 +429,16 @@ extern "C" size_t spai_pcg_workspace_bytes(int64_t n, int64_t maxit) {
 }
 
 static int launch_iteration(spai_pcg* s) {
+  if (!s->fused && s->tma) {
+    const unsigned g = (unsigned)num_sms();
+    pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+    pcg_u1_tma<<<g, kTmaWarps * 32, s->smemA, s->stream>>>(s->n, s->nslices, s->A, s->wmaxA, s->v, s->sc);
+    pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+    if (s->hasM) pcg_u2_tma<<<g, kTmaWarps * 32, s->smemM, s->stream>>>(s->n, s->nslices, s->M, s->wmaxM, s->v, s->sc);
+    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
+    SPAI_LAUNCH_CHECK("pcg unfused TMA iteration");
+    return SPAI_OK;
+  }
   if (!s->fused) {
     pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
     pcg_u1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v, s->sc);
@@ -384,6 +493,29 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
     const char* e = getenv("SPAI_PCG_FUSED");
     if (e && *e) s->fused = *e != '0';
   }
+  {  // TMA staging: needs the widest slice of A (and M) to fit a 2-stage ring per warp
+    int* d = nullptr;
+    SPAI_CUDA(cudaMalloc(&d, 2 * sizeof(int)));
+    SPAI_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(int), s->stream));
+    const unsigned wb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((s->nslices + 255) / 256, num_sms() * 8));
+    width_max_kernel<<<wb, 256, 0, s->stream>>>(s->nslices, s->A.sliceptr, d);
+    if (s->hasM) width_max_kernel<<<wb, 256, 0, s->stream>>>(s->nslices, s->M.sliceptr, d + 1);
+    int h[2] = {0, 0};
+    SPAI_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
+    SPAI_CUDA(cudaStreamSynchronize(s->stream));
+    SPAI_CUDA(cudaFree(d));
+    s->wmaxA = std::max(h[0], 1);
+    s->wmaxM = std::max(h[1], 1);
+    s->smemA = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(s->wmaxA);
+    s->smemM = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(s->wmaxM);
+    const char* e = getenv("SPAI_PCG_TMA");
+    const bool want = !(e && *e == '0');
+    s->tma = want && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024 && s->nslices >= 148 * 8;
+    if (s->tma) {
+      SPAI_CUDA(cudaFuncSetAttribute(pcg_u1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemA));
+      SPAI_CUDA(cudaFuncSetAttribute(pcg_u2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemM));
+    }
+  }
   if (std::max(s->blocks1, s->blocks2) > (unsigned)num_sms() * 32) {
     set_error("grid larger than the partials buffer");
     delete s;
@@ -406,6 +538,12 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
 extern "C" int spai_pcg_set_fused(spai_pcg* s, int fused) {
   if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
   s->fused = fused != 0;
+  return SPAI_OK;
+}
+
+extern "C" int spai_pcg_set_tma(spai_pcg* s, int tma) {
+  if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
+  s->tma = tma != 0 && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024;
   return SPAI_OK;
 }
 

@@ -42,3 +42,85 @@ __device__ __forceinline__ double sell_row(const Sell& A, int64_t s, int lane, c
 }
 
 }  // namespace spai
+
+namespace spai {
+
+// ---- TMA-staged SELL-32: every warp owns a 2-stage shared-memory ring; lane 0
+// streams whole slices (values + column indices are contiguous per slice) with
+// cp.async.bulk (SASS UBLKCP) while the warp gathers x for the previous slice.
+// The TMA engine keeps ~2 slices per warp in flight without register cost.
+constexpr int kTmaWarps = 8;        // warps per CTA (one persistent CTA per SM)
+constexpr int kTmaStages = 2;
+
+struct SellTmaSmem {
+  // per warp: [mbar x kTmaStages][vals stage x kTmaStages][cols stage x kTmaStages]
+  static __host__ __device__ size_t stage_vals(int wmax) { return (size_t)wmax * kSell * 8; }
+  static __host__ __device__ size_t stage_cols(int wmax) { return (size_t)wmax * kSell * 4; }
+  static __host__ __device__ size_t warp_bytes(int wmax) {
+    return 64 + kTmaStages * (stage_vals(wmax) + stage_cols(wmax));
+  }
+};
+
+// Calls epi(s, acc) for every slice s of this warp (acc = this lane's row sum).
+template <class XF, class EPI>
+__device__ __forceinline__ void sell_tma_loop(int64_t nslices, const Sell& A, int wmax,
+                                              unsigned char* wbase, const XF& xf, const EPI& epi) {
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  uint64_t* full = reinterpret_cast<uint64_t*>(wbase);
+  double* sv0 = reinterpret_cast<double*>(wbase + 64);
+  const size_t svb = SellTmaSmem::stage_vals(wmax), scb = SellTmaSmem::stage_cols(wmax);
+  double* sv[kTmaStages];
+  int32_t* sc[kTmaStages];
+#pragma unroll
+  for (int st = 0; st < kTmaStages; ++st) {
+    sv[st] = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(sv0) + st * svb);
+    sc[st] = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(sv0) + kTmaStages * svb + st * scb);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int64_t s, int st) {
+    const int64_t off = A.sliceptr[s];
+    const uint32_t cnt = (uint32_t)(A.sliceptr[s + 1] - off);
+    mbar_arrive_expect_tx(&full[st], cnt * 12u);
+    bulk_g2s(sv[st], A.vals + off, cnt * 8u, &full[st]);
+    bulk_g2s(sc[st], A.cols + off, cnt * 4u, &full[st]);
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < kTmaStages; ++st)
+      if (gw + st * nw < nslices) issue(gw + st * nw, st);
+  }
+  int i = 0;
+  for (int64_t s = gw; s < nslices; s += nw, ++i) {
+    const int st = i % kTmaStages;
+    const uint32_t phase = (uint32_t)((i / kTmaStages) & 1);
+    const int wdt = (int)((A.sliceptr[s + 1] - A.sliceptr[s]) >> 5);
+    mbar_wait(&full[st], phase);
+    const double* __restrict__ v = sv[st] + lane;
+    const int32_t* __restrict__ c = sc[st] + lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    int k = 0;
+    for (; k + 3 <= wdt; k += 3) {
+      const int32_t c0 = c[(k + 0) * kSell], c1 = c[(k + 1) * kSell], c2 = c[(k + 2) * kSell];
+      a0 = fma(v[(k + 0) * kSell], xf(c0), a0);
+      a1 = fma(v[(k + 1) * kSell], xf(c1), a1);
+      a2 = fma(v[(k + 2) * kSell], xf(c2), a2);
+    }
+    for (; k < wdt; ++k) a0 = fma(v[k * kSell], xf(c[k * kSell]), a0);
+    __syncwarp();                              // stage fully consumed by the warp
+    if (lane == 0 && s + kTmaStages * nw < nslices) {
+      fence_proxy_async();
+      issue(s + kTmaStages * nw, st);
+    }
+    epi(s, (a0 + a1) + a2);
+  }
+}
+
+}  // namespace spai

@@ -244,6 +244,9 @@ class DevicePCG:
         self.h = h
         self.launched = 0
 
+    def set_tma(self, tma: bool):
+        _lib.check(self.lib.spai_pcg_set_tma(self.h, 1 if tma else 0), "spai_pcg_set_tma")
+
     def set_fused(self, fused: bool):
         _lib.check(self.lib.spai_pcg_set_fused(self.h, 1 if fused else 0), "spai_pcg_set_fused")
 

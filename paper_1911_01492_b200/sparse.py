@@ -148,10 +148,10 @@ class CsrMatrix:
 
 
 class _PatternCache:
-    __slots__ = ("csc", "sym", "tiles", "sell")
+    __slots__ = ("csc", "sym", "tiles", "sell", "sell_wmax")
 
     def __init__(self):
-        self.csc = self.sym = self.tiles = self.sell = None
+        self.csc = self.sym = self.tiles = self.sell = self.sell_wmax = None
 
 
 class DeviceCsr:
@@ -307,6 +307,30 @@ class DeviceCsr:
         _lib.check(_lib.load().spai_sell_spmv(self.nrows, ptr(sliceptr), ptr(cols), ptr(vals),
                                               ptr(x.contiguous()), ptr(out), stream_handle()),
                    "spai_sell_spmv")
+        return out
+
+    def sell_width(self) -> int:
+        """Widest SELL-32 slice in slots (cached per pattern)."""
+        sliceptr, _ = self.sell()
+        if getattr(self._pat, "sell_wmax", None) is None:
+            self._pat.sell_wmax = int(((sliceptr[1:] - sliceptr[:-1]) // 32).max().item()) \
+                if sliceptr.numel() > 1 else 1
+        return self._pat.sell_wmax
+
+    def matvec_sell_tma(self, x, out=None):
+        """y = A x with the TMA-staged SELL-32 kernel."""
+        torch = _require_cuda()
+        if x.numel() != self.ncols:
+            raise DimensionMismatchError(
+                f"spmv: {self.ncols} columns vs vector of {x.numel()}")
+        if out is None:
+            out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
+        sliceptr, cols = self.sell()
+        vals = self.sell_values()
+        _lib.check(_lib.load().spai_sell_spmv_tma(self.nrows, ptr(sliceptr), ptr(cols), ptr(vals),
+                                                  self.sell_width(), ptr(x.contiguous()),
+                                                  ptr(out), stream_handle()),
+                   "spai_sell_spmv_tma")
         return out
 
     def tiles(self):

@@ -68,9 +68,12 @@ with torch.cuda.stream(s):
     e1.record(s)
     e1.synchronize()
     t = e0.elapsed_time(e1) / 256
-    for fused in (False, True):
+    t = timed(lambda: A.matvec_sell_tma(x, out=y), 20)
+    out["spmv_sell_tma_ms"], out["spmv_sell_tma_gbs"] = t, sp / t / 1e6
+    for fused, tma in ((False, True), (False, False), (True, False)):
         pu = DevicePCG(A, S, 1e-30, 100000)
         pu.set_fused(fused)
+        pu.set_tma(tma)
         pu.start(b)
         pu.advance(64)
         torch.cuda.synchronize()
@@ -78,7 +81,7 @@ with torch.cuda.stream(s):
         pu.advance(128)
         e1.record(s)
         e1.synchronize()
-        out[f"pcg_iter_ms_fused{int(fused)}"] = e0.elapsed_time(e1) / 128
+        out[f"pcg_iter_ms_fused{int(fused)}_tma{int(tma)}"] = e0.elapsed_time(e1) / 128
         pu.close()
     st = pcg.poll()
     b_it = 24 * nnz + 16 * (n + 1) + 88 * n

@@ -297,7 +297,7 @@ def test_spmv_matches_oracle():
         assert np.max(np.abs(y - yr)) <= tol
         dA = A.device()
         xd = torch.from_numpy(x).cuda()
-        for y2 in (dA.matvec_sell(xd), dA.matvec_tma(xd)):
+        for y2 in (dA.matvec_sell(xd), dA.matvec_tma(xd), dA.matvec_sell_tma(xd)):
             assert np.max(np.abs(y2.cpu().numpy() - yr)) <= tol
     with pytest.raises(pb.DimensionMismatchError):
         pb.spmv(A, np.ones(A.ncols + 1))
@@ -429,3 +429,29 @@ def test_large_3d_spai_cg_properties():
     assert float(torch.linalg.norm(r)) <= 1e-7 * float(torch.linalg.norm(b))
     h = np.array(rec.residual_norms)
     assert h[-1] <= 1e-8 * rec.initial_residual
+
+
+def test_pcg_tma_and_ldg_paths_agree_with_oracle():
+    """At a size where U1/U2 take the TMA-staged SELL path (>= 1184 slices)."""
+    from paper_1911_01492_b200.krylov import DevicePCG
+    A = pb.q1_device((40, 40, 40))
+    S = pb.spai1_symmetric_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    hists = {}
+    for tma, fused in ((True, False), (False, False), (False, True)):
+        s = DevicePCG(A, S, 1e-8, 500)
+        s.set_fused(fused)
+        s.set_tma(tma)
+        s.start(b)
+        st = s.run()
+        assert st[0] == 1
+        hists[(tma, fused)] = s.history(st[1])
+        s.close()
+    ref = hists[(True, False)]
+    for k, h in hists.items():
+        assert len(h) == len(ref)
+        assert np.max(np.abs(h - ref) / ref) <= 1e-10, k
+    Ah, Sh = A.to_host(), S.to_host()
+    _, rr = oracle.pcg_classic(_ocsr(Ah), _ocsr(Sh), b.cpu().numpy(), tol=1e-8, maxit=500)
+    assert abs(rr.iterations - len(ref)) <= 1
+    assert _hist_rel(ref, rr.residual_norms) <= HIST_TOL
