@@ -108,6 +108,15 @@ int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
                   size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
                   void* stream);
 
+/* Same, restricted to the columns [c0, c1) (row-partitioned global SPAI:
+ * a rank assembles its owned columns plus one ghost plane on a local copy
+ * of A that carries three ghost planes).                                 */
+int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr,
+                        const int32_t* colidx, const double* vals,
+                        const int64_t* cscptr, const int32_t* cscrow,
+                        const int64_t* csc2csr, const double* cscval, int64_t c0,
+                        int64_t c1, double* m_csc, void* ws, size_t ws_bytes,
+                        int64_t* bad_col, int64_t* n_fallback, void* stream);
 /* Toggle the symbolic-plan replay (default on; env SPAI_NO_PLANS=1 disables):
  * columns with identical relative structure share one precomputed plan.   */
 int spai_set_assembly_plans(int enable);
@@ -207,6 +216,32 @@ int spai_pcg_history(spai_pcg* s, double* host_out, int64_t count);
 /* Device pointers of the state vectors (x, r, p, z).                      */
 int spai_pcg_vectors(spai_pcg* s, double** x, double** r, double** p, double** z);
 int spai_pcg_destroy(spai_pcg* s);
+
+/* ------------------------------------------------------------------ K8 multi-GPU
+ * Per-rank kernels of the row-partitioned PCG (replaces RankSystem,
+ * krylov.py:196-232, driving _solve_classic).  `xext` vectors are laid out
+ * [halo_lo | owned | halo_hi]; local SELL matrices index into them and the
+ * owned part starts at own_off.  mode: 0 y = A x; 1 U1 at iteration 1
+ * (out = [(p,q),(p,r),(r,r)]); 2 U1 (out = [(p,q)]); 3 U2 (out =
+ * [(z,r),(r,r)]); 4 U2 without preconditioner (z = r).  `out` receives this
+ * rank's partial sums; after an all-gather over ranks, reduce_step sums
+ * them in commsim's ascending-rank pairwise order (commsim.py:336-347) and
+ * runs the scalar recurrence (stage 1 after A p, stage 2 after M r).      */
+size_t spai_dist_scal_bytes(void);
+size_t spai_dist_partials_bytes(void);
+int spai_dist_scal_init(void* scal, double tol, int64_t maxit, void* stream);
+int spai_dist_scal_read(const void* scal, int* status, int64_t* it, double* norm0,
+                        double* norm, double* aux, void* stream);
+int spai_dist_spmv(int mode, int64_t n, const int64_t* sliceptr, const int32_t* cols,
+                   const double* vals, const double* xext, int64_t own_off, double* y,
+                   const double* raux, void* partials_ws, double* out,
+                   const void* scal, void* stream);
+int spai_dist_update_p(int64_t n, double* p, const double* z, const void* scal,
+                       void* stream);
+int spai_dist_update_xr(int64_t n, double* x, double* r, const double* p,
+                        const double* q, const void* scal, void* stream);
+int spai_dist_reduce_step(int nranks, const double* gathered, int K, int stage,
+                          void* scal, double* hist, void* stream);
 
 #ifdef __cplusplus
 }

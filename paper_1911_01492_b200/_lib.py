@@ -51,6 +51,17 @@ _SIGS = {
                              C.POINTER(_i64), C.POINTER(_i64), _vp]),
     "spai_csc_values": (_i32, [_i64, _vp, _vp, _vp, C.POINTER(_i32), _vp]),
     "spai_set_assembly_plans": (_i32, [_i32]),
+    "spai_assemble_range": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp,
+                                   _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "spai_dist_scal_bytes": (_sz, []),
+    "spai_dist_partials_bytes": (_sz, []),
+    "spai_dist_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),
+    "spai_dist_scal_read": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),
+                                   C.POINTER(_dbl), C.POINTER(_dbl), _vp]),
+    "spai_dist_spmv": (_i32, [_i32, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dist_update_p": (_i32, [_i64, _vp, _vp, _vp, _vp]),
+    "spai_dist_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dist_reduce_step": (_i32, [_i32, _vp, _i32, _i32, _vp, _vp, _vp]),
     "spai_csc_to_csr_values": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_symmetrize": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_csr_spmv": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 gram_hash_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
                  const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
                  double* __restrict__ m_csc, AsmWs ws, const int32_t* __restrict__ list,
-                 const int* __restrict__ nlist) {
+                 const int* __restrict__ nlist, int64_t c0) {
   using S = HashSmem<NJ, CAPL, MW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -139,10 +139,10 @@ gram_hash_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __re
 
   const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
-  const int64_t count = list ? (int64_t)*nlist : n;
+  const int64_t count = list ? (int64_t)*nlist : n - c0;
   for (int64_t f = gw; f < count; f += nw) {
     __syncwarp();
-    const int64_t k = list ? (int64_t)list[f] : f;
+    const int64_t k = list ? (int64_t)list[f] : c0 + f;
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
     if (nj == 0) { if (lane == 0) report(ws, k, kErrEmpty); continue; }
@@ -542,11 +542,11 @@ __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int
 // (A) signature of every column: hash of (nj, list lengths, relative rows)
 __global__ void __launch_bounds__(256)
 plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __restrict__ cscrow,
-                PlanWs pw) {
+                PlanWs pw, int64_t c0) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t k = w0; k < n; k += nw) {
+  for (int64_t k = c0 + w0; k < n; k += nw) {
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
     if (nj == 0 || nj > kPlanNJ) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
                    const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
                    const double* __restrict__ cscval, double* __restrict__ m_csc, AsmWs ws,
-                   PlanWs pw, int32_t* __restrict__ direct, int* __restrict__ ndirect) {
+                   PlanWs pw, int32_t* __restrict__ direct, int* __restrict__ ndirect, int64_t c0) {
   using S = ReplaySmem<NJ, CAPL>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -813,7 +813,7 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
   if (lane == 0) lval[kPadIdx] = 0.0;   // target of padding ops
   const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
-  for (int64_t k = gw; k < n; k += nw) {
+  for (int64_t k = c0 + gw; k < n; k += nw) {
     __syncwarp();
     const int slot = pw.plan_slot[k];
     const int pi = slot >= 0 ? pw.slot_plan[slot] : -1;
@@ -884,18 +884,19 @@ template <int NJ, int CAPL, int WARPS>
 static int launch_replay(int64_t n, const double* vals, const int64_t* cscptr,
                          const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
                          double* m_csc, AsmWs ws, PlanWs pw, int32_t* direct, int* ndirect,
-                         cudaStream_t s) {
+                         int64_t c0, cudaStream_t s) {
   const size_t smem = ReplaySmem<NJ, CAPL>::bytes * WARPS;
   auto kern = plan_replay_kernel<NJ, CAPL, WARPS>;
   SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SPAI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
   if (per_sm < 1) per_sm = 1;
-  int64_t blocks = (n + WARPS - 1) / WARPS;
+  int64_t blocks = (n - c0 + WARPS - 1) / WARPS;
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, WARPS * 32, smem, s>>>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc,
-                                                  ws, pw, direct, ndirect);
+                                                  ws, pw, direct, ndirect, c0);
   SPAI_LAUNCH_CHECK("plan_replay_kernel");
   return SPAI_OK;
 }
@@ -913,7 +914,7 @@ template <int NJ, int CAPL, int MW, int WARPS>
 static int launch_hash(int64_t n, const double* vals, const int64_t* cscptr,
                        const int32_t* cscrow, const int64_t* csc2csr, double* m_csc,
                        AsmWs ws, const int32_t* list, const int* nlist, int64_t count,
-                       cudaStream_t s) {
+                       int64_t c0, cudaStream_t s) {
   const size_t smem = HashSmem<NJ, CAPL, MW>::bytes * WARPS;
   auto kern = gram_hash_kernel<NJ, CAPL, MW, WARPS>;
   SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -925,7 +926,7 @@ static int launch_hash(int64_t n, const double* vals, const int64_t* cscptr,
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, WARPS * 32, smem, s>>>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws,
-                                                  list, nlist);
+                                                  list, nlist, c0);
   SPAI_LAUNCH_CHECK("gram_hash_kernel");
   return SPAI_OK;
 }
@@ -971,37 +972,39 @@ extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
 }
 
 template <int NJ, int CAPL, int MW, int WARPS>
-static int assemble_all(int64_t n, const double* vals, const int64_t* cscptr,
+static int assemble_all(int64_t c0, int64_t n, const double* vals, const int64_t* cscptr,
                         const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
                         double* m_csc, AsmWs ws, PlanWs pw, int32_t* direct, int* ndirect,
                         bool use_plans, cudaStream_t s) {
+  // columns [c0, n) are assembled (n is the end of the range here)
   int nd = 0;
+  const int64_t ncols = n - c0;
   if (use_plans) {
     SPAI_CUDA(cudaMemsetAsync(pw.keys, 0, (size_t)kPlanTable * 8, s));
-    plan_sig_kernel<<<(unsigned)std::min<int64_t>((n * 32 + 255) / 256, num_sms() * 8), 256, 0, s>>>(
-        n, cscptr, cscrow, pw);
+    plan_sig_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ncols * 32 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
+        n, cscptr, cscrow, pw, c0);
     SPAI_LAUNCH_CHECK("plan_sig_kernel");
     int np = 0;
     SPAI_CUDA(cudaMemcpyAsync(&np, pw.nplans, 4, cudaMemcpyDeviceToHost, s));
     SPAI_CUDA(cudaStreamSynchronize(s));
-    if (np > 0 && np <= kMaxPlans && (int64_t)np * 4 <= n) {
+    if (np > 0 && np <= kMaxPlans && (int64_t)np * 4 <= ncols) {
       const size_t bsm = sizeof(BuildSmem) * kBuildWarps;
       SPAI_CUDA(cudaFuncSetAttribute(plan_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
       plan_build_kernel<<<kPlanTable / kBuildWarps / 8, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw);
       SPAI_LAUNCH_CHECK("plan_build_kernel");
       constexpr int RNJ = NJ;
       int st = launch_replay<RNJ, CAPL, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
-                                          direct, ndirect, s);
+                                          direct, ndirect, c0, s);
       if (st) return st;
       SPAI_CUDA(cudaMemcpyAsync(&nd, ndirect, 4, cudaMemcpyDeviceToHost, s));
       SPAI_CUDA(cudaStreamSynchronize(s));
       if (nd == 0) return SPAI_OK;
       return launch_hash<NJ, CAPL, MW, WARPS>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, direct,
-                                              ndirect, nd, s);
+                                              ndirect, nd, 0, s);
     }
   }
   return launch_hash<NJ, CAPL, MW, WARPS>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, nullptr,
-                                          nullptr, n, s);
+                                          nullptr, ncols, c0, s);
 }
 
 }  // namespace spai
@@ -1015,18 +1018,20 @@ extern "C" int spai_set_assembly_plans(int enable) {
   return SPAI_OK;
 }
 
-extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
-                             const int32_t* colidx, const double* vals,
-                             const int64_t* cscptr, const int32_t* cscrow,
-                             const int64_t* csc2csr, const double* cscval_in, double* m_csc, void* wsp,
-                             size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
-                             void* stream) {
+extern "C" int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr,
+                                   const int32_t* colidx, const double* vals,
+                                   const int64_t* cscptr, const int32_t* cscrow,
+                                   const int64_t* csc2csr, const double* cscval_in,
+                                   int64_t c0, int64_t c1, double* m_csc, void* wsp,
+                                   size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
+                                   void* stream) {
   (void)rowptr; (void)colidx; (void)nnz;
+  if (c0 < 0 || c1 > n || c0 > c1) { set_error("bad column range [%lld, %lld)", (long long)c0, (long long)c1); return SPAI_E_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
   if (bad_col) *bad_col = -1;
   if (n_fallback) *n_fallback = 0;
-  if (n == 0) return SPAI_OK;
+  if (c1 == c0) return SPAI_OK;
   if (g_use_plans < 0) {
     const char* e = getenv("SPAI_NO_PLANS");
     g_use_plans = (e && *e && *e != '0') ? 0 : 1;
@@ -1063,10 +1068,10 @@ extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
   const double* cscval = cscval_in;   // NULL: values gathered through csc2csr
   const bool plans = g_use_plans == 1;
   int st;
-  if (hmax <= 8)       st = assemble_all<8, 64, 4, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
-  else if (hmax <= 16) st = assemble_all<16, 256, 4, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
-  else if (hmax <= 28) st = assemble_all<28, 784, 4, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
-  else                 st = assemble_all<32, 1024, 8, 4>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
+  if (hmax <= 8)       st = assemble_all<8, 64, 4, 8>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
+  else if (hmax <= 16) st = assemble_all<16, 256, 4, 8>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
+  else if (hmax <= 28) st = assemble_all<28, 784, 4, 8>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
+  else                 st = assemble_all<32, 1024, 8, 4>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
   if (st) return st;
   int counts[2] = {0, 0};
   SPAI_CUDA(cudaMemcpyAsync(counts, ws.nmerge, 8, cudaMemcpyDeviceToHost, s));
@@ -1101,6 +1106,16 @@ extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
     return SPAI_E_UNSUPPORTED;
   }
   return SPAI_OK;
+}
+
+extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
+                             const int32_t* colidx, const double* vals,
+                             const int64_t* cscptr, const int32_t* cscrow,
+                             const int64_t* csc2csr, const double* cscval, double* m_csc,
+                             void* ws, size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
+                             void* stream) {
+  return spai_assemble_range(n, nnz, rowptr, colidx, vals, cscptr, cscrow, csc2csr, cscval, 0, n,
+                             m_csc, ws, ws_bytes, bad_col, n_fallback, stream);
 }
 
 extern "C" int spai_csc_values(int64_t nnz, const int64_t* csc2csr, const double* vals,

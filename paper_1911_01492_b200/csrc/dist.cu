@@ -1,0 +1,241 @@
+// Row-partitioned (multi-GPU) classic PCG: the per-rank device kernels.
+//
+// Replaces RankSystem (krylov.py:196-232) + _solve_classic (krylov.py:301-345)
+// on one GPU per rank.  Vectors that are multiplied (p for A p, r for M r)
+// live in "extended" buffers [halo_lo | owned | halo_hi] so the local SpMV
+// reads the halo in place after the NCCL exchange; the local matrices use
+// column indices into that buffer.  Each reduction:
+//   spmv_dots -> per-rank partials (deterministic)  -> all_gather (NCCL)
+//   -> reduce_step: ascending-rank pairwise tree sum (commsim.py:336-347,
+//      so every rank sees bit-identical values) + the scalar recurrence.
+// Nothing synchronises with the host inside an iteration.
+#include "sell.cuh"
+#include "spmv_core.cuh"
+
+namespace spai {
+
+enum { dRunning = 0, dConverged = 1, dMaxit = 2, dBreakdown = 3, dDivergence = 4 };
+
+struct DistScal {
+  double rho, lambda, beta, norm0, norm, tol, aux;
+  long long it, maxit;
+  int status, pad0, pad1, pad2;
+  unsigned int ticket, pad3;
+};
+
+// MODE 0: plain y = A x;  1: U1 first iteration [(p,q),(p,r),(r,r)];
+// 2: U1 [(p,q)];  3: U2 [(z,r),(r,r)] with z = y, r = x;  4: U2 without M (z = r)
+template <int MODE>
+__global__ void __launch_bounds__(kSpmvThreads)
+dist_spmv_kernel(int64_t n, int64_t nslices, Sell A, const double* __restrict__ xext,
+                 int64_t own_off, double* __restrict__ y, const double* __restrict__ raux,
+                 double* partials, unsigned int* ticket, double* out, const DistScal* sc) {
+  if (MODE != 0 && sc->status != dRunning) return;
+  constexpr int K = MODE == 1 ? 3 : (MODE == 2 ? 1 : 2);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
+  const double* __restrict__ xo = xext + own_off;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  for (int64_t s = w0; s < nslices; s += nw) {
+    double v = 0.0;
+    if (MODE != 4) v = sell_row(A, s, lane, [&](int32_t j) { return __ldg(xext + j); });
+    const int64_t i = s * kSell + lane;
+    if (i < n) {
+      const double xi = xo[i];
+      if (MODE == 4) v = xi;
+      y[i] = v;
+      if (MODE == 1) {
+        const double ri = raux[i];
+        acc[0] = fma(xi, v, acc[0]);
+        acc[1] = fma(xi, ri, acc[1]);
+        acc[2] = fma(ri, ri, acc[2]);
+      } else if (MODE == 2) {
+        acc[0] = fma(xi, v, acc[0]);
+      } else if (MODE >= 3) {
+        acc[0] = fma(v, xi, acc[0]);
+        acc[1] = fma(xi, xi, acc[1]);
+      }
+    }
+  }
+  if (MODE == 0) return;
+  grid_finalize<K>(acc, partials, ticket, [&](double (&tot)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = tot[k];
+  });
+}
+
+// p = z + beta p (in place on the owned part), skipped at iteration 1
+__global__ void dist_update_p(int64_t n, double* __restrict__ p, const double* __restrict__ z,
+                              const DistScal* sc) {
+  if (sc->status != dRunning || sc->it == 0) return;
+  const double beta = sc->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+// x += lambda p, r -= lambda q (owned parts)
+__global__ void dist_update_xr(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                               const double* __restrict__ p, const double* __restrict__ q,
+                               const DistScal* sc) {
+  if (sc->status != dRunning) return;
+  const double lambda = sc->lambda;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    r[i] = fma(-lambda, q[i], r[i]);
+    x[i] = fma(lambda, p[i], x[i]);
+  }
+}
+
+// gathered[rank * K + k] -> commsim _tree_sum over ranks, then the scalar step.
+// stage 1 = after A p (K = 3 at it 1, else 1); stage 2 = after M r (K = 2).
+__global__ void dist_reduce_step(int nranks, const double* __restrict__ gathered, int K, int stage,
+                                 DistScal* sc, double* __restrict__ hist) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (sc->status != dRunning) return;
+  double tot[3];
+  for (int k = 0; k < K; ++k) {
+    double buf[64];
+    int m = nranks;
+    for (int r = 0; r < m; ++r) buf[r] = gathered[r * K + k];
+    while (m > 1) {                        // ((a+b)+(c+d))...: commsim.py:336-347
+      int o = 0;
+      for (int i = 0; i < m; i += 2) buf[o++] = (i + 1 < m) ? buf[i] + buf[i + 1] : buf[i];
+      m = o;
+    }
+    tot[k] = buf[0];
+  }
+  if (stage == 1) {
+    const bool first = sc->it == 0;
+    double rho;
+    const double delta = tot[0];
+    if (first) {
+      rho = tot[1];
+      sc->rho = rho;
+      sc->norm0 = sqrt(tot[2]);
+      sc->it = 1;
+      if (sc->norm0 == 0.0) { sc->norm = 0.0; sc->status = dConverged; return; }
+    } else {
+      rho = sc->rho;
+      sc->it += 1;
+    }
+    if (!isfinite(delta) || !isfinite(rho)) { sc->status = dDivergence; return; }
+    if (delta <= 0.0) {
+      if (rho == 0.0) {
+        if (first) sc->norm = sc->norm0;
+        sc->status = dConverged;
+      } else {
+        sc->aux = delta;
+        sc->status = dBreakdown;
+      }
+      return;
+    }
+    sc->lambda = rho / delta;
+  } else {
+    const double rho_new = tot[0], rr = tot[1];
+    if (!isfinite(rho_new) || !isfinite(rr)) { sc->status = dDivergence; return; }
+    const double norm = sqrt(rr);
+    hist[sc->it - 1] = norm;
+    sc->norm = norm;
+    sc->beta = rho_new / sc->rho;
+    sc->rho = rho_new;
+    if (norm <= sc->tol * sc->norm0) sc->status = dConverged;
+    else if (sc->it >= sc->maxit) sc->status = dMaxit;
+  }
+}
+
+unsigned sell_blocks(const void* kern, int64_t nslices);
+
+}  // namespace spai
+
+using namespace spai;
+
+extern "C" size_t spai_dist_scal_bytes(void) { return sizeof(DistScal); }
+
+extern "C" int spai_dist_scal_init(void* scal, double tol, int64_t maxit, void* stream) {
+  DistScal h{};
+  h.tol = tol;
+  h.maxit = maxit;
+  h.norm = INFINITY;
+  h.norm0 = NAN;
+  h.status = dRunning;
+  SPAI_CUDA(cudaMemcpyAsync(scal, &h, sizeof(h), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  SPAI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return SPAI_OK;
+}
+
+extern "C" int spai_dist_scal_read(const void* scal, int* status, int64_t* it, double* norm0,
+                                   double* norm, double* aux, void* stream) {
+  DistScal h;
+  SPAI_CUDA(cudaMemcpyAsync(&h, scal, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  SPAI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  *status = h.status;
+  *it = h.it;
+  *norm0 = h.norm0;
+  *norm = h.norm;
+  *aux = h.aux;
+  return SPAI_OK;
+}
+
+extern "C" size_t spai_dist_partials_bytes(void) {
+  return 256 + (size_t)num_sms() * 32 * 3 * sizeof(double);
+}
+
+extern "C" int spai_dist_spmv(int mode, int64_t n, const int64_t* sliceptr, const int32_t* cols,
+                              const double* vals, const double* xext, int64_t own_off, double* y,
+                              const double* raux, void* partials_ws, double* out,
+                              const void* scal, void* stream) {
+  const int64_t ns = (n + kSell - 1) / kSell;
+  if (ns == 0) {
+    if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
+    return SPAI_OK;
+  }
+  static unsigned blocks = 0;
+  if (!blocks) blocks = sell_blocks((const void*)dist_spmv_kernel<1>, 1 << 30);
+  const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (ns * 32 + 255) / 256));
+  unsigned int* ticket = (unsigned int*)partials_ws;
+  double* part = (double*)((char*)partials_ws + 256);
+  Sell A{sliceptr, cols, vals};
+  const DistScal* sc = (const DistScal*)scal;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (mode) {
+    case 0: dist_spmv_kernel<0><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 1: dist_spmv_kernel<1><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 2: dist_spmv_kernel<2><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 3: dist_spmv_kernel<3><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 4: dist_spmv_kernel<4><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    default: set_error("bad dist_spmv mode %d", mode); return SPAI_E_ARG;
+  }
+  SPAI_LAUNCH_CHECK("dist_spmv_kernel");
+  return SPAI_OK;
+}
+
+extern "C" int spai_dist_update_p(int64_t n, double* p, const double* z, const void* scal,
+                                  void* stream) {
+  if (n == 0) return SPAI_OK;
+  const unsigned b = (unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8);
+  dist_update_p<<<b, 256, 0, (cudaStream_t)stream>>>(n, p, z, (const DistScal*)scal);
+  SPAI_LAUNCH_CHECK("dist_update_p");
+  return SPAI_OK;
+}
+
+extern "C" int spai_dist_update_xr(int64_t n, double* x, double* r, const double* p,
+                                   const double* q, const void* scal, void* stream) {
+  if (n == 0) return SPAI_OK;
+  const unsigned b = (unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8);
+  dist_update_xr<<<b, 256, 0, (cudaStream_t)stream>>>(n, x, r, p, q, (const DistScal*)scal);
+  SPAI_LAUNCH_CHECK("dist_update_xr");
+  return SPAI_OK;
+}
+
+extern "C" int spai_dist_reduce_step(int nranks, const double* gathered, int K, int stage,
+                                     void* scal, double* hist, void* stream) {
+  if (nranks < 1 || nranks > 64) { set_error("nranks must be 1..64"); return SPAI_E_ARG; }
+  dist_reduce_step<<<1, 32, 0, (cudaStream_t)stream>>>(nranks, gathered, K, stage,
+                                                       (DistScal*)scal, hist);
+  SPAI_LAUNCH_CHECK("dist_reduce_step");
+  return SPAI_OK;
+}

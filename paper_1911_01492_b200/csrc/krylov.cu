@@ -509,7 +509,7 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
     s->smemA = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(s->wmaxA);
     s->smemM = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(s->wmaxM);
     const char* e = getenv("SPAI_PCG_TMA");
-    const bool want = !(e && *e == '0');
+    const bool want = e && *e == '1';   // measured slower than the LDG SELL path
     s->tma = want && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024 && s->nslices >= 148 * 8;
     if (s->tma) {
       SPAI_CUDA(cudaFuncSetAttribute(pcg_u1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemA));

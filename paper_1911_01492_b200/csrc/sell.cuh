@@ -97,21 +97,35 @@ __device__ __forceinline__ void sell_tma_loop(int64_t nslices, const Sell& A, in
     for (int st = 0; st < kTmaStages; ++st)
       if (gw + st * nw < nslices) issue(gw + st * nw, st);
   }
+  // slice offsets are prefetched one slice ahead so the refill is not stuck
+  // behind a dependent global load
+  int64_t off_next = gw < nslices ? A.sliceptr[gw] : 0;
+  int64_t end_next = gw < nslices ? A.sliceptr[gw + 1] : 0;
   int i = 0;
   for (int64_t s = gw; s < nslices; s += nw, ++i) {
     const int st = i % kTmaStages;
     const uint32_t phase = (uint32_t)((i / kTmaStages) & 1);
-    const int wdt = (int)((A.sliceptr[s + 1] - A.sliceptr[s]) >> 5);
+    const int wdt = (int)((end_next - off_next) >> 5);
+    if (s + nw < nslices) { off_next = A.sliceptr[s + nw]; end_next = A.sliceptr[s + nw + 1]; }
     mbar_wait(&full[st], phase);
     const double* __restrict__ v = sv[st] + lane;
     const int32_t* __restrict__ c = sc[st] + lane;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     int k = 0;
-    for (; k + 3 <= wdt; k += 3) {
-      const int32_t c0 = c[(k + 0) * kSell], c1 = c[(k + 1) * kSell], c2 = c[(k + 2) * kSell];
-      a0 = fma(v[(k + 0) * kSell], xf(c0), a0);
-      a1 = fma(v[(k + 1) * kSell], xf(c1), a1);
-      a2 = fma(v[(k + 2) * kSell], xf(c2), a2);
+    // 9 independent gathers in flight per lane (27 = 3 x 9 for the 3D stencil)
+    for (; k + 9 <= wdt; k += 9) {
+      int32_t cc[9];
+      double xv[9];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) cc[u] = c[(k + u) * kSell];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) xv[u] = xf(cc[u]);
+#pragma unroll
+      for (int u = 0; u < 9; u += 3) {
+        a0 = fma(v[(k + u) * kSell], xv[u], a0);
+        a1 = fma(v[(k + u + 1) * kSell], xv[u + 1], a1);
+        a2 = fma(v[(k + u + 2) * kSell], xv[u + 2], a2);
+      }
     }
     for (; k < wdt; ++k) a0 = fma(v[k * kSell], xf(c[k * kSell]), a0);
     __syncwarp();                              // stage fully consumed by the warp

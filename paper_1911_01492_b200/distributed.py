@@ -1,0 +1,398 @@
+"""Row-partitioned multi-GPU SPAI(1)-PCG (one process per GPU, NCCL).
+
+Replaces the reference's simulated multi-rank path: `partition_1d_strips`
+(grids.py:99-139), `extract_local_system` (grids.py:142-158), `RankSystem`
+(krylov.py:196-232), `fused_allreduce` / `_tree_sum` (commsim.py:578-585,
+336-347) and `halo_exchange` (commsim.py:588-596) driving `_solve_classic`
+(krylov.py:301-345).
+
+* Partition: contiguous slabs of whole grid planes (y-lines in 2D, z-planes
+  in 3D), heights differing by at most one plane, extra planes to the lowest
+  ranks (grids.py:112-118).
+* Vectors that get multiplied live in extended buffers
+  [halo_lo | owned | halo_hi] (one plane per side); the halo is refreshed
+  with NCCL send/recv before every SpMV.
+* Reductions: each rank's partial sums (deterministic kernel) are
+  all-gathered and summed on the device in the reference's ascending-rank
+  pairwise order, so every rank -- and every rank count -- sees
+  bit-identical scalars, as in commsim.py:336-347.
+* SPAI(1) scope:
+  - "global" (default): the result equals single-GPU SPAI(1).  Each rank
+    generates A on its slab plus three ghost planes, assembles the columns
+    of its slab plus one ghost plane (spai_assemble_range) and symmetrises;
+    no communication besides the solve.
+  - "block_local": the reference multi-rank semantics, M = spai1(A_FF) of
+    the owned block (cli.py:239-240), so iteration counts depend on P.
+
+The per-rank compute is a backend object; `GpuBackend` calls the C-ABI
+kernels.  Tests drive the same orchestration with a CPU test double over
+gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import BreakdownError, DivergenceError, InvalidPartitionError
+from .krylov import ConvergenceRecord
+
+
+# ------------------------------------------------------------------ partition
+@dataclass
+class SlabPartition:
+    """Contiguous plane slabs (grids.py:99-139 rule, along the slowest axis)."""
+
+    nplanes: int
+    plane: int          # rows per plane
+    nranks: int
+
+    def __post_init__(self):
+        if self.nranks < 1:
+            raise InvalidPartitionError("need at least one rank")
+        if self.nranks > self.nplanes:
+            raise InvalidPartitionError(
+                f"cannot split {self.nplanes} grid rows into {self.nranks} strips")
+
+    def planes(self, rank: int):
+        base, extra = divmod(self.nplanes, self.nranks)
+        lo = rank * base + min(rank, extra)
+        return lo, lo + base + (1 if rank < extra else 0)
+
+    def rows(self, rank: int):
+        lo, hi = self.planes(rank)
+        return lo * self.plane, hi * self.plane
+
+    def halo(self, rank: int):
+        """(rows below, rows above) this rank needs: one plane per neighbour."""
+        return (self.plane if rank > 0 else 0,
+                self.plane if rank < self.nranks - 1 else 0)
+
+
+# ------------------------------------------------------------------ comm
+class TorchComm:
+    """torch.distributed plumbing: all-gather of partial sums, plane halos."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.size = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.reductions = 0
+        # gloo cannot move CUDA tensors point-to-point: stage through the host
+        # (used only to exercise the multi-rank GPU path on a single device)
+        self.stage = dist.is_initialized() and dist.get_backend(group) == "gloo"
+
+    def allgather(self, out, gathered):
+        """gathered[r*K:(r+1)*K] = out of rank r (K = out.numel())."""
+        self.reductions += 1
+        if self.size == 1:
+            gathered.copy_(out)
+            return
+        if self.stage and out.is_cuda:
+            g = gathered.cpu()
+            self.dist.all_gather_into_tensor(g, out.cpu(), group=self.group)
+            gathered.copy_(g)
+            return
+        self.dist.all_gather_into_tensor(gathered, out, group=self.group)
+
+    def halo(self, xext, own_off: int, n_own: int, hlo: int, hhi: int):
+        """Fill xext[:hlo] from rank-1's last rows, xext[own_off+n_own:] from rank+1."""
+        if self.size == 1:
+            return
+        if self.stage and xext.is_cuda:
+            h = xext.cpu()
+            self.halo(h, own_off, n_own, hlo, hhi)
+            if hlo:
+                xext[:hlo].copy_(h[:hlo])
+            if hhi:
+                xext[own_off + n_own:own_off + n_own + hhi].copy_(h[own_off + n_own:own_off + n_own + hhi])
+            return
+        d = self.dist
+        ops = []
+        r = self.rank
+        if hlo:
+            ops.append(d.P2POp(d.irecv, xext[:hlo], r - 1, self.group))
+            ops.append(d.P2POp(d.isend, xext[own_off:own_off + hlo], r - 1, self.group))
+        if hhi:
+            ops.append(d.P2POp(d.irecv, xext[own_off + n_own:own_off + n_own + hhi], r + 1,
+                               self.group))
+            ops.append(d.P2POp(d.isend, xext[own_off + n_own - hhi:own_off + n_own], r + 1,
+                               self.group))
+        if ops:
+            for w in d.batch_isend_irecv(ops):
+                w.wait()
+
+
+# ------------------------------------------------------------------ local system
+@dataclass
+class LocalRankSystem:
+    """One rank's operators: rows = owned rows, columns index the extended
+    vector [halo_lo | owned | halo_hi]."""
+
+    n_own: int
+    hlo: int
+    hhi: int
+    A: object                 # backend matrix (owned rows x extended columns)
+    M: object | None          # same layout (global or block-local SPAI), None = identity
+    b: object                 # owned right-hand side
+
+    @property
+    def n_ext(self):
+        return self.hlo + self.n_own + self.hhi
+
+
+# ------------------------------------------------------------------ GPU backend
+class GpuBackend:
+    """Per-rank compute through the C-ABI (dist_* kernels, SELL-32 operators)."""
+
+    def __init__(self, device=None):
+        import torch
+        from .sparse import _require_cuda
+        _require_cuda()
+        self.torch = torch
+        self.lib = _lib.load()
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+
+    def _s(self):
+        from .sparse import stream_handle
+        return stream_handle()
+
+    # vectors
+    def zeros(self, n):
+        return self.torch.zeros(n, dtype=self.torch.float64, device=self.dev)
+
+    def scal(self, tol, maxit):
+        t = self.torch.empty(self.lib.spai_dist_scal_bytes(), dtype=self.torch.uint8,
+                             device=self.dev)
+        _lib.check(self.lib.spai_dist_scal_init(_p(t), float(tol), int(maxit), self._s()),
+                   "spai_dist_scal_init")
+        return t
+
+    def partials(self):
+        return self.torch.empty(self.lib.spai_dist_partials_bytes(), dtype=self.torch.uint8,
+                                device=self.dev)
+
+    def read(self, scal):
+        st, it = C.c_int(0), C.c_int64(0)
+        n0, nr, aux = C.c_double(0), C.c_double(0), C.c_double(0)
+        _lib.check(self.lib.spai_dist_scal_read(_p(scal), C.byref(st), C.byref(it), C.byref(n0),
+                                                C.byref(nr), C.byref(aux), self._s()),
+                   "spai_dist_scal_read")
+        return st.value, it.value, n0.value, nr.value, aux.value
+
+    def spmv(self, mode, M, xext, own_off, y, raux, ws, out, scal):
+        if M is None:       # identity preconditioner (mode 4)
+            _lib.check(self.lib.spai_dist_spmv(4, y.numel(), None, None, None, _p(xext), own_off,
+                                               _p(y), None, _p(ws), _p(out), _p(scal),
+                                               self._s()), "spai_dist_spmv")
+            return
+        sliceptr, cols = M.sell()
+        vals = M.sell_values()
+        _lib.check(self.lib.spai_dist_spmv(mode, M.nrows, _p(sliceptr), _p(cols), _p(vals),
+                                           _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out),
+                                           _p(scal), self._s()), "spai_dist_spmv")
+
+    def update_p(self, p_own, z, scal):
+        _lib.check(self.lib.spai_dist_update_p(z.numel(), _p(p_own), _p(z), _p(scal), self._s()),
+                   "spai_dist_update_p")
+
+    def update_xr(self, x, r_own, p_own, q, scal):
+        _lib.check(self.lib.spai_dist_update_xr(x.numel(), _p(x), _p(r_own), _p(p_own), _p(q),
+                                                _p(scal), self._s()), "spai_dist_update_xr")
+
+    def reduce_step(self, nranks, gathered, K, stage, scal, hist):
+        _lib.check(self.lib.spai_dist_reduce_step(nranks, _p(gathered), K, stage, _p(scal),
+                                                  _p(hist), self._s()), "spai_dist_reduce_step")
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+# ------------------------------------------------------------------ solver
+class DistributedPCG:
+    """Classic PCG on a row partition; device-resident, host polls every `chunk`."""
+
+    def __init__(self, system: LocalRankSystem, comm, backend, tol=1e-8, maxit=1000,
+                 chunk=16):
+        self.sys, self.comm, self.be = system, comm, backend
+        self.tol, self.maxit, self.chunk = tol, int(maxit), int(chunk)
+        be = backend
+        n, ne = system.n_own, system.n_ext
+        self.x = be.zeros(n)
+        self.pext = be.zeros(ne)
+        self.rext = be.zeros(ne)
+        self.q = be.zeros(n)
+        self.z = be.zeros(n)
+        self.out = be.zeros(3)
+        self.gathered = be.zeros(3 * comm.size)
+        self.hist = be.zeros(self.maxit)
+        self.ws = be.partials()
+        self.scal = be.scal(tol, maxit)
+        self.launched = 0
+
+    def _own(self, v):
+        return v[self.sys.hlo:self.sys.hlo + self.sys.n_own]
+
+    def start(self):
+        s, be, c = self.sys, self.be, self.comm
+        self._own(self.rext).copy_(s.b)
+        c.halo(self.rext, s.hlo, s.n_own, s.hlo, s.hhi)
+        # p = M r (owned part of p_ext); z is scratch here
+        if s.M is None:
+            self._own(self.pext).copy_(self._own(self.rext))
+        else:
+            be.spmv(0, s.M, self.rext, s.hlo, self._own(self.pext), None, self.ws, self.out,
+                    self.scal)
+
+    def iteration(self, first: bool):
+        s, be, c = self.sys, self.be, self.comm
+        p_own, r_own = self._own(self.pext), self._own(self.rext)
+        if not first:
+            be.update_p(p_own, self.z, self.scal)
+        c.halo(self.pext, s.hlo, s.n_own, s.hlo, s.hhi)
+        K1 = 3 if first else 1
+        be.spmv(1 if first else 2, s.A, self.pext, s.hlo, self.q, r_own, self.ws, self.out,
+                self.scal)
+        c.allgather(self.out[:K1], self.gathered[:K1 * c.size])
+        be.reduce_step(c.size, self.gathered, K1, 1, self.scal, self.hist)
+        be.update_xr(self.x, r_own, p_own, self.q, self.scal)
+        c.halo(self.rext, s.hlo, s.n_own, s.hlo, s.hhi)
+        be.spmv(3, s.M, self.rext, s.hlo, self.z, None, self.ws, self.out, self.scal)
+        c.allgather(self.out[:2], self.gathered[:2 * c.size])
+        be.reduce_step(c.size, self.gathered, 2, 2, self.scal, self.hist)
+        self.launched += 1
+
+    def run(self):
+        self.start()
+        done = 0
+        while True:
+            n = min(self.chunk, self.maxit - done) if done < self.maxit else 1
+            for _ in range(n):
+                self.iteration(first=(done == 0))
+                done += 1
+            st = self.be.read(self.scal)
+            if st[0] != 0:
+                return st
+            if done >= self.maxit:
+                return st
+
+    def solve(self):
+        """Returns (x_owned, ConvergenceRecord) with _solve_classic semantics."""
+        status, it, norm0, norm, aux = self.run()
+        if status == 3:
+            raise BreakdownError(f"indefinite curvature <p,Ap> = {aux}")
+        if status == 4:
+            raise DivergenceError("non-finite value in solver recurrence")
+        rec = ConvergenceRecord(variant="classic", vector_memory_units=4,
+                                extra_vector_ops_units=0)
+        rec.initial_residual = norm0
+        early = status == 1 and (norm0 == 0.0 or not (norm <= self.tol * norm0))
+        noted = it - 1 if early else it
+        if norm0 == 0.0:
+            norm = 0.0
+        h = self.hist[:noted].cpu().numpy() if noted > 0 else np.zeros(0)
+        rec.residual_norms = [float(v) for v in h]
+        rec.reductions_cum = [2 * (i + 1) for i in range(noted)]
+        rec.overlapped_cum = [0] * noted
+        rec.iterations = it
+        rec.converged = status == 1
+        rec.final_residual = norm
+        rec.total_reductions = 2 * noted + (1 if early else 0)
+        rec.launched_iterations = self.launched
+        return self.x, rec
+
+
+# ------------------------------------------------------------------ local operators
+def _rebase(dcsr, row0, row1, col0, ncols_ext):
+    """Rows [row0,row1) of a DeviceCsr with columns shifted by -col0 (device ops)."""
+    import torch
+    from .sparse import DeviceCsr
+    rp = dcsr.rowptr[row0:row1 + 1]
+    lo, hi = int(rp[0].item()), int(rp[-1].item())
+    rowptr = (rp - lo).contiguous()
+    colidx = (dcsr.colidx[lo:hi] - col0).to(torch.int32).contiguous()
+    vals = dcsr.vals[lo:hi].contiguous()
+    out = DeviceCsr(row1 - row0, ncols_ext, rowptr, colidx, vals)
+    return out
+
+
+def q1_rank_system(dims, part: SlabPartition, rank: int, spai_scope="global", eps=None,
+                   conv=None, h=1.0, precondition=True):
+    """Rank-local operators of the Q1 matrix on `dims` (x fastest, slabs along the
+    last axis), generated directly on this GPU.  b = A 1 restricted to the rank."""
+    from .grids import q1_stencil
+    table, stored = q1_stencil(len(dims), eps, conv, h)
+    return stencil_rank_system(dims, table, stored, part, rank, spai_scope, precondition)
+
+
+def stencil_rank_system(dims, table, stored, part: SlabPartition, rank: int,
+                        spai_scope="global", precondition=True):
+    """Rank-local operators of a 3^d box-stencil matrix (see grids.stencil_device)."""
+    import torch
+    from .grids import stencil_device
+    from .precond import spai1_symmetric_device
+
+    def gen(nz_sub):
+        return stencil_device(dims[:-1] + (nz_sub,), table, stored)
+
+    dims = tuple(int(d) for d in dims)
+    nz = dims[-1]
+    plane = int(np.prod(dims[:-1]))
+    assert part.nplanes == nz and part.plane == plane
+    z0, z1 = part.planes(rank)
+    hlo, hhi = part.halo(rank)
+    n_own = (z1 - z0) * plane
+    n_ext = hlo + n_own + hhi
+    # A with one ghost plane per side -> local SpMV operator
+    e0, e1 = max(z0 - 1, 0), min(z1 + 1, nz)
+    A1 = gen(e1 - e0)
+    A_loc = _rebase(A1, (z0 - e0) * plane, (z1 - e0) * plane, 0, n_ext)
+    ones = torch.ones(A1.nrows, dtype=torch.float64, device=A1.vals.device)
+    b = A1.matvec(ones)[(z0 - e0) * plane:(z1 - e0) * plane].clone()
+    M_loc = None
+    if precondition and spai_scope == "global":
+        g0, g1 = max(z0 - 3, 0), min(z1 + 3, nz)
+        A3 = gen(g1 - g0)
+        S3 = _symmetric_range(A3, (e0 - g0) * plane, (e1 - g0) * plane)
+        M_loc = _rebase(S3, (z0 - g0) * plane, (z1 - g0) * plane, (e0 - g0) * plane, n_ext)
+        M_loc._pat = A_loc._pat          # identical pattern and column layout
+    elif precondition and spai_scope == "block_local":
+        Sff = spai1_symmetric_device(gen(z1 - z0))
+        M_loc = _rebase(Sff, 0, Sff.nrows, -hlo, n_ext)
+    elif precondition:
+        raise ValueError(f"unknown spai_scope {spai_scope!r}")
+    return LocalRankSystem(n_own, hlo, hhi, A_loc, M_loc, b)
+
+
+def _symmetric_range(A, c0, c1):
+    """0.5 (M + M^T) on pattern(A) where M's columns [c0, c1) are assembled
+    (entries whose row and column are both in range are exact)."""
+    import torch
+    from .sparse import ptr, stream_handle
+    from .precond import _raise_assembly
+    lib = _lib.load()
+    cscptr, cscrow, csc2csr = A.csc()
+    assert A.structurally_symmetric()
+    cscval = A.csc_values()
+    m_csc = torch.zeros(A.nnz, dtype=torch.float64, device=A.vals.device)
+    wsb = lib.spai_assemble_workspace_bytes(A.nrows)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
+    bad, nfb = C.c_int64(-1), C.c_int64(0)
+    st = lib.spai_assemble_range(A.nrows, A.nnz, ptr(A.rowptr), ptr(A.colidx), ptr(A.vals),
+                                 ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(cscval), c0, c1,
+                                 ptr(m_csc), ptr(ws), wsb, C.byref(bad), C.byref(nfb),
+                                 stream_handle())
+    _lib.check(st, "spai_assemble_range")
+    if st != _lib.SPAI_OK:
+        _raise_assembly(st, bad.value)
+    vals = torch.empty_like(m_csc)
+    _lib.check(lib.spai_symmetrize(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals), stream_handle()),
+               "spai_symmetrize")
+    return A.with_values(vals)

@@ -327,10 +327,12 @@ class DeviceCsr:
             out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
         sliceptr, cols = self.sell()
         vals = self.sell_values()
-        _lib.check(_lib.load().spai_sell_spmv_tma(self.nrows, ptr(sliceptr), ptr(cols), ptr(vals),
-                                                  self.sell_width(), ptr(x.contiguous()),
-                                                  ptr(out), stream_handle()),
-                   "spai_sell_spmv_tma")
+        st = _lib.check(_lib.load().spai_sell_spmv_tma(self.nrows, ptr(sliceptr), ptr(cols),
+                                                       ptr(vals), self.sell_width(),
+                                                       ptr(x.contiguous()), ptr(out),
+                                                       stream_handle()), "spai_sell_spmv_tma")
+        if st != _lib.SPAI_OK:
+            raise _lib.NativeLibraryError(_lib.last_error())
         return out
 
     def tiles(self):

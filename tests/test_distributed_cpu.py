@@ -1,0 +1,99 @@
+"""Multi-rank host logic on CPU: world_size-2 gloo, the real orchestration
+(paper_1911_01492_b200.distributed) with the CPU test double of the kernels,
+checked against the reference's own multi-rank (block-local SPAI) golden run
+(tests/golden: ftkrylov.cli._solve_once with partition.ranks = 2 and 4)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1911_01492_b200.distributed import DistributedPCG, SlabPartition, TorchComm
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, nx, ny, q):
+    import sys
+    sys.path.insert(0, REPO)
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from dist_numpy_backend import NumpyBackend, fd5_rank_system
+        part = SlabPartition(ny, nx, world)
+        sysr = fd5_rank_system(nx, ny, part, rank)
+        solver = DistributedPCG(sysr, TorchComm(), NumpyBackend(), tol=1e-8, maxit=5000)
+        x, rec = solver.solve()
+        r0, r1 = part.rows(rank)
+        q.put((rank, r0, r1, x.numpy().copy(), rec.iterations, list(rec.residual_norms),
+               rec.total_reductions, rec.reductions_cum))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, nx=32, ny=32):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, ny, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(out)
+
+
+def test_slab_partition_matches_reference_rule():
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        import ftkrylov as fk
+    except ImportError:
+        pytest.skip("reference not present")
+    for nx, ny, p in ((8, 10, 4), (5, 7, 3), (6, 6, 6), (9, 4, 1)):
+        ref = fk.partition_1d_strips(fk.StructuredGrid(nx, ny), p)
+        part = SlabPartition(ny, nx, p)
+        for r in range(p):
+            r0, r1 = part.rows(r)
+            assert np.array_equal(ref.owned[r], np.arange(r0, r1))
+            hlo, hhi = part.halo(r)
+            assert len(ref.halo[r]) == hlo + hhi
+    with pytest.raises(Exception):
+        SlabPartition(3, 4, 5)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_two_rank_block_local_matches_reference(golden, world):
+    out = _run(world)
+    its = {o[4] for o in out}
+    assert len(its) == 1                      # every rank sees the same scalars
+    it = its.pop()
+    ref_its = int(golden[f"multirank/fd5_32x32/{world}/its"])
+    ref_hist = golden[f"multirank/fd5_32x32/{world}/hist"]
+    assert abs(it - ref_its) <= 1
+    h = np.asarray(out[0][5])
+    m = min(len(h), len(ref_hist))
+    assert np.max(np.abs(h[:m] - ref_hist[:m]) / ref_hist[:m]) <= 1e-8
+    x = np.zeros(32 * 32)
+    for _, r0, r1, xr, *_ in out:
+        x[r0:r1] = xr
+    xref = golden[f"multirank/fd5_32x32/{world}/x"]
+    assert np.max(np.abs(x - xref)) <= 1e-6 * np.max(np.abs(xref))
+    assert out[0][6] == 2 * it                # two fused reductions per iteration
+    assert out[0][7] == [2 * (i + 1) for i in range(it)]

@@ -1,0 +1,120 @@
+"""Multi-rank GPU path.  Only one GPU is available in this environment, so:
+P = 1 through the distributed code (TorchComm without a process group), and
+P = 2 as two processes on the same GPU over gloo (host-staged halos; the
+ranks never wait on each other's kernels).  On an 8 x B200 box the same code
+runs with the NCCL backend."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.distributed as dist            # noqa: E402
+import torch.multiprocessing as mp          # noqa: E402
+
+import paper_1911_01492_b200 as pb          # noqa: E402
+from paper_1911_01492_b200.distributed import (DistributedPCG, GpuBackend,  # noqa: E402
+                                               SlabPartition, TorchComm,
+                                               q1_rank_system, stencil_rank_system)
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _single_gpu(dims, tol=1e-8):
+    A = pb.q1_device(dims)
+    S = pb.spai1_symmetric_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    x, rec = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                      pb.SolverConfig(tol=tol, maxit=2000))
+    return A, S, x, rec
+
+
+def test_one_rank_distributed_equals_single_gpu():
+    dims = (20, 18, 16)
+    _, S, x1, rec1 = _single_gpu(dims)
+    part = SlabPartition(dims[-1], dims[0] * dims[1], 1)
+    sysr = q1_rank_system(dims, part, 0)
+    # global SPAI on one rank == single-GPU SPAI (same values on the pattern)
+    assert torch.allclose(sysr.M.vals, S.vals, rtol=0, atol=1e-14 * float(S.vals.abs().max()))
+    x, rec = DistributedPCG(sysr, TorchComm(), GpuBackend(), tol=1e-8, maxit=2000).solve()
+    assert rec.iterations == rec1.iterations
+    h, h1 = np.array(rec.residual_norms), np.array(rec1.residual_norms)
+    assert np.max(np.abs(h - h1) / h1) <= 1e-10
+    assert float((x - x1).abs().max()) <= 1e-9
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    import sys
+    sys.path.insert(0, REPO)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1911_01492_b200.grids import fd5_stencil
+        if case == "q1_global":
+            dims = (20, 18, 16)
+            part = SlabPartition(dims[-1], dims[0] * dims[1], world)
+            sysr = q1_rank_system(dims, part, rank, "global")
+        else:
+            dims = (32, 32)
+            part = SlabPartition(32, 32, world)
+            t, st = fd5_stencil()
+            sysr = stencil_rank_system(dims, t, st, part, rank, "block_local")
+        x, rec = DistributedPCG(sysr, TorchComm(), GpuBackend(), tol=1e-8, maxit=2000).solve()
+        r0, r1 = part.rows(rank)
+        q.put((rank, r0, r1, x.cpu().numpy(), rec.iterations, list(rec.residual_norms)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=600) for _ in range(world))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return out
+
+
+def test_two_ranks_global_spai_is_rank_invariant():
+    dims = (20, 18, 16)
+    _, _, x1, rec1 = _single_gpu(dims)
+    out = _run(2, "q1_global")
+    assert {o[4] for o in out} == {rec1.iterations}
+    h = np.array(out[0][5])
+    h1 = np.array(rec1.residual_norms)
+    assert np.max(np.abs(h - h1) / h1) <= 1e-8
+    x = np.zeros(x1.numel())
+    for _, r0, r1, xr, *_ in out:
+        x[r0:r1] = xr
+    assert np.max(np.abs(x - x1.cpu().numpy())) <= 1e-7
+
+
+def test_two_ranks_block_local_matches_reference(golden):
+    out = _run(2, "fd5_block_local")
+    it = out[0][4]
+    assert abs(it - int(golden["multirank/fd5_32x32/2/its"])) <= 1
+    ref = golden["multirank/fd5_32x32/2/hist"]
+    h = np.array(out[0][5])
+    m = min(len(h), len(ref))
+    assert np.max(np.abs(h[:m] - ref[:m]) / ref[:m]) <= 1e-8
