@@ -544,6 +544,10 @@ extern "C" int spai_pcg_set_fused(spai_pcg* s, int fused) {
 extern "C" int spai_pcg_set_tma(spai_pcg* s, int tma) {
   if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
   s->tma = tma != 0 && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024;
+  if (s->tma) {
+    SPAI_CUDA(cudaFuncSetAttribute(pcg_u1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemA));
+    SPAI_CUDA(cudaFuncSetAttribute(pcg_u2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemM));
+  }
   return SPAI_OK;
 }
 

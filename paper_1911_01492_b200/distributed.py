@@ -175,7 +175,8 @@ class GpuBackend:
         return t
 
     def partials(self):
-        return self.torch.empty(self.lib.spai_dist_partials_bytes(), dtype=self.torch.uint8,
+        # the first word is the last-block ticket of the deterministic reduction: must start at 0
+        return self.torch.zeros(self.lib.spai_dist_partials_bytes(), dtype=self.torch.uint8,
                                 device=self.dev)
 
     def read(self, scal):
