@@ -336,40 +336,68 @@ def q1_rank_system(dims, part: SlabPartition, rank: int, spai_scope="global", ep
 def stencil_rank_system(dims, table, stored, part: SlabPartition, rank: int,
                         spai_scope="global", precondition=True):
     """Rank-local operators of a 3^d box-stencil matrix (see grids.stencil_device)."""
-    import torch
-    from .grids import stencil_device
-    from .precond import spai1_symmetric_device
+    rs = RankSetup(dims, table, stored, part, rank, spai_scope)
+    return rs.system(rs.preconditioner() if precondition else None)
 
-    def gen(nz_sub):
-        return stencil_device(dims[:-1] + (nz_sub,), table, stored)
 
-    dims = tuple(int(d) for d in dims)
-    nz = dims[-1]
-    plane = int(np.prod(dims[:-1]))
-    assert part.nplanes == nz and part.plane == plane
-    z0, z1 = part.planes(rank)
-    hlo, hhi = part.halo(rank)
-    n_own = (z1 - z0) * plane
-    n_ext = hlo + n_own + hhi
-    # A with one ghost plane per side -> local SpMV operator
-    e0, e1 = max(z0 - 1, 0), min(z1 + 1, nz)
-    A1 = gen(e1 - e0)
-    A_loc = _rebase(A1, (z0 - e0) * plane, (z1 - e0) * plane, 0, n_ext)
-    ones = torch.ones(A1.nrows, dtype=torch.float64, device=A1.vals.device)
-    b = A1.matvec(ones)[(z0 - e0) * plane:(z1 - e0) * plane].clone()
-    M_loc = None
-    if precondition and spai_scope == "global":
-        g0, g1 = max(z0 - 3, 0), min(z1 + 3, nz)
-        A3 = gen(g1 - g0)
-        S3 = _symmetric_range(A3, (e0 - g0) * plane, (e1 - g0) * plane)
-        M_loc = _rebase(S3, (z0 - g0) * plane, (z1 - g0) * plane, (e0 - g0) * plane, n_ext)
-        M_loc._pat = A_loc._pat          # identical pattern and column layout
-    elif precondition and spai_scope == "block_local":
-        Sff = spai1_symmetric_device(gen(z1 - z0))
-        M_loc = _rebase(Sff, 0, Sff.nrows, -hlo, n_ext)
-    elif precondition:
-        raise ValueError(f"unknown spai_scope {spai_scope!r}")
-    return LocalRankSystem(n_own, hlo, hhi, A_loc, M_loc, b)
+class RankSetup:
+    """Two-phase construction so a benchmark can time the SPAI(1) setup alone:
+    __init__ generates this rank's matrices in HBM (A with one ghost plane for
+    the SpMV, A with three ghost planes for global SPAI(1)); preconditioner()
+    runs transpose + assembly + symmetrisation on the device."""
+
+    def __init__(self, dims, table, stored, part: SlabPartition, rank: int,
+                 spai_scope="global"):
+        import torch
+        from .grids import stencil_device
+        self.dims = tuple(int(d) for d in dims)
+        self.table, self.stored, self.part, self.rank = table, stored, part, rank
+        self.scope = spai_scope
+        nz = self.dims[-1]
+        self.plane = plane = int(np.prod(self.dims[:-1]))
+        assert part.nplanes == nz and part.plane == plane
+        z0, z1 = part.planes(rank)
+        self.z0, self.z1 = z0, z1
+        self.hlo, self.hhi = part.halo(rank)
+        self.n_own = (z1 - z0) * plane
+        self.n_ext = self.hlo + self.n_own + self.hhi
+        self.e0, self.e1 = max(z0 - 1, 0), min(z1 + 1, nz)
+        gen = self._gen
+        A1 = gen(self.e1 - self.e0)
+        self.A_loc = _rebase(A1, (z0 - self.e0) * plane, (z1 - self.e0) * plane, 0, self.n_ext)
+        ones = torch.ones(A1.nrows, dtype=torch.float64, device=A1.vals.device)
+        self.b = A1.matvec(ones)[(z0 - self.e0) * plane:(z1 - self.e0) * plane].clone()
+        self.g0, self.g1 = max(z0 - 3, 0), min(z1 + 3, nz)
+        if spai_scope == "global":
+            self.A_spai = gen(self.g1 - self.g0)
+        elif spai_scope == "block_local":
+            self.A_spai = gen(z1 - z0)
+        else:
+            raise ValueError(f"unknown spai_scope {spai_scope!r}")
+
+    def _gen(self, nz_sub):
+        from .grids import stencil_device
+        return stencil_device(self.dims[:-1] + (nz_sub,), self.table, self.stored)
+
+    def preconditioner(self):
+        from .precond import spai1_symmetric_device
+        from .sparse import DeviceCsr
+        plane = self.plane
+        if self.scope == "global":
+            A3 = self.A_spai
+            A3 = DeviceCsr(A3.nrows, A3.ncols, A3.rowptr, A3.colidx, A3.vals)   # fresh CSC
+            S3 = _symmetric_range(A3, (self.e0 - self.g0) * plane, (self.e1 - self.g0) * plane)
+            M = _rebase(S3, (self.z0 - self.g0) * plane, (self.z1 - self.g0) * plane,
+                        (self.e0 - self.g0) * plane, self.n_ext)
+            M._pat = self.A_loc._pat      # identical pattern and column layout
+            return M
+        Aff = self.A_spai
+        Sff = spai1_symmetric_device(DeviceCsr(Aff.nrows, Aff.ncols, Aff.rowptr, Aff.colidx,
+                                               Aff.vals))
+        return _rebase(Sff, 0, Sff.nrows, -self.hlo, self.n_ext)
+
+    def system(self, M):
+        return LocalRankSystem(self.n_own, self.hlo, self.hhi, self.A_loc, M, self.b)
 
 
 def _symmetric_range(A, c0, c1):
