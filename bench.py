@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--n", type=int, default=400, help="grid points per axis")
+    ap.add_argument("--grid", type=int, default=400, help="grid points per axis")
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=20000)
     ap.add_argument("--no-e2e", action="store_true")
@@ -195,7 +195,7 @@ def run_ours(args):
         return run_distributed(args, world, rank, local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
-    N = args.n
+    N = args.grid
     dims = (N, N, N)
     with torch.cuda.stream(stream):
         A = pb.q1_device(dims)
@@ -362,7 +362,7 @@ def run_distributed(args, world, rank, local):
     from paper_1911_01492_b200.distributed import (DistributedPCG, GpuBackend, RankSetup,
                                                    SlabPartition, TorchComm)
 
-    N = args.n
+    N = args.grid
     dims = (N, N, N)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
