@@ -164,25 +164,35 @@ int spai_axpby(int64_t n, double a, const double* x, double b, double* y,
                void* stream);
 
 /* ------------------------------------------------------------------ K5b
- * SELL-32 (sliced ELL, slice height 32, rows not reordered): the solve-phase
- * format.  Element (row 32 s + lane, slot k) sits at sliceptr[s] + 32 k + lane;
- * padding slots hold column = row, value 0.  sliceptr has nslices+1 int64
- * entries (nslices = spai_sell_nslices(n)); the padded size is sliceptr[nslices].
- * Matrices on the same pattern (A, SPAI(1) M) share sliceptr and cols.     */
+ * SELL-32, the solve-phase format (slice = 32 consecutive rows = one warp).
+ * Values: vals[sliceptr[s] + 32 k + lane].  Columns per slice, cdesc[s]:
+ *   < 0  relative slice: all rows use the sorted offsets
+ *        cols[-cdesc-1 .. -cdesc-1+w) (col = row + offset, w <= 32);
+ *   >= 0 explicit slice: cols[cdesc + 32 k + lane].
+ * Build: spai_sell_layout (synchronous; returns the value and column array
+ * sizes) -> allocate -> spai_sell_fill_cols -> spai_sell_fill_vals (per
+ * matrix on the pattern; A and its SPAI(1) M share sliceptr/cdesc/cols).   */
 int64_t spai_sell_nslices(int64_t n);
-int spai_sell_layout(int64_t n, const int64_t* rowptr, int64_t* sliceptr, void* stream);
+size_t spai_sell_scratch_bytes(int64_t n);
+int spai_sell_layout(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                     int allow_relative, int64_t* sliceptr, void* scratch,
+                     int64_t* nvals, int64_t* ncolentries, void* stream);
 int spai_sell_fill_cols(int64_t n, const int64_t* rowptr, const int32_t* colidx,
-                        const int64_t* sliceptr, int32_t* cols, void* stream);
-int spai_sell_fill_vals(int64_t n, const int64_t* rowptr, const double* csr_vals,
-                        const int64_t* sliceptr, double* vals, void* stream);
-int spai_sell_spmv(int64_t n, const int64_t* sliceptr, const int32_t* cols,
-                   const double* vals, const double* x, double* y, void* stream);
+                        const int64_t* sliceptr, const void* scratch, int64_t* cdesc,
+                        int32_t* cols, void* stream);
+int spai_sell_fill_vals(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                        const double* csr_vals, const int64_t* sliceptr,
+                        const int64_t* cdesc, const int32_t* cols, double* vals,
+                        void* stream);
+int spai_sell_spmv(int64_t n, int64_t ncols, const int64_t* sliceptr,
+                   const int64_t* cdesc, const int32_t* cols, const double* vals,
+                   const double* x, double* y, void* stream);
 /* TMA-staged SELL-32 SpMV: one persistent CTA of 8 warps per SM, each warp
  * streams its slices with cp.async.bulk into a 2-stage shared-memory ring.
  * wmax = widest slice (in slots); needs 8*2*wmax*384 B <= 200 KB.          */
-int spai_sell_spmv_tma(int64_t n, const int64_t* sliceptr, const int32_t* cols,
-                       const double* vals, int wmax, const double* x, double* y,
-                       void* stream);
+int spai_sell_spmv_tma(int64_t n, int64_t ncols, const int64_t* sliceptr,
+                       const int64_t* cdesc, const int32_t* cols, const double* vals,
+                       int wmax, const double* x, double* y, void* stream);
 
 /* ------------------------------------------------------------------ K8
  * Device-resident classic PCG (replaces _solve_classic, krylov.py:301-345)
@@ -193,10 +203,10 @@ int spai_sell_spmv_tma(int64_t n, const int64_t* sliceptr, const int32_t* cols,
 typedef struct spai_pcg spai_pcg;     /* opaque solver state               */
 size_t spai_pcg_workspace_bytes(int64_t n, int64_t maxit);
 int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
-                    const int32_t* cols, const double* A_vals,
-                    const int64_t* m_sliceptr, const int32_t* m_cols,
-                    const double* M_vals, double tol, int64_t maxit, void* ws,
-                    size_t ws_bytes, void* stream);
+                    const int64_t* cdesc, const int32_t* cols, const double* A_vals,
+                    const int64_t* m_sliceptr, const int64_t* m_cdesc,
+                    const int32_t* m_cols, const double* M_vals, double tol,
+                    int64_t maxit, void* ws, size_t ws_bytes, void* stream);
 /* 0 (default): 4 kernels per iteration (vector updates in their own
  * kernels, one gather per stored entry); 1: 2 kernels (vector updates
  * recomputed inside the SpMV gathers).  Same arithmetic, same results.    */
@@ -232,7 +242,8 @@ size_t spai_dist_partials_bytes(void);
 int spai_dist_scal_init(void* scal, double tol, int64_t maxit, void* stream);
 int spai_dist_scal_read(const void* scal, int* status, int64_t* it, double* norm0,
                         double* norm, double* aux, void* stream);
-int spai_dist_spmv(int mode, int64_t n, const int64_t* sliceptr, const int32_t* cols,
+int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
+                   const int64_t* cdesc, const int32_t* cols,
                    const double* vals, const double* xext, int64_t own_off, double* y,
                    const double* raux, void* partials_ws, double* out,
                    const void* scal, void* stream);

@@ -58,7 +58,8 @@ _SIGS = {
     "spai_dist_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),
     "spai_dist_scal_read": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),
                                    C.POINTER(_dbl), C.POINTER(_dbl), _vp]),
-    "spai_dist_spmv": (_i32, [_i32, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dist_spmv": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
+                              _vp, _vp]),
     "spai_dist_update_p": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_dist_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_dist_reduce_step": (_i32, [_i32, _vp, _i32, _i32, _vp, _vp, _vp]),
@@ -72,14 +73,16 @@ _SIGS = {
     "spai_fused_dots": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "spai_axpby": (_i32, [_i64, _dbl, _vp, _dbl, _vp, _vp]),
     "spai_sell_nslices": (_i64, [_i64]),
-    "spai_sell_layout": (_i32, [_i64, _vp, _vp, _vp]),
-    "spai_sell_fill_cols": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
-    "spai_sell_fill_vals": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
-    "spai_sell_spmv": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "spai_sell_spmv_tma": (_i32, [_i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "spai_sell_scratch_bytes": (_sz, [_i64]),
+    "spai_sell_layout": (_i32, [_i64, _vp, _vp, _i32, _vp, _vp, C.POINTER(_i64), C.POINTER(_i64),
+                                _vp]),
+    "spai_sell_fill_cols": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_sell_fill_vals": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_sell_spmv": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_sell_spmv_tma": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "spai_pcg_workspace_bytes": (_sz, [_i64, _i64]),
-    "spai_pcg_create": (_i32, [C.POINTER(_vp), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _dbl,
-                               _i64, _vp, _sz, _vp]),
+    "spai_pcg_create": (_i32, [C.POINTER(_vp), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _dbl, _i64, _vp, _sz, _vp]),
     "spai_pcg_set_fused": (_i32, [_vp, _i32]),
     "spai_pcg_set_tma": (_i32, [_vp, _i32]),
     "spai_pcg_start": (_i32, [_vp, _vp, _vp]),

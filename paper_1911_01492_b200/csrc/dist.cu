@@ -184,7 +184,8 @@ extern "C" size_t spai_dist_partials_bytes(void) {
   return 256 + (size_t)num_sms() * 32 * 3 * sizeof(double);
 }
 
-extern "C" int spai_dist_spmv(int mode, int64_t n, const int64_t* sliceptr, const int32_t* cols,
+extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
+                              const int64_t* cdesc, const int32_t* cols,
                               const double* vals, const double* xext, int64_t own_off, double* y,
                               const double* raux, void* partials_ws, double* out,
                               const void* scal, void* stream) {
@@ -198,7 +199,7 @@ extern "C" int spai_dist_spmv(int mode, int64_t n, const int64_t* sliceptr, cons
   const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (ns * 32 + 255) / 256));
   unsigned int* ticket = (unsigned int*)partials_ws;
   double* part = (double*)((char*)partials_ws + 256);
-  Sell A{sliceptr, cols, vals};
+  Sell A{sliceptr, cdesc, cols, vals, ncols};
   const DistScal* sc = (const DistScal*)scal;
   cudaStream_t s = (cudaStream_t)stream;
   switch (mode) {

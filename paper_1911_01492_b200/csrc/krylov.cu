@@ -457,18 +457,19 @@ static int launch_iteration(spai_pcg* s) {
 }
 
 extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
-                               const int32_t* cols, const double* A_vals,
-                               const int64_t* m_sliceptr, const int32_t* m_cols,
-                               const double* M_vals, double tol, int64_t maxit, void* ws,
-                               size_t ws_bytes, void* stream) {
+                               const int64_t* cdesc, const int32_t* cols, const double* A_vals,
+                               const int64_t* m_sliceptr, const int64_t* m_cdesc,
+                               const int32_t* m_cols, const double* M_vals, double tol,
+                               int64_t maxit, void* ws, size_t ws_bytes, void* stream) {
   if (!out || n <= 0 || maxit < 1) { set_error("spai_pcg_create: bad arguments"); return SPAI_E_ARG; }
   if (ws_bytes < spai_pcg_workspace_bytes(n, maxit)) { set_error("pcg workspace too small"); return SPAI_E_ARG; }
   spai_pcg* s = new spai_pcg();
   s->n = n;
   s->nslices = (n + kSell - 1) / kSell;
-  s->A = Sell{sliceptr, cols, A_vals};
+  s->A = Sell{sliceptr, cdesc, cols, A_vals, n};
   s->hasM = M_vals != nullptr;
-  s->M = Sell{m_sliceptr ? m_sliceptr : sliceptr, m_cols ? m_cols : cols, M_vals};
+  s->M = m_sliceptr ? Sell{m_sliceptr, m_cdesc, m_cols, M_vals, n}
+                    : Sell{sliceptr, cdesc, cols, M_vals, n};
   s->tol = tol;
   s->maxit = maxit;
   s->stream = (cudaStream_t)stream;

@@ -1,59 +1,88 @@
-// SELL-32 (sliced ELL, slice height = warp width, no row sorting) used by the
-// solve-phase kernels.  Element (row r = 32 s + lane, slot k) lives at
-// sliceptr[s] + 32 k + lane, so a warp (one slice, one row per lane) reads
-// every value/index stream with perfectly coalesced 256 B / 128 B requests
-// and has `width` independent loads in flight per lane.  Padding slots hold
-// column = the row itself (valid address, cached) and value 0.
-// For the 27-point 400^3 matrix the padding is < 0.6 % of nnz.
+// SELL-32 (sliced ELL, slice height = warp width, rows not reordered) used by
+// the solve-phase kernels.  Value (row r = 32 s + lane, slot k) lives at
+// vals[sliceptr[s] + 32 k + lane]: a warp (one slice, one row per lane) reads
+// the value stream with perfectly coalesced 256 B requests.
+//
+// Column structure, per slice (cdesc[s]):
+//  * relative (cdesc < 0): every row of the slice uses the same sorted set of
+//    relative offsets rel[k] = col - row (the union over the slice's rows,
+//    <= 32 entries) stored once at cols[-cdesc-1 ...]; slot k of row r is
+//    column r + rel[k].  Rows lacking an offset get an explicit zero there.
+//    This is the common case for stencil/FEM matrices and removes the 4 B
+//    per-entry index stream (12 -> ~8.1 B per stored entry).
+//  * explicit (cdesc >= 0): per-entry column indices at cols[cdesc + 32 k + lane]
+//    (padding = own row with value 0), used for irregular slices.
+// Padding columns are clamped into [0, ncols) so they are always valid loads.
 #pragma once
 #include "common.cuh"
 
 namespace spai {
 
 constexpr int kSell = 32;
+constexpr int kRelMax = 32;     // max relative offsets per slice
 
 struct Sell {
-  const int64_t* __restrict__ sliceptr;   // [nslices+1] element offsets
-  const int32_t* __restrict__ cols;       // [padded]
+  const int64_t* __restrict__ sliceptr;   // [nslices+1] value offsets (32 * width per slice)
+  const int64_t* __restrict__ cdesc;      // [nslices] column descriptor (see above)
+  const int32_t* __restrict__ cols;       // relative tables and explicit blocks
   const double* __restrict__ vals;        // [padded]
+  int64_t ncols;                          // columns of the operator (gather bound)
 };
 
-// acc = sum_k vals[k] * xf(cols[k]) for this lane's row of slice s
+// acc = sum_k vals[k] * xf(col_k) for this lane's row of slice s
 template <class XF>
 __device__ __forceinline__ double sell_row(const Sell& A, int64_t s, int lane, const XF& xf) {
   const int64_t off = A.sliceptr[s];
   const int w = (int)((A.sliceptr[s + 1] - off) >> 5);
+  const int64_t cd = A.cdesc[s];
   const double* __restrict__ v = A.vals + off + lane;
-  const int32_t* __restrict__ c = A.cols + off + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int k = 0;
-  for (; k + 4 <= w; k += 4) {
-    const int32_t c0 = __ldg(c + (k + 0) * kSell), c1 = __ldg(c + (k + 1) * kSell);
-    const int32_t c2 = __ldg(c + (k + 2) * kSell), c3 = __ldg(c + (k + 3) * kSell);
-    const double v0 = ldg_stream(v + (k + 0) * kSell), v1 = ldg_stream(v + (k + 1) * kSell);
-    const double v2 = ldg_stream(v + (k + 2) * kSell), v3 = ldg_stream(v + (k + 3) * kSell);
-    a0 = fma(v0, xf(c0), a0);
-    a1 = fma(v1, xf(c1), a1);
-    a2 = fma(v2, xf(c2), a2);
-    a3 = fma(v3, xf(c3), a3);
+  if (cd < 0) {
+    const int32_t* __restrict__ rt = A.cols + (-cd - 1);
+    const int32_t myrel = lane < w ? __ldg(rt + lane) : 0;
+    const int64_t row = s * kSell + lane;
+    const int64_t hi = A.ncols - 1;
+    auto col = [&](int kk) -> int32_t {
+      const int64_t c = row + __shfl_sync(0xffffffffu, myrel, kk);
+      return (int32_t)(c < 0 ? 0 : (c > hi ? hi : c));
+    };
+    for (; k + 4 <= w; k += 4) {
+      const int32_t c0 = col(k), c1 = col(k + 1), c2 = col(k + 2), c3 = col(k + 3);
+      const double v0 = ldg_stream(v + (k + 0) * kSell), v1 = ldg_stream(v + (k + 1) * kSell);
+      const double v2 = ldg_stream(v + (k + 2) * kSell), v3 = ldg_stream(v + (k + 3) * kSell);
+      a0 = fma(v0, xf(c0), a0);
+      a1 = fma(v1, xf(c1), a1);
+      a2 = fma(v2, xf(c2), a2);
+      a3 = fma(v3, xf(c3), a3);
+    }
+    for (; k < w; ++k) a0 = fma(ldg_stream(v + k * kSell), xf(col(k)), a0);
+  } else {
+    const int32_t* __restrict__ c = A.cols + cd + lane;
+    for (; k + 4 <= w; k += 4) {
+      const int32_t c0 = __ldg(c + (k + 0) * kSell), c1 = __ldg(c + (k + 1) * kSell);
+      const int32_t c2 = __ldg(c + (k + 2) * kSell), c3 = __ldg(c + (k + 3) * kSell);
+      const double v0 = ldg_stream(v + (k + 0) * kSell), v1 = ldg_stream(v + (k + 1) * kSell);
+      const double v2 = ldg_stream(v + (k + 2) * kSell), v3 = ldg_stream(v + (k + 3) * kSell);
+      a0 = fma(v0, xf(c0), a0);
+      a1 = fma(v1, xf(c1), a1);
+      a2 = fma(v2, xf(c2), a2);
+      a3 = fma(v3, xf(c3), a3);
+    }
+    for (; k < w; ++k) a0 = fma(ldg_stream(v + k * kSell), xf(__ldg(c + k * kSell)), a0);
   }
-  for (; k < w; ++k) a0 = fma(ldg_stream(v + k * kSell), xf(__ldg(c + k * kSell)), a0);
   return (a0 + a1) + (a2 + a3);
 }
 
-}  // namespace spai
-
-namespace spai {
-
 // ---- TMA-staged SELL-32: every warp owns a 2-stage shared-memory ring; lane 0
-// streams whole slices (values + column indices are contiguous per slice) with
-// cp.async.bulk (SASS UBLKCP) while the warp gathers x for the previous slice.
-// The TMA engine keeps ~2 slices per warp in flight without register cost.
+// streams whole slices (values, and the index block of explicit slices, are
+// contiguous per slice) with cp.async.bulk (SASS UBLKCP) while the warp
+// gathers x for the previous slice.  Measured slower than sell_row on B200
+// (gather latency with 8 warps/SM); kept as an option (spai_pcg_set_tma).
 constexpr int kTmaWarps = 8;        // warps per CTA (one persistent CTA per SM)
 constexpr int kTmaStages = 2;
 
 struct SellTmaSmem {
-  // per warp: [mbar x kTmaStages][vals stage x kTmaStages][cols stage x kTmaStages]
   static __host__ __device__ size_t stage_vals(int wmax) { return (size_t)wmax * kSell * 8; }
   static __host__ __device__ size_t stage_cols(int wmax) { return (size_t)wmax * kSell * 4; }
   static __host__ __device__ size_t warp_bytes(int wmax) {
@@ -61,7 +90,6 @@ struct SellTmaSmem {
   }
 };
 
-// Calls epi(s, acc) for every slice s of this warp (acc = this lane's row sum).
 template <class XF, class EPI>
 __device__ __forceinline__ void sell_tma_loop(int64_t nslices, const Sell& A, int wmax,
                                               unsigned char* wbase, const XF& xf, const EPI& epi) {
@@ -88,36 +116,41 @@ __device__ __forceinline__ void sell_tma_loop(int64_t nslices, const Sell& A, in
   auto issue = [&](int64_t s, int st) {
     const int64_t off = A.sliceptr[s];
     const uint32_t cnt = (uint32_t)(A.sliceptr[s + 1] - off);
-    mbar_arrive_expect_tx(&full[st], cnt * 12u);
+    const int64_t cd = A.cdesc[s];
+    mbar_arrive_expect_tx(&full[st], cnt * (cd >= 0 ? 12u : 8u));
     bulk_g2s(sv[st], A.vals + off, cnt * 8u, &full[st]);
-    bulk_g2s(sc[st], A.cols + off, cnt * 4u, &full[st]);
+    if (cd >= 0) bulk_g2s(sc[st], A.cols + cd, cnt * 4u, &full[st]);
   };
   if (lane == 0) {
 #pragma unroll
     for (int st = 0; st < kTmaStages; ++st)
       if (gw + st * nw < nslices) issue(gw + st * nw, st);
   }
-  // slice offsets are prefetched one slice ahead so the refill is not stuck
-  // behind a dependent global load
-  int64_t off_next = gw < nslices ? A.sliceptr[gw] : 0;
-  int64_t end_next = gw < nslices ? A.sliceptr[gw + 1] : 0;
+  const int64_t hi = A.ncols - 1;
   int i = 0;
   for (int64_t s = gw; s < nslices; s += nw, ++i) {
     const int st = i % kTmaStages;
     const uint32_t phase = (uint32_t)((i / kTmaStages) & 1);
-    const int wdt = (int)((end_next - off_next) >> 5);
-    if (s + nw < nslices) { off_next = A.sliceptr[s + nw]; end_next = A.sliceptr[s + nw + 1]; }
+    const int64_t off = A.sliceptr[s];
+    const int wdt = (int)((A.sliceptr[s + 1] - off) >> 5);
+    const int64_t cd = A.cdesc[s];
+    const int32_t myrel = (cd < 0 && lane < wdt) ? __ldg(A.cols + (-cd - 1) + lane) : 0;
+    const int64_t row = s * kSell + lane;
     mbar_wait(&full[st], phase);
     const double* __restrict__ v = sv[st] + lane;
     const int32_t* __restrict__ c = sc[st] + lane;
+    auto colk = [&](int kk) -> int32_t {
+      if (cd >= 0) return c[kk * kSell];
+      const int64_t cc = row + __shfl_sync(0xffffffffu, myrel, kk);
+      return (int32_t)(cc < 0 ? 0 : (cc > hi ? hi : cc));
+    };
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     int k = 0;
-    // 9 independent gathers in flight per lane (27 = 3 x 9 for the 3D stencil)
     for (; k + 9 <= wdt; k += 9) {
       int32_t cc[9];
       double xv[9];
 #pragma unroll
-      for (int u = 0; u < 9; ++u) cc[u] = c[(k + u) * kSell];
+      for (int u = 0; u < 9; ++u) cc[u] = colk(k + u);
 #pragma unroll
       for (int u = 0; u < 9; ++u) xv[u] = xf(cc[u]);
 #pragma unroll
@@ -127,7 +160,7 @@ __device__ __forceinline__ void sell_tma_loop(int64_t nslices, const Sell& A, in
         a2 = fma(v[(k + u + 2) * kSell], xv[u + 2], a2);
       }
     }
-    for (; k < wdt; ++k) a0 = fma(v[k * kSell], xf(c[k * kSell]), a0);
+    for (; k < wdt; ++k) a0 = fma(v[k * kSell], xf(colk(k)), a0);
     __syncwarp();                              // stage fully consumed by the warp
     if (lane == 0 && s + kTmaStages * nw < nslices) {
       fence_proxy_async();

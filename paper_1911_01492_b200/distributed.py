@@ -189,15 +189,16 @@ class GpuBackend:
 
     def spmv(self, mode, M, xext, own_off, y, raux, ws, out, scal):
         if M is None:       # identity preconditioner (mode 4)
-            _lib.check(self.lib.spai_dist_spmv(4, y.numel(), None, None, None, _p(xext), own_off,
-                                               _p(y), None, _p(ws), _p(out), _p(scal),
-                                               self._s()), "spai_dist_spmv")
+            _lib.check(self.lib.spai_dist_spmv(4, y.numel(), xext.numel(), None, None, None, None,
+                                               _p(xext), own_off, _p(y), None, _p(ws), _p(out),
+                                               _p(scal), self._s()), "spai_dist_spmv")
             return
-        sliceptr, cols = M.sell()
+        sliceptr, cdesc, cols = M.sell()
         vals = M.sell_values()
-        _lib.check(self.lib.spai_dist_spmv(mode, M.nrows, _p(sliceptr), _p(cols), _p(vals),
-                                           _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out),
-                                           _p(scal), self._s()), "spai_dist_spmv")
+        _lib.check(self.lib.spai_dist_spmv(mode, M.nrows, M.ncols, _p(sliceptr), _p(cdesc),
+                                           _p(cols), _p(vals), _p(xext), own_off, _p(y),
+                                           _p(raux), _p(ws), _p(out), _p(scal), self._s()),
+                   "spai_dist_spmv")
 
     def update_p(self, p_own, z, scal):
         _lib.check(self.lib.spai_dist_update_p(z.numel(), _p(p_own), _p(z), _p(scal), self._s()),

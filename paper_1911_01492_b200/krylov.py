@@ -221,24 +221,27 @@ class DevicePCG:
         self.A, self.M = A, M
         self.n = A.nrows
         self.maxit = int(maxit)
-        sliceptr, cols = A.sell()
+        sliceptr, cdesc, cols = A.sell()
         a_vals = A.sell_values()
+        z = C.c_void_p(0)
         if M is not None:
+            if M.rowptr is A.rowptr and M.colidx is A.colidx:
+                M._pat = A._pat
             m_vals = M.sell_values()
-            if M._pat is A._pat or (M.rowptr is A.rowptr and M.colidx is A.colidx):
-                m_sp, m_cols = C.c_void_p(0), C.c_void_p(0)
+            if M._pat is A._pat:
+                m_sp, m_cd, m_cols = z, z, z
             else:
-                msp, mc = M.sell()
-                m_sp, m_cols = ptr(msp), ptr(mc)
+                msp, mcd, mc = M.sell()
+                m_sp, m_cd, m_cols = ptr(msp), ptr(mcd), ptr(mc)
         else:
-            m_vals, m_sp, m_cols = None, C.c_void_p(0), C.c_void_p(0)
+            m_vals, m_sp, m_cd, m_cols = None, z, z, z
         wsb = self.lib.spai_pcg_workspace_bytes(self.n, self.maxit)
         self.ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
-        self._keep = (sliceptr, cols, a_vals, m_vals, M)
+        self._keep = (sliceptr, cdesc, cols, a_vals, m_vals, M)
         h = C.c_void_p()
         st = self.lib.spai_pcg_create(
-            C.byref(h), A.nrows, ptr(sliceptr), ptr(cols), ptr(a_vals), m_sp, m_cols,
-            ptr(m_vals) if m_vals is not None else C.c_void_p(0),
+            C.byref(h), A.nrows, ptr(sliceptr), ptr(cdesc), ptr(cols), ptr(a_vals), m_sp, m_cd,
+            m_cols, ptr(m_vals) if m_vals is not None else C.c_void_p(0),
             float(tol), self.maxit, ptr(self.ws), wsb, stream_handle())
         _lib.check(st, "spai_pcg_create")
         self.h = h

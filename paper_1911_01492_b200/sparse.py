@@ -264,35 +264,50 @@ class DeviceCsr:
         return self._pat.sym
 
     # K5b: SELL-32 layout (solve-phase format), shared by matrices on one pattern
+    allow_relative_sell = True
+
     def sell(self):
-        """(sliceptr int64[nslices+1], cols int32[padded]) (cached per pattern)."""
+        """(sliceptr int64[ns+1], cdesc int64[ns], cols int32[...]) (cached per pattern)."""
         if self._pat.sell is None:
             torch = _require_cuda()
             lib = _lib.load()
             ns = lib.spai_sell_nslices(self.nrows)
             dev = self.vals.device
             sliceptr = torch.empty(ns + 1, dtype=torch.int64, device=dev)
-            _lib.check(lib.spai_sell_layout(self.nrows, ptr(self.rowptr), ptr(sliceptr),
+            scratch = torch.empty(lib.spai_sell_scratch_bytes(self.nrows), dtype=torch.uint8,
+                                  device=dev)
+            nv, nc = C.c_int64(0), C.c_int64(0)
+            _lib.check(lib.spai_sell_layout(self.nrows, ptr(self.rowptr), ptr(self.colidx),
+                                            1 if self.allow_relative_sell else 0, ptr(sliceptr),
+                                            ptr(scratch), C.byref(nv), C.byref(nc),
                                             stream_handle()), "spai_sell_layout")
-            padded = int(sliceptr[-1].item())
-            cols = torch.empty(max(padded, 1), dtype=torch.int32, device=dev)
+            cdesc = torch.empty(max(ns, 1), dtype=torch.int64, device=dev)
+            cols = torch.empty(max(nc.value, 1), dtype=torch.int32, device=dev)
             _lib.check(lib.spai_sell_fill_cols(self.nrows, ptr(self.rowptr), ptr(self.colidx),
-                                               ptr(sliceptr), ptr(cols), stream_handle()),
-                       "spai_sell_fill_cols")
-            self._pat.sell = (sliceptr, cols)
-        return self._pat.sell
+                                               ptr(sliceptr), ptr(scratch), ptr(cdesc), ptr(cols),
+                                               stream_handle()), "spai_sell_fill_cols")
+            self._pat.sell = (sliceptr, cdesc, cols, nv.value)
+        return self._pat.sell[:3]
 
     def sell_values(self):
         """Values of this matrix in its SELL-32 layout (cached)."""
         if self._sell_vals is None:
             torch = _require_cuda()
-            sliceptr, cols = self.sell()
-            vals = torch.empty(cols.numel(), dtype=torch.float64, device=self.vals.device)
+            sliceptr, cdesc, cols = self.sell()
+            nv = self._pat.sell[3]
+            vals = torch.empty(max(nv, 1), dtype=torch.float64, device=self.vals.device)
             _lib.check(_lib.load().spai_sell_fill_vals(self.nrows, ptr(self.rowptr),
-                                                       ptr(self.vals), ptr(sliceptr), ptr(vals),
-                                                       stream_handle()), "spai_sell_fill_vals")
+                                                       ptr(self.colidx), ptr(self.vals),
+                                                       ptr(sliceptr), ptr(cdesc), ptr(cols),
+                                                       ptr(vals), stream_handle()),
+                       "spai_sell_fill_vals")
             self._sell_vals = vals
         return self._sell_vals
+
+    def sell_stats(self):
+        """(padded values, column entries, relative slices, slices)."""
+        sliceptr, cdesc, cols = self.sell()
+        return (self._pat.sell[3], cols.numel(), int((cdesc < 0).sum().item()), cdesc.numel())
 
     def matvec_sell(self, x, out=None):
         """y = A x with the SELL-32 kernel."""
@@ -302,16 +317,16 @@ class DeviceCsr:
                 f"spmv: {self.ncols} columns vs vector of {x.numel()}")
         if out is None:
             out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
-        sliceptr, cols = self.sell()
+        sliceptr, cdesc, cols = self.sell()
         vals = self.sell_values()
-        _lib.check(_lib.load().spai_sell_spmv(self.nrows, ptr(sliceptr), ptr(cols), ptr(vals),
-                                              ptr(x.contiguous()), ptr(out), stream_handle()),
-                   "spai_sell_spmv")
+        _lib.check(_lib.load().spai_sell_spmv(self.nrows, self.ncols, ptr(sliceptr), ptr(cdesc),
+                                              ptr(cols), ptr(vals), ptr(x.contiguous()),
+                                              ptr(out), stream_handle()), "spai_sell_spmv")
         return out
 
     def sell_width(self) -> int:
         """Widest SELL-32 slice in slots (cached per pattern)."""
-        sliceptr, _ = self.sell()
+        sliceptr = self.sell()[0]
         if getattr(self._pat, "sell_wmax", None) is None:
             self._pat.sell_wmax = int(((sliceptr[1:] - sliceptr[:-1]) // 32).max().item()) \
                 if sliceptr.numel() > 1 else 1
@@ -325,9 +340,10 @@ class DeviceCsr:
                 f"spmv: {self.ncols} columns vs vector of {x.numel()}")
         if out is None:
             out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
-        sliceptr, cols = self.sell()
+        sliceptr, cdesc, cols = self.sell()
         vals = self.sell_values()
-        st = _lib.check(_lib.load().spai_sell_spmv_tma(self.nrows, ptr(sliceptr), ptr(cols),
+        st = _lib.check(_lib.load().spai_sell_spmv_tma(self.nrows, self.ncols, ptr(sliceptr),
+                                                       ptr(cdesc), ptr(cols),
                                                        ptr(vals), self.sell_width(),
                                                        ptr(x.contiguous()), ptr(out),
                                                        stream_handle()), "spai_sell_spmv_tma")

@@ -55,6 +55,7 @@ with torch.cuda.stream(s):
     out["sell_layout_ms"] = timed(lambda: DeviceCsr(n, n, A.rowptr, A.colidx, A.vals).sell_values(), 2)
     out["csc_values_ms"] = timed(lambda: DeviceCsr(n, n, A.rowptr, A.colidx, A.vals, structure_of=A).csc_values(), 2)
     A.sell_values()
+    out["sell_stats"] = A.sell_stats()
     t = timed(lambda: A.matvec_sell(x, out=y), 20)
     out["spmv_sell_ms"], out["spmv_sell_gbs"] = t, sp / t / 1e6
     b = A.matvec(torch.ones(n, dtype=torch.float64, device=dev))

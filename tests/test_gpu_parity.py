@@ -306,6 +306,33 @@ def test_spmv_matches_oracle():
         pb.spmv(A, np.ones(A.ncols + 1))
 
 
+def test_sell_relative_and_explicit_slices():
+    rng = np.random.default_rng(9)
+    A = pb.assemble_q1((37, 11, 9), conv=(1.0, 2.0, 0.5))
+    dA = A.device()
+    nv, nc, nrel, ns = dA.sell_stats()
+    assert nrel == ns                    # every stencil slice is relative
+    assert nc <= 32 * ns                 # one offset table per slice, no index stream
+    x = rng.standard_normal(A.ncols)
+    yr = oracle.spmv(_ocsr(A), x)
+    y = dA.matvec_sell(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.max(np.abs(y - yr)) <= 1e-13 * np.max(np.abs(yr))
+    # same matrix forced to explicit slices
+    E = pb.DeviceCsr(A.nrows, A.ncols, dA.rowptr, dA.colidx, dA.vals)
+    E.allow_relative_sell = False
+    assert E.sell_stats()[2] == 0
+    y2 = E.matvec_sell(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.max(np.abs(y2 - yr)) <= 1e-13 * np.max(np.abs(yr))
+    # mixed: random pattern (explicit) with a band (relative)
+    R = _random_symmetric_pattern(3000, 3000, 3)
+    dR = R.device()
+    assert 0 < dR.sell_stats()[2] <= dR.sell_stats()[3]
+    xr = rng.standard_normal(R.ncols)
+    yref = oracle.spmv(_ocsr(R), xr)
+    got = dR.matvec_sell(torch.from_numpy(xr).cuda()).cpu().numpy()
+    assert np.max(np.abs(got - yref)) <= 1e-13 * np.max(np.abs(yref))
+
+
 def test_fused_dots_deterministic():
     n = 1_000_003
     g = torch.Generator(device="cuda").manual_seed(1)
