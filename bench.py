@@ -251,9 +251,14 @@ def run_ours(args):
     t_asm = statistics.mean(t for t, _, _ in times)
     t_sol = statistics.mean(t for _, t, _ in times)
     hbm, peak_kind = peaks()
-    # algorithmic bytes of one reference PCG iteration (krylov.py:315-339):
-    # A.p and M.r (12 B/stored entry + x gather 8 + y write 8 each) + vector updates
-    b_it = 24 * nnz + 104 * n
+    # compulsory bytes of one PCG iteration in the solve format (krylov.py:315-339
+    # op sequence): A.p and M.r stream 8 B per stored SELL value (the relative
+    # SELL slices carry no per-entry column index), x gather + y write per SpMV,
+    # and the vector updates -> 2 * 8 * nvals + 104 * n.  The CSR/int32 figure of
+    # SURVEY.md 8(d) (24 * nnz + 104 * n) is reported alongside.
+    nvals = A.sell_stats()[0]
+    b_it = 16 * nvals + 104 * n
+    b_it_csr = 24 * nnz + 104 * n
     solve_gbs = b_it * its / t_sol / 1e9
 
     # ---- SpMV alone (K5 plain and TMA-staged) with CUDA events
@@ -261,7 +266,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         xx = torch.rand(n, dtype=torch.float64, device=dev)
         yy = torch.empty_like(xx)
-        sp_bytes = 12 * nnz + 8 * (n + 1) + 16 * n
+        sp_bytes = 8 * nvals + 16 * n          # relative SELL: values + x + y
         for name, fn in (("sell", lambda: A.matvec_sell(xx, out=yy)),
                          ("csr", lambda: A.matvec(xx, out=yy)),
                          ("csr_tma", lambda: A.matvec_tma(xx, out=yy))):
@@ -340,7 +345,9 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "PCG iteration (pcg_v1 + pcg_u1 + pcg_v2 + pcg_u2)",
                          "achieved": solve_gbs, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": solve_gbs / hbm, "traffic": None,
-                         "algorithmic_bytes_per_iteration": b_it},
+                         "algorithmic_bytes_per_iteration": b_it,
+                         "csr_int32_bytes_per_iteration": b_it_csr,
+                         "sell_padded_values": nvals},
             "clocks": clocks,
             "gpu_launches": gpu_launches,
             "e2e": e2e,

@@ -41,22 +41,34 @@ __device__ __forceinline__ double sell_row(const Sell& A, int64_t s, int lane, c
   if (cd < 0) {
     const int32_t* __restrict__ rt = A.cols + (-cd - 1);
     const int32_t myrel = lane < w ? __ldg(rt + lane) : 0;
-    const int64_t row = s * kSell + lane;
-    const int64_t hi = A.ncols - 1;
-    auto col = [&](int kk) -> int32_t {
-      const int64_t c = row + __shfl_sync(0xffffffffu, myrel, kk);
-      return (int32_t)(c < 0 ? 0 : (c > hi ? hi : c));
-    };
-    for (; k + 4 <= w; k += 4) {
-      const int32_t c0 = col(k), c1 = col(k + 1), c2 = col(k + 2), c3 = col(k + 3);
-      const double v0 = ldg_stream(v + (k + 0) * kSell), v1 = ldg_stream(v + (k + 1) * kSell);
-      const double v2 = ldg_stream(v + (k + 2) * kSell), v3 = ldg_stream(v + (k + 3) * kSell);
-      a0 = fma(v0, xf(c0), a0);
-      a1 = fma(v1, xf(c1), a1);
-      a2 = fma(v2, xf(c2), a2);
-      a3 = fma(v3, xf(c3), a3);
+    const int64_t row0 = s * kSell;
+    const int32_t rlo = __shfl_sync(0xffffffffu, myrel, 0);
+    const int32_t rhi = __shfl_sync(0xffffffffu, myrel, w - 1);
+    if (row0 + rlo >= 0 && row0 + (kSell - 1) + rhi < A.ncols) {
+      // interior slice: no clamping, 9 values + 9 gathers in flight per lane
+      const int32_t row = (int32_t)(row0 + lane);
+      for (; k + 9 <= w; k += 9) {
+        double vv[9], xv[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) vv[u] = ldg_stream(v + (k + u) * kSell);
+#pragma unroll
+        for (int u = 0; u < 9; ++u) xv[u] = xf(row + __shfl_sync(0xffffffffu, myrel, k + u));
+#pragma unroll
+        for (int u = 0; u < 9; u += 3) {
+          a0 = fma(vv[u], xv[u], a0);
+          a1 = fma(vv[u + 1], xv[u + 1], a1);
+          a2 = fma(vv[u + 2], xv[u + 2], a2);
+        }
+      }
+      for (; k < w; ++k) a3 = fma(ldg_stream(v + k * kSell), xf(row + __shfl_sync(0xffffffffu, myrel, k)), a3);
+    } else {
+      const int64_t row = row0 + lane;
+      const int64_t hi = A.ncols - 1;
+      for (; k < w; ++k) {
+        const int64_t c = row + __shfl_sync(0xffffffffu, myrel, k);
+        a0 = fma(ldg_stream(v + k * kSell), xf((int32_t)(c < 0 ? 0 : (c > hi ? hi : c))), a0);
+      }
     }
-    for (; k < w; ++k) a0 = fma(ldg_stream(v + k * kSell), xf(col(k)), a0);
   } else {
     const int32_t* __restrict__ c = A.cols + cd + lane;
     for (; k + 4 <= w; k += 4) {

@@ -323,8 +323,14 @@ def test_sell_relative_and_explicit_slices():
     assert E.sell_stats()[2] == 0
     y2 = E.matvec_sell(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.max(np.abs(y2 - yr)) <= 1e-13 * np.max(np.abs(yr))
-    # mixed: random pattern (explicit) with a band (relative)
-    R = _random_symmetric_pattern(3000, 3000, 3)
+    # mixed: a band (relative slices) plus scattered far entries (explicit slices)
+    n = 3000
+    rows = np.concatenate([np.arange(n)] + [np.arange(n - d) for d in (1, 2)] +
+                          [np.arange(d, n) for d in (1, 2)] + [rng.integers(0, n // 3, 200)])
+    cols = np.concatenate([np.arange(n)] + [np.arange(d, n) for d in (1, 2)] +
+                          [np.arange(n - d) for d in (1, 2)] + [rng.integers(0, n, 200)])
+    key = np.unique(rows * n + cols)
+    R = pb.CsrMatrix.from_coo(n, n, key // n, key % n, rng.standard_normal(len(key)))
     dR = R.device()
     assert 0 < dR.sell_stats()[2] <= dR.sell_stats()[3]
     xr = rng.standard_normal(R.ncols)
