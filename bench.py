@@ -266,10 +266,11 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         xx = torch.rand(n, dtype=torch.float64, device=dev)
         yy = torch.empty_like(xx)
-        sp_bytes = 8 * nvals + 16 * n          # relative SELL: values + x + y
-        for name, fn in (("sell", lambda: A.matvec_sell(xx, out=yy)),
-                         ("csr", lambda: A.matvec(xx, out=yy)),
-                         ("csr_tma", lambda: A.matvec_tma(xx, out=yy))):
+        sell_bytes = 8 * nvals + 16 * n                      # relative SELL: values + x + y
+        csr_bytes = 12 * nnz + 8 * (n + 1) + 16 * n          # CSR: values + int32 cols + rowptr
+        for name, fn, sp_bytes in (("sell", lambda: A.matvec_sell(xx, out=yy), sell_bytes),
+                                   ("csr", lambda: A.matvec(xx, out=yy), csr_bytes),
+                                   ("csr_tma", lambda: A.matvec_tma(xx, out=yy), csr_bytes)):
             for _ in range(3):
                 fn()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
