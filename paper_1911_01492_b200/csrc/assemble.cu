@@ -539,7 +539,53 @@ __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int
   return true;
 }
 
-// (A) signature of every column: hash of (nj, list lengths, relative rows)
+// (A0) exact class of every CSC column: its relative row pattern (rows - c)
+__global__ void __launch_bounds__(256)
+class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __restrict__ cscrow,
+             PlanWs pw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w0; c < n; c += nw) {
+    const int64_t lo = cscptr[c];
+    const int len = (int)(cscptr[c + 1] - lo);
+    if (len > 32 || len == 0) { if (lane == 0) pw.col_class[c] = -1; continue; }
+    const int32_t rel = lane < len ? cscrow[lo + lane] - (int32_t)c : 0;
+    uint64_t h = lane < len ? mix64(((uint64_t)(lane + 1) << 32) ^ (uint32_t)rel) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    h = mix64(h ^ (uint64_t)len);
+    if (h == 0) h = 1;
+    int slot = (int)(h & (kClassTable - 1)), result = -1;
+    for (int probe = 0; probe < kClassTable; ++probe) {
+      unsigned long long prev = 0;
+      if (lane == 0) prev = atomicCAS(pw.ckeys + slot, 0ull, (unsigned long long)h);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == 0ull) {                      // new class: publish the representative
+        if (lane == 0) { atomicExch(pw.crep + slot, (int32_t)c); atomicAdd(pw.nclass, 1); }
+        result = slot;
+        break;
+      }
+      if (prev == h) {                         // same hash: compare the patterns exactly
+        int32_t r = -1;
+        if (lane == 0) {
+          volatile int32_t* rp = pw.crep + slot;
+          while ((r = *rp) < 0) {}
+        }
+        r = __shfl_sync(0xffffffffu, r, 0);
+        const int64_t rlo = cscptr[r];
+        const int rlen = (int)(cscptr[r + 1] - rlo);
+        const bool same = rlen == len &&
+                          __all_sync(0xffffffffu, lane >= len || cscrow[rlo + lane] - r == rel);
+        if (same) { result = slot; break; }
+      }
+      slot = (slot + 1) & (kClassTable - 1);
+    }
+    if (lane == 0) pw.col_class[c] = result;
+  }
+}
+
+// (A) signature of every column: (nj, J_a - k, class(J_a)) -> plan-table slot
 __global__ void __launch_bounds__(256)
 plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __restrict__ cscrow,
                 PlanWs pw, int64_t c0) {
@@ -550,26 +596,22 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
     if (nj == 0 || nj > kPlanNJ) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
-    int len = 0, c = 0;
-    int64_t clo = 0;
-    if (lane < nj) { c = cscrow[jlo + lane]; clo = cscptr[c]; len = (int)(cscptr[c + 1] - clo); }
-    int incl = len;
+    int c = 0, cls = 0, len = 0;
+    if (lane < nj) {
+      c = cscrow[jlo + lane];
+      cls = pw.col_class[c];
+      len = (int)(cscptr[c + 1] - cscptr[c]);
+    }
+    int total = len;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    if (__any_sync(0xffffffffu, lane < nj && cls < 0) || total > kPadIdx) {
+      if (lane == 0) pw.plan_slot[k] = -1;
+      continue;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total > kPadIdx) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
-    uint64_t h = 0;
-    if (lane < nj) h += mix64(((uint64_t)(0x10000 + lane) << 32) ^ (uint32_t)len);
-    for (int a = 0; a < nj; ++a) {
-      const int la = __shfl_sync(0xffffffffu, len, a);
-      const int64_t src = __shfl_sync(0xffffffffu, clo, a);
-      const int off = __shfl_sync(0xffffffffu, incl, a) - la;
-      for (int t = lane; t < la; t += 32)
-        h += mix64(((uint64_t)(off + t) << 32) ^ (uint32_t)(cscrow[src + t] - (int32_t)k));
-    }
+    uint64_t h = lane < nj ? mix64(((uint64_t)(lane + 1) << 48) ^ ((uint64_t)(uint32_t)cls << 32) ^
+                                   (uint32_t)(c - (int32_t)k))
+                           : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
     h = mix64(h ^ (uint64_t)nj);
@@ -641,9 +683,13 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
         reinterpret_cast<uint8_t*>(P + kPO_listid)[S.loff[a] + t] = (uint8_t)a;
       }
     __syncwarp();
+    if (lane < nj) {
+      const int32_t cj = cscrow[jlo + lane];
+      P[kPO_jrel + lane] = (uint32_t)(cj - (int32_t)k0);
+      P[kPO_jcls + lane] = (uint32_t)pw.col_class[cj];
+    }
     for (int e = lane; e < total; e += 32) {
       const int32_t r = S.lrow[e];
-      P[kPO_relofs + e] = (uint32_t)(r - (int32_t)k0);
       uint32_t h = ((uint32_t)r * 2654435761u) >> 23;
       while (true) {
         const int32_t prev = atomicCAS(&S.keys[h], -1, r);
@@ -826,36 +872,28 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
       continue;
     }
     const int total = (int)P[kPH_total];
-    int len = 0;
+    // exact structural match: J_a - k and the class of every J member (the class
+    // fixes column J_a's relative row pattern, hence the list and its length)
+    bool bad = false;
     int64_t clo = 0;
-    if (lane < nj) { const int c = cscrow[jlo + lane]; clo = cscptr[c]; len = (int)(cscptr[c + 1] - clo); }
-    int incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+    if (lane < nj) {
+      const int c = cscrow[jlo + lane];
+      bad = (uint32_t)(c - (int32_t)k) != P[kPO_jrel + lane] ||
+            (uint32_t)pw.col_class[c] != P[kPO_jcls + lane];
+      clo = cscptr[c];
     }
-    bool bad = lane < nj && (incl - len) != (int)P[kPO_loff + lane];
-    if (lane == 31) bad |= incl != total;
     if (total > CAPL || __any_sync(0xffffffffu, bad)) {
       if (lane == 0) direct[atomicAdd(ndirect, 1)] = (int32_t)k;
       continue;
     }
-    if (lane < nj) lsrc[lane] = clo - (incl - len);      // entry e of list a sits at lsrc[a] + e
+    if (lane < nj) lsrc[lane] = clo - (int64_t)P[kPO_loff + lane];   // entry e of list a: lsrc[a] + e
     __syncwarp();
     const uint8_t* listid = reinterpret_cast<const uint8_t*>(P + kPO_listid);
-    const uint32_t* relofs = P + kPO_relofs;
     for (int e = lane; e < total; e += 32) {
       const int64_t q = lsrc[listid[e]] + e;
-      const int32_t r = cscrow[q];
-      bad |= (uint32_t)(r - (int32_t)k) != relofs[e];
       lval[e] = cscval ? cscval[q] : vals[csc2csr[q]];
     }
     for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
-    if (__any_sync(0xffffffffu, bad)) {
-      if (lane == 0) direct[atomicAdd(ndirect, 1)] = (int32_t)k;
-      continue;
-    }
     __syncwarp();
     // product program; padding ops multiply the zero slot and never store
     const uint32_t* ops = P + kPO_ops + lane;
@@ -952,22 +990,22 @@ __global__ void csc_to_csr_kernel(int64_t nnz, const int64_t* __restrict__ csc2c
 }
 
 // Structurally symmetric pattern: CSC position q of (row i, col k) equals the
-// CSR position of (k, i), so M^T in CSR order is m_csc itself and
-// S[p] = 0.5*(M[p] + M^T[p]) with p = csc2csr[q].
+// CSR position of (k, i), so M^T in CSR order is m_csc itself, and csc2csr is
+// an involution (the transpose permutation).  Gather form:
+//   S[p] = 0.5 * (M[p] + M^T[p]) = 0.5 * (m_csc[csc2csr[p]] + m_csc[p]),
+// coalesced writes and reads, one gathered read per entry.
 __global__ void symmetrize_kernel(int64_t nnz, const int64_t* __restrict__ csc2csr,
                                   const double* __restrict__ m_csc, double* __restrict__ s_csr) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = csc2csr[q];
-    s_csr[p] = 0.5 * (m_csc[q] + m_csc[p]);
-  }
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz;
+       p += (int64_t)gridDim.x * blockDim.x)
+    s_csr[p] = 0.5 * (m_csc[csc2csr[p]] + m_csc[p]);
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
-  return 1024 + 4 * align256((size_t)n * sizeof(int32_t)) +
-         align256((size_t)kPlanTable * 16) +
+  return 1024 + 5 * align256((size_t)n * sizeof(int32_t)) +
+         align256((size_t)kPlanTable * 16) + align256((size_t)kClassTable * 12) +
          align256((size_t)kMaxPlans * kPlanWords * sizeof(uint32_t));
 }
 
@@ -981,6 +1019,13 @@ static int assemble_all(int64_t c0, int64_t n, const double* vals, const int64_t
   const int64_t ncols = n - c0;
   if (use_plans) {
     SPAI_CUDA(cudaMemsetAsync(pw.keys, 0, (size_t)kPlanTable * 8, s));
+    SPAI_CUDA(cudaMemsetAsync(pw.ckeys, 0, (size_t)kClassTable * 8, s));
+    SPAI_CUDA(cudaMemsetAsync(pw.crep, 0xFF, (size_t)kClassTable * 4, s));
+    SPAI_CUDA(cudaMemsetAsync(pw.nclass, 0, 4, s));
+    // classes of every column referenced by the range (all columns: cheap)
+    class_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((pw.ntot * 32 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
+        pw.ntot, cscptr, cscrow, pw);
+    SPAI_LAUNCH_CHECK("class_kernel");
     plan_sig_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ncols * 32 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
         n, cscptr, cscrow, pw, c0);
     SPAI_LAUNCH_CHECK("plan_sig_kernel");
@@ -1046,19 +1091,25 @@ extern "C" int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr
   int* ndirect = (int*)(b + 20);
   pw.nplans = (int*)(b + 24);
   pw.nbuilt = (int*)(b + 28);
+  pw.nclass = (int*)(b + 32);
+  pw.ntot = n;
   unsigned char* p = b + 256;
   const size_t lb = align256((size_t)n * sizeof(int32_t));
   ws.merge_list = (int32_t*)p; p += lb;
   ws.qr_list = (int32_t*)p; p += lb;
   int32_t* direct = (int32_t*)p; p += lb;
   pw.plan_slot = (int32_t*)p; p += lb;
+  pw.col_class = (int32_t*)p; p += lb;
+  pw.ckeys = (unsigned long long*)p;
+  pw.crep = (int32_t*)(p + (size_t)kClassTable * 8);
+  p += align256((size_t)kClassTable * 12);
   pw.keys = (unsigned long long*)p;
   pw.rep = (int32_t*)(p + (size_t)kPlanTable * 8);
   pw.slot_plan = (int32_t*)(p + (size_t)kPlanTable * 12);
   p += align256((size_t)kPlanTable * 16);
   pw.plans = (uint32_t*)p;
   static const unsigned long long init_err = ~0ull;
-  SPAI_CUDA(cudaMemsetAsync(b + 8, 0, 24, s));
+  SPAI_CUDA(cudaMemsetAsync(b + 8, 0, 32, s));
   SPAI_CUDA(cudaMemcpyAsync(ws.err, &init_err, 8, cudaMemcpyHostToDevice, s));
   maxlen_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8), 256, 0, s>>>(n, cscptr, maxlen);
   SPAI_LAUNCH_CHECK("maxlen_kernel");

@@ -6,14 +6,19 @@
 // structured FEM matrix, and each of the boundary classes) therefore share
 // all index work: I_k, local ranks, the sparse overlap structure of
 // G = (A^T A)[J,J] and the position of e_k.  A plan stores that once:
-//   - loff[nj+1], listid[e], relofs[e]   (verifies a column matches exactly)
+//   - jrel[a] = J_a - k, jcls[a] = class of column J_a  (exact match key)
+//   - loff[nj+1], listid[e]
 //   - rhsidx[a]                          (entry holding A[k, J_a], or -1)
 //   - ops[t*32 + lane]                   (lane-balanced product program:
 //                                          G[p] += lval[ea] * lval[eb])
 // The numeric kernel then only gathers values, replays the product program
 // and factors G -- no hashing, sorting or searching per column.  Exact
-// verification of relofs keeps the result bit-identical in pattern semantics
-// to a from-scratch column (a mismatch sends the column to the direct path).
+// A column's structure is fixed exactly by J_k's relative offsets and the
+// *class* of every J member, where the class of a CSC column is its exact
+// relative row pattern (de-duplicated with full comparison, class_kernel).
+// The replay verifies (jrel, jcls) exactly, so a column can only use a plan
+// built from a column with identical relative structure; a mismatch sends it
+// to the direct path.
 #pragma once
 #include "common.cuh"
 
@@ -32,8 +37,10 @@ constexpr int kPH_nj = 0, kPH_total = 1, kPH_nsteps = 2;
 constexpr int kPO_loff = 4;
 constexpr int kPO_rhs = kPO_loff + kPlanNJ + 1;
 constexpr int kPO_listid = kPO_rhs + kPlanNJ;                 // uint8, packed
-constexpr int kPO_relofs = kPO_listid + kPlanCap / 4;
-constexpr int kPO_ops = kPO_relofs + kPlanCap;
+constexpr int kPO_jrel = kPO_listid + kPlanCap / 4;
+constexpr int kPO_jcls = kPO_jrel + kPlanNJ;
+constexpr int kPO_ops = kPO_jcls + kPlanNJ;
+constexpr int kClassTable = 8192;    // column-class hash table (exact de-dup)
 constexpr int kPlanWords = ((kPO_ops + 32 * kPlanSteps) + 31) & ~31;
 
 __device__ __forceinline__ uint32_t op_pack(int ea, int eb, int p, bool last) {
@@ -52,6 +59,11 @@ struct PlanWs {
   int32_t* rep;               // [kPlanTable]  representative column
   int32_t* slot_plan;         // [kPlanTable]  plan index of a slot (-1 invalid)
   int32_t* plan_slot;         // [n]           table slot of each column (-1 = direct)
+  unsigned long long* ckeys;  // [kClassTable] column-class hashes
+  int32_t* crep;              // [kClassTable] representative column (-1 until published)
+  int32_t* col_class;         // [n]           class of every column (-1 = none)
+  int* nclass;                // distinct classes
+  int64_t ntot;               // columns of the matrix (class kernel range)
   int* nplans;                // distinct signatures
   int* nbuilt;                // plans built
   uint32_t* plans;            // [kMaxPlans * kPlanWords]
