@@ -227,6 +227,30 @@ int spai_pcg_history(spai_pcg* s, double* host_out, int64_t count);
 int spai_pcg_vectors(spai_pcg* s, double** x, double** r, double** p, double** z);
 int spai_pcg_destroy(spai_pcg* s);
 
+/* ------------------------------------------------------------------ K9
+ * Device-resident right-preconditioned BiCGStab (kind 1) and preconditioned
+ * Richardson x += relax * M (b - A x) (kind 2) on SELL-32 operators; the
+ * reference has neither, their definitions are oracle/krylov.py
+ * (bicgstab_right, richardson).  x0 = 0.  Richardson stops on tol only when
+ * use_tol != 0 (else it runs maxit sweeps, e.g. as a smoother).
+ * poll: status 0 running, 1 converged, 2 maxit, 3 breakdown (kind: 1 rho=0,
+ * 2 (r^,v)=0, 3 (t,t)=0, 4 omega=0), 4 divergence.                         */
+typedef struct spai_ksolver spai_ksolver;
+size_t spai_ksolver_workspace_bytes(int64_t n, int64_t maxit);
+int spai_ksolver_create(spai_ksolver** out, int kind, int64_t n, const int64_t* sliceptr,
+                        const int64_t* cdesc, const int32_t* cols, const double* A_vals,
+                        const int64_t* m_sliceptr, const int64_t* m_cdesc,
+                        const int32_t* m_cols, const double* M_vals, double tol,
+                        int use_tol, double relax, int64_t maxit, void* ws,
+                        size_t ws_bytes, void* stream);
+int spai_ksolver_start(spai_ksolver* s, const double* b);
+int spai_ksolver_advance(spai_ksolver* s, int64_t iters);
+int spai_ksolver_poll(spai_ksolver* s, int* status, int64_t* iterations, double* norm0,
+                      double* norm, int* breakdown_kind);
+int spai_ksolver_history(spai_ksolver* s, double* host_out, int64_t count);
+int spai_ksolver_x(spai_ksolver* s, double** x);
+int spai_ksolver_destroy(spai_ksolver* s);
+
 /* ------------------------------------------------------------------ K8 multi-GPU
  * Per-rank kernels of the row-partitioned PCG (replaces RankSystem,
  * krylov.py:196-232, driving _solve_classic).  `xext` vectors are laid out

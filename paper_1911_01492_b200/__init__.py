@@ -21,8 +21,9 @@ from .precond import (IdentityPreconditioner, JacobiPreconditioner,
                       drop_exact_zeros, jacobi, make_spai1_factory,
                       pattern_sets, set_assembly_plans, spai1, spai1_device,
                       spai1_symmetric_device)
-from .krylov import (ConvergenceRecord, DevicePCG, KrylovState, LocalSystem,
-                     SolverConfig, VARIANTS, fused_dots_device,
-                     memory_accounting, reduction_rate, solve)
+from .krylov import (ConvergenceRecord, DeviceKrylov, DevicePCG, KrylovState,
+                     LocalSystem, SolverConfig, VARIANTS, bicgstab,
+                     fused_dots_device, memory_accounting, reduction_rate,
+                     richardson, solve)
 
 __version__ = "0.1.0"

@@ -53,6 +53,16 @@ _SIGS = {
     "spai_set_assembly_plans": (_i32, [_i32]),
     "spai_assemble_range": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp,
                                    _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "spai_ksolver_workspace_bytes": (_sz, [_i64, _i64]),
+    "spai_ksolver_create": (_i32, [C.POINTER(_vp), _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                   _vp, _dbl, _i32, _dbl, _i64, _vp, _sz, _vp]),
+    "spai_ksolver_start": (_i32, [_vp, _vp]),
+    "spai_ksolver_advance": (_i32, [_vp, _i64]),
+    "spai_ksolver_poll": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),
+                                 C.POINTER(_dbl), C.POINTER(_i32)]),
+    "spai_ksolver_history": (_i32, [_vp, _vp, _i64]),
+    "spai_ksolver_x": (_i32, [_vp, C.POINTER(_vp)]),
+    "spai_ksolver_destroy": (_i32, [_vp]),
     "spai_dist_scal_bytes": (_sz, []),
     "spai_dist_partials_bytes": (_sz, []),
     "spai_dist_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),

@@ -815,6 +815,7 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
       int nsteps = step;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsteps = max(nsteps, __shfl_xor_sync(0xffffffffu, nsteps, o));
+      nsteps = (nsteps + 1) & ~1;              // the replay consumes ops in pairs
       ok = nsteps <= kPlanSteps;
       if (ok)
         for (int t = step; t < nsteps; ++t) ops[t * 32 + lane] = kNop;
@@ -897,12 +898,16 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
     __syncwarp();
     // product program; padding ops multiply the zero slot and never store
     const uint32_t* ops = P + kPO_ops + lane;
-    double s = 0.0;
-#pragma unroll 4
-    for (int t = 0; t < nsteps; ++t) {
-      const uint32_t op = ops[t * 32];
-      s = fma(lval[op & 1023u], lval[(op >> 10) & 1023u], s);
-      if (op >> 31) { G[(op >> 20) & 1023u] = s; s = 0.0; }
+    // two accumulators (even / odd steps) halve the FMA dependency chain; a
+    // pair's products are consecutive steps, summed as s0 + s1 at its end
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll 2
+    for (int t = 0; t < nsteps; t += 2) {
+      const uint32_t o0 = ops[t * 32], o1 = ops[(t + 1) * 32];
+      s0 = fma(lval[o0 & 1023u], lval[(o0 >> 10) & 1023u], s0);
+      if (o0 >> 31) { G[(o0 >> 20) & 1023u] = s0 + s1; s0 = 0.0; s1 = 0.0; }
+      s1 = fma(lval[o1 & 1023u], lval[(o1 >> 10) & 1023u], s1);
+      if (o1 >> 31) { G[(o1 >> 20) & 1023u] = s0 + s1; s0 = 0.0; s1 = 0.0; }
     }
     __syncwarp();
     double y = 0.0;

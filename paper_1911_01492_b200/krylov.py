@@ -399,3 +399,127 @@ def _finish(solver, rec, cfg, status, it, norm0, norm, aux, on_device):
     rec.launched_iterations = solver.launched
     x = solver.vectors()[0].clone()
     return (x if on_device else x.cpu().numpy()), rec
+
+
+# ------------------------------------------------------------------ BiCGStab / Richardson
+_BREAKDOWN_MSG = {1: "rho = 0 in BiCGStab", 2: "(r_hat, v) = 0 in BiCGStab",
+                  3: "(t, t) = 0 in BiCGStab", 4: "omega = 0 in BiCGStab"}
+
+
+class DeviceKrylov:
+    """Owner of a native `spai_ksolver` (K9): kind 1 BiCGStab, kind 2 Richardson."""
+
+    def __init__(self, kind, A: DeviceCsr, M: DeviceCsr | None, tol, maxit, relax=1.0,
+                 use_tol=True):
+        torch = _require_cuda()
+        self.lib = _lib.load()
+        self.n, self.maxit, self.kind = A.nrows, int(maxit), kind
+        sliceptr, cdesc, cols = A.sell()
+        a_vals = A.sell_values()
+        z = C.c_void_p(0)
+        m_vals, m_sp, m_cd, m_cols = None, z, z, z
+        if M is not None:
+            if M.rowptr is A.rowptr and M.colidx is A.colidx:
+                M._pat = A._pat
+            m_vals = M.sell_values()
+            if M._pat is not A._pat:
+                msp, mcd, mc = M.sell()
+                m_sp, m_cd, m_cols = ptr(msp), ptr(mcd), ptr(mc)
+        wsb = self.lib.spai_ksolver_workspace_bytes(self.n, self.maxit)
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
+        self._keep = (sliceptr, cdesc, cols, a_vals, m_vals, M)
+        h = C.c_void_p()
+        _lib.check(self.lib.spai_ksolver_create(
+            C.byref(h), kind, self.n, ptr(sliceptr), ptr(cdesc), ptr(cols), ptr(a_vals),
+            m_sp, m_cd, m_cols, ptr(m_vals) if m_vals is not None else z, float(tol),
+            1 if use_tol else 0, float(relax), self.maxit, ptr(self.ws), wsb, stream_handle()),
+            "spai_ksolver_create")
+        self.h = h
+        self.launched = 0
+
+    def run(self, b, chunk=32):
+        _lib.check(self.lib.spai_ksolver_start(self.h, ptr(b)), "spai_ksolver_start")
+        while True:
+            st = self.poll()
+            if st[0] != 0:
+                return st
+            self.launched += chunk
+            _lib.check(self.lib.spai_ksolver_advance(self.h, chunk), "spai_ksolver_advance")
+
+    def poll(self):
+        st, it, n0, nr, bk = C.c_int(0), C.c_int64(0), C.c_double(0), C.c_double(0), C.c_int(0)
+        _lib.check(self.lib.spai_ksolver_poll(self.h, C.byref(st), C.byref(it), C.byref(n0),
+                                              C.byref(nr), C.byref(bk)), "spai_ksolver_poll")
+        return st.value, it.value, n0.value, nr.value, bk.value
+
+    def history(self, count):
+        out = np.zeros(max(count, 0))
+        if count > 0:
+            _lib.check(self.lib.spai_ksolver_history(self.h, out.ctypes.data, count),
+                       "spai_ksolver_history")
+        return out
+
+    def x(self):
+        p = C.c_void_p()
+        _lib.check(self.lib.spai_ksolver_x(self.h, C.byref(p)), "spai_ksolver_x")
+        return _wrap_device(p.value, self.n).clone()
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.spai_ksolver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _krylov_run(kind, system, b, tol, maxit, relax=1.0, use_tol=True):
+    torch = _require_cuda()
+    if isinstance(system, (CsrMatrix, DeviceCsr)):
+        system = LocalSystem(system)
+    on_device = isinstance(b, torch.Tensor) and b.is_cuda
+    bd = b.to(torch.float64).contiguous() if on_device else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(b, dtype=np.float64))).to("cuda")
+    if bd.numel() != system.n:
+        raise DimensionMismatchError("right-hand side length mismatch")
+    s = DeviceKrylov(kind, system.device_A, system.device_M(), tol, maxit, relax, use_tol)
+    try:
+        status, it, norm0, norm, bk = s.run(bd)
+        if status == 3:
+            raise BreakdownError(_BREAKDOWN_MSG.get(bk, "breakdown"))
+        if status == 4:
+            raise DivergenceError("non-finite value in solver recurrence")
+        rec = ConvergenceRecord(variant="bicgstab" if kind == 1 else "richardson")
+        rec.initial_residual = norm0
+        rec.iterations = it
+        rec.residual_norms = [float(v) for v in s.history(it)]
+        if kind == 1:
+            rec.reductions_cum = [1 + 3 * (i + 1) for i in range(it)]
+            rec.total_reductions = 1 + 3 * it
+            rec.converged = status == 1
+        else:
+            rec.reductions_cum = [i + 1 for i in range(it)]
+            rec.total_reductions = it
+            rec.converged = bool(use_tol) and norm <= tol * norm0
+        rec.overlapped_cum = [0] * it
+        rec.final_residual = norm if it > 0 else norm0
+        rec.launched_iterations = s.launched
+        x = s.x()
+        return (x if on_device else x.cpu().numpy()), rec
+    finally:
+        s.close()
+
+
+def bicgstab(system, b, tol=1e-8, maxit=1000):
+    """Right-preconditioned BiCGStab on the GPU (oracle: oracle/krylov.py bicgstab_right)."""
+    return _krylov_run(1, system, b, tol, maxit)
+
+
+def richardson(system, b, omega=1.0, maxit=100, tol=None):
+    """x += omega M (b - A x) from x0 = 0 on the GPU (oracle: oracle/krylov.py richardson).
+    With tol=None it runs exactly `maxit` sweeps (smoother use)."""
+    return _krylov_run(2, system, b, 1e-300 if tol is None else tol, maxit, omega,
+                       tol is not None)

@@ -491,3 +491,43 @@ def test_pcg_tma_and_ldg_paths_agree_with_oracle():
     _, rr = oracle.pcg_classic(_ocsr(Ah), _ocsr(Sh), b.cpu().numpy(), tol=1e-8, maxit=500)
     assert abs(rr.iterations - len(ref)) <= 1
     assert _hist_rel(ref, rr.residual_norms) <= HIST_TOL
+
+
+# ------------------------------------------------------------------ K9 BiCGStab / Richardson
+@pytest.mark.parametrize("dims,conv", [((24, 20), (4.0, -2.0)), ((12, 11, 10), (1.0, 0.5, 0.25))])
+def test_bicgstab_matches_oracle(dims, conv):
+    A = pb.assemble_q1(dims, conv=conv)
+    b = pb.make_rhs(None, A)
+    M = pb.spai1(A)
+    x, rec = pb.bicgstab(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(M)), b, tol=1e-10,
+                         maxit=500)
+    xr, rr = oracle.bicgstab_right(_ocsr(A), _ocsr(M), b, tol=1e-10, maxit=500)
+    assert rec.converged and abs(rec.iterations - rr.iterations) <= 1
+    h, hr = np.array(rec.residual_norms), np.array(rr.residual_norms)
+    m = min(len(h), len(hr))
+    head = hr[:m] > 1e-6 * rr.initial_residual
+    assert np.max(np.abs(h[:m] - hr[:m])[head] / hr[:m][head]) <= HIST_TOL
+    assert np.max(np.abs(x - 1.0)) <= 1e-7
+    assert rec.total_reductions == 1 + 3 * rec.iterations
+    # without preconditioner as well
+    _, r0 = pb.bicgstab(pb.LocalSystem(A, None), b, tol=1e-10, maxit=2000)
+    assert r0.iterations > rec.iterations
+
+
+def test_richardson_matches_oracle_fixed_sweeps():
+    """configs[0]: 2D Q1 64x64, SPAI(1)-preconditioned Richardson, fixed sweeps."""
+    A = pb.assemble_q1((64, 64))
+    b = pb.make_rhs(None, A)
+    M = pb.spai1(A)
+    x, rec = pb.richardson(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(M)), b, omega=1.0,
+                           maxit=100)
+    xr, rr = oracle.richardson(_ocsr(A), _ocsr(M), b, omega=1.0, maxit=100)
+    assert rec.iterations == 100 and not rec.converged
+    h, hr = np.array(rec.residual_norms), np.array(rr.residual_norms)
+    assert np.max(np.abs(h - hr) / hr) <= HIST_TOL
+    assert np.max(np.abs(x - xr)) <= 1e-10 * np.max(np.abs(xr))
+    # with a tolerance it stops at the oracle's iteration
+    _, rt = pb.richardson(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(M)), b, omega=1.0,
+                          maxit=5000, tol=1e-3)
+    _, rrt = oracle.richardson(_ocsr(A), _ocsr(M), b, omega=1.0, maxit=5000, tol=1e-3)
+    assert rt.converged and abs(rt.iterations - rrt.iterations) <= 1
