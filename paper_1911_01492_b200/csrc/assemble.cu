@@ -818,7 +818,8 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
       nsteps = (nsteps + 1) & ~1;              // the replay consumes ops in pairs
       ok = nsteps <= kPlanSteps;
       if (ok)
-        for (int t = step; t < nsteps; ++t) ops[t * 32 + lane] = kNop;
+        for (int t = step; t < nsteps; ++t)   // padding: 0 * 0 from the zero slot lval[total]
+          ops[t * 32 + lane] = (uint32_t)total | ((uint32_t)total << 10);
       if (lane == 0) P[kPH_nsteps] = ok ? (uint32_t)nsteps : 0xFFFFFFFFu;
     } else if (lane == 0) {
       P[kPH_nsteps] = 0xFFFFFFFFu;
@@ -837,14 +838,14 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
 template <int NJ, int CAPL>
 struct ReplaySmem {
   static constexpr size_t off_lval = 0;                          // values + zero slot 1023
-  static constexpr size_t off_G = (size_t)(kPadIdx + 1) * 8;
+  static constexpr size_t off_G = (((size_t)(CAPL + 1) * 8) + 15) & ~(size_t)15;
   static constexpr size_t off_col = (off_G + (size_t)tri(NJ) * 8 + 15) & ~(size_t)15;
   static constexpr size_t off_lsrc = off_col + 32 * 8;
   static constexpr size_t bytes = (off_lsrc + (size_t)NJ * 8 + 15) & ~(size_t)15;
 };
 
-template <int NJ, int CAPL, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 2)
+template <int NJ, int CAPL, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
 plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __restrict__ cscptr,
                    const int32_t* __restrict__ cscrow, const int64_t* __restrict__ csc2csr,
                    const double* __restrict__ cscval, double* __restrict__ m_csc, AsmWs ws,
@@ -857,7 +858,6 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
   double* G = reinterpret_cast<double*>(base + S::off_G);
   double* colbuf = reinterpret_cast<double*>(base + S::off_col);
   int64_t* lsrc = reinterpret_cast<int64_t*>(base + S::off_lsrc);
-  if (lane == 0) lval[kPadIdx] = 0.0;   // target of padding ops
   const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   for (int64_t k = c0 + gw; k < n; k += nw) {
@@ -894,6 +894,7 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
       const int64_t q = lsrc[listid[e]] + e;
       lval[e] = cscval ? cscval[q] : vals[csc2csr[q]];
     }
+    if (lane == 0) lval[total] = 0.0;     // zero slot read by the padding ops
     for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
     __syncwarp();
     // product program; padding ops multiply the zero slot and never store
@@ -923,13 +924,13 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
   }
 }
 
-template <int NJ, int CAPL, int WARPS>
+template <int NJ, int CAPL, int WARPS, int MINB>
 static int launch_replay(int64_t n, const double* vals, const int64_t* cscptr,
                          const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
                          double* m_csc, AsmWs ws, PlanWs pw, int32_t* direct, int* ndirect,
                          int64_t c0, cudaStream_t s) {
   const size_t smem = ReplaySmem<NJ, CAPL>::bytes * WARPS;
-  auto kern = plan_replay_kernel<NJ, CAPL, WARPS>;
+  auto kern = plan_replay_kernel<NJ, CAPL, WARPS, MINB>;
   SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SPAI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
@@ -1043,8 +1044,13 @@ static int assemble_all(int64_t c0, int64_t n, const double* vals, const int64_t
       plan_build_kernel<<<kPlanTable / kBuildWarps / 8, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw);
       SPAI_LAUNCH_CHECK("plan_build_kernel");
       constexpr int RNJ = NJ;
-      int st = launch_replay<RNJ, CAPL, 8>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
-                                          direct, ndirect, c0, s);
+      static int cfg = -1;
+      if (cfg < 0) { const char* e = getenv("SPAI_REPLAY_CFG"); cfg = e ? atoi(e) : 1; }
+      int st = cfg == 0
+          ? launch_replay<RNJ, CAPL, 8, 2>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
+                                           direct, ndirect, c0, s)
+          : launch_replay<RNJ, CAPL, 4, 5>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
+                                           direct, ndirect, c0, s);
       if (st) return st;
       SPAI_CUDA(cudaMemcpyAsync(&nd, ndirect, 4, cudaMemcpyDeviceToHost, s));
       SPAI_CUDA(cudaStreamSynchronize(s));

@@ -29,8 +29,7 @@ constexpr int kPlanCap = 1024;       // max gathered entries per column
 constexpr int kPlanSteps = 192;      // max product-program length per lane
 constexpr int kPlanTable = 8192;     // signature hash-table slots (power of 2)
 constexpr int kMaxPlans = 2048;
-constexpr int kPadIdx = 1023;        // zero value slot read by padding ops
-constexpr uint32_t kNop = (uint32_t)kPadIdx | ((uint32_t)kPadIdx << 10);   // 0*0, never stores
+constexpr int kPadIdx = 1023;        // max entries+1 on the plan path (pad ops read slot `total`)
 
 // plan layout in 32-bit words
 constexpr int kPH_nj = 0, kPH_total = 1, kPH_nsteps = 2;
