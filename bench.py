@@ -51,6 +51,28 @@ def parse():
     return ap.parse_args()
 
 
+def profiled_traffic():
+    """DRAM bytes per PCG iteration from the committed ncu --set full capture
+    (dram__bytes_read.sum + dram__bytes_write.sum of pcg_v1 + pcg_u1 + pcg_v2 +
+    pcg_u2 at 400^3), or None."""
+    path = os.path.join(REPO, "profiles", "r01_ncu_full_400_final.json")
+    try:
+        rows = json.load(open(path))
+    except Exception:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    seen, total = set(), 0.0
+    for r in rows:
+        name = r.get("Kernel Name", "").split("(")[0].replace("void ", "").split("<")[0]
+        if name in seen or name not in ("pcg_v1", "pcg_u1", "pcg_v2", "pcg_u2"):
+            continue
+        seen.add(name)
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            val, unit = r[key].split()
+            total += float(val) * scale[unit]
+    return total if len(seen) == 4 else None
+
+
 def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
