@@ -51,11 +51,14 @@ def parse():
     return ap.parse_args()
 
 
-def profiled_traffic():
+PROFILE_FULL = {"sell": "r01_ncu_full_400_final.json", "ssell": "r01_ncu_full_400_ssell.json"}
+
+
+def profiled_traffic(fmt):
     """DRAM bytes per PCG iteration from the committed ncu --set full capture
-    (dram__bytes_read.sum + dram__bytes_write.sum of pcg_v1 + pcg_u1 + pcg_v2 +
-    pcg_u2 at 400^3), or None."""
-    path = os.path.join(REPO, "profiles", "r01_ncu_full_400_final.json")
+    of the same operator format (dram__bytes_read.sum + dram__bytes_write.sum
+    of pcg_v1 + pcg_u1 + pcg_v2 + pcg_u2 at 400^3), or None."""
+    path = os.path.join(REPO, "profiles", PROFILE_FULL[fmt])
     try:
         rows = json.load(open(path))
     except Exception:
@@ -118,8 +121,11 @@ class Clocks:
             reasons = sorted({names[i] for r in rows for i in range(4)
                               if r[3 + i].lower() in ("active", "1", "yes")})
             load = [s for s in sm if s > 0.5 * mx] or sm
+            pw = [float(r[2]) for r in rows if r[2].replace(".", "", 1).isdigit()]
+            capped = sum(1 for r in rows if r[6].lower() in ("active", "1", "yes"))
             return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons,
-                    "samples": len(rows)}
+                    "samples": len(rows), "power_w_median": statistics.median(pw) if pw else None,
+                    "power_w_max": max(pw) if pw else None, "power_cap_samples": capped}
         except Exception as e:  # no nvidia-smi
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
 
@@ -263,6 +269,8 @@ def run_ours(args):
         total_s = t_start.elapsed_time(t_end) / 1e3
         gpu_launches = launches["n"]
     clocks = clk.summary()
+    print(json.dumps({"step_times_s": [(round(a, 4), round(b, 4), it) for a, b, it in times]}),
+          file=sys.stderr, flush=True)
     if world > 1:
         t = torch.tensor([total_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -278,7 +286,13 @@ def run_ours(args):
     # SELL slices carry no per-entry column index), x gather + y write per SpMV,
     # and the vector updates -> 2 * 8 * nvals + 104 * n.  The CSR/int32 figure of
     # SURVEY.md 8(d) (24 * nnz + 104 * n) is reported alongside.
-    nvals = A.sell_stats()[0]
+    fmt = getattr(rec, "operator_format", "sell")
+    if fmt == "ssell":
+        # symmetric half storage (K5c): each operator streams its upper-triangle
+        # values once (8 B x 32 x nslices x w); the mirrored reads hit L2
+        nvals = 32 * ((n + 31) // 32) * len(A.ssell_offsets())
+    else:
+        nvals = A.sell_stats()[0]
     b_it = 16 * nvals + 104 * n
     b_it_csr = 24 * nnz + 104 * n
     solve_gbs = b_it * its / t_sol / 1e9
@@ -288,11 +302,15 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         xx = torch.rand(n, dtype=torch.float64, device=dev)
         yy = torch.empty_like(xx)
-        sell_bytes = 8 * nvals + 16 * n                      # relative SELL: values + x + y
+        sell_bytes = 8 * A.sell_stats()[0] + 16 * n          # relative SELL: values + x + y
         csr_bytes = 12 * nnz + 8 * (n + 1) + 16 * n          # CSR: values + int32 cols + rowptr
-        for name, fn, sp_bytes in (("sell", lambda: A.matvec_sell(xx, out=yy), sell_bytes),
+        kernels = [("sell", lambda: A.matvec_sell(xx, out=yy), sell_bytes)]
+        if A.ssell_values() is not None:
+            ssell_bytes = 8 * 32 * ((n + 31) // 32) * len(A.ssell_offsets()) + 16 * n
+            kernels.insert(0, ("ssell", lambda: A.matvec_ssell(xx, out=yy), ssell_bytes))
+        for name, fn, sp_bytes in kernels + [
                                    ("csr", lambda: A.matvec(xx, out=yy), csr_bytes),
-                                   ("csr_tma", lambda: A.matvec_tma(xx, out=yy), csr_bytes)):
+                                   ("csr_tma", lambda: A.matvec_tma(xx, out=yy), csr_bytes)]:
             for _ in range(3):
                 fn()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -367,10 +385,14 @@ def run_ours(args):
             "spmv": spmv,
             "roofline": {"bound": "hbm", "kernel": "PCG iteration (pcg_v1 + pcg_u1 + pcg_v2 + pcg_u2)",
                          "achieved": solve_gbs, "peak": hbm, "peak_kind": peak_kind,
-                         "unit": "GB/s", "frac": solve_gbs / hbm, "traffic": None,
+                         "unit": "GB/s", "frac": solve_gbs / hbm,
+                         "traffic": profiled_traffic(fmt) if N == 400 else None,
+                         "traffic_source": f"profiles/{PROFILE_FULL[fmt]} "
+                                           "(ncu --set full, bytes per PCG iteration)",
                          "algorithmic_bytes_per_iteration": b_it,
                          "csr_int32_bytes_per_iteration": b_it_csr,
-                         "sell_padded_values": nvals},
+                         "operator_format": fmt,
+                         "stored_values_per_operator": nvals},
             "clocks": clocks,
             "gpu_launches": gpu_launches,
             "e2e": e2e,

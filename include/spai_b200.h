@@ -194,6 +194,33 @@ int spai_sell_spmv_tma(int64_t n, int64_t ncols, const int64_t* sliceptr,
                        const int64_t* cdesc, const int32_t* cols, const double* vals,
                        int wmax, const double* x, double* y, void* stream);
 
+/* ------------------------------------------------------------------ K5c
+ * Symmetric half-storage SELL-32 (the apply_A / apply_M of a numerically
+ * symmetric operator, sparse.py:191-202 / precond.py:121-122): only the
+ * upper-triangle entries a(i, i + g[k]) are stored, the strict lower
+ * triangle is read back from them (each value read from HBM once, its
+ * mirror read hits L2).  g[0..w) = the sorted distinct upper offsets
+ * (host array, w <= 16).                                                 */
+/* Synchronous: the distinct offsets col - row >= 0; *w = 0 when there are
+ * more than 16 (not eligible).                                           */
+int spai_ssell_offsets(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                       int32_t* g_out, int* w, void* stream);
+/* values needed for U: 32 * ceil(n / 32) * w                               */
+size_t spai_ssell_vals_count(int64_t n, int w);
+/* Synchronous: fills U and checks every strictly-lower entry against its
+ * mirror bit for bit (*is_symmetric).  The pattern must be structurally
+ * symmetric (spai_structure_is_symmetric).                                */
+int spai_ssell_fill(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                    const double* vals, const int32_t* g, int w, double* U,
+                    int* is_symmetric, void* stream);
+int spai_ssell_spmv(int64_t n, const int32_t* g, int w, const double* U,
+                    const double* x, double* y, void* stream);
+/* Same product; each warp streams its next slices' upper values into a
+ * shared-memory ring with cp.async.bulk (TMA) while it gathers.  w must be
+ * 3, 5 or 14 (other widths use spai_ssell_spmv).                          */
+int spai_ssell_spmv_tma(int64_t n, const int32_t* g, int w, const double* U,
+                          const double* x, double* y, void* stream);
+
 /* ------------------------------------------------------------------ K8
  * Device-resident classic PCG (replaces _solve_classic, krylov.py:301-345)
  * on SELL-32 operators.  M_vals = NULL means no preconditioner (apply_M =
@@ -207,6 +234,11 @@ int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
                     const int64_t* m_sliceptr, const int64_t* m_cdesc,
                     const int32_t* m_cols, const double* M_vals, double tol,
                     int64_t maxit, void* ws, size_t ws_bytes, void* stream);
+/* Same solver on symmetric half-storage operators (K5c): A_U and M_U share
+ * the offset table g (same pattern); M_U = NULL means no preconditioner.  */
+int spai_pcg_create_sym(spai_pcg** out, int64_t n, const int32_t* g, int w,
+                        const double* A_U, const double* M_U, double tol,
+                        int64_t maxit, void* ws, size_t ws_bytes, void* stream);
 /* 0 (default): 4 kernels per iteration (vector updates in their own
  * kernels, one gather per stored entry); 1: 2 kernels (vector updates
  * recomputed inside the SpMV gathers).  Same arithmetic, same results.    */

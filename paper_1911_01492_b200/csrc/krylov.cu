@@ -12,8 +12,28 @@
 // between graphs.
 #include "sell.cuh"
 #include "spmv_core.cuh"
+#include "ssell.cuh"
 
 namespace spai {
+
+// the two solve-phase operator formats behind one row() interface
+struct SellOp {
+  static constexpr int kMinBlocks = 0;   // as plain __launch_bounds__(kSpmvThreads)
+  Sell m;
+  template <class XF>
+  __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
+    return sell_row(m, s, lane, xf);
+  }
+};
+template <int WM>
+struct SymOp {
+  static constexpr int kMinBlocks = 4;
+  SymSell m;
+  template <class XF>
+  __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
+    return ssell_row<WM>(m, s, lane, xf);
+  }
+};
 
 enum { kRunning = 0, kConverged = 1, kMaxit = 2, kBreakdown = 3, kDivergence = 4 };
 
@@ -163,8 +183,9 @@ pcg_v1(int64_t n, PcgVecs v, const PcgScal* sc) {
     pnew[i] = fma(beta, pold[i], v.z[i]);
 }
 
-__global__ void __launch_bounds__(kSpmvThreads)
-pcg_u1(int64_t n, int64_t nslices, Sell A, PcgVecs v, PcgScal* sc) {
+template <class OP>
+__global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
+pcg_u1(int64_t n, int64_t nslices, OP A, PcgVecs v, PcgScal* sc) {
   if (sc->status != kRunning) return;
   const bool first = sc->it == 0;
   const int lane = threadIdx.x & 31;
@@ -176,7 +197,7 @@ pcg_u1(int64_t n, int64_t nslices, Sell A, PcgVecs v, PcgScal* sc) {
   const double* __restrict__ r = sc->rcur ? v.r1 : v.r0;
   double acc[3] = {0.0, 0.0, 0.0};
   for (int64_t s = w0; s < nslices; s += nw) {
-    const double q = sell_row(A, s, lane, [&](int32_t j) { return __ldg(p + j); });
+    const double q = A.row(s, lane, [&](int32_t j) { return __ldg(p + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) {
       v.q[i] = q;
@@ -232,9 +253,9 @@ pcg_v2(int64_t n, PcgVecs v, const PcgScal* sc) {
   }
 }
 
-template <bool HAS_M>
-__global__ void __launch_bounds__(kSpmvThreads)
-pcg_u2(int64_t n, int64_t nslices, Sell M, PcgVecs v, PcgScal* sc) {
+template <bool HAS_M, class OP>
+__global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
+pcg_u2(int64_t n, int64_t nslices, OP M, PcgVecs v, PcgScal* sc) {
   if (sc->status != kRunning) return;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
@@ -243,7 +264,7 @@ pcg_u2(int64_t n, int64_t nslices, Sell M, PcgVecs v, PcgScal* sc) {
   double acc[2] = {0.0, 0.0};
   for (int64_t s = w0; s < nslices; s += nw) {
     double zi = 0.0;
-    if (HAS_M) zi = sell_row(M, s, lane, [&](int32_t j) { return __ldg(rnew + j); });
+    if (HAS_M) zi = M.row(s, lane, [&](int32_t j) { return __ldg(rnew + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) {
       const double rn = rnew[i];
@@ -364,37 +385,39 @@ __global__ void width_max_kernel(int64_t nslices, const int64_t* sliceptr, int* 
 }
 
 // start: r = b - A x0 (or b), p = M r (or r)
-template <bool HAS_X0>
-__global__ void __launch_bounds__(kSpmvThreads)
-pcg_start_r(int64_t n, int64_t nslices, Sell A, const double* __restrict__ x,
+template <bool HAS_X0, class OP>
+__global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
+pcg_start_r(int64_t n, int64_t nslices, OP A, const double* __restrict__ x,
             const double* __restrict__ b, double* __restrict__ r) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   for (int64_t s = w0; s < nslices; s += nw) {
     double ax = 0.0;
-    if (HAS_X0) ax = sell_row(A, s, lane, [&](int32_t j) { return __ldg(x + j); });
+    if (HAS_X0) ax = A.row(s, lane, [&](int32_t j) { return __ldg(x + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) r[i] = HAS_X0 ? b[i] - ax : b[i];
   }
 }
 
-template <bool HAS_M>
-__global__ void __launch_bounds__(kSpmvThreads)
-pcg_start_p(int64_t n, int64_t nslices, Sell M, const double* __restrict__ r,
+template <bool HAS_M, class OP>
+__global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
+pcg_start_p(int64_t n, int64_t nslices, OP M, const double* __restrict__ r,
             double* __restrict__ p) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   for (int64_t s = w0; s < nslices; s += nw) {
     double mr = 0.0;
-    if (HAS_M) mr = sell_row(M, s, lane, [&](int32_t j) { return __ldg(r + j); });
+    if (HAS_M) mr = M.row(s, lane, [&](int32_t j) { return __ldg(r + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) p[i] = HAS_M ? mr : r[i];
   }
 }
 
 unsigned sell_blocks(const void* kern, int64_t nslices);
+unsigned ssell_blocks(const void* kern, int64_t nslices);
+bool make_symsell(const int32_t* g, int w, const double* U, int64_t n, SymSell* out);
 
 }  // namespace spai
 
@@ -417,6 +440,9 @@ struct spai_pcg {
   bool tma = false;     // TMA-staged SELL slices (set when the stage fits in smem)
   int wmaxA = 0, wmaxM = 0;
   size_t smemA = 0, smemM = 0;
+  bool sym = false;     // symmetric half-storage operators (ssell.cuh) for A and M
+  SymSell As{}, Ms{};
+  unsigned sblocks = 1;
   cudaGraphExec_t graph = nullptr;
 };
 
@@ -428,23 +454,38 @@ extern "C" size_t spai_pcg_workspace_bytes(int64_t n, int64_t maxit) {
          align256((size_t)num_sms() * 32 * 3 * sizeof(double)) + align256(sizeof(PcgScal)) + 256;
 }
 
+template <int WM>
+static void launch_sym_iteration(spai_pcg* s) {
+  const SymOp<WM> A{s->As}, M{s->Ms};
+  pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  pcg_u1<<<s->sblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v, s->sc);
+  pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  if (s->hasM) pcg_u2<true><<<s->sblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, M, s->v, s->sc);
+  else pcg_u2<false><<<s->sblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, M, s->v, s->sc);
+}
+
 static int launch_iteration(spai_pcg* s) {
+  if (s->sym) {
+    SPAI_SSELL_DISPATCH(s->As.w, launch_sym_iteration<WM>(s));
+    SPAI_LAUNCH_CHECK("pcg symmetric iteration");
+    return SPAI_OK;
+  }
   if (!s->fused && s->tma) {
     const unsigned g = (unsigned)num_sms();
     pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
     pcg_u1_tma<<<g, kTmaWarps * 32, s->smemA, s->stream>>>(s->n, s->nslices, s->A, s->wmaxA, s->v, s->sc);
     pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
     if (s->hasM) pcg_u2_tma<<<g, kTmaWarps * 32, s->smemM, s->stream>>>(s->n, s->nslices, s->M, s->wmaxM, s->v, s->sc);
-    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
+    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
     SPAI_LAUNCH_CHECK("pcg unfused TMA iteration");
     return SPAI_OK;
   }
   if (!s->fused) {
     pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
-    pcg_u1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v, s->sc);
+    pcg_u1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->A}, s->v, s->sc);
     pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
-    if (s->hasM) pcg_u2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
-    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
+    if (s->hasM) pcg_u2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
+    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
     SPAI_LAUNCH_CHECK("pcg unfused iteration");
     return SPAI_OK;
   }
@@ -454,6 +495,19 @@ static int launch_iteration(spai_pcg* s) {
   else pcg_k2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
   SPAI_LAUNCH_CHECK("pcg_k2");
   return SPAI_OK;
+}
+
+static void carve_workspace(spai_pcg* s, void* ws) {
+  char* p = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  const size_t vb = align256((size_t)s->n * sizeof(double));
+  double** vecs[8] = {&s->v.x, &s->v.r0, &s->v.r1, &s->v.p0, &s->v.p1, &s->v.q, &s->v.z, &s->b};
+  for (int i = 0; i < 8; ++i) { *vecs[i] = (double*)p; p += vb; }
+  s->v.hist = (double*)p;
+  p += align256((size_t)s->maxit * sizeof(double));
+  s->v.partials = (double*)p;
+  p += align256((size_t)num_sms() * 32 * 3 * sizeof(double));
+  s->sc = (PcgScal*)p;
+  s->host_init = new PcgScal();
 }
 
 extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
@@ -522,29 +576,57 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
     delete s;
     return SPAI_E_ARG;
   }
-  char* p = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  const size_t vb = align256((size_t)n * sizeof(double));
-  double** vecs[8] = {&s->v.x, &s->v.r0, &s->v.r1, &s->v.p0, &s->v.p1, &s->v.q, &s->v.z, &s->b};
-  for (int i = 0; i < 8; ++i) { *vecs[i] = (double*)p; p += vb; }
-  s->v.hist = (double*)p;
-  p += align256((size_t)maxit * sizeof(double));
-  s->v.partials = (double*)p;
-  p += align256((size_t)num_sms() * 32 * 3 * sizeof(double));
-  s->sc = (PcgScal*)p;
-  s->host_init = new PcgScal();
+  carve_workspace(s, ws);
+  *out = s;
+  return SPAI_OK;
+}
+
+// Symmetric half-storage operators (ssell.cuh): A and M share the offset
+// table g[0..w) (same pattern); M_U may be null (no preconditioner).
+extern "C" int spai_pcg_create_sym(spai_pcg** out, int64_t n, const int32_t* g, int w,
+                                   const double* A_U, const double* M_U, double tol,
+                                   int64_t maxit, void* ws, size_t ws_bytes, void* stream) {
+  if (!out || n <= 0 || maxit < 1 || !A_U) { set_error("spai_pcg_create_sym: bad arguments"); return SPAI_E_ARG; }
+  if (ws_bytes < spai_pcg_workspace_bytes(n, maxit)) { set_error("pcg workspace too small"); return SPAI_E_ARG; }
+  SymSell As, Ms;
+  if (!make_symsell(g, w, A_U, n, &As) || !make_symsell(g, w, M_U ? M_U : A_U, n, &Ms)) {
+    set_error("spai_pcg_create_sym: bad offset table");
+    return SPAI_E_ARG;
+  }
+  spai_pcg* s = new spai_pcg();
+  s->n = n;
+  s->nslices = (n + kSell - 1) / kSell;
+  s->sym = true;
+  s->As = As;
+  s->Ms = Ms;
+  s->hasM = M_U != nullptr;
+  s->tol = tol;
+  s->maxit = maxit;
+  s->stream = (cudaStream_t)stream;
+  if (s->stream == nullptr) {
+    cudaError_t e = cudaStreamCreate(&s->stream);
+    if (e != cudaSuccess) { delete s; return cuda_fail(e, "cudaStreamCreate"); }
+    s->own_stream = true;
+  }
+  SPAI_SSELL_DISPATCH(w, s->sblocks = std::min(
+      ssell_blocks((const void*)pcg_u1<SymOp<WM>>, s->nslices),
+      ssell_blocks((const void*)pcg_u2<true, SymOp<WM>>, s->nslices)));
+  s->vblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kSpmvThreads - 1) / kSpmvThreads,
+                                                                (int64_t)num_sms() * 8));
+  carve_workspace(s, ws);
   *out = s;
   return SPAI_OK;
 }
 
 extern "C" int spai_pcg_set_fused(spai_pcg* s, int fused) {
   if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
-  s->fused = fused != 0;
+  s->fused = fused != 0 && !s->sym;
   return SPAI_OK;
 }
 
 extern "C" int spai_pcg_set_tma(spai_pcg* s, int tma) {
   if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
-  s->tma = tma != 0 && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024;
+  s->tma = tma != 0 && !s->sym && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024;
   if (s->tma) {
     SPAI_CUDA(cudaFuncSetAttribute(pcg_u1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemA));
     SPAI_CUDA(cudaFuncSetAttribute(pcg_u2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemM));
@@ -552,20 +634,30 @@ extern "C" int spai_pcg_set_tma(spai_pcg* s, int tma) {
   return SPAI_OK;
 }
 
+template <class OP>
+static void launch_start(spai_pcg* s, const OP& A, const OP& M, unsigned b1, unsigned b2, bool x0) {
+  if (x0) pcg_start_r<true><<<b1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v.x, s->b, s->v.r0);
+  else pcg_start_r<false><<<b1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v.x, s->b, s->v.r0);
+  if (s->hasM) pcg_start_p<true><<<b2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, M, s->v.r0, s->v.p0);
+  else pcg_start_p<false><<<b2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, M, s->v.r0, s->v.p0);
+}
+
+template <int WM>
+static void launch_sym_start(spai_pcg* s, bool x0) {
+  launch_start(s, SymOp<WM>{s->As}, SymOp<WM>{s->Ms}, s->sblocks, s->sblocks, x0);
+}
+
 extern "C" int spai_pcg_start(spai_pcg* s, const double* b, const double* x0) {
   const size_t vb = (size_t)s->n * sizeof(double);
   SPAI_CUDA(cudaMemcpyAsync(s->b, b, vb, cudaMemcpyDeviceToDevice, s->stream));
-  if (x0) {
-    SPAI_CUDA(cudaMemcpyAsync(s->v.x, x0, vb, cudaMemcpyDeviceToDevice, s->stream));
-    pcg_start_r<true><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v.x, s->b, s->v.r0);
+  if (x0) SPAI_CUDA(cudaMemcpyAsync(s->v.x, x0, vb, cudaMemcpyDeviceToDevice, s->stream));
+  else SPAI_CUDA(cudaMemsetAsync(s->v.x, 0, vb, s->stream));
+  if (s->sym) {
+    SPAI_SSELL_DISPATCH(s->As.w, launch_sym_start<WM>(s, x0 != nullptr));
   } else {
-    SPAI_CUDA(cudaMemsetAsync(s->v.x, 0, vb, s->stream));
-    pcg_start_r<false><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v.x, s->b, s->v.r0);
+    launch_start(s, SellOp{s->A}, SellOp{s->M}, s->blocks1, s->blocks2, x0 != nullptr);
   }
-  SPAI_LAUNCH_CHECK("pcg_start_r");
-  if (s->hasM) pcg_start_p<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v.r0, s->v.p0);
-  else pcg_start_p<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v.r0, s->v.p0);
-  SPAI_LAUNCH_CHECK("pcg_start_p");
+  SPAI_LAUNCH_CHECK("pcg_start");
   PcgScal* h = s->host_init;   // lives as long as the solver: safe for the async copy
   *h = PcgScal{};
   h->tol = s->tol;

@@ -215,18 +215,41 @@ _STATUS = {0: "running", 1: "converged", 2: "maxit", 3: "breakdown", 4: "diverge
 class DevicePCG:
     """Owner of a native `spai_pcg` solver (C-ABI K8)."""
 
-    def __init__(self, A: DeviceCsr, M: DeviceCsr | None, tol: float, maxit: int):
+    def __init__(self, A: DeviceCsr, M: DeviceCsr | None, tol: float, maxit: int,
+                 symmetric: bool | None = None):
+        """symmetric: None = use the half-storage operators (K5c) when A and M
+        are bit-for-bit symmetric on one pattern; False = always SELL-32."""
         torch = _require_cuda()
         self.lib = _lib.load()
         self.A, self.M = A, M
         self.n = A.nrows
         self.maxit = int(maxit)
+        self.launched = 0
+        if M is not None and M.rowptr is A.rowptr and M.colidx is A.colidx:
+            M._pat = A._pat
+        # symmetric operators on one pattern: half-storage SELL (K5c)
+        g = A.ssell_offsets() if symmetric is not False else None
+        a_u = A.ssell_values() if g else None
+        m_u = M.ssell_values() if (a_u is not None and M is not None and M._pat is A._pat) \
+            else None
+        self.symmetric = a_u is not None and (M is None or m_u is not None)
+        if self.symmetric:
+            wsb = self.lib.spai_pcg_workspace_bytes(self.n, self.maxit)
+            self.ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
+            garr = (C.c_int32 * len(g))(*g)
+            self._keep = (a_u, m_u, M, garr)
+            h = C.c_void_p()
+            st = self.lib.spai_pcg_create_sym(
+                C.byref(h), A.nrows, C.cast(garr, C.c_void_p), len(g), ptr(a_u),
+                ptr(m_u) if m_u is not None else C.c_void_p(0), float(tol), self.maxit,
+                ptr(self.ws), wsb, stream_handle())
+            _lib.check(st, "spai_pcg_create_sym")
+            self.h = h
+            return
         sliceptr, cdesc, cols = A.sell()
         a_vals = A.sell_values()
         z = C.c_void_p(0)
         if M is not None:
-            if M.rowptr is A.rowptr and M.colidx is A.colidx:
-                M._pat = A._pat
             m_vals = M.sell_values()
             if M._pat is A._pat:
                 m_sp, m_cd, m_cols = z, z, z
@@ -397,6 +420,7 @@ def _finish(solver, rec, cfg, status, it, norm0, norm, aux, on_device):
     rec.total_reductions = 2 * noted + (1 if early else 0)
     rec.total_overlapped = 0
     rec.launched_iterations = solver.launched
+    rec.operator_format = "ssell" if getattr(solver, "symmetric", False) else "sell"
     x = solver.vectors()[0].clone()
     return (x if on_device else x.cpu().numpy()), rec
 
@@ -419,8 +443,6 @@ class DeviceKrylov:
         z = C.c_void_p(0)
         m_vals, m_sp, m_cd, m_cols = None, z, z, z
         if M is not None:
-            if M.rowptr is A.rowptr and M.colidx is A.colidx:
-                M._pat = A._pat
             m_vals = M.sell_values()
             if M._pat is not A._pat:
                 msp, mcd, mc = M.sell()

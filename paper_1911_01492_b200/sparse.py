@@ -148,10 +148,10 @@ class CsrMatrix:
 
 
 class _PatternCache:
-    __slots__ = ("csc", "sym", "tiles", "sell", "sell_wmax")
+    __slots__ = ("csc", "sym", "tiles", "sell", "sell_wmax", "ssell")
 
     def __init__(self):
-        self.csc = self.sym = self.tiles = self.sell = self.sell_wmax = None
+        self.csc = self.sym = self.tiles = self.sell = self.sell_wmax = self.ssell = None
 
 
 class DeviceCsr:
@@ -169,6 +169,7 @@ class DeviceCsr:
         self._pat = structure_of._pat if structure_of is not None else _PatternCache()
         self._sell_vals = None
         self._cscval = None
+        self._ssell_vals = None
 
     @classmethod
     def from_host(cls, A: CsrMatrix) -> "DeviceCsr":
@@ -349,6 +350,66 @@ class DeviceCsr:
                                                        stream_handle()), "spai_sell_spmv_tma")
         if st != _lib.SPAI_OK:
             raise _lib.NativeLibraryError(_lib.last_error())
+        return out
+
+    # K5c: symmetric half-storage SELL-32 (numerically symmetric operators)
+    allow_symmetric_sell = True
+
+    def ssell_offsets(self):
+        """Sorted upper offsets g (tuple) of the half-storage layout, or None when
+        the pattern is not eligible (not square / not structurally symmetric /
+        more than 16 distinct offsets).  Cached per pattern."""
+        if self._pat.ssell is None:
+            if not self.allow_symmetric_sell or self.nrows != self.ncols or self.nrows == 0 \
+                    or not self.structurally_symmetric():
+                self._pat.ssell = ()
+            else:
+                g = (C.c_int32 * 16)()
+                w = C.c_int(0)
+                _lib.check(_lib.load().spai_ssell_offsets(
+                    self.nrows, ptr(self.rowptr), ptr(self.colidx), C.cast(g, C.c_void_p),
+                    C.byref(w), stream_handle()), "spai_ssell_offsets")
+                self._pat.ssell = tuple(g[k] for k in range(w.value))
+        return self._pat.ssell or None
+
+    def ssell_values(self):
+        """Half-storage values U (device tensor), or None when this matrix is not
+        numerically symmetric bit for bit (cached)."""
+        if self._ssell_vals is None:
+            g = self.ssell_offsets()
+            if g is None:
+                self._ssell_vals = False
+            else:
+                torch = _require_cuda()
+                lib = _lib.load()
+                cnt = lib.spai_ssell_vals_count(self.nrows, len(g))
+                U = torch.empty(max(cnt, 1), dtype=torch.float64, device=self.vals.device)
+                garr = (C.c_int32 * len(g))(*g)
+                ok = C.c_int(0)
+                _lib.check(lib.spai_ssell_fill(self.nrows, ptr(self.rowptr), ptr(self.colidx),
+                                               ptr(self.vals), C.cast(garr, C.c_void_p), len(g),
+                                               ptr(U), C.byref(ok), stream_handle()),
+                           "spai_ssell_fill")
+                self._ssell_vals = U if ok.value else False
+        return self._ssell_vals if self._ssell_vals is not False else None
+
+    def matvec_ssell(self, x, out=None, tma=False):
+        """y = A x with the symmetric half-storage kernel (K5c); tma selects the
+        TMA-staged variant."""
+        torch = _require_cuda()
+        if x.numel() != self.ncols:
+            raise DimensionMismatchError(
+                f"spmv: {self.ncols} columns vs vector of {x.numel()}")
+        U = self.ssell_values()
+        if U is None:
+            raise ValueError("matrix is not eligible for symmetric half storage")
+        if out is None:
+            out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
+        g = self.ssell_offsets()
+        garr = (C.c_int32 * len(g))(*g)
+        fn = _lib.load().spai_ssell_spmv_tma if tma else _lib.load().spai_ssell_spmv
+        _lib.check(fn(self.nrows, C.cast(garr, C.c_void_p), len(g), ptr(U), ptr(x.contiguous()),
+                      ptr(out), stream_handle()), "spai_ssell_spmv")
         return out
 
     def tiles(self):

@@ -56,6 +56,11 @@ with torch.cuda.stream(s):
     out["csc_values_ms"] = timed(lambda: DeviceCsr(n, n, A.rowptr, A.colidx, A.vals, structure_of=A).csc_values(), 2)
     A.sell_values()
     out["sell_stats"] = A.sell_stats()
+    if A.ssell_values() is not None:
+        w = len(A.ssell_offsets())
+        t = timed(lambda: A.matvec_ssell(x, out=y), 20)
+        out["spmv_ssell_ms"] = t
+        out["spmv_ssell_gbs"] = (8 * w * 32 * ((n + 31) // 32) + 16 * n) / t / 1e6
     t = timed(lambda: A.matvec_sell(x, out=y), 20)
     out["spmv_sell_ms"], out["spmv_sell_gbs"] = t, sp / t / 1e6
     b = A.matvec(torch.ones(n, dtype=torch.float64, device=dev))
@@ -71,8 +76,9 @@ with torch.cuda.stream(s):
     t = e0.elapsed_time(e1) / 256
     t = timed(lambda: A.matvec_sell_tma(x, out=y), 20)
     out["spmv_sell_tma_ms"], out["spmv_sell_tma_gbs"] = t, sp / t / 1e6
-    for fused, tma in ((False, True), (False, False), (True, False)):
-        pu = DevicePCG(A, S, 1e-30, 100000)
+    for fused, tma, sym in ((False, True, False), (False, False, False), (True, False, False),
+                            (False, False, None)):
+        pu = DevicePCG(A, S, 1e-30, 100000, symmetric=sym)
         pu.set_fused(fused)
         pu.set_tma(tma)
         pu.start(b)
@@ -82,7 +88,8 @@ with torch.cuda.stream(s):
         pu.advance(128)
         e1.record(s)
         e1.synchronize()
-        out[f"pcg_iter_ms_fused{int(fused)}_tma{int(tma)}"] = e0.elapsed_time(e1) / 128
+        out[f"pcg_iter_ms_fused{int(fused)}_tma{int(tma)}_sym{int(sym is None)}"] = \
+            e0.elapsed_time(e1) / 128
         pu.close()
     st = pcg.poll()
     b_it = 24 * nnz + 16 * (n + 1) + 88 * n

@@ -339,6 +339,61 @@ def test_sell_relative_and_explicit_slices():
     assert np.max(np.abs(got - yref)) <= 1e-13 * np.max(np.abs(yref))
 
 
+@pytest.mark.parametrize("make,w", [
+    (lambda: pb.assemble_poisson(pb.StructuredGrid(50, 40)), 3),
+    (lambda: pb.assemble_q1((100, 90)), 5),
+    (lambda: pb.assemble_q1((33, 21, 9)), 14),
+    (lambda: pb.assemble_q1((40, 40, 40), eps=(1.0, 1e-2, 1.0)), 14),
+    (lambda: pb.assemble_q1((1, 1, 1)), 1),
+    (lambda: pb.assemble_q1((31, 1, 1)), 2),
+])
+def test_symmetric_half_storage_spmv(make, w):
+    """K5c: upper-triangle storage, mirror read back; same product as CSR."""
+    rng = np.random.default_rng(11)
+    A = make()
+    dA = A.device()
+    g = dA.ssell_offsets()
+    assert g is not None and len(g) == w and list(g) == sorted(g) and g[0] == 0
+    U = dA.ssell_values()
+    assert U is not None
+    assert U.numel() == 32 * ((A.nrows + 31) // 32) * w
+    x = rng.standard_normal(A.ncols)
+    yr = oracle.spmv(_ocsr(A), x)
+    for tma in (False, True):
+        y = dA.matvec_ssell(torch.from_numpy(x).cuda(), tma=tma).cpu().numpy()
+        assert np.max(np.abs(y - yr)) <= 1e-13 * max(np.max(np.abs(yr)), 1.0)
+    # the SPAI(1) preconditioner is symmetric bit for bit, shares the table
+    if A.nrows > 1:
+        S = pb.spai1_symmetric_device(dA)
+        assert S.ssell_offsets() == g and S.ssell_values() is not None
+        ys = S.matvec_ssell(torch.from_numpy(x).cuda()).cpu().numpy()
+        ysr = oracle.spmv(_ocsr(S.to_host()), x)
+        assert np.max(np.abs(ys - ysr)) <= 1e-13 * max(np.max(np.abs(ysr)), 1.0)
+
+
+def test_symmetric_half_storage_rejects_ineligible():
+    # numerically nonsymmetric (convection): same pattern, no half storage
+    C_ = pb.assemble_q1((12, 11, 10), conv=(1.0, 0.5, 0.25)).device()
+    assert C_.ssell_offsets() is not None and C_.ssell_values() is None
+    # one flipped value breaks bit-exact symmetry
+    A = pb.assemble_q1((20, 20)).device()
+    v = A.vals.clone()
+    v[4] = v[4] * (1 + 1e-15)          # entry (1, 0): its mirror (0, 1) keeps the old value
+    B = A.with_values(v)
+    assert A.ssell_values() is not None and B.ssell_values() is None
+    # more than 16 distinct upper offsets
+    R = _random_symmetric_pattern(500, 4000, 5, dense_cols=())
+    assert R.device().ssell_offsets() is None
+    # PCG falls back to SELL-32 for the nonsymmetric-valued M
+    from paper_1911_01492_b200.krylov import DevicePCG
+    s = DevicePCG(A, B, 1e-8, 100)
+    assert not s.symmetric
+    s.close()
+    s = DevicePCG(A, A, 1e-8, 100)
+    assert s.symmetric
+    s.close()
+
+
 def test_fused_dots_deterministic():
     n = 1_000_003
     g = torch.Generator(device="cuda").manual_seed(1)
@@ -474,16 +529,18 @@ def test_pcg_tma_and_ldg_paths_agree_with_oracle():
     S = pb.spai1_symmetric_device(A)
     b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
     hists = {}
-    for tma, fused in ((True, False), (False, False), (False, True)):
-        s = DevicePCG(A, S, 1e-8, 500)
+    for tma, fused, sym in ((True, False, False), (False, False, False), (False, True, False),
+                            (False, False, None)):
+        s = DevicePCG(A, S, 1e-8, 500, symmetric=sym)
+        assert s.symmetric == (sym is None)
         s.set_fused(fused)
         s.set_tma(tma)
         s.start(b)
         st = s.run()
         assert st[0] == 1
-        hists[(tma, fused)] = s.history(st[1])
+        hists[(tma, fused, sym)] = s.history(st[1])
         s.close()
-    ref = hists[(True, False)]
+    ref = hists[(True, False, False)]
     for k, h in hists.items():
         assert len(h) == len(ref)
         assert np.max(np.abs(h - ref) / ref) <= 1e-10, k
