@@ -640,7 +640,7 @@ struct BuildSmem {
   uint32_t mask[kPlanNJ * 8];
   uint16_t pre[kPlanNJ * 8];
   int16_t cnt[tri(kPlanNJ)];
-  uint8_t assign[tri(kPlanNJ)];
+  int16_t order[tri(kPlanNJ)];
   int32_t loff[kPlanNJ + 1];
   int32_t loads[32];
   int64_t lsrc[kPlanNJ];
@@ -760,7 +760,8 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
       if (lane <= nj) P[kPO_loff + lane] = (uint32_t)S.loff[lane];
       if (lane == 0) P[kPO_loff + nj] = (uint32_t)total;
       __syncwarp();
-      // overlap count per pair, then longest-processing-time lane assignment
+      // overlap count per pair; the nonzero ones sorted by count (descending)
+      // and dealt 32 per round
       const int np = tri(nj);
       int maxc = 0;
       for (int p = lane; p < np; p += 32) {
@@ -776,51 +777,54 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
       for (int o = 16; o > 0; o >>= 1) maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, o));
       __syncwarp();
       if (lane == 0) {
-        for (int l = 0; l < 32; ++l) S.loads[l] = 0;
-        for (int p = 0; p < np; ++p) S.assign[p] = 255;
+        int pos = 0;
         for (int c = maxc; c >= 1; --c)
           for (int p = 0; p < np; ++p)
-            if (S.cnt[p] == c) {
-              int best = 0;
-              for (int l = 1; l < 32; ++l) if (S.loads[l] < S.loads[best]) best = l;
-              S.assign[p] = (uint8_t)best;
-              S.loads[best] += c;
-            }
+            if (S.cnt[p] == c) S.order[pos++] = (int16_t)p;
+        S.loads[0] = pos;
       }
       __syncwarp();
-      // emit the product program of this lane
-      int step = 0;
+      const int nent = S.loads[0];
+      const int nrounds = (nent + 31) / 32;
+      uint16_t* rdst = reinterpret_cast<uint16_t*>(P + kPO_rdst);
       uint32_t* ops = P + kPO_ops;
-      for (int p = 0; p < np; ++p) {
-        if (S.assign[p] != lane) continue;
-        int a, b;
-        tri_decode(p, a, b);
-        int remaining = S.cnt[p];
+      int t0 = 0;
+      for (int r = 0; r < nrounds; ++r) {
+        const int len = (S.cnt[S.order[32 * r]] + 1) & ~1;   // even: replayed in pairs
+        if (lane == 0) P[kPO_rlen + r] = (uint32_t)len;
+        const int e = 32 * r + lane;
+        const int p = e < nent ? S.order[e] : -1;
+        rdst[r * 32 + lane] = p >= 0 ? (uint16_t)p : (uint16_t)0xFFFF;
+        int step = 0;
+        if (p >= 0 && t0 + len <= kPlanSteps) {
+          int a, b;
+          tri_decode(p, a, b);
 #pragma unroll
-        for (int wd = 0; wd < 8; ++wd) {
-          const uint32_t ma = S.mask[a * 8 + wd], mb = S.mask[b * 8 + wd];
-          uint32_t both = ma & mb;
-          while (both) {
-            const int bit = __ffs(both) - 1;
-            both &= both - 1u;
-            const uint32_t below = (1u << bit) - 1u;
-            const int ea = S.loff[a] + S.pre[a * 8 + wd] + __popc(ma & below);
-            const int eb = S.loff[b] + S.pre[b * 8 + wd] + __popc(mb & below);
-            --remaining;
-            if (step < kPlanSteps) ops[step * 32 + lane] = op_pack(ea, eb, p, remaining == 0);
-            ++step;
+          for (int wd = 0; wd < 8; ++wd) {
+            const uint32_t ma = S.mask[a * 8 + wd], mb = S.mask[b * 8 + wd];
+            uint32_t both = ma & mb;
+            while (both) {
+              const int bit = __ffs(both) - 1;
+              both &= both - 1u;
+              const uint32_t below = (1u << bit) - 1u;
+              const int ea = S.loff[a] + S.pre[a * 8 + wd] + __popc(ma & below);
+              const int eb = S.loff[b] + S.pre[b * 8 + wd] + __popc(mb & below);
+              ops[(t0 + step) * 32 + lane] = op_pack(ea, eb);
+              ++step;
+            }
           }
         }
+        // padding: 0 * 0 from the zero slot lval[total]
+        for (; step < len && t0 + step < kPlanSteps; ++step)
+          ops[(t0 + step) * 32 + lane] = op_pack(total, total);
+        t0 += len;
       }
-      int nsteps = step;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nsteps = max(nsteps, __shfl_xor_sync(0xffffffffu, nsteps, o));
-      nsteps = (nsteps + 1) & ~1;              // the replay consumes ops in pairs
-      ok = nsteps <= kPlanSteps;
-      if (ok)
-        for (int t = step; t < nsteps; ++t)   // padding: 0 * 0 from the zero slot lval[total]
-          ops[t * 32 + lane] = (uint32_t)total | ((uint32_t)total << 10);
-      if (lane == 0) P[kPH_nsteps] = ok ? (uint32_t)nsteps : 0xFFFFFFFFu;
+      ok = t0 <= kPlanSteps;
+      if (lane == 0) {
+        P[kPH_nsteps] = ok ? (uint32_t)t0 : 0xFFFFFFFFu;
+        P[kPH_nrounds] = (uint32_t)nrounds;
+        P[kPO_rlen + nrounds] = 0u;
+      }
     } else if (lane == 0) {
       P[kPH_nsteps] = 0xFFFFFFFFu;
     }
@@ -897,18 +901,31 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
     if (lane == 0) lval[total] = 0.0;     // zero slot read by the padding ops
     for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
     __syncwarp();
-    // product program; padding ops multiply the zero slot and never store
-    const uint32_t* ops = P + kPO_ops + lane;
-    // two accumulators (even / odd steps) halve the FMA dependency chain; a
-    // pair's products are consecutive steps, summed as s0 + s1 at its end
-    double s0 = 0.0, s1 = 0.0;
+    // product program in rounds (plan.cuh): every lane accumulates one G entry
+    // per round (rounds have even length: two accumulators for even / odd
+    // steps); one flat loop so the op loads run ahead across rounds
+    {
+      const uint32_t* ops = P + kPO_ops + lane;
+      const uint16_t* rdst = reinterpret_cast<const uint16_t*>(P + kPO_rdst) + lane;
+      const unsigned char* lv = reinterpret_cast<const unsigned char*>(lval);
+      int r = 0, rend = (int)P[kPO_rlen];
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll 2
-    for (int t = 0; t < nsteps; t += 2) {
-      const uint32_t o0 = ops[t * 32], o1 = ops[(t + 1) * 32];
-      s0 = fma(lval[o0 & 1023u], lval[(o0 >> 10) & 1023u], s0);
-      if (o0 >> 31) { G[(o0 >> 20) & 1023u] = s0 + s1; s0 = 0.0; s1 = 0.0; }
-      s1 = fma(lval[o1 & 1023u], lval[(o1 >> 10) & 1023u], s1);
-      if (o1 >> 31) { G[(o1 >> 20) & 1023u] = s0 + s1; s0 = 0.0; s1 = 0.0; }
+      for (int t = 0; t < nsteps; t += 2) {
+        const uint32_t o0 = ops[t * 32], o1 = ops[(t + 1) * 32];
+        s0 = fma(*reinterpret_cast<const double*>(lv + (o0 & 0xFFFFu)),
+                 *reinterpret_cast<const double*>(lv + (o0 >> 16)), s0);
+        s1 = fma(*reinterpret_cast<const double*>(lv + (o1 & 0xFFFFu)),
+                 *reinterpret_cast<const double*>(lv + (o1 >> 16)), s1);
+        if (t + 2 == rend) {
+          const uint16_t d = rdst[r * 32];
+          if (d != 0xFFFFu) G[d] = s0 + s1;
+          s0 = 0.0;
+          s1 = 0.0;
+          ++r;
+          rend += (int)P[kPO_rlen + r];
+        }
+      }
     }
     __syncwarp();
     double y = 0.0;

@@ -9,8 +9,12 @@
 //   - jrel[a] = J_a - k, jcls[a] = class of column J_a  (exact match key)
 //   - loff[nj+1], listid[e]
 //   - rhsidx[a]                          (entry holding A[k, J_a], or -1)
-//   - ops[t*32 + lane]                   (lane-balanced product program:
-//                                          G[p] += lval[ea] * lval[eb])
+//   - product program in "rounds": the G entries with a nonzero overlap are
+//     sorted by overlap length and dealt 32 per round (one per lane); round r
+//     runs rlen[r] steps (rounded up to even), step t of lane l is ops[t*32 + l] = the byte
+//     offsets of its two factors in the value list (lo | hi << 16), shorter
+//     entries padded with 0 * 0 from the zero slot, and ends with one store
+//     G[rdst[r][l]] -- no per-step bookkeeping.
 // The numeric kernel then only gathers values, replays the product program
 // and factors G -- no hashing, sorting or searching per column.  Exact
 // A column's structure is fixed exactly by J_k's relative offsets and the
@@ -32,18 +36,21 @@ constexpr int kMaxPlans = 2048;
 constexpr int kPadIdx = 1023;        // max entries+1 on the plan path (pad ops read slot `total`)
 
 // plan layout in 32-bit words
-constexpr int kPH_nj = 0, kPH_total = 1, kPH_nsteps = 2;
+constexpr int kPH_nj = 0, kPH_total = 1, kPH_nsteps = 2, kPH_nrounds = 3;
+constexpr int kMaxRounds = (kPlanNJ * (kPlanNJ + 1) / 2 + 31) / 32;   // 17
 constexpr int kPO_loff = 4;
 constexpr int kPO_rhs = kPO_loff + kPlanNJ + 1;
 constexpr int kPO_listid = kPO_rhs + kPlanNJ;                 // uint8, packed
 constexpr int kPO_jrel = kPO_listid + kPlanCap / 4;
 constexpr int kPO_jcls = kPO_jrel + kPlanNJ;
-constexpr int kPO_ops = kPO_jcls + kPlanNJ;
+constexpr int kPO_rlen = kPO_jcls + kPlanNJ;                  // [kMaxRounds]
+constexpr int kPO_rdst = kPO_rlen + kMaxRounds + 1;           // uint16 [kMaxRounds][32]
+constexpr int kPO_ops = kPO_rdst + kMaxRounds * 16;
 constexpr int kClassTable = 8192;    // column-class hash table (exact de-dup)
 constexpr int kPlanWords = ((kPO_ops + 32 * kPlanSteps) + 31) & ~31;
 
-__device__ __forceinline__ uint32_t op_pack(int ea, int eb, int p, bool last) {
-  return (uint32_t)ea | ((uint32_t)eb << 10) | ((uint32_t)p << 20) | (last ? 0x80000000u : 0u);
+__device__ __forceinline__ uint32_t op_pack(int ea, int eb) {   // byte offsets of two doubles
+  return (uint32_t)(ea * 8) | ((uint32_t)(eb * 8) << 16);
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
