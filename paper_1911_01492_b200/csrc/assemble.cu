@@ -1200,8 +1200,8 @@ extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,
 extern "C" int spai_csc_values(int64_t nnz, const int64_t* csc2csr, const double* vals,
                                double* cscval, int* identical, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  int* d = nullptr;
-  SPAI_CUDA(cudaMallocAsync(&d, sizeof(int), s));
+  int* d = small_scratch();
+  if (!d) { set_error("scratch allocation failed"); return SPAI_E_CUDA; }
   SPAI_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
   if (nnz > 0) {
     int64_t blocks = std::min<int64_t>((nnz + 255) / 256, (int64_t)num_sms() * 16);
@@ -1210,7 +1210,6 @@ extern "C" int spai_csc_values(int64_t nnz, const int64_t* csc2csr, const double
   }
   int h = 0;
   SPAI_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPAI_CUDA(cudaFreeAsync(d, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
   *identical = h ? 0 : 1;
   return SPAI_OK;

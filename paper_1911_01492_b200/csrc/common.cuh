@@ -32,6 +32,12 @@ int cuda_fail(cudaError_t e, const char* where);
 
 constexpr int kNumSMs = 148;
 
+// A small persistent device buffer (256 ints per device) for the status flags
+// that synchronous entry points read back; avoids per-call allocations (and
+// the stream-ordered pool's map / trim work).  The callers synchronise before
+// returning, so consecutive calls never overlap on it.
+int* small_scratch();
+
 inline int num_sms() {
   static int n = -1;
   if (n < 0) {

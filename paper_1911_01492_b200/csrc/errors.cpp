@@ -21,6 +21,15 @@ int cuda_fail(cudaError_t e, const char* where) {
   return SPAI_E_CUDA;
 }
 
+int* small_scratch() {
+  static int* bufs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!bufs[dev] && cudaMalloc(&bufs[dev], 256 * sizeof(int)) != cudaSuccess) bufs[dev] = nullptr;
+  return bufs[dev];
+}
+
 }  // namespace spai
 
 extern "C" const char* spai_last_error(void) { return spai::g_err; }

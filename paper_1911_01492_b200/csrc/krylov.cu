@@ -549,8 +549,8 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
     if (e && *e) s->fused = *e != '0';
   }
   {  // TMA staging: needs the widest slice of A (and M) to fit a 2-stage ring per warp
-    int* d = nullptr;
-    SPAI_CUDA(cudaMalloc(&d, 2 * sizeof(int)));
+    int* d = small_scratch();
+    if (!d) { delete s; set_error("scratch allocation failed"); return SPAI_E_CUDA; }
     SPAI_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(int), s->stream));
     const unsigned wb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((s->nslices + 255) / 256, num_sms() * 8));
     width_max_kernel<<<wb, 256, 0, s->stream>>>(s->nslices, s->A.sliceptr, d);
@@ -558,7 +558,6 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
     int h[2] = {0, 0};
     SPAI_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
     SPAI_CUDA(cudaStreamSynchronize(s->stream));
-    SPAI_CUDA(cudaFree(d));
     s->wmaxA = std::max(h[0], 1);
     s->wmaxM = std::max(h[1], 1);
     s->smemA = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(s->wmaxA);

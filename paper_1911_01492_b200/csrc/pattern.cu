@@ -102,8 +102,8 @@ static int run_pattern(int64_t n, const int64_t* cscptr, const int32_t* cscrow, 
                        cudaStream_t s) {
   if (c0 < 0 || c1 > n || c0 > c1) { set_error("bad column range [%lld, %lld)", (long long)c0, (long long)c1); return SPAI_E_ARG; }
   if (c1 == c0) return SPAI_OK;
-  int* err = nullptr;
-  SPAI_CUDA(cudaMallocAsync(&err, 2 * sizeof(int), s));
+  int* err = small_scratch();
+  if (!err) { set_error("scratch allocation failed"); return SPAI_E_CUDA; }
   int init[2] = {0, INT32_MAX};
   SPAI_CUDA(cudaMemcpyAsync(err, init, sizeof(init), cudaMemcpyHostToDevice, s));
   int64_t blocks = (c1 - c0 + kPatWarps - 1) / kPatWarps;
@@ -114,7 +114,6 @@ static int run_pattern(int64_t n, const int64_t* cscptr, const int32_t* cscrow, 
   SPAI_LAUNCH_CHECK("pattern_kernel");
   int h[2];
   SPAI_CUDA(cudaMemcpyAsync(h, err, sizeof(h), cudaMemcpyDeviceToHost, s));
-  SPAI_CUDA(cudaFreeAsync(err, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
   if (h[0] & 2) { set_error("column %d has no stored entries", h[1]); return SPAI_E_EMPTY_COLUMN; }
   if (h[0] & 1) { set_error("column %d: candidate rows exceed %d", h[1], kPatCap); return SPAI_E_UNSUPPORTED; }

@@ -173,8 +173,8 @@ extern "C" int spai_ssell_offsets(int64_t n, const int64_t* rowptr, const int32_
   *w_out = 0;
   if (n <= 0) return SPAI_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  int* d = nullptr;
-  SPAI_CUDA(cudaMallocAsync(&d, (kOffTable + 1) * sizeof(int), s));
+  int* d = small_scratch();
+  if (!d) { set_error("scratch allocation failed"); return SPAI_E_CUDA; }
   SPAI_CUDA(cudaMemsetAsync(d, 0xff, kOffTable * sizeof(int), s));
   SPAI_CUDA(cudaMemsetAsync(d + kOffTable, 0, sizeof(int), s));
   const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 8));
@@ -183,7 +183,6 @@ extern "C" int spai_ssell_offsets(int64_t n, const int64_t* rowptr, const int32_
   int h[kOffTable + 1];
   SPAI_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
-  SPAI_CUDA(cudaFreeAsync(d, s));
   if (h[kOffTable]) return SPAI_OK;   // too many distinct offsets: not eligible
   int cnt = 0;
   for (int t = 0; t < kOffTable; ++t)
@@ -208,8 +207,8 @@ extern "C" int spai_ssell_fill(int64_t n, const int64_t* rowptr, const int32_t* 
   if (!make_symsell(g, w, U, n, &A)) { set_error("ssell: bad offset table"); return SPAI_E_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   SPAI_CUDA(cudaMemsetAsync(U, 0, spai_ssell_vals_count(n, w) * sizeof(double), s));
-  int* bad = nullptr;
-  SPAI_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  int* bad = small_scratch();
+  if (!bad) { set_error("scratch allocation failed"); return SPAI_E_CUDA; }
   SPAI_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 16));
   ssell_fill_kernel<<<b, 256, 0, s>>>(n, rowptr, colidx, vals, A, U, bad);
@@ -219,7 +218,6 @@ extern "C" int spai_ssell_fill(int64_t n, const int64_t* rowptr, const int32_t* 
   int h = 1;
   SPAI_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
-  SPAI_CUDA(cudaFreeAsync(bad, s));
   *is_symmetric = h == 0;
   return SPAI_OK;
 }

@@ -295,15 +295,14 @@ extern "C" int spai_csr_transpose(int64_t nrows, int64_t ncols, int64_t nnz,
 extern "C" int spai_structure_is_symmetric(int64_t n, int64_t nnz, const int64_t* rowptr,
                                            const int32_t* colidx, const int64_t* cscptr,
                                            const int32_t* cscrow, int* is_sym) {
-  int* d = nullptr;
-  SPAI_CUDA(cudaMalloc(&d, sizeof(int)));
+  int* d = small_scratch();
+  if (!d) { set_error("scratch allocation failed"); return SPAI_E_CUDA; }
   SPAI_CUDA(cudaMemset(d, 0, sizeof(int)));
   sym_check_kernel<<<grid_for(nnz > n ? nnz : n + 1, 256), 256>>>(n, nnz, rowptr, colidx,
                                                                    cscptr, cscrow, d);
   SPAI_LAUNCH_CHECK("sym_check_kernel");
   int h = 0;
   SPAI_CUDA(cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost));
-  SPAI_CUDA(cudaFree(d));
   *is_sym = h ? 0 : 1;
   return SPAI_OK;
 }
@@ -313,8 +312,8 @@ extern "C" int spai_csr_transpose_symmetric(int64_t n, int64_t nnz, const int64_
                                             int* is_sym, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   (void)nnz;
-  int* d = nullptr;
-  SPAI_CUDA(cudaMallocAsync(&d, sizeof(int), s));
+  int* d = small_scratch();
+  if (!d) { set_error("scratch allocation failed"); return SPAI_E_CUDA; }
   SPAI_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
   if (n > 0) {
     sym_transpose_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, rowptr, colidx, csc2csr, d);
@@ -322,7 +321,6 @@ extern "C" int spai_csr_transpose_symmetric(int64_t n, int64_t nnz, const int64_
   }
   int h = 0;
   SPAI_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPAI_CUDA(cudaFreeAsync(d, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
   *is_sym = h ? 0 : 1;
   return SPAI_OK;
