@@ -22,7 +22,8 @@ from .problems import (fd5_poisson, q1_stencil, fd5_stencil, stencil_csr,
                        make_rhs_ones, Csr)
 from .spai import (transpose, pattern_sets, spai1_columns, spai1,
                    symmetrize_same_pattern, symmetrize_dense_reference)
-from .krylov import (spmv, pcg_classic, bicgstab_right, richardson,
+from .krylov import (spmv, pcg_classic, pcg_chronopoulos_gear, pcg_gropp, pcg_pipelined,
+                     PCG_VARIANTS, bicgstab_right, richardson,
                      Record, tree_sum)
 
 __all__ = [

@@ -4,6 +4,10 @@
 * `pcg_classic`   restates `krylov.py:294-345` (`_initial`, `_solve_classic`)
                   with `LocalSystem.fused_dots` = list of np.dot
                   (`krylov.py:179-183`) and `_Run.note` (`krylov.py:271-277`).
+* `pcg_chronopoulos_gear`, `pcg_gropp`, `pcg_pipelined` restate
+                  `krylov.py:348-399`, `:402-459`, `:461-535` (single-rank
+                  LocalSystem, identical op order, same reduction / overlap
+                  accounting, breakdown messages and termination rules).
 * `tree_sum`      restates `commsim.py:336-347` (ascending-rank pairwise tree).
 * `bicgstab_right`, `richardson`: NO reference exists (SPEC.md:343 lists
   BiCGStab as a non-goal; Richardson is only mentioned at SPEC.md:257).  These
@@ -37,7 +41,9 @@ class Record:
     final_residual: float = float("nan")
     residual_norms: list = field(default_factory=list)
     reductions_cum: list = field(default_factory=list)
+    overlapped_cum: list = field(default_factory=list)
     total_reductions: int = 0
+    total_overlapped: int = 0
 
 
 def spmv(A, x):
@@ -130,6 +136,208 @@ def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None):
         rho = rho_new
     converged = norm0 is not None and norm <= tol * norm0
     return finish(x, norm, it, converged)
+
+
+class _Acc:
+    """`_Run` bookkeeping (krylov.py:251-285): reduction / overlap counters."""
+
+    def __init__(self, variant):
+        self.rec = Record(variant)
+        self.red = 0
+        self.ovl = 0
+
+    def dots(self, pairs, overlapped=False):
+        self.red += 1
+        self.ovl += 1 if overlapped else 0
+        return [float(np.dot(a, b)) for a, b in pairs]
+
+    def note(self, norm):
+        if not math.isfinite(norm):
+            raise Divergence("non-finite residual norm")
+        self.rec.residual_norms.append(norm)
+        self.rec.reductions_cum.append(self.red)
+        self.rec.overlapped_cum.append(self.ovl)
+
+    def finish(self, x, nrm, its, conv):
+        r = self.rec
+        r.iterations, r.converged, r.final_residual = its, conv, nrm
+        r.total_reductions, r.total_overlapped = self.red, self.ovl
+        return x, r
+
+
+def _start(A, b, x0):
+    """`krylov.py:294-298`."""
+    b = np.asarray(b, dtype=np.float64)
+    if x0 is None:
+        return np.zeros(A.nrows), b.copy()
+    x = np.array(x0, dtype=np.float64, copy=True)
+    return x, b - spmv(A, x)
+
+
+def _apply_m(M):
+    return (lambda v: v.copy()) if M is None else (lambda v: spmv(M, v))
+
+
+def pcg_chronopoulos_gear(A, M, b, tol=1e-8, maxit=1000, x0=None):
+    """`krylov.py:348-399`: one fused reduction [(r,u),(w,u),(r,r)] per
+    iteration; the norm seen at iteration it is ||r_{it-1}||."""
+    am = _apply_m(M)
+    acc = _Acc("chronopoulos_gear")
+    x, r = _start(A, b, x0)
+    u = am(r)
+    w = spmv(A, u)
+    p = q = None
+    norm0 = None
+    gamma_prev = alpha = 0.0
+    norm = float("inf")
+    converged = False
+    it = 0
+    while it < maxit:
+        it += 1
+        gamma, delta, rr = acc.dots([(r, u), (w, u), (r, r)])
+        _finite(gamma, delta, rr)
+        norm = math.sqrt(rr)
+        if it == 1:
+            norm0 = norm
+            acc.rec.initial_residual = norm0
+            if norm0 == 0.0:
+                return acc.finish(x, 0.0, it, True)
+            beta = 0.0
+            denom = delta
+        else:
+            acc.note(norm)
+            if norm <= tol * norm0:
+                converged = True
+                break
+            beta = gamma / gamma_prev
+            denom = delta - beta * gamma / alpha
+        if denom <= 0.0:
+            if gamma == 0.0:
+                return acc.finish(x, norm, it, True)
+            raise Breakdown(f"indefinite curvature estimate {denom}")
+        alpha = gamma / denom
+        if it == 1:
+            p, q = u.copy(), w.copy()
+        else:
+            p = u + beta * p
+            q = w + beta * q
+        x = x + alpha * p
+        r = r - alpha * q
+        u = am(r)
+        w = spmv(A, u)
+        gamma_prev = gamma
+    return acc.finish(x, norm, it, converged)
+
+
+def pcg_gropp(A, M, b, tol=1e-8, maxit=1000, x0=None):
+    """`krylov.py:402-459`: two overlapped reductions per iteration."""
+    am = _apply_m(M)
+    acc = _Acc("gropp")
+    x, r = _start(A, b, x0)
+    u = am(r)
+    p = u.copy()
+    s = spmv(A, p)
+    norm0 = None
+    gamma = 0.0
+    norm = float("inf")
+    it = 0
+    while it < maxit:
+        if norm0 is not None and norm <= tol * norm0:
+            break
+        it += 1
+        if it == 1:
+            vals = acc.dots([(p, s), (r, u), (r, r)], overlapped=True)
+        else:
+            vals = acc.dots([(p, s)], overlapped=True)
+        t = am(s)
+        if it == 1:
+            delta, gamma, rr0 = vals
+            norm0 = math.sqrt(rr0)
+            acc.rec.initial_residual = norm0
+            if norm0 == 0.0:
+                return acc.finish(x, 0.0, it, True)
+        else:
+            delta = vals[0]
+        _finite(delta, gamma)
+        if delta <= 0.0:
+            if gamma == 0.0:
+                return acc.finish(x, norm if it > 1 else norm0, it, True)
+            raise Breakdown(f"indefinite curvature <p,Ap> = {delta}")
+        lam = gamma / delta
+        x = x + lam * p
+        r = r - lam * s
+        u = u - lam * t
+        gamma_new, rr = acc.dots([(r, u), (r, r)], overlapped=True)
+        t = spmv(A, u)
+        _finite(gamma_new, rr)
+        norm = math.sqrt(rr)
+        acc.note(norm)
+        beta = gamma_new / gamma
+        p = u + beta * p
+        s = t + beta * s
+        gamma = gamma_new
+    converged = norm0 is not None and norm <= tol * norm0
+    return acc.finish(x, norm, it, converged)
+
+
+def pcg_pipelined(A, M, b, tol=1e-8, maxit=1000, x0=None):
+    """`krylov.py:461-535`: one overlapped reduction per iteration, the
+    recurrences for M r, A M r, M A M r, A M A M r carried alongside."""
+    am = _apply_m(M)
+    acc = _Acc("pipelined")
+    x, r = _start(A, b, x0)
+    p = am(r)
+    q = spmv(A, p)
+    pending = acc.dots([(p, r), (p, q), (r, r)], overlapped=True)
+    s = am(q)
+    t = spmv(A, s)
+    z, w = p.copy(), q.copy()
+    u = v = None
+    norm0 = None
+    rho_prev = alpha_prev = 0.0
+    norm = float("inf")
+    converged = False
+    it = 0
+    while it < maxit:
+        it += 1
+        rho, alpha_tilde, rr = pending
+        _finite(rho, alpha_tilde, rr)
+        norm = math.sqrt(rr)
+        if it == 1:
+            norm0 = norm
+            acc.rec.initial_residual = norm0
+            if norm0 == 0.0:
+                return acc.finish(x, 0.0, it, True)
+            alpha = alpha_tilde
+        else:
+            acc.note(norm)
+            if norm <= tol * norm0:
+                converged = True
+                break
+            ratio = rho / rho_prev
+            alpha = alpha_tilde - alpha_prev * ratio * ratio
+            p = z + ratio * p
+            q = w + ratio * q
+            s = v + ratio * s
+            t = u + ratio * t
+        if alpha <= 0.0:
+            if rho == 0.0:
+                return acc.finish(x, norm, it, True)
+            raise Breakdown(f"indefinite curvature estimate {alpha}")
+        lam = rho / alpha
+        x = x + lam * p
+        r = r - lam * q
+        z = z - lam * s
+        w = w - lam * t
+        pending = acc.dots([(z, r), (z, w), (r, r)], overlapped=True)
+        v = am(w)
+        u = spmv(A, v)
+        rho_prev, alpha_prev = rho, alpha
+    return acc.finish(x, norm, it, converged)
+
+
+PCG_VARIANTS = {"chronopoulos_gear": pcg_chronopoulos_gear, "gropp": pcg_gropp,
+                "pipelined": pcg_pipelined}
 
 
 def bicgstab_right(A, M, b, tol=1e-8, maxit=1000):

@@ -96,6 +96,34 @@ def solve_cases():
     return out
 
 
+def variant_cases():
+    """All four reference PCG variants (krylov.py:301-535) with sym-SPAI(1)
+    and with Jacobi, b = A*1, x0 = 0."""
+    out = {}
+    raw = {"preconditioner": {"kind": "spai1"}}
+    factory = ExperimentConfig(raw).make_precond_factory()
+    probs = {
+        "fd5_48x48": fk.assemble_poisson(fk.StructuredGrid(48, 48)),
+        "q1_3d_9x9x9": ref_csr(oracle.stencil_csr((9, 9, 9), *oracle.q1_stencil(3))),
+    }
+    for name, A in probs.items():
+        b = fk.spmv(A, np.ones(A.nrows))
+        for pre, P in (("spai", factory(A)), ("jacobi", fk.jacobi(A))):
+            for variant in fk.VARIANTS:
+                cfg = fk.SolverConfig(variant=variant, tol=1e-10, maxit=5000)
+                x, rec = fk.solve(fk.LocalSystem(A, P), b, cfg)
+                M = P.M if pre == "spai" else fk.CsrMatrix(
+                    A.nrows, A.ncols, np.arange(A.nrows + 1), np.arange(A.nrows),
+                    P.inv_diag.copy())          # inv_diag * r == diagonal spmv
+                out[(name, pre, variant)] = dict(
+                    A=A, b=b, x=x, M=M, hist=np.array(rec.residual_norms),
+                    red=np.array(rec.reductions_cum), ovl=np.array(rec.overlapped_cum),
+                    its=rec.iterations, norm0=rec.initial_residual,
+                    tred=rec.total_reductions, tovl=rec.total_overlapped,
+                    final=rec.final_residual)
+    return out
+
+
 def multirank_cases():
     """Reference multi-rank block-local SPAI runs (cli.py:234-253)."""
     from ftkrylov.cli import _solve_once
@@ -149,6 +177,22 @@ def main():
         data[f"solve/{name}/S_col"] = d["sym"].col_indices
         data[f"solve/{name}/S_ptr"] = d["sym"].row_offsets
         print(f"solve {name}: its={d['its']}")
+    for (name, pre, variant), d in variant_cases().items():
+        key = f"variant/{name}/{pre}/{variant}"
+        if variant == "classic":
+            data[f"variant/{name}/A_ptr"] = d["A"].row_offsets
+            data[f"variant/{name}/A_col"] = d["A"].col_indices
+            data[f"variant/{name}/A_val"] = d["A"].values
+            data[f"variant/{name}/b"] = d["b"]
+            M = d["M"]
+            data[f"variant/{name}/{pre}/M_ptr"] = M.row_offsets
+            data[f"variant/{name}/{pre}/M_col"] = M.col_indices
+            data[f"variant/{name}/{pre}/M_val"] = M.values
+        for k in ("x", "hist", "red", "ovl"):
+            data[f"{key}/{k}"] = d[k]
+        for k in ("its", "norm0", "tred", "tovl", "final"):
+            data[f"{key}/{k}"] = np.array(d[k])
+        print(f"variant {key}: its={d['its']}")
     for ranks, d in multirank_cases().items():
         data[f"multirank/fd5_32x32/{ranks}/hist"] = d["hist"]
         data[f"multirank/fd5_32x32/{ranks}/its"] = np.array(d["its"])

@@ -94,6 +94,33 @@ def test_pcg_matches_reference(golden):
         assert np.array_equal(np.array(rec.reductions_cum), golden[f"{pre}/red"])
 
 
+VARIANT_ORACLES = {"classic": oracle.pcg_classic,
+                   "chronopoulos_gear": oracle.pcg_chronopoulos_gear,
+                   "gropp": oracle.pcg_gropp, "pipelined": oracle.pcg_pipelined}
+
+
+@pytest.mark.parametrize("variant", list(VARIANT_ORACLES))
+def test_pcg_variants_match_reference(golden, variant):
+    """krylov.py:301-535: every variant's restatement reproduces the reference
+    run bit for bit (history, accounting, iterations, solution)."""
+    for name in ("fd5_48x48", "q1_3d_9x9x9"):
+        A = _csr(golden, f"variant/{name}")
+        b = golden[f"variant/{name}/b"]
+        for pre in ("spai", "jacobi"):
+            M = _csr(golden, f"variant/{name}/{pre}", "M")
+            key = f"variant/{name}/{pre}/{variant}"
+            x, rec = VARIANT_ORACLES[variant](A, M, b, tol=1e-10, maxit=5000)
+            assert rec.iterations == int(golden[f"{key}/its"]), key
+            assert np.array_equal(np.array(rec.residual_norms), golden[f"{key}/hist"]), key
+            assert np.array_equal(np.array(rec.reductions_cum), golden[f"{key}/red"]), key
+            if variant != "classic":
+                assert np.array_equal(np.array(rec.overlapped_cum), golden[f"{key}/ovl"]), key
+                assert rec.total_overlapped == int(golden[f"{key}/tovl"]), key
+            assert rec.total_reductions == int(golden[f"{key}/tred"]), key
+            assert rec.final_residual == float(golden[f"{key}/final"]), key
+            assert np.array_equal(x, golden[f"{key}/x"]), key
+
+
 def test_oracle_sym_spai_equals_reference_solve_input(golden):
     for name in golden_names(golden, "solve"):
         pre = f"solve/{name}"
