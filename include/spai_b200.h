@@ -259,6 +259,37 @@ int spai_pcg_history(spai_pcg* s, double* host_out, int64_t count);
 int spai_pcg_vectors(spai_pcg* s, double** x, double** r, double** p, double** z);
 int spai_pcg_destroy(spai_pcg* s);
 
+/* ------------------------------------------------------------------ K10
+ * Device-resident communication-reducing PCG variants (replace
+ * _solve_chronopoulos_gear / _solve_gropp / _solve_pipelined,
+ * krylov.py:348-535): variant 1 = chronopoulos_gear, 2 = gropp,
+ * 3 = pipelined.  Operators: SELL-32 (m_sliceptr = NULL: M shares A's
+ * layout; M_vals = NULL: no preconditioner) or, when A_U != NULL, symmetric
+ * half storage with
+ * offset table g[0..w) (M_U may be NULL).  Workspace from
+ * spai_cgv_workspace_bytes; the record (notes, reductions, overlaps,
+ * iterations, final norm, breakdown value) follows the reference exactly. */
+typedef struct spai_cgv spai_cgv;
+size_t spai_cgv_workspace_bytes(int64_t n, int64_t maxit);
+int spai_cgv_create(spai_cgv** out, int variant, int64_t n, const int64_t* sliceptr,
+                    const int64_t* cdesc, const int32_t* cols, const double* A_vals,
+                    const int64_t* m_sliceptr, const int64_t* m_cdesc,
+                    const int32_t* m_cols, const double* M_vals,
+                    const int32_t* g, int w, const double* A_U,
+                    const double* M_U, double tol, int64_t maxit, void* ws,
+                    size_t ws_bytes, void* stream);
+int spai_cgv_start(spai_cgv* s, const double* b, const double* x0);
+int spai_cgv_advance(spai_cgv* s, int64_t iters);
+/* state[7] = status (0 running, 1 converged, 2 maxit, 3 breakdown,
+ * 4 divergence), iterations, notes, reductions, overlapped, completed
+ * bodies, divergence kind; norms[3] = norm0, final norm, breakdown value   */
+int spai_cgv_poll(spai_cgv* s, int64_t* state, double* norms);
+/* host_out[3 * count]: residual norms, reductions_cum, overlapped_cum      */
+int spai_cgv_history(spai_cgv* s, double* host_out, int64_t count);
+/* device pointers of x r p q z w s t u v                                  */
+int spai_cgv_vectors(spai_cgv* s, double** out10);
+int spai_cgv_destroy(spai_cgv* s);
+
 /* ------------------------------------------------------------------ K9
  * Device-resident right-preconditioned BiCGStab (kind 1) and preconditioned
  * Richardson x += relax * M (b - A x) (kind 2) on SELL-32 operators; the

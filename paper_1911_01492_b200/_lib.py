@@ -97,6 +97,15 @@ _SIGS = {
     "spai_ssell_spmv_tma": (_i32, [_i64, _vp, _i32, _vp, _vp, _vp, _vp]),
     "spai_pcg_create_sym": (_i32, [C.POINTER(_vp), _i64, _vp, _i32, _vp, _vp, _dbl, _i64, _vp,
                                    _sz, _vp]),
+    "spai_cgv_workspace_bytes": (_sz, [_i64, _i64]),
+    "spai_cgv_create": (_i32, [C.POINTER(_vp), _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _vp, _vp, _i32, _vp, _vp, _dbl, _i64, _vp, _sz, _vp]),
+    "spai_cgv_start": (_i32, [_vp, _vp, _vp]),
+    "spai_cgv_advance": (_i32, [_vp, _i64]),
+    "spai_cgv_poll": (_i32, [_vp, _vp, _vp]),
+    "spai_cgv_history": (_i32, [_vp, _vp, _i64]),
+    "spai_cgv_vectors": (_i32, [_vp, _vp]),
+    "spai_cgv_destroy": (_i32, [_vp]),
     "spai_pcg_workspace_bytes": (_sz, [_i64, _i64]),
     "spai_pcg_create": (_i32, [C.POINTER(_vp), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                _dbl, _i64, _vp, _sz, _vp]),

@@ -10,30 +10,9 @@
 // tests) on the device; a status word turns later launches into no-ops, so a
 // CUDA graph of 16 iterations is replayed blindly and the host only polls
 // between graphs.
-#include "sell.cuh"
-#include "spmv_core.cuh"
-#include "ssell.cuh"
+#include "ops.cuh"
 
 namespace spai {
-
-// the two solve-phase operator formats behind one row() interface
-struct SellOp {
-  static constexpr int kMinBlocks = 0;   // as plain __launch_bounds__(kSpmvThreads)
-  Sell m;
-  template <class XF>
-  __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
-    return sell_row(m, s, lane, xf);
-  }
-};
-template <int WM>
-struct SymOp {
-  static constexpr int kMinBlocks = 4;
-  SymSell m;
-  template <class XF>
-  __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
-    return ssell_row<WM>(m, s, lane, xf);
-  }
-};
 
 enum { kRunning = 0, kConverged = 1, kMaxit = 2, kBreakdown = 3, kDivergence = 4 };
 

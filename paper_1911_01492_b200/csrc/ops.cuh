@@ -1,0 +1,45 @@
+// The two solve-phase operator formats behind one row() interface, shared
+// by the Krylov kernels: relative/explicit SELL-32 (sell.cuh) and symmetric
+// half storage (ssell.cuh).  kMinBlocks feeds __launch_bounds__.
+#pragma once
+#include "sell.cuh"
+#include "spmv_core.cuh"
+#include "ssell.cuh"
+
+namespace spai {
+
+// the two solve-phase operator formats behind one row() interface
+struct SellOp {
+  static constexpr int kMinBlocks = 0;   // as plain __launch_bounds__(kSpmvThreads)
+  Sell m;
+  template <class XF>
+  __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
+    return sell_row(m, s, lane, xf);
+  }
+};
+template <int WM>
+struct SymOp {
+  static constexpr int kMinBlocks = 4;
+  SymSell m;
+  template <class XF>
+  __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
+    return ssell_row<WM>(m, s, lane, xf);
+  }
+};
+
+
+// warp-per-slice grid-stride loop: epi(s, i, y_i) for the rows i < n
+template <class OP, class XF, class EPI>
+__device__ __forceinline__ void op_rows(const OP& A, int64_t n, int64_t nslices, const XF& xf,
+                                        const EPI& epi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
+  for (int64_t s = w0; s < nslices; s += nw) {
+    const double y = A.row(s, lane, xf);
+    const int64_t i = s * kSell + lane;
+    if (i < n) epi(i, y);
+  }
+}
+
+}  // namespace spai

@@ -20,13 +20,13 @@ from . import _lib
 from .errors import BreakdownError, DimensionMismatchError, DivergenceError
 from .precond import IdentityPreconditioner, Preconditioner, SparseMatrixPreconditioner
 from .sparse import (CsrMatrix, DeviceCsr, _require_cuda, _torch, as_device, ptr,
-                     stream_handle)
+                     share_pattern, stream_handle)
 
 VARIANTS = ("classic", "chronopoulos_gear", "gropp", "pipelined")
 _VARIANT_BUFFERS = {"classic": 4, "chronopoulos_gear": 6, "gropp": 6, "pipelined": 10}
 _REDUCTIONS_PER_ITER = {"classic": 2, "chronopoulos_gear": 1, "gropp": 2, "pipelined": 1}
 _EXTRA_OPS = {"classic": 0, "chronopoulos_gear": 1, "gropp": 2, "pipelined": 5}
-DEVICE_VARIANTS = ("classic",)
+DEVICE_VARIANTS = VARIANTS
 
 
 def _check_variant(variant):
@@ -225,8 +225,7 @@ class DevicePCG:
         self.n = A.nrows
         self.maxit = int(maxit)
         self.launched = 0
-        if M is not None and M.rowptr is A.rowptr and M.colidx is A.colidx:
-            M._pat = A._pat
+        share_pattern(A, M)
         # symmetric operators on one pattern: half-storage SELL (K5c)
         g = A.ssell_offsets() if symmetric is not False else None
         a_u = A.ssell_values() if g else None
@@ -326,6 +325,162 @@ class DevicePCG:
             pass
 
 
+_CGV_CODES = {"chronopoulos_gear": 1, "gropp": 2, "pipelined": 3}
+# the reference's KrylovState buffers per variant (krylov.py:33-38)
+_CGV_STATE = {"chronopoulos_gear": ("x", "r", "u", "w", "p", "q"),
+              "gropp": ("x", "r", "u", "p", "s", "t"),
+              "pipelined": ("x", "r", "p", "q", "z", "w", "s", "t", "u", "v")}
+_CGV_BREAKDOWN = {"chronopoulos_gear": "indefinite curvature estimate {}",
+                  "gropp": "indefinite curvature <p,Ap> = {}",
+                  "pipelined": "indefinite curvature estimate {}"}
+
+
+class DeviceCGV:
+    """Owner of a native `spai_cgv` solver (C-ABI K10): the reference's
+    communication-reducing PCG variants (krylov.py:348-535) on the device."""
+
+    def __init__(self, variant: str, A: DeviceCsr, M: DeviceCsr | None, tol: float, maxit: int,
+                 symmetric: bool | None = None):
+        torch = _require_cuda()
+        self.lib = _lib.load()
+        self.variant = variant
+        self.n = A.nrows
+        self.maxit = int(maxit)
+        self.launched = 0
+        share_pattern(A, M)
+        z = C.c_void_p(0)
+        g = A.ssell_offsets() if symmetric is not False else None
+        a_u = A.ssell_values() if g else None
+        m_u = M.ssell_values() if (a_u is not None and M is not None and M._pat is A._pat) \
+            else None
+        self.symmetric = a_u is not None and (M is None or m_u is not None)
+        wsb = self.lib.spai_cgv_workspace_bytes(self.n, self.maxit)
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
+        h = C.c_void_p()
+        if self.symmetric:
+            garr = (C.c_int32 * len(g))(*g)
+            self._keep = (a_u, m_u, M, garr)
+            args = (z, z, z, z, z, z, z, z, C.cast(garr, C.c_void_p), len(g), ptr(a_u),
+                    ptr(m_u) if m_u is not None else z)
+        else:
+            sliceptr, cdesc, cols = A.sell()
+            a_vals = A.sell_values()
+            m_vals = M.sell_values() if M is not None else None
+            m_lay = (z, z, z)
+            if M is not None and M._pat is not A._pat:
+                msp, mcd, mc = M.sell()
+                m_lay = (ptr(msp), ptr(mcd), ptr(mc))
+            self._keep = (sliceptr, cdesc, cols, a_vals, m_vals, M)
+            args = (ptr(sliceptr), ptr(cdesc), ptr(cols), ptr(a_vals), *m_lay,
+                    ptr(m_vals) if m_vals is not None else z, z, 0, z, z)
+        st = self.lib.spai_cgv_create(C.byref(h), _CGV_CODES[variant], self.n, *args, float(tol),
+                                      self.maxit, ptr(self.ws), wsb, stream_handle())
+        _lib.check(st, "spai_cgv_create")
+        self.h = h
+
+    def start(self, b, x0=None):
+        _lib.check(self.lib.spai_cgv_start(self.h, ptr(b), ptr(x0) if x0 is not None
+                                           else C.c_void_p(0)), "spai_cgv_start")
+
+    def advance(self, iters: int):
+        self.launched += int(iters)
+        _lib.check(self.lib.spai_cgv_advance(self.h, int(iters)), "spai_cgv_advance")
+
+    def poll(self):
+        """dict(status, it, notes, red, ovl, done, div_kind, norm0, norm, aux)"""
+        state = np.zeros(7, dtype=np.int64)
+        norms = np.zeros(3)
+        _lib.check(self.lib.spai_cgv_poll(self.h, state.ctypes.data, norms.ctypes.data),
+                   "spai_cgv_poll")
+        keys = ("status", "it", "notes", "red", "ovl", "done", "div_kind")
+        d = {k: int(v) for k, v in zip(keys, state)}
+        d.update(norm0=float(norms[0]), norm=float(norms[1]), aux=float(norms[2]))
+        return d
+
+    def history(self, count: int):
+        out = np.zeros(3 * max(count, 0))
+        if count > 0:
+            _lib.check(self.lib.spai_cgv_history(self.h, out.ctypes.data, count),
+                       "spai_cgv_history")
+        return out[:count], out[count:2 * count], out[2 * count:]
+
+    def state(self, names):
+        """KrylovState-ready dict of torch views of the named buffers."""
+        arr = (C.c_void_p * 10)()
+        _lib.check(self.lib.spai_cgv_vectors(self.h, C.cast(arr, C.c_void_p)), "spai_cgv_vectors")
+        order = ("x", "r", "p", "q", "z", "w", "s", "t", "u", "v")
+        return {k: _wrap_device(arr[order.index(k)], self.n) for k in names}
+
+    def run(self, chunk: int = 64):
+        while True:
+            st = self.poll()
+            if st["status"] != 0:
+                return st
+            self.advance(chunk)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.spai_cgv_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _solve_variant(system, bd, cfg, x0d, callback, on_device):
+    """krylov.py:235-248 for the non-classic variants, on the device (K10)."""
+    solver = DeviceCGV(cfg.variant, system.device_A, system.device_M(), cfg.tol, cfg.maxit)
+    try:
+        solver.start(bd, x0d)
+        rec = ConvergenceRecord(variant=cfg.variant,
+                                vector_memory_units=memory_accounting(cfg.variant),
+                                extra_vector_ops_units=_EXTRA_OPS[cfg.variant])
+        names = _CGV_STATE[cfg.variant]
+        if callback is None:
+            st = solver.run()
+        else:
+            seen = 0
+            while True:
+                st = solver.poll()
+                if st["done"] > seen:
+                    seen = st["done"]
+                    _fill_variant_record(rec, solver, st, cfg)
+                    vec = {k: t.cpu().numpy() for k, t in solver.state(names).items()}
+                    callback(seen, KrylovState(cfg.variant, **vec), rec)
+                if st["status"] != 0:
+                    break
+                solver.advance(1)
+        if st["status"] == 3:
+            raise BreakdownError(_CGV_BREAKDOWN[cfg.variant].format(st["aux"]))
+        if st["status"] == 4:
+            raise DivergenceError("non-finite residual norm" if st["div_kind"] == 2
+                                  else "non-finite value in solver recurrence")
+        _fill_variant_record(rec, solver, st, cfg)
+        rec.iterations = st["it"]
+        rec.converged = st["status"] == 1
+        rec.final_residual = st["norm"]
+        rec.total_reductions = st["red"]
+        rec.total_overlapped = st["ovl"]
+        rec.launched_iterations = solver.launched
+        rec.operator_format = "ssell" if solver.symmetric else "sell"
+        x = solver.state(("x",))["x"].clone()
+        return (x if on_device else x.cpu().numpy()), rec
+    finally:
+        solver.close()
+
+
+def _fill_variant_record(rec, solver, st, cfg):
+    rec.initial_residual = st["norm0"]
+    if cfg.record_history:
+        h, red, ovl = solver.history(st["notes"])
+        rec.residual_norms = [float(v) for v in h]
+        rec.reductions_cum = [int(v) for v in red]
+        rec.overlapped_cum = [int(v) for v in ovl]
+
+
 def _wrap_device(addr: int, n: int):
     """Zero-copy torch view of n doubles at a device address (kept alive by owner)."""
     torch = _torch()
@@ -359,14 +514,13 @@ def solve(system, b, cfg: SolverConfig, x0=None, callback=None):
         if b.numel() != system.n:
             raise DimensionMismatchError("right-hand side length mismatch")
         bd = b.to(torch.float64).contiguous()
-    if cfg.variant not in DEVICE_VARIANTS:
-        raise NotImplementedError(
-            f"variant {cfg.variant!r} is not on the device path yet (classic only)")
     x0d = None
     if x0 is not None:
         x0d = x0 if isinstance(x0, torch.Tensor) else torch.from_numpy(
             np.asarray(x0, dtype=np.float64)).to("cuda")
         x0d = x0d.to(torch.float64).contiguous()
+    if cfg.variant != "classic":
+        return _solve_variant(system, bd, cfg, x0d, callback, on_device)
     solver = DevicePCG(system.device_A, system.device_M(), cfg.tol, cfg.maxit)
     try:
         solver.start(bd, x0d)

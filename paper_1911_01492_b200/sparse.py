@@ -455,6 +455,17 @@ class DeviceCsr:
         return out
 
 
+def share_pattern(A: DeviceCsr, M: DeviceCsr | None) -> None:
+    """Let M reuse A's pattern-derived layouts when both hold the same CSR
+    structure (identical tensors, or equal contents)."""
+    if M is None or M._pat is A._pat or M.nrows != A.nrows or M.nnz != A.nnz:
+        return
+    torch = _torch()
+    if (M.rowptr is A.rowptr and M.colidx is A.colidx) or (
+            torch.equal(M.rowptr, A.rowptr) and torch.equal(M.colidx, A.colidx)):
+        M._pat = A._pat
+
+
 def as_device(A) -> DeviceCsr:
     if isinstance(A, DeviceCsr):
         return A
