@@ -38,7 +38,8 @@ enum {
   SPAI_E_DIVERGENCE = 6,     /* DivergenceError, krylov.py:288-291                 */
   SPAI_E_PATTERN = 7,        /* pattern not structurally symmetric                 */
   SPAI_E_UNSUPPORTED = 8,    /* local problem larger than the kernel limits        */
-  SPAI_E_EMPTY_COLUMN = 9    /* column without stored entries (precond.py:188)     */
+  SPAI_E_EMPTY_COLUMN = 9,   /* column without stored entries (precond.py:188)     */
+  SPAI_E_FORMAT = 10         /* MatrixMarketError, sparse.py:66-70,272-300         */
 };
 
 const char* spai_last_error(void);
@@ -340,6 +341,26 @@ int spai_dist_update_xr(int64_t n, double* x, double* r, const double* p,
                         const double* q, const void* scal, void* stream);
 int spai_dist_reduce_step(int nranks, const double* gathered, int K, int stage,
                           void* scal, double* hist, void* stream);
+
+/* ------------------------------------------------------------------ host I/O
+ * Matrix Market / vector files and COO -> CSR (replace sparse.py:58-75,
+ * 272-330), multithreaded host code (nthreads <= 0: all hardware threads);
+ * host pointers.  Format errors return SPAI_E_FORMAT with the reference's
+ * message in spai_last_error().                                            */
+int spai_mm_read_header(const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz,
+                        int* symmetric);
+/* 0-based COO in file order, symmetric off-diagonals mirrored (room for
+ * 2 * nnz entries when symmetric); *count = entries written               */
+int spai_mm_read_coo(const char* path, int64_t* rows, int64_t* cols, double* vals,
+                     int64_t* count, int nthreads);
+/* from_coo semantics: (row, col) order, duplicates rejected                */
+int spai_coo_to_csr(int64_t nrows, int64_t count, const int64_t* rows, const int64_t* cols,
+                    const double* vals, int64_t* rowptr, int64_t* out_cols, double* out_vals,
+                    int nthreads);
+int spai_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* rowptr,
+                  const int64_t* colidx, const double* vals, int nthreads);
+int spai_vec_write(const char* path, int64_t n, const double* x);
+int spai_vec_read(const char* path, double* x, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,8 @@ from .errors import (BreakdownError, ConfigError, DimensionMismatchError,
                      InvalidPartitionError, MatrixMarketError,
                      RecoveryFailedError, SingularDiagonalError)
 from ._lib import NativeLibraryError
-from .sparse import CsrMatrix, DeviceCsr, as_device, spmv
+from .sparse import (CsrMatrix, DeviceCsr, as_device, read_matrix_market, read_vector, spmv,
+                     write_matrix_market, write_vector)
 from .grids import (Anisotropy, StructuredGrid, assemble_poisson, assemble_q1,
                     fd5_stencil, make_rhs, q1_device, q1_stencil, stencil_device)
 from .precond import (IdentityPreconditioner, JacobiPreconditioner,

@@ -22,6 +22,7 @@ SPAI_E_DIVERGENCE = 6
 SPAI_E_PATTERN = 7
 SPAI_E_UNSUPPORTED = 8
 SPAI_E_EMPTY_COLUMN = 9
+SPAI_E_FORMAT = 10
 
 
 class NativeLibraryError(RuntimeError):
@@ -119,6 +120,13 @@ _SIGS = {
     "spai_pcg_vectors": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                                 C.POINTER(_vp)]),
     "spai_pcg_destroy": (_i32, [_vp]),
+    "spai_mm_read_header": (_i32, [C.c_char_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
+                                   C.POINTER(_i32)]),
+    "spai_mm_read_coo": (_i32, [C.c_char_p, _vp, _vp, _vp, C.POINTER(_i64), _i32]),
+    "spai_coo_to_csr": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
+    "spai_mm_write": (_i32, [C.c_char_p, _i64, _i64, _vp, _vp, _vp, _i32]),
+    "spai_vec_write": (_i32, [C.c_char_p, _i64, _vp]),
+    "spai_vec_read": (_i32, [C.c_char_p, _vp, _i64, C.POINTER(_i64)]),
 }
 
 _lib = None

@@ -13,6 +13,7 @@ K5; host arrays go through HBM, device tensors stay there.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -92,6 +93,8 @@ class CsrMatrix:
         rows = np.asarray(rows, dtype=np.int64)
         cols = np.asarray(cols, dtype=np.int64)
         vals = np.asarray(vals, dtype=np.float64)
+        if len(rows) >= _NATIVE_COO_MIN and rows.size and rows.min() >= 0 and rows.max() < nrows:
+            return cls._from_coo_native(nrows, ncols, rows, cols, vals)
         order = np.lexsort((cols, rows))
         rows, cols, vals = rows[order], cols[order], vals[order]
         if len(rows) > 1:
@@ -103,6 +106,20 @@ class CsrMatrix:
         np.add.at(offsets, rows + 1, 1)
         np.cumsum(offsets, out=offsets)
         return cls(nrows, ncols, offsets, cols, vals)
+
+    @classmethod
+    def _from_coo_native(cls, nrows, ncols, rows, cols, vals) -> "CsrMatrix":
+        """Same result as the lexsort path, multithreaded host code (mmio.cpp)."""
+        lib = _lib.load()
+        rows, cols, vals = (np.ascontiguousarray(a) for a in (rows, cols, vals))
+        rowptr = np.empty(nrows + 1, dtype=np.int64)
+        oc = np.empty(len(rows), dtype=np.int64)
+        ov = np.empty(len(rows), dtype=np.float64)
+        st = lib.spai_coo_to_csr(nrows, len(rows), rows.ctypes.data, cols.ctypes.data,
+                                 vals.ctypes.data, rowptr.ctypes.data, oc.ctypes.data,
+                                 ov.ctypes.data, 0)
+        _io_check(st, "spai_coo_to_csr")
+        return cls(nrows, ncols, rowptr, oc, ov)
 
     @classmethod
     def from_dense(cls, dense, tol: float = 0.0) -> "CsrMatrix":
@@ -494,3 +511,66 @@ def spmv(A, x):
     dA = as_device(A)
     y = dA.matvec(torch.from_numpy(x).to("cuda"))
     return y.cpu().numpy()
+
+
+# ---------------------------------------------------------------- file I/O
+# Matrix Market and vector files (sparse.py:270-330): native multithreaded
+# host code (csrc/mmio.cpp), same format rules and error texts.
+_NATIVE_COO_MIN = 1 << 20
+
+
+def _io_check(st, what):
+    if st == _lib.SPAI_E_FORMAT:
+        raise MatrixMarketError(_lib.last_error())
+    _lib.check(st, what)
+
+
+def read_matrix_market(path) -> CsrMatrix:
+    """sparse.py:272-308: coordinate real general|symmetric -> CsrMatrix."""
+    lib = _lib.load()
+    p = os.fsencode(os.fspath(path))
+    nr, nc, nz, sym = C.c_int64(0), C.c_int64(0), C.c_int64(0), C.c_int(0)
+    _io_check(lib.spai_mm_read_header(p, C.byref(nr), C.byref(nc), C.byref(nz), C.byref(sym)),
+              "spai_mm_read_header")
+    cap = max(int(nz.value), 0) * (2 if sym.value else 1)
+    rows = np.empty(max(cap, 1), dtype=np.int64)
+    cols = np.empty(max(cap, 1), dtype=np.int64)
+    vals = np.empty(max(cap, 1), dtype=np.float64)
+    cnt = C.c_int64(0)
+    _io_check(lib.spai_mm_read_coo(p, rows.ctypes.data, cols.ctypes.data, vals.ctypes.data,
+                                   C.byref(cnt), 0), "spai_mm_read_coo")
+    k = int(cnt.value)
+    return CsrMatrix.from_coo(int(nr.value), int(nc.value), rows[:k], cols[:k], vals[:k])
+
+
+def write_matrix_market(A, path) -> None:
+    """sparse.py:311-318 (general, one line per stored entry, %.17g)."""
+    if isinstance(A, DeviceCsr):
+        A = A.to_host()
+    rp = np.ascontiguousarray(A.row_offsets, dtype=np.int64)
+    ci = np.ascontiguousarray(A.col_indices, dtype=np.int64)
+    va = np.ascontiguousarray(A.values, dtype=np.float64)
+    st = _lib.load().spai_mm_write(os.fsencode(os.fspath(path)), A.nrows, A.ncols,
+                                   rp.ctypes.data, ci.ctypes.data, va.ctypes.data, 0)
+    _io_check(st, "spai_mm_write")
+
+
+def read_vector(path) -> np.ndarray:
+    """sparse.py:321-322 (np.loadtxt(path, ndmin=1) of a one-column file)."""
+    lib = _lib.load()
+    p = os.fsencode(os.fspath(path))
+    n = C.c_int64(0)
+    _io_check(lib.spai_vec_read(p, None, 0, C.byref(n)), "spai_vec_read")
+    out = np.empty(int(n.value), dtype=np.float64)
+    if out.size:
+        _io_check(lib.spai_vec_read(p, out.ctypes.data, out.size, C.byref(n)), "spai_vec_read")
+    return out
+
+
+def write_vector(x, path) -> None:
+    """sparse.py:325-329 (one value per line, %.17g)."""
+    if hasattr(x, "is_cuda") and x.is_cuda:
+        x = x.cpu().numpy()
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).ravel())
+    _io_check(_lib.load().spai_vec_write(os.fsencode(os.fspath(path)), x.size, x.ctypes.data),
+              "spai_vec_write")
