@@ -342,6 +342,36 @@ int spai_dist_update_xr(int64_t n, double* x, double* r, const double* p,
 int spai_dist_reduce_step(int nranks, const double* gathered, int K, int stage,
                           void* scal, double* hist, void* stream);
 
+/* ------------------------------------------------------------------ K11
+ * Geometric multigrid V-cycle with SPAI(1)-Richardson smoothing (config C4;
+ * no reference counterpart beyond the transfer operators of
+ * precond.py:303-397).  dims[3 * l + a] = level-l grid size along axis a
+ * (x fastest; each level halves the previous one rounding up).  Level
+ * operators as in K10 (SELL-32 or half storage); the coarsest level needs
+ * only A and the dense row-major inverse (spai_mg_set_coarse).             */
+typedef struct spai_mg spai_mg;
+int spai_mg_create(spai_mg** out, int dim, int nlevels, const int64_t* dims, int nu_pre,
+                   int nu_post, double omega);
+int spai_mg_set_level(spai_mg* g, int level, const int64_t* sliceptr, const int64_t* cdesc,
+                      const int32_t* cols, const double* A_vals, const double* M_vals,
+                      const int32_t* gofs, int w, const double* A_U, const double* M_U);
+int spai_mg_set_coarse(spai_mg* g, const double* Ainv);
+/* x = V(b), one V-cycle on the stream                                      */
+int spai_mg_apply(spai_mg* g, const double* b, double* x, void* stream);
+int spai_mg_destroy(spai_mg* g);
+/* A_c = P^T A P on the coarse 3^d box pattern (rowptr_c/colidx_c given);
+ * synchronous, SPAI_E_PATTERN if A couples nodes outside the 3^d box      */
+int spai_mg_galerkin(int dim, const int64_t* dims_f, const int64_t* rowptr_f,
+                     const int32_t* colidx_f, const double* vals_f, const int64_t* rowptr_c,
+                     const int32_t* colidx_c, double* vals_c, void* stream);
+/* r_c = P^T r_f ; x_f += P e_c                                             */
+int spai_mg_restrict(int dim, const int64_t* dims_f, const double* rf, double* rc, void* stream);
+int spai_mg_prolong_add(int dim, const int64_t* dims_f, const double* ec, double* xf,
+                        void* stream);
+/* classic PCG (K8) preconditioned by one V-cycle per iteration; the solver
+ * must not outlive g                                                        */
+int spai_pcg_set_preconditioner_mg(spai_pcg* s, const spai_mg* g);
+
 /* ------------------------------------------------------------------ host I/O
  * Matrix Market / vector files and COO -> CSR (replace sparse.py:58-75,
  * 272-330), multithreaded host code (nthreads <= 0: all hardware threads);

@@ -80,7 +80,7 @@ def _finite(*s):
 
 def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None):
     """`krylov.py:301-345`. M is a CSR (applied by spmv) or None."""
-    apply_M = (lambda v: v.copy()) if M is None else (lambda v: spmv(M, v))
+    apply_M = (lambda v: v.copy()) if M is None else (M if callable(M) else (lambda v: spmv(M, v)))
     rec = Record("classic")
     red = 0
     b = np.asarray(b, dtype=np.float64)

@@ -22,6 +22,8 @@ from .precond import (IdentityPreconditioner, JacobiPreconditioner,
                       drop_exact_zeros, jacobi, make_spai1_factory,
                       pattern_sets, set_assembly_plans, spai1, spai1_device,
                       spai1_symmetric_device)
+from .multigrid import (Hierarchy, MultigridPreconditioner, build_hierarchy, prolongate_full,
+                        restrict_full)
 from .krylov import (ConvergenceRecord, DeviceKrylov, DevicePCG, KrylovState,
                      LocalSystem, SolverConfig, VARIANTS, bicgstab,
                      fused_dots_device, memory_accounting, reduction_rate,

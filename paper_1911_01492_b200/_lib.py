@@ -120,6 +120,15 @@ _SIGS = {
     "spai_pcg_vectors": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                                 C.POINTER(_vp)]),
     "spai_pcg_destroy": (_i32, [_vp]),
+    "spai_mg_create": (_i32, [C.POINTER(_vp), _i32, _i32, _vp, _i32, _i32, _dbl]),
+    "spai_mg_set_level": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "spai_mg_set_coarse": (_i32, [_vp, _vp]),
+    "spai_mg_apply": (_i32, [_vp, _vp, _vp, _vp]),
+    "spai_mg_destroy": (_i32, [_vp]),
+    "spai_mg_galerkin": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_mg_restrict": (_i32, [_i32, _vp, _vp, _vp, _vp]),
+    "spai_mg_prolong_add": (_i32, [_i32, _vp, _vp, _vp, _vp]),
+    "spai_pcg_set_preconditioner_mg": (_i32, [_vp, _vp]),
     "spai_mm_read_header": (_i32, [C.c_char_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                                    C.POINTER(_i32)]),
     "spai_mm_read_coo": (_i32, [C.c_char_p, _vp, _vp, _vp, C.POINTER(_i64), _i32]),

@@ -354,6 +354,45 @@ pcg_u2_tma(int64_t n, int64_t nslices, Sell M, int wmax, PcgVecs v, PcgScal* sc)
   });
 }
 
+// ---- external preconditioner (multigrid V-cycle, K11): r lives in r0 (no
+// double buffering), z = V(r) is written by the V-cycle kernels between V2ext
+// and Zext, p alternates as usual.
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_v2_ext(int64_t n, PcgVecs v, const PcgScal* sc) {
+  if (sc->status != kRunning) return;
+  const double lambda = sc->lambda;
+  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
+  for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kSpmvThreads) {
+    v.r0[i] = fma(-lambda, v.q[i], v.r0[i]);
+    v.x[i] = fma(lambda, p[i], v.x[i]);
+  }
+}
+
+// [(z,r),(r,r)] -> beta, norm, status (pcg_u2's finalize without the r swap)
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_z_ext(int64_t n, PcgVecs v, PcgScal* sc) {
+  if (sc->status != kRunning) return;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kSpmvThreads) {
+    const double rn = v.r0[i];
+    acc[0] = fma(v.z[i], rn, acc[0]);
+    acc[1] = fma(rn, rn, acc[1]);
+  }
+  grid_finalize<2>(acc, v.partials, &sc->ticket2, [&](double (&tot)[2]) {
+    const double rho_new = tot[0], rr = tot[1];
+    if (!isfinite(rho_new) || !isfinite(rr)) { sc->status = kDivergence; return; }
+    const double norm = sqrt(rr);
+    v.hist[sc->it - 1] = norm;
+    sc->norm = norm;
+    sc->beta = rho_new / sc->rho;
+    sc->rho = rho_new;
+    if (norm <= sc->tol * sc->norm0) sc->status = kConverged;
+    else if (sc->it >= sc->maxit) sc->status = kMaxit;
+  });
+}
+
 __global__ void width_max_kernel(int64_t nslices, const int64_t* sliceptr, int* out) {
   int m = 0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices;
@@ -402,6 +441,10 @@ bool make_symsell(const int32_t* g, int w, const double* U, int64_t n, SymSell* 
 
 using namespace spai;
 
+struct spai_mg;
+int spai_mg_enqueue(const spai_mg* g, const double* b, double* x, const int* status,
+                    cudaStream_t st);
+
 struct spai_pcg {
   int64_t n = 0, nslices = 0;
   Sell A{}, M{};
@@ -422,6 +465,7 @@ struct spai_pcg {
   bool sym = false;     // symmetric half-storage operators (ssell.cuh) for A and M
   SymSell As{}, Ms{};
   unsigned sblocks = 1;
+  const spai_mg* mg = nullptr;   // external preconditioner (multigrid V-cycle)
   cudaGraphExec_t graph = nullptr;
 };
 
@@ -443,7 +487,28 @@ static void launch_sym_iteration(spai_pcg* s) {
   else pcg_u2<false><<<s->sblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, M, s->v, s->sc);
 }
 
+template <class OP>
+static int launch_mg_iteration(spai_pcg* s, const OP& A, unsigned blocks) {
+  pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  pcg_u1<<<blocks, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v, s->sc);
+  pcg_v2_ext<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  if (int st = spai_mg_enqueue(s->mg, s->v.r0, s->v.z, &s->sc->status, s->stream)) return st;
+  pcg_z_ext<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  return SPAI_OK;
+}
+
 static int launch_iteration(spai_pcg* s) {
+  if (s->mg) {
+    int st;
+    if (s->sym) {
+      SPAI_SSELL_DISPATCH(s->As.w, st = launch_mg_iteration(s, SymOp<WM>{s->As}, s->sblocks));
+    } else {
+      st = launch_mg_iteration(s, SellOp{s->A}, s->blocks1);
+    }
+    if (st) return st;
+    SPAI_LAUNCH_CHECK("pcg multigrid iteration");
+    return SPAI_OK;
+  }
   if (s->sym) {
     SPAI_SSELL_DISPATCH(s->As.w, launch_sym_iteration<WM>(s));
     SPAI_LAUNCH_CHECK("pcg symmetric iteration");
@@ -596,15 +661,24 @@ extern "C" int spai_pcg_create_sym(spai_pcg** out, int64_t n, const int32_t* g, 
   return SPAI_OK;
 }
 
+extern "C" int spai_pcg_set_preconditioner_mg(spai_pcg* s, const spai_mg* mg) {
+  if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
+  s->mg = mg;
+  s->hasM = false;
+  s->fused = false;
+  s->tma = false;
+  return SPAI_OK;
+}
+
 extern "C" int spai_pcg_set_fused(spai_pcg* s, int fused) {
   if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
-  s->fused = fused != 0 && !s->sym;
+  s->fused = fused != 0 && !s->sym && !s->mg;
   return SPAI_OK;
 }
 
 extern "C" int spai_pcg_set_tma(spai_pcg* s, int tma) {
   if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
-  s->tma = tma != 0 && !s->sym && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024;
+  s->tma = tma != 0 && !s->sym && !s->mg && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024;
   if (s->tma) {
     SPAI_CUDA(cudaFuncSetAttribute(pcg_u1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemA));
     SPAI_CUDA(cudaFuncSetAttribute(pcg_u2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemM));
@@ -627,15 +701,6 @@ static void launch_sym_start(spai_pcg* s, bool x0) {
 
 extern "C" int spai_pcg_start(spai_pcg* s, const double* b, const double* x0) {
   const size_t vb = (size_t)s->n * sizeof(double);
-  SPAI_CUDA(cudaMemcpyAsync(s->b, b, vb, cudaMemcpyDeviceToDevice, s->stream));
-  if (x0) SPAI_CUDA(cudaMemcpyAsync(s->v.x, x0, vb, cudaMemcpyDeviceToDevice, s->stream));
-  else SPAI_CUDA(cudaMemsetAsync(s->v.x, 0, vb, s->stream));
-  if (s->sym) {
-    SPAI_SSELL_DISPATCH(s->As.w, launch_sym_start<WM>(s, x0 != nullptr));
-  } else {
-    launch_start(s, SellOp{s->A}, SellOp{s->M}, s->blocks1, s->blocks2, x0 != nullptr);
-  }
-  SPAI_LAUNCH_CHECK("pcg_start");
   PcgScal* h = s->host_init;   // lives as long as the solver: safe for the async copy
   *h = PcgScal{};
   h->tol = s->tol;
@@ -644,6 +709,31 @@ extern "C" int spai_pcg_start(spai_pcg* s, const double* b, const double* x0) {
   h->norm0 = NAN;
   h->status = kRunning;
   SPAI_CUDA(cudaMemcpyAsync(s->sc, h, sizeof(PcgScal), cudaMemcpyHostToDevice, s->stream));
+  SPAI_CUDA(cudaMemcpyAsync(s->b, b, vb, cudaMemcpyDeviceToDevice, s->stream));
+  if (x0) SPAI_CUDA(cudaMemcpyAsync(s->v.x, x0, vb, cudaMemcpyDeviceToDevice, s->stream));
+  else SPAI_CUDA(cudaMemsetAsync(s->v.x, 0, vb, s->stream));
+  if (s->mg) {                 // r0 = b - A x0; p0 = V(r0)
+    const bool hx = x0 != nullptr;
+    if (s->sym) {
+      SPAI_SSELL_DISPATCH(s->As.w, {
+        const SymOp<WM> A{s->As};
+        if (hx) pcg_start_r<true><<<s->sblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v.x, s->b, s->v.r0);
+        else pcg_start_r<false><<<s->sblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v.x, s->b, s->v.r0);
+      });
+    } else {
+      const SellOp A{s->A};
+      if (hx) pcg_start_r<true><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v.x, s->b, s->v.r0);
+      else pcg_start_r<false><<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, A, s->v.x, s->b, s->v.r0);
+    }
+    SPAI_LAUNCH_CHECK("pcg_start_r");
+    return spai_mg_enqueue(s->mg, s->v.r0, s->v.p0, &s->sc->status, s->stream);
+  }
+  if (s->sym) {
+    SPAI_SSELL_DISPATCH(s->As.w, launch_sym_start<WM>(s, x0 != nullptr));
+  } else {
+    launch_start(s, SellOp{s->A}, SellOp{s->M}, s->blocks1, s->blocks2, x0 != nullptr);
+  }
+  SPAI_LAUNCH_CHECK("pcg_start");
   return SPAI_OK;
 }
 

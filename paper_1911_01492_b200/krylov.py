@@ -216,9 +216,10 @@ class DevicePCG:
     """Owner of a native `spai_pcg` solver (C-ABI K8)."""
 
     def __init__(self, A: DeviceCsr, M: DeviceCsr | None, tol: float, maxit: int,
-                 symmetric: bool | None = None):
+                 symmetric: bool | None = None, mg=None):
         """symmetric: None = use the half-storage operators (K5c) when A and M
-        are bit-for-bit symmetric on one pattern; False = always SELL-32."""
+        are bit-for-bit symmetric on one pattern; False = always SELL-32.
+        mg: a MultigridPreconditioner applied (one V-cycle) instead of M."""
         torch = _require_cuda()
         self.lib = _lib.load()
         self.A, self.M = A, M
@@ -244,6 +245,7 @@ class DevicePCG:
                 ptr(self.ws), wsb, stream_handle())
             _lib.check(st, "spai_pcg_create_sym")
             self.h = h
+            self._attach_mg(mg)
             return
         sliceptr, cdesc, cols = A.sell()
         a_vals = A.sell_values()
@@ -268,6 +270,15 @@ class DevicePCG:
         _lib.check(st, "spai_pcg_create")
         self.h = h
         self.launched = 0
+        self._attach_mg(mg)
+
+    def _attach_mg(self, mg):
+        self.mg = mg
+        if mg is not None:
+            if mg.n != self.n:
+                raise DimensionMismatchError("multigrid preconditioner size mismatch")
+            _lib.check(self.lib.spai_pcg_set_preconditioner_mg(self.h, mg.h),
+                       "spai_pcg_set_preconditioner_mg")
 
     def set_tma(self, tma: bool):
         _lib.check(self.lib.spai_pcg_set_tma(self.h, 1 if tma else 0), "spai_pcg_set_tma")
@@ -520,8 +531,14 @@ def solve(system, b, cfg: SolverConfig, x0=None, callback=None):
             np.asarray(x0, dtype=np.float64)).to("cuda")
         x0d = x0d.to(torch.float64).contiguous()
     if cfg.variant != "classic":
+        if hasattr(getattr(system, "M", None), "nu_pre"):
+            raise NotImplementedError("the multigrid preconditioner runs with the classic variant")
         return _solve_variant(system, bd, cfg, x0d, callback, on_device)
-    solver = DevicePCG(system.device_A, system.device_M(), cfg.tol, cfg.maxit)
+    mg = getattr(system, "M", None)
+    if mg is not None and hasattr(mg, "nu_pre") and hasattr(mg, "device_apply"):
+        solver = DevicePCG(system.device_A, None, cfg.tol, cfg.maxit, mg=mg)
+    else:
+        solver = DevicePCG(system.device_A, system.device_M(), cfg.tol, cfg.maxit)
     try:
         solver.start(bd, x0d)
         rec = ConvergenceRecord(variant=cfg.variant, vector_memory_units=4,
