@@ -124,6 +124,26 @@ def variant_cases():
     return out
 
 
+def block_cases():
+    """block_solve (krylov.py:552-690) with Jacobi, the three Gram modes, and
+    exactly dependent right-hand sides."""
+    out = {}
+    A = fk.assemble_poisson(fk.StructuredGrid(12, 12))
+    rng = np.random.default_rng(4)
+    B = rng.standard_normal((A.nrows, 4))
+    c = rng.standard_normal(A.nrows)
+    Bdep = np.column_stack([c, 2.0 * c, c - 0.5 * c])
+    M = fk.jacobi(A)
+    for name, mode, bs, rhs in (("full", "full", None, B), ("blockdiag", "block_diagonal", 2, B),
+                                ("diagonal", "diagonal", None, B), ("dependent", "full", None, Bdep)):
+        cfg = fk.SolverConfig(variant="classic", tol=1e-9, maxit=400)
+        X, recs = fk.block_solve(A, fk.MultiVector(rhs), M, cfg, gram_mode=mode, block_size=bs)
+        out[name] = dict(A=A, B=rhs, dinv=M.inv_diag.copy(), X=X.values, mode=mode, bs=bs or 0,
+                         hist=[np.array(r.residual_norms) for r in recs],
+                         its=np.array([r.iterations for r in recs]))
+    return out
+
+
 def multirank_cases():
     """Reference multi-rank block-local SPAI runs (cli.py:234-253)."""
     from ftkrylov.cli import _solve_once
@@ -193,6 +213,20 @@ def main():
         for k in ("its", "norm0", "tred", "tovl", "final"):
             data[f"{key}/{k}"] = np.array(d[k])
         print(f"variant {key}: its={d['its']}")
+    for name, d in block_cases().items():
+        key = f"block/{name}"
+        data[f"{key}/A_ptr"] = d["A"].row_offsets
+        data[f"{key}/A_col"] = d["A"].col_indices
+        data[f"{key}/A_val"] = d["A"].values
+        data[f"{key}/B"] = d["B"]
+        data[f"{key}/dinv"] = d["dinv"]
+        data[f"{key}/X"] = d["X"]
+        data[f"{key}/mode"] = np.array(d["mode"])
+        data[f"{key}/bs"] = np.array(d["bs"])
+        data[f"{key}/its"] = d["its"]
+        for j, h in enumerate(d["hist"]):
+            data[f"{key}/hist{j}"] = h
+        print(f"block {name}: its={list(d['its'])}")
     for ranks, d in multirank_cases().items():
         data[f"multirank/fd5_32x32/{ranks}/hist"] = d["hist"]
         data[f"multirank/fd5_32x32/{ranks}/its"] = np.array(d["its"])
