@@ -372,6 +372,26 @@ int spai_mg_prolong_add(int dim, const int64_t* dims_f, const double* ec, double
  * must not outlive g                                                        */
 int spai_pcg_set_preconditioner_mg(spai_pcg* s, const spai_mg* g);
 
+/* ------------------------------------------------------------------ K12
+ * Multi-right-hand-side kernels for block CG (replace spmm_multi /
+ * dot_block, sparse.py:133-236, and block_solve's updates, krylov.py:552-690).
+ * Blocks are row-interleaved (n, k) device arrays, 1 <= k <= 16.  Operator:
+ * SELL-32 (sliceptr/cdesc/cols/vals) or, when U != NULL, half storage (g, w). */
+int spai_blk_spmm(int64_t n, int k, const int64_t* sliceptr, const int64_t* cdesc,
+                  const int32_t* cols, const double* vals, const int32_t* g, int w,
+                  const double* U, const double* X, double* Y, void* stream);
+size_t spai_blk_gram_workspace_bytes(int k);
+/* synchronous: G_host[a * k + b] = sum_i X[i, a] Y[i, b] (fixed-order sums) */
+int spai_blk_gram(int64_t n, int k, const double* X, const double* Y, void* ws,
+                  double* G_host, void* stream);
+/* X[:, j] += sum_{i: grp[i] == grp[j]} P[:, i] alpha[i, j], R[:, j] -= ... Q,
+ * for the columns with mask[j] != 0 (alpha, grp, mask: device arrays)      */
+int spai_blk_update(int64_t n, int k, double* X, const double* P, double* R, const double* Q,
+                    const double* alpha, const int* grp, const int* mask, void* stream);
+/* P[:, j] = Z[:, j] + sum_{i: grp[i] == grp[j]} P[:, i] beta[i, j] (mask[j])  */
+int spai_blk_pupdate(int64_t n, int k, double* P, const double* Z, const double* beta,
+                     const int* grp, const int* mask, void* stream);
+
 /* ------------------------------------------------------------------ host I/O
  * Matrix Market / vector files and COO -> CSR (replace sparse.py:58-75,
  * 272-330), multithreaded host code (nthreads <= 0: all hardware threads);

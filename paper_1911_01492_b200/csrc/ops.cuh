@@ -16,6 +16,10 @@ struct SellOp {
   __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
     return sell_row(m, s, lane, xf);
   }
+  template <class F>
+  __device__ __forceinline__ void foreach(int64_t s, int lane, const F& f) const {
+    sell_foreach(m, s, lane, f);
+  }
 };
 template <int WM>
 struct SymOp {
@@ -24,6 +28,10 @@ struct SymOp {
   template <class XF>
   __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
     return ssell_row<WM>(m, s, lane, xf);
+  }
+  template <class F>
+  __device__ __forceinline__ void foreach(int64_t s, int lane, const F& f) const {
+    ssell_foreach(m, s, lane, f);
   }
 };
 

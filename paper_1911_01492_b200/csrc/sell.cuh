@@ -86,6 +86,29 @@ __device__ __forceinline__ double sell_row(const Sell& A, int64_t s, int lane, c
   return (a0 + a1) + (a2 + a3);
 }
 
+// f(value, column) for every stored slot of this lane's row of slice s
+// (padding slots have value 0 and a valid clamped column)
+template <class F>
+__device__ __forceinline__ void sell_foreach(const Sell& A, int64_t s, int lane, const F& f) {
+  const int64_t off = A.sliceptr[s];
+  const int w = (int)((A.sliceptr[s + 1] - off) >> 5);
+  const int64_t cd = A.cdesc[s];
+  const double* __restrict__ v = A.vals + off + lane;
+  if (cd < 0) {
+    const int32_t* __restrict__ rt = A.cols + (-cd - 1);
+    const int32_t myrel = lane < w ? __ldg(rt + lane) : 0;
+    const int64_t row = s * kSell + lane;
+    const int64_t hi = A.ncols - 1;
+    for (int k = 0; k < w; ++k) {
+      const int64_t c = row + __shfl_sync(0xffffffffu, myrel, k);
+      f(ldg_stream(v + k * kSell), (int32_t)(c < 0 ? 0 : (c > hi ? hi : c)));
+    }
+  } else {
+    const int32_t* __restrict__ c = A.cols + cd + lane;
+    for (int k = 0; k < w; ++k) f(ldg_stream(v + k * kSell), __ldg(c + k * kSell));
+  }
+}
+
 // ---- TMA-staged SELL-32: every warp owns a 2-stage shared-memory ring; lane 0
 // streams whole slices (values, and the index block of explicit slices, are
 // contiguous per slice) with cp.async.bulk (SASS UBLKCP) while the warp

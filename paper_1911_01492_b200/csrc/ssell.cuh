@@ -111,6 +111,23 @@ __device__ __forceinline__ double ssell_row_generic(const SymSell& A, const doub
   return a0 + a1;
 }
 
+// f(value, column) for every coupling of row i = 32 s + lane: the stored
+// upper slots, then the mirrored lower ones (out-of-range neighbours skipped)
+template <class F>
+__device__ __forceinline__ void ssell_foreach(const SymSell& A, int64_t s, int lane, const F& f) {
+  const int64_t sw = (int64_t)A.w * kSell;
+  const double* __restrict__ up = A.vals + s * sw + lane;
+  const int64_t i = s * kSell + lane;
+  const int32_t myg = ssell_lane_offset(A, lane);
+  for (int k = 0; k < A.w; ++k) {
+    const int32_t g = __shfl_sync(0xffffffffu, myg, k);
+    const double vu = __ldg(up + k * kSell);
+    if (i + g < A.n) f(vu, (int32_t)(i + g));
+    const int64_t j = i - g;
+    if (g > 0 && j >= 0 && j < A.n) f(__ldg(A.vals + (j >> 5) * sw + k * kSell + (j & 31)), (int32_t)j);
+  }
+}
+
 template <int W, class XF>
 __device__ __forceinline__ double ssell_row(const SymSell& A, int64_t s, int lane, const XF& xf) {
   const int64_t row0 = s * kSell;
