@@ -384,6 +384,9 @@ size_t spai_blk_gram_workspace_bytes(int k);
 /* synchronous: G_host[a * k + b] = sum_i X[i, a] Y[i, b] (fixed-order sums) */
 int spai_blk_gram(int64_t n, int k, const double* X, const double* Y, void* ws,
                   double* G_host, void* stream);
+/* synchronous: both G1 = X1^T Y1 and G2 = X2^T Y2 in one pass              */
+int spai_blk_gram2(int64_t n, int k, const double* X1, const double* Y1, const double* X2,
+                   const double* Y2, void* ws, double* G1_host, double* G2_host, void* stream);
 /* X[:, j] += sum_{i: grp[i] == grp[j]} P[:, i] alpha[i, j], R[:, j] -= ... Q,
  * for the columns with mask[j] != 0 (alpha, grp, mask: device arrays)      */
 int spai_blk_update(int64_t n, int k, double* X, const double* P, double* R, const double* Q,

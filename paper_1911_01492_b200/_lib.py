@@ -132,6 +132,7 @@ _SIGS = {
     "spai_blk_spmm": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp]),
     "spai_blk_gram_workspace_bytes": (_sz, [_i32]),
     "spai_blk_gram": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "spai_blk_gram2": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_blk_update": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_blk_pupdate": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_mm_read_header": (_i32, [C.c_char_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),

@@ -121,6 +121,14 @@ class _Gram:
                                              out.ctypes.data, stream_handle()), "spai_blk_gram")
         return out.reshape(self.k, self.k)
 
+    def pair(self, X1, Y1, X2, Y2, n):
+        g1 = np.zeros(self.k * self.k)
+        g2 = np.zeros(self.k * self.k)
+        _lib.check(_lib.load().spai_blk_gram2(n, self.k, ptr(X1), ptr(Y1), ptr(X2), ptr(Y2),
+                                              ptr(self.ws), g1.ctypes.data, g2.ctypes.data,
+                                              stream_handle()), "spai_blk_gram2")
+        return g1.reshape(self.k, self.k), g2.reshape(self.k, self.k)
+
 
 def _to_dev(V):
     torch = _require_cuda()
@@ -283,8 +291,7 @@ def block_solve(A, B: MultiVector, M, cfg, gram_mode: str = "full",
         it += 1
         act = np.array(sorted(active))
         opA.spmm(P, Q, k)
-        G_pq = gram(P, Q, n)
-        G_zr = gram(Z, R, n)
+        G_pq, G_zr = gram.pair(P, Q, Z, R, n)
         alpha = np.zeros((k, k))
         grp_id = -1 - np.arange(k)
         mask = np.zeros(k, dtype=bool)
@@ -311,7 +318,8 @@ def block_solve(A, B: MultiVector, M, cfg, gram_mode: str = "full",
                                            ptr(grp_d), ptr(mask_d), stream_handle()),
                        "spai_blk_update")
         apply_m(R, Z)
-        rr = np.diag(gram(R, R, n))
+        G_rr, G_zr_new = gram.pair(R, R, Z, R, n)
+        rr = np.diag(G_rr)
         done = []
         for j in act:
             norm = float(np.sqrt(rr[j]))
@@ -330,7 +338,6 @@ def block_solve(A, B: MultiVector, M, cfg, gram_mode: str = "full",
         act = np.array(sorted(active))
         if not len(act):
             break
-        G_zr_new = gram(Z, R, n)
         beta = np.zeros((k, k))
         grp_id = -1 - np.arange(k)
         mask = np.zeros(k, dtype=bool)
