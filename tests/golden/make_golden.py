@@ -144,6 +144,27 @@ def block_cases():
     return out
 
 
+def hierarchy_cases():
+    """build_hierarchy / restrict_full / prolongate_full (precond.py:303-397)."""
+    out = {}
+    rng = np.random.default_rng(11)
+    for nx, ny, levels in ((9, 7, 3), (16, 16, 4), (5, 4, 2)):
+        H = fk.build_hierarchy(fk.StructuredGrid(nx, ny), levels)
+        x = rng.standard_normal(nx * ny)
+        d = {"x": x, "levels": levels}
+        for l, (dims, R, P) in enumerate(H.levels):
+            d[f"{l}/dims"] = np.array(dims)
+            for tag, Mx in (("R", R), ("P", P)):
+                d[f"{l}/{tag}_ptr"] = Mx.row_offsets
+                d[f"{l}/{tag}_col"] = Mx.col_indices
+                d[f"{l}/{tag}_val"] = Mx.values
+            c = fk.restrict_full(H, x, l)
+            d[f"{l}/restrict"] = c
+            d[f"{l}/round_trip"] = fk.prolongate_full(H, c, l)
+        out[f"{nx}x{ny}x{levels}"] = d
+    return out
+
+
 def multirank_cases():
     """Reference multi-rank block-local SPAI runs (cli.py:234-253)."""
     from ftkrylov.cli import _solve_once
@@ -227,6 +248,10 @@ def main():
         for j, h in enumerate(d["hist"]):
             data[f"{key}/hist{j}"] = h
         print(f"block {name}: its={list(d['its'])}")
+    for name, d in hierarchy_cases().items():
+        for k, v in d.items():
+            data[f"hier/{name}/{k}"] = np.asarray(v)
+        print(f"hierarchy {name}")
     for ranks, d in multirank_cases().items():
         data[f"multirank/fd5_32x32/{ranks}/hist"] = d["hist"]
         data[f"multirank/fd5_32x32/{ranks}/its"] = np.array(d["its"])

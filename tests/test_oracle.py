@@ -177,3 +177,23 @@ def test_block_solve_matches_reference(golden, name):
     for j, r in enumerate(recs):
         assert r.iterations == int(its[j])
         assert np.array_equal(np.array(r.residual_norms), golden[f"{key}/hist{j}"])
+
+
+@pytest.mark.parametrize("name", ["9x7x3", "16x16x4", "5x4x2"])
+def test_hierarchy_transfers_match_reference(golden, name):
+    """precond.py:303-397: the restated transfer operators, restriction and
+    prolongation reproduce the reference bit for bit."""
+    from oracle import multigrid as omg
+    pre = f"hier/{name}"
+    nx, ny, levels = (int(t) for t in name.split("x"))
+    h = omg.build_hierarchy(nx, ny, levels)
+    x = golden[f"{pre}/x"]
+    for l, (dims, R, P) in enumerate(h):
+        assert tuple(golden[f"{pre}/{l}/dims"]) == tuple(dims)
+        for tag, M in (("R", R), ("P", P)):
+            assert np.array_equal(M.row_offsets, golden[f"{pre}/{l}/{tag}_ptr"])
+            assert np.array_equal(M.col_indices, golden[f"{pre}/{l}/{tag}_col"])
+            assert np.array_equal(M.values, golden[f"{pre}/{l}/{tag}_val"])
+        c = omg.restrict_full(h, x, l)
+        assert np.array_equal(c, golden[f"{pre}/{l}/restrict"])
+        assert np.array_equal(omg.prolongate_full(h, c, l), golden[f"{pre}/{l}/round_trip"])
