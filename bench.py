@@ -436,10 +436,11 @@ def run_distributed(args, world, rank, local):
         M = rs.preconditioner()
         e1.record(stream)
         solver = DistributedPCG(rs.system(M), comm, be, tol=args.tol, maxit=args.maxit, chunk=32)
-        _, rec = solver.solve()
+        x, rec = solver.solve()
         e2.record(stream)
         e2.synchronize()
         launches["n"] += 12 + 8 * rec.launched_iterations
+        step.x = x
         return e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3, rec
 
     with torch.cuda.stream(stream):
@@ -458,17 +459,45 @@ def run_distributed(args, world, rank, local):
             te.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
-    total = torch.tensor([ts.elapsed_time(te) / 1e3, max(t[0] for t in times)],
+    # e2e: every step copies this rank's inputs (the slab matrices it assembles
+    # and multiplies with, and b) from pinned host memory and reads x back
+    e2e_s, h2d, d2h, e2e_steps = 0.0, 0, 0, 0
+    if not args.no_e2e:
+        with torch.cuda.stream(stream):
+            dev_in = [rs.A_spai.rowptr, rs.A_spai.colidx, rs.A_spai.vals, rs.A_ext.rowptr,
+                      rs.A_ext.colidx, rs.A_ext.vals, rs.b]
+            host_in = [t.cpu().pin_memory() for t in dev_in]
+            h_x = torch.empty(rs.n_own, dtype=torch.float64).pin_memory()
+            h2d = sum(t.numel() * t.element_size() for t in host_in)
+            d2h = h_x.numel() * 8
+            e2e_steps = max(1, min(args.steps, 3))
+            dist.barrier()
+            torch.cuda.synchronize()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(stream)
+            for _ in range(e2e_steps):
+                for d, h in zip(dev_in, host_in):
+                    d.copy_(h, non_blocking=True)
+                step()
+                h_x.copy_(step.x, non_blocking=True)
+            eb.record(stream)
+            eb.synchronize()
+            e2e_s = ea.elapsed_time(eb) / 1e3
+    total = torch.tensor([ts.elapsed_time(te) / 1e3, max(t[0] for t in times), e2e_s],
                          dtype=torch.float64, device=dev)
     dist.all_reduce(total, op=dist.ReduceOp.MAX)
-    total_s, asm_max = float(total[0]), float(total[1])
+    total_s, asm_max, e2e_s = float(total[0]), float(total[1]), float(total[2])
     its = times[-1][2].iterations
     n = N ** 3
     value = sum(n * t[2].iterations for t in times) / total_s
     t_sol = statistics.mean(t[1] for t in times)
     hbm, peak_kind = peaks()
     nnz_local = rs.A_loc.nnz
-    b_it = 24 * nnz_local + 104 * rs.n_own
+    sysr = rs.system(rs.preconditioner())
+    if sysr.A_op is not None:          # half storage of the extended blocks
+        b_it = 8 * (sysr.A_op.U.numel() + sysr.M_op.U.numel()) + 104 * rs.n_own
+    else:
+        b_it = 24 * nnz_local + 104 * rs.n_own
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -477,7 +506,8 @@ def run_distributed(args, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"configs[2]: 3D Q1 Poisson {N}^3 ({n} DOF), SPAI(1)+CG, "
                                    f"b=A*1, x0=0, tol {args.tol}, z-slab partition",
-                       "n_dof": n, "iterations": its, "parallelism": f"rows x{world} (NCCL)",
+                       "n_dof": n, "iterations": its,
+                       "parallelism": f"rows x{world} ({dist.get_backend()})",
                        "spai_scope": "global"},
             "assembly": {"ms_max_rank": asm_max * 1e3, "cols_per_s": n / asm_max},
             "solve": {"ms": t_sol * 1e3, "iterations": its, "dof_it_per_s": n * its / t_sol,
@@ -487,7 +517,10 @@ def run_distributed(args, world, rank, local):
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": b_it * its / t_sol / 1e9 / hbm, "traffic": None},
             "clocks": clk.summary(), "gpu_launches": launches["n"],
-            "e2e": None, "cpu_baseline": None,
+            "e2e": ({"value": e2e_steps * n * its / e2e_s, "unit": UNIT,
+                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                     "per": "rank 0 (every rank copies its own slab)"} if e2e_s > 0 else None),
+            "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

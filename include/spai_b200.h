@@ -335,6 +335,12 @@ int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
                    const double* vals, const double* xext, int64_t own_off, double* y,
                    const double* raux, void* partials_ws, double* out,
                    const void* scal, void* stream);
+/* same on a half-storage extended principal submatrix (n_ext rows, owned
+ * rows [r0, r0 + n)), offsets g[0..w)                                       */
+int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext, const int32_t* g, int w,
+                       const double* U, const double* xext, int64_t own_off, double* y,
+                       const double* raux, void* partials_ws, double* out, const void* scal,
+                       void* stream);
 int spai_dist_update_p(int64_t n, double* p, const double* z, const void* scal,
                        void* stream);
 int spai_dist_update_xr(int64_t n, double* x, double* r, const double* p,

@@ -71,6 +71,8 @@ _SIGS = {
                                    C.POINTER(_dbl), C.POINTER(_dbl), _vp]),
     "spai_dist_spmv": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp]),
+    "spai_dist_spmv_sym": (_i32, [_i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i64, _vp, _vp,
+                                  _vp, _vp, _vp, _vp]),
     "spai_dist_update_p": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_dist_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_dist_reduce_step": (_i32, [_i32, _vp, _i32, _i32, _vp, _vp, _vp]),

@@ -9,8 +9,7 @@
 //   -> reduce_step: ascending-rank pairwise tree sum (commsim.py:336-347,
 //      so every rank sees bit-identical values) + the scalar recurrence.
 // Nothing synchronises with the host inside an iteration.
-#include "sell.cuh"
-#include "spmv_core.cuh"
+#include "ops.cuh"
 
 namespace spai {
 
@@ -25,11 +24,15 @@ struct DistScal {
 
 // MODE 0: plain y = A x;  1: U1 first iteration [(p,q),(p,r),(r,r)];
 // 2: U1 [(p,q)];  3: U2 [(z,r),(r,r)] with z = y, r = x;  4: U2 without M (z = r)
-template <int MODE>
-__global__ void __launch_bounds__(kSpmvThreads)
-dist_spmv_kernel(int64_t n, int64_t nslices, Sell A, const double* __restrict__ xext,
-                 int64_t own_off, double* __restrict__ y, const double* __restrict__ raux,
-                 double* partials, unsigned int* ticket, double* out, const DistScal* sc) {
+// The operator's rows are slices [s0, s1); row 32 s + lane is owned row
+// i = 32 s + lane - r0 (SELL: the owned rows themselves, r0 = 0; half
+// storage: the extended principal submatrix, r0 = halo below).
+template <int MODE, class OP>
+__global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
+dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
+                 const double* __restrict__ xext, int64_t own_off, double* __restrict__ y,
+                 const double* __restrict__ raux, double* partials, unsigned int* ticket,
+                 double* out, const DistScal* sc) {
   if (MODE != 0 && sc->status != dRunning) return;
   constexpr int K = MODE == 1 ? 3 : (MODE == 2 ? 1 : 2);
   const int lane = threadIdx.x & 31;
@@ -39,11 +42,11 @@ dist_spmv_kernel(int64_t n, int64_t nslices, Sell A, const double* __restrict__ 
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  for (int64_t s = w0; s < nslices; s += nw) {
+  for (int64_t s = s0 + w0; s < s1; s += nw) {
     double v = 0.0;
-    if (MODE != 4) v = sell_row(A, s, lane, [&](int32_t j) { return __ldg(xext + j); });
-    const int64_t i = s * kSell + lane;
-    if (i < n) {
+    if (MODE != 4) v = A.row(s, lane, [&](int32_t j) { return __ldg(xext + j); });
+    const int64_t i = s * kSell + lane - r0;
+    if (i >= 0 && i < n) {
       const double xi = xo[i];
       if (MODE == 4) v = xi;
       y[i] = v;
@@ -148,6 +151,25 @@ __global__ void dist_reduce_step(int nranks, const double* __restrict__ gathered
 }
 
 unsigned sell_blocks(const void* kern, int64_t nslices);
+unsigned ssell_blocks(const void* kern, int64_t nslices);
+bool make_symsell(const int32_t* g, int w, const double* U, int64_t n, SymSell* out);
+
+template <class OP>
+static int dist_launch(int mode, unsigned b, int64_t n, int64_t s0, int64_t s1, int64_t r0,
+                       const OP& A, const double* xext, int64_t own_off, double* y,
+                       const double* raux, double* part, unsigned int* ticket, double* out,
+                       const DistScal* sc, cudaStream_t s) {
+  switch (mode) {
+    case 0: dist_spmv_kernel<0, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 1: dist_spmv_kernel<1, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 2: dist_spmv_kernel<2, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 3: dist_spmv_kernel<3, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 4: dist_spmv_kernel<4, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    default: set_error("bad dist_spmv mode %d", mode); return SPAI_E_ARG;
+  }
+  SPAI_LAUNCH_CHECK("dist_spmv_kernel");
+  return SPAI_OK;
+}
 
 }  // namespace spai
 
@@ -195,23 +217,40 @@ extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t*
     return SPAI_OK;
   }
   static unsigned blocks = 0;
-  if (!blocks) blocks = sell_blocks((const void*)dist_spmv_kernel<1>, 1 << 30);
+  if (!blocks) blocks = sell_blocks((const void*)dist_spmv_kernel<1, SellOp>, 1 << 30);
   const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (ns * 32 + 255) / 256));
   unsigned int* ticket = (unsigned int*)partials_ws;
   double* part = (double*)((char*)partials_ws + 256);
-  Sell A{sliceptr, cdesc, cols, vals, ncols};
-  const DistScal* sc = (const DistScal*)scal;
-  cudaStream_t s = (cudaStream_t)stream;
-  switch (mode) {
-    case 0: dist_spmv_kernel<0><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 1: dist_spmv_kernel<1><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 2: dist_spmv_kernel<2><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 3: dist_spmv_kernel<3><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 4: dist_spmv_kernel<4><<<b, kSpmvThreads, 0, s>>>(n, ns, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    default: set_error("bad dist_spmv mode %d", mode); return SPAI_E_ARG;
+  const SellOp A{Sell{sliceptr, cdesc, cols, vals, ncols}};
+  return dist_launch(mode, b, n, 0, ns, 0, A, xext, own_off, y, raux, part, ticket, out,
+                     (const DistScal*)scal, (cudaStream_t)stream);
+}
+
+// Same on the half-storage extended principal submatrix (n_ext rows; the
+// owned rows are [r0, r0 + n)).
+extern "C" int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext,
+                                  const int32_t* g, int w, const double* U, const double* xext,
+                                  int64_t own_off, double* y, const double* raux,
+                                  void* partials_ws, double* out, const void* scal,
+                                  void* stream) {
+  if (n == 0) {
+    if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
+    return SPAI_OK;
   }
-  SPAI_LAUNCH_CHECK("dist_spmv_kernel");
-  return SPAI_OK;
+  SymSell A;
+  if (!make_symsell(g, w, U, n_ext, &A)) { set_error("dist_spmv_sym: bad offset table"); return SPAI_E_ARG; }
+  const int64_t s0 = r0 / kSell, s1 = (r0 + n + kSell - 1) / kSell;
+  unsigned int* ticket = (unsigned int*)partials_ws;
+  double* part = (double*)((char*)partials_ws + 256);
+  int st = SPAI_OK;
+  SPAI_SSELL_DISPATCH(w, {
+    const SymOp<WM> op{A};
+    const unsigned b = std::max(1u, std::min(ssell_blocks((const void*)dist_spmv_kernel<1, SymOp<WM>>, s1 - s0),
+                                             (unsigned)num_sms() * 32));
+    st = dist_launch(mode, b, n, s0, s1, r0, op, xext, own_off, y, raux, part, ticket, out,
+                     (const DistScal*)scal, (cudaStream_t)stream);
+  });
+  return st;
 }
 
 extern "C" int spai_dist_update_p(int64_t n, double* p, const double* z, const void* scal,

@@ -141,10 +141,28 @@ class LocalRankSystem:
     A: object                 # backend matrix (owned rows x extended columns)
     M: object | None          # same layout (global or block-local SPAI), None = identity
     b: object                 # owned right-hand side
+    A_op: object | None = None   # optional faster form of A used by the solver
+    M_op: object | None = None   # (SymExtOperator: half storage of the extended block)
 
     @property
     def n_ext(self):
         return self.hlo + self.n_own + self.hhi
+
+
+class SymExtOperator:
+    """Half storage (K5c) of the symmetric principal submatrix of A (or S) on
+    the extended index range [halo_lo | owned | halo_hi]; its rows
+    [r0, r0 + n_own) are the owned rows of the local operator, and their
+    couplings into the halo are read back from the halo rows' upper slots."""
+
+    def __init__(self, ext, n_own: int, r0: int):
+        g = ext.ssell_offsets()
+        U = ext.ssell_values() if g else None
+        if U is None:
+            raise ValueError("extended block is not exactly symmetric")
+        self.ext, self.U, self.g = ext, U, g
+        self.garr = (C.c_int32 * len(g))(*g)
+        self.n_own, self.r0, self.n_ext = int(n_own), int(r0), int(ext.nrows)
 
 
 # ------------------------------------------------------------------ GPU backend
@@ -188,6 +206,12 @@ class GpuBackend:
         return st.value, it.value, n0.value, nr.value, aux.value
 
     def spmv(self, mode, M, xext, own_off, y, raux, ws, out, scal):
+        if isinstance(M, SymExtOperator):
+            _lib.check(self.lib.spai_dist_spmv_sym(
+                mode, M.n_own, M.r0, M.n_ext, C.cast(M.garr, C.c_void_p), len(M.g), _p(M.U),
+                _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out), _p(scal), self._s()),
+                "spai_dist_spmv_sym")
+            return
         if M is None:       # identity preconditioner (mode 4)
             _lib.check(self.lib.spai_dist_spmv(4, y.numel(), xext.numel(), None, None, None, None,
                                                _p(xext), own_off, _p(y), None, _p(ws), _p(out),
@@ -250,8 +274,8 @@ class DistributedPCG:
         if s.M is None:
             self._own(self.pext).copy_(self._own(self.rext))
         else:
-            be.spmv(0, s.M, self.rext, s.hlo, self._own(self.pext), None, self.ws, self.out,
-                    self.scal)
+            be.spmv(0, s.M_op or s.M, self.rext, s.hlo, self._own(self.pext), None, self.ws,
+                    self.out, self.scal)
 
     def iteration(self, first: bool):
         s, be, c = self.sys, self.be, self.comm
@@ -260,13 +284,13 @@ class DistributedPCG:
             be.update_p(p_own, self.z, self.scal)
         c.halo(self.pext, s.hlo, s.n_own, s.hlo, s.hhi)
         K1 = 3 if first else 1
-        be.spmv(1 if first else 2, s.A, self.pext, s.hlo, self.q, r_own, self.ws, self.out,
-                self.scal)
+        be.spmv(1 if first else 2, s.A_op or s.A, self.pext, s.hlo, self.q, r_own, self.ws,
+                self.out, self.scal)
         c.allgather(self.out[:K1], self.gathered[:K1 * c.size])
         be.reduce_step(c.size, self.gathered, K1, 1, self.scal, self.hist)
         be.update_xr(self.x, r_own, p_own, self.q, self.scal)
         c.halo(self.rext, s.hlo, s.n_own, s.hlo, s.hhi)
-        be.spmv(3, s.M, self.rext, s.hlo, self.z, None, self.ws, self.out, self.scal)
+        be.spmv(3, s.M_op or s.M, self.rext, s.hlo, self.z, None, self.ws, self.out, self.scal)
         c.allgather(self.out[:2], self.gathered[:2 * c.size])
         be.reduce_step(c.size, self.gathered, 2, 2, self.scal, self.hist)
         self.launched += 1
@@ -365,6 +389,8 @@ class RankSetup:
         self.e0, self.e1 = max(z0 - 1, 0), min(z1 + 1, nz)
         gen = self._gen
         A1 = gen(self.e1 - self.e0)
+        self.A_ext = A1                # principal submatrix on the extended range
+        self.S_ext = None
         self.A_loc = _rebase(A1, (z0 - self.e0) * plane, (z1 - self.e0) * plane, 0, self.n_ext)
         ones = torch.ones(A1.nrows, dtype=torch.float64, device=A1.vals.device)
         self.b = A1.matvec(ones)[(z0 - self.e0) * plane:(z1 - self.e0) * plane].clone()
@@ -391,14 +417,39 @@ class RankSetup:
             M = _rebase(S3, (self.z0 - self.g0) * plane, (self.z1 - self.g0) * plane,
                         (self.e0 - self.g0) * plane, self.n_ext)
             M._pat = self.A_loc._pat      # identical pattern and column layout
+            self.S_ext = _principal(S3, (self.e0 - self.g0) * plane, (self.e1 - self.g0) * plane,
+                                    self.A_ext)
             return M
         Aff = self.A_spai
         Sff = spai1_symmetric_device(DeviceCsr(Aff.nrows, Aff.ncols, Aff.rowptr, Aff.colidx,
                                                Aff.vals))
         return _rebase(Sff, 0, Sff.nrows, -self.hlo, self.n_ext)
 
-    def system(self, M):
-        return LocalRankSystem(self.n_own, self.hlo, self.hhi, self.A_loc, M, self.b)
+    def system(self, M, symmetric: bool = True):
+        """symmetric: solve with half-storage operators of the extended blocks
+        when A and S are exactly symmetric (global scope); else SELL-32."""
+        sysr = LocalRankSystem(self.n_own, self.hlo, self.hhi, self.A_loc, M, self.b)
+        if symmetric and M is not None and self.S_ext is not None:
+            try:
+                sysr.A_op = SymExtOperator(self.A_ext, self.n_own, self.hlo)
+                sysr.M_op = SymExtOperator(self.S_ext, self.n_own, self.hlo)
+            except ValueError:
+                sysr.A_op = sysr.M_op = None
+        return sysr
+
+
+def _principal(S, a, b, like):
+    """Rows and columns [a, b) of S as a matrix on `like`'s pattern (the
+    extended-range stencil matrix), or None if the patterns differ."""
+    import torch
+    rp = S.rowptr[a:b + 1]
+    lo, hi = int(rp[0].item()), int(rp[-1].item())
+    cols = S.colidx[lo:hi]
+    keep = (cols >= a) & (cols < b)
+    sub_cols = (cols[keep] - a).to(torch.int32)
+    if sub_cols.numel() != like.nnz or not torch.equal(sub_cols, like.colidx):
+        return None
+    return like.with_values(S.vals[lo:hi][keep].contiguous())
 
 
 def _symmetric_range(A, c0, c1):

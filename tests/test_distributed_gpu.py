@@ -49,6 +49,27 @@ def test_one_rank_distributed_equals_single_gpu():
     assert float((x - x1).abs().max()) <= 1e-9
 
 
+def test_half_storage_rank_operators_match_sell():
+    """The extended-block half-storage operators (SymExtOperator) give the
+    same solve as the SELL-32 local operators."""
+    from paper_1911_01492_b200.distributed import RankSetup, SymExtOperator
+    from paper_1911_01492_b200.grids import q1_stencil
+    dims = (20, 18, 16)
+    t, st = q1_stencil(3)
+    part = SlabPartition(dims[-1], dims[0] * dims[1], 1)
+    rs = RankSetup(dims, t, st, part, 0, "global")
+    M = rs.preconditioner()
+    hists = []
+    for sym in (True, False):
+        sysr = rs.system(M, symmetric=sym)
+        assert isinstance(sysr.A_op, SymExtOperator) == sym
+        x, rec = DistributedPCG(sysr, TorchComm(), GpuBackend(), tol=1e-8, maxit=2000).solve()
+        hists.append((rec.iterations, np.array(rec.residual_norms), x))
+    assert hists[0][0] == hists[1][0]
+    assert np.max(np.abs(hists[0][1] - hists[1][1]) / hists[1][1]) <= 1e-10
+    assert float((hists[0][2] - hists[1][2]).abs().max()) <= 1e-10
+
+
 def _port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
