@@ -559,7 +559,12 @@ class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __res
     int slot = (int)(h & (kClassTable - 1)), result = -1;
     for (int probe = 0; probe < kClassTable; ++probe) {
       unsigned long long prev = 0;
-      if (lane == 0) prev = atomicCAS(pw.ckeys + slot, 0ull, (unsigned long long)h);
+      if (lane == 0) {
+        // plain (L2) read first: nearly every column finds an existing class,
+        // and an atomic on the few hot slots would serialise the whole grid
+        prev = __ldcg(pw.ckeys + slot);
+        if (prev == 0ull) prev = atomicCAS(pw.ckeys + slot, 0ull, (unsigned long long)h);
+      }
       prev = __shfl_sync(0xffffffffu, prev, 0);
       if (prev == 0ull) {                      // new class: publish the representative
         if (lane == 0) { atomicExch(pw.crep + slot, (int32_t)c); atomicAdd(pw.nclass, 1); }
@@ -620,7 +625,8 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
       int slot = (int)(h & (kPlanTable - 1));
       int found = -1;
       for (int probe = 0; probe < kPlanTable; ++probe) {
-        const unsigned long long prev = atomicCAS(pw.keys + slot, 0ull, (unsigned long long)h);
+        unsigned long long prev = __ldcg(pw.keys + slot);      // read first (see class_kernel)
+        if (prev == 0ull) prev = atomicCAS(pw.keys + slot, 0ull, (unsigned long long)h);
         if (prev == 0ull) { pw.rep[slot] = (int32_t)k; atomicAdd(pw.nplans, 1); found = slot; break; }
         if (prev == h) { found = slot; break; }
         slot = (slot + 1) & (kPlanTable - 1);
