@@ -815,14 +815,14 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
               const uint32_t below = (1u << bit) - 1u;
               const int ea = S.loff[a] + S.pre[a * 8 + wd] + __popc(ma & below);
               const int eb = S.loff[b] + S.pre[b * 8 + wd] + __popc(mb & below);
-              ops[(t0 + step) * 32 + lane] = op_pack(ea, eb);
+              ops[op_index(t0 + step, lane)] = op_pack(ea, eb);
               ++step;
             }
           }
         }
         // padding: 0 * 0 from the zero slot lval[total]
         for (; step < len && t0 + step < kPlanSteps; ++step)
-          ops[(t0 + step) * 32 + lane] = op_pack(total, total);
+          ops[op_index(t0 + step, lane)] = op_pack(total, total);
         t0 += len;
       }
       ok = t0 <= kPlanSteps;
@@ -911,14 +911,15 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
     // per round (rounds have even length: two accumulators for even / odd
     // steps); one flat loop so the op loads run ahead across rounds
     {
-      const uint32_t* ops = P + kPO_ops + lane;
+      const uint2* ops = reinterpret_cast<const uint2*>(P + kPO_ops) + lane;
       const uint16_t* rdst = reinterpret_cast<const uint16_t*>(P + kPO_rdst) + lane;
       const unsigned char* lv = reinterpret_cast<const unsigned char*>(lval);
       int r = 0, rend = (int)P[kPO_rlen];
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll 2
       for (int t = 0; t < nsteps; t += 2) {
-        const uint32_t o0 = ops[t * 32], o1 = ops[(t + 1) * 32];
+        const uint2 oo = ops[(t >> 1) * 32];     // steps t, t + 1 in one 8-byte load
+        const uint32_t o0 = oo.x, o1 = oo.y;
         s0 = fma(*reinterpret_cast<const double*>(lv + (o0 & 0xFFFFu)),
                  *reinterpret_cast<const double*>(lv + (o0 >> 16)), s0);
         s1 = fma(*reinterpret_cast<const double*>(lv + (o1 & 0xFFFFu)),
@@ -947,13 +948,145 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
   }
 }
 
+// Pipelined replay: the next column's values are gathered with cp.async into
+// the value buffer while this column's Cholesky and solves run (the buffer is
+// dead once the product program and the right-hand side have read it), so
+// the gather latency overlaps arithmetic instead of stalling the warp.
+__device__ __forceinline__ void cp_async_8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_all() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct ReplayCol {            // a prepared column: its plan (nullptr = none) and CSC offset
+  const uint32_t* P;
+  int64_t jlo;
+};
+
 template <int NJ, int CAPL, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
+plan_replay_pipe_kernel(int64_t n, const double* __restrict__ vals,
+                        const int64_t* __restrict__ cscptr, const int32_t* __restrict__ cscrow,
+                        const int64_t* __restrict__ csc2csr, const double* __restrict__ cscval,
+                        double* __restrict__ m_csc, AsmWs ws, PlanWs pw,
+                        int32_t* __restrict__ direct, int* __restrict__ ndirect, int64_t c0) {
+  using S = ReplaySmem<NJ, CAPL>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = smem_raw + (size_t)w * S::bytes;
+  double* lval = reinterpret_cast<double*>(base + S::off_lval);
+  double* G = reinterpret_cast<double*>(base + S::off_G);
+  double* colbuf = reinterpret_cast<double*>(base + S::off_col);
+  int64_t* lsrc = reinterpret_cast<int64_t*>(base + S::off_lsrc);
+  const int64_t gw = blockIdx.x * (int64_t)WARPS + w;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+
+  // plan lookup + exact structural check of column k; on success the value
+  // gather is issued (cp.async) into lval
+  auto prep = [&](int64_t k) -> ReplayCol {
+    ReplayCol c{nullptr, 0};
+    if (k >= n) return c;
+    const int slot = pw.plan_slot[k];
+    const int pi = slot >= 0 ? pw.slot_plan[slot] : -1;
+    const uint32_t* P = pi >= 0 ? pw.plans + (size_t)pi * kPlanWords : nullptr;
+    const int nsteps = P ? (int)P[kPH_nsteps] : -1;
+    const int64_t jlo = cscptr[k];
+    const int nj = (int)(cscptr[k + 1] - jlo);
+    bool ok = !(nsteps < 0 || nj > NJ || (int)P[kPH_nj] != nj);
+    int total = 0;
+    int64_t clo = 0;
+    if (ok) {
+      total = (int)P[kPH_total];
+      bool bad = false;
+      if (lane < nj) {
+        const int cc = cscrow[jlo + lane];
+        bad = (uint32_t)(cc - (int32_t)k) != P[kPO_jrel + lane] ||
+              (uint32_t)pw.col_class[cc] != P[kPO_jcls + lane];
+        clo = cscptr[cc];
+      }
+      ok = total <= CAPL && !__any_sync(0xffffffffu, bad);
+    }
+    if (!ok) {
+      if (lane == 0) direct[atomicAdd(ndirect, 1)] = (int32_t)k;
+      return c;
+    }
+    if (lane < nj) lsrc[lane] = clo - (int64_t)P[kPO_loff + lane];
+    __syncwarp();
+    const uint8_t* listid = reinterpret_cast<const uint8_t*>(P + kPO_listid);
+    for (int e = lane; e < total; e += 32) {
+      const int64_t q = lsrc[listid[e]] + e;
+      cp_async_8(lval + e, cscval ? cscval + q : vals + csc2csr[q]);
+    }
+    c.jlo = jlo;
+    c.P = P;
+    return c;
+  };
+
+  ReplayCol cur = prep(c0 + gw);
+  cp_async_commit_all();
+  for (int64_t k = c0 + gw; k < n; k += nw) {
+    if (!cur.P) {
+      cur = prep(k + nw);
+      cp_async_commit_all();
+      continue;
+    }
+    const uint32_t* P = cur.P;
+    const int nj = (int)P[kPH_nj], total = (int)P[kPH_total], nsteps = (int)P[kPH_nsteps];
+    cp_async_wait_all();
+    if (lane == 0) lval[total] = 0.0;     // zero slot read by the padding ops
+    for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
+    __syncwarp();
+    {
+      const uint2* ops = reinterpret_cast<const uint2*>(P + kPO_ops) + lane;
+      const uint16_t* rdst = reinterpret_cast<const uint16_t*>(P + kPO_rdst) + lane;
+      const unsigned char* lv = reinterpret_cast<const unsigned char*>(lval);
+      int r = 0, rend = (int)P[kPO_rlen];
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll 2
+      for (int t = 0; t < nsteps; t += 2) {
+        const uint2 oo = ops[(t >> 1) * 32];
+        const uint32_t o0 = oo.x, o1 = oo.y;
+        s0 = fma(*reinterpret_cast<const double*>(lv + (o0 & 0xFFFFu)),
+                 *reinterpret_cast<const double*>(lv + (o0 >> 16)), s0);
+        s1 = fma(*reinterpret_cast<const double*>(lv + (o1 & 0xFFFFu)),
+                 *reinterpret_cast<const double*>(lv + (o1 >> 16)), s1);
+        if (t + 2 == rend) {
+          const uint16_t d = rdst[r * 32];
+          if (d != 0xFFFFu) G[d] = s0 + s1;
+          s0 = 0.0;
+          s1 = 0.0;
+          ++r;
+          rend += (int)P[kPO_rlen + r];
+        }
+      }
+    }
+    __syncwarp();
+    double y = 0.0;
+    if (lane < nj) {
+      const int ridx = (int)P[kPO_rhs + lane];
+      if (ridx >= 0) y = lval[ridx];
+    }
+    __syncwarp();                        // lval is dead: gather the next column
+    const ReplayCol nxt = prep(k + nw);
+    cp_async_commit_all();
+    if (!chol_solve_padded<NJ>(G, colbuf, nj, lane, y)) {
+      if (lane == 0) to_qr(ws, k);
+    } else if (lane < nj) {
+      m_csc[cur.jlo + lane] = y;
+    }
+    cur = nxt;
+  }
+  cp_async_wait_all();
+}
+
+template <int NJ, int CAPL, int WARPS, int MINB, bool PIPE = false>
 static int launch_replay(int64_t n, const double* vals, const int64_t* cscptr,
                          const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
                          double* m_csc, AsmWs ws, PlanWs pw, int32_t* direct, int* ndirect,
                          int64_t c0, cudaStream_t s) {
   const size_t smem = ReplaySmem<NJ, CAPL>::bytes * WARPS;
-  auto kern = plan_replay_kernel<NJ, CAPL, WARPS, MINB>;
+  auto kern = PIPE ? plan_replay_pipe_kernel<NJ, CAPL, WARPS, MINB>
+                   : plan_replay_kernel<NJ, CAPL, WARPS, MINB>;
   SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SPAI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
@@ -1068,10 +1201,16 @@ static int assemble_all(int64_t c0, int64_t n, const double* vals, const int64_t
       SPAI_LAUNCH_CHECK("plan_build_kernel");
       constexpr int RNJ = NJ;
       static int cfg = -1;
-      if (cfg < 0) { const char* e = getenv("SPAI_REPLAY_CFG"); cfg = e ? atoi(e) : 1; }
+      if (cfg < 0) { const char* e = getenv("SPAI_REPLAY_CFG"); cfg = e ? atoi(e) : 3; }
       int st = cfg == 0
           ? launch_replay<RNJ, CAPL, 8, 2>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
                                            direct, ndirect, c0, s)
+          : cfg == 2
+          ? launch_replay<RNJ, CAPL, 4, 5, true>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc,
+                                                 ws, pw, direct, ndirect, c0, s)
+          : cfg == 3
+          ? launch_replay<RNJ, CAPL, 8, 2, true>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc,
+                                                 ws, pw, direct, ndirect, c0, s)
           : launch_replay<RNJ, CAPL, 4, 5>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
                                            direct, ndirect, c0, s);
       if (st) return st;

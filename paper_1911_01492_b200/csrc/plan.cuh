@@ -45,9 +45,14 @@ constexpr int kPO_jrel = kPO_listid + kPlanCap / 4;
 constexpr int kPO_jcls = kPO_jrel + kPlanNJ;
 constexpr int kPO_rlen = kPO_jcls + kPlanNJ;                  // [kMaxRounds]
 constexpr int kPO_rdst = kPO_rlen + kMaxRounds + 1;           // uint16 [kMaxRounds][32]
-constexpr int kPO_ops = kPO_rdst + kMaxRounds * 16;
+constexpr int kPO_ops = (kPO_rdst + kMaxRounds * 16 + 31) & ~31;   // 128-B aligned (8-byte op pairs)
 constexpr int kClassTable = 8192;    // column-class hash table (exact de-dup)
 constexpr int kPlanWords = ((kPO_ops + 32 * kPlanSteps) + 31) & ~31;
+
+// steps t and t + 1 of a lane are adjacent words (one 8-byte load per pair)
+__host__ __device__ __forceinline__ int op_index(int t, int lane) {
+  return (t >> 1) * 64 + lane * 2 + (t & 1);
+}
 
 __device__ __forceinline__ uint32_t op_pack(int ea, int eb) {   // byte offsets of two doubles
   return (uint32_t)(ea * 8) | ((uint32_t)(eb * 8) << 16);
