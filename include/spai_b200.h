@@ -401,6 +401,11 @@ int spai_blk_update(int64_t n, int k, double* X, const double* P, double* R, con
 int spai_blk_pupdate(int64_t n, int k, double* P, const double* Z, const double* beta,
                      const int* grp, const int* mask, void* stream);
 
+/* ------------------------------------------------------------------ probe
+ * FP64 CUDA-core throughput probe for the assembly roofline: launches
+ * independent DFMA chains on the stream, *flops = operations performed.    */
+int spai_dfma_probe(int64_t iters, double* scratch, double* flops, void* stream);
+
 /* ------------------------------------------------------------------ host I/O
  * Matrix Market / vector files and COO -> CSR (replace sparse.py:58-75,
  * 272-330), multithreaded host code (nthreads <= 0: all hardware threads);

@@ -137,6 +137,7 @@ _SIGS = {
     "spai_blk_gram2": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_blk_update": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_blk_pupdate": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dfma_probe": (_i32, [_i64, _vp, C.POINTER(_dbl), _vp]),
     "spai_mm_read_header": (_i32, [C.c_char_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                                    C.POINTER(_i32)]),
     "spai_mm_read_coo": (_i32, [C.c_char_p, _vp, _vp, _vp, C.POINTER(_i64), _i32]),
