@@ -155,6 +155,23 @@ class CsrMatrix:
         return CsrMatrix.from_coo(self.ncols, self.nrows, self.col_indices, rows,
                                   self.values)
 
+    def submatrix(self, row_idx, col_idx) -> "CsrMatrix":
+        """Rows `row_idx`, columns remapped onto `col_idx`, others dropped
+        (sparse.py:114-131), vectorised."""
+        row_idx = np.asarray(row_idx, dtype=np.int64)
+        col_idx = np.asarray(col_idx, dtype=np.int64)
+        colmap = -np.ones(self.ncols, dtype=np.int64)
+        colmap[col_idx] = np.arange(len(col_idx))
+        lens = self.row_offsets[row_idx + 1] - self.row_offsets[row_idx]
+        starts = np.repeat(self.row_offsets[row_idx], lens)
+        within = np.arange(int(lens.sum())) - np.repeat(np.cumsum(lens) - lens, lens)
+        pos = starts + within
+        new_rows = np.repeat(np.arange(len(row_idx)), lens)
+        mapped = colmap[self.col_indices[pos]]
+        keep = mapped >= 0
+        return CsrMatrix.from_coo(len(row_idx), len(col_idx), new_rows[keep], mapped[keep],
+                                  self.values[pos][keep])
+
     # ---- device side
     def device(self) -> "DeviceCsr":
         """HBM copy of this matrix (cached; re-uploaded if the arrays were replaced)."""

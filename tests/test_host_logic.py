@@ -89,3 +89,29 @@ def test_record_csv_format():
     rec = pb.ConvergenceRecord(variant="classic", residual_norms=[1.0, 0.5],
                                reductions_cum=[2, 4], overlapped_cum=[0, 0])
     assert rec.to_csv().splitlines()[1] == "1,1,2,0"
+
+
+def test_submatrix_matches_row_loop():
+    """sparse.py:114-131 (row-by-row extraction with column remap)."""
+    import paper_1911_01492_b200 as pb
+    rng = np.random.default_rng(0)
+    d = rng.standard_normal((30, 25))
+    d[rng.random((30, 25)) < 0.7] = 0.0
+    A = pb.CsrMatrix.from_dense(d)
+    ri = rng.permutation(30)[:12]
+    ci = rng.permutation(25)[:10]
+    B = A.submatrix(ri, ci)
+    assert np.array_equal(B.to_dense(), d[np.ix_(ri, ci)])
+    colmap = {int(c): k for k, c in enumerate(ci)}
+    rows, cols, vals = [], [], []
+    for new_i, i in enumerate(ri):
+        cs, vs = A.row(int(i))
+        for c, v in zip(cs, vs):
+            if int(c) in colmap:
+                rows.append(new_i)
+                cols.append(colmap[int(c)])
+                vals.append(v)
+    R = pb.CsrMatrix.from_coo(len(ri), len(ci), rows, cols, vals)
+    assert np.array_equal(B.row_offsets, R.row_offsets)
+    assert np.array_equal(B.col_indices, R.col_indices)
+    assert np.array_equal(B.values, R.values)
