@@ -15,8 +15,10 @@ from .errors import (BreakdownError, ConfigError, DimensionMismatchError,
 from ._lib import NativeLibraryError
 from .sparse import (CsrMatrix, DeviceCsr, as_device, read_matrix_market, read_vector, spmv,
                      write_matrix_market, write_vector)
-from .grids import (Anisotropy, StructuredGrid, assemble_poisson, assemble_q1,
-                    fd5_stencil, make_rhs, q1_device, q1_stencil, stencil_device)
+from .grids import (Anisotropy, Partition, StructuredGrid, assemble_poisson, assemble_q1,
+                    extract_local_system, fd5_stencil, make_rhs, partition_1d_strips,
+                    q1_device, q1_stencil, stencil_device)
+from .distributed import RankSystem
 from .precond import (IdentityPreconditioner, JacobiPreconditioner,
                       Preconditioner, SparseMatrixPreconditioner, SpaiStats,
                       drop_exact_zeros, jacobi, make_spai1_factory,

@@ -477,3 +477,138 @@ def _symmetric_range(A, c0, c1):
     _lib.check(lib.spai_symmetrize(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals), stream_handle()),
                "spai_symmetrize")
     return A.with_values(vals)
+
+
+# ------------------------------------------------------------------ reference RankSystem
+class _Token:
+    def __init__(self, vals):
+        self._vals = list(vals)
+
+    def ready(self):
+        return True
+
+    def valid(self):
+        return True
+
+    def wait(self):
+        return self
+
+    def get(self):
+        return self._vals
+
+
+def _tree_sum_rows(rows):
+    """commsim.py:336-347: ascending-rank pairwise sums of per-rank lists."""
+    rows = [list(r) for r in rows]
+    while len(rows) > 1:
+        nxt = []
+        for i in range(0, len(rows), 2):
+            nxt.append([a + b for a, b in zip(rows[i], rows[i + 1])] if i + 1 < len(rows)
+                       else rows[i])
+        rows = nxt
+    return rows[0]
+
+
+class RankSystem:
+    """One rank of a strip partition (krylov.py:196-232) over torch.distributed.
+
+    The reference protocol (apply_A with halo exchange, block-local apply_M,
+    fused_dots completed by an ascending-rank tree sum) works on host vectors
+    for host-driven loops; `solve(RankSystem, b_local, cfg)` instead runs the
+    device multi-rank PCG (DistributedPCG) on the same operators: A_FF and A_FH
+    become one extended-column operator, M (block-local) is padded with zero
+    halo columns."""
+
+    def __init__(self, A_ff, A_fh, part, rank, comm=None, M=None):
+        self.A_ff, self.A_fh, self.part, self.rank = A_ff, A_fh, part, rank
+        self.comm = comm if comm is not None else TorchComm()
+        self.M = M
+        self.n = A_ff.nrows
+
+    # -- halo bookkeeping for the strip partition (grids.py:99-139)
+    def _exchange(self, x):
+        import torch
+        d = self.comm.dist
+        own0 = int(self.part.owned[self.rank][0]) if self.n else 0
+        parts = []
+        reqs = []
+        recvs = []
+        for nbr, shared in self.part.neighbors[self.rank]:
+            need = [s for r, s in self.part.neighbors[nbr] if r == self.rank][0]
+            send = torch.from_numpy(np.ascontiguousarray(np.asarray(x)[need - own0]))
+            recv = torch.empty(len(shared), dtype=torch.float64)
+            reqs.append(d.P2POp(d.isend, send, nbr, self.comm.group))
+            reqs.append(d.P2POp(d.irecv, recv, nbr, self.comm.group))
+            recvs.append(recv)
+        if reqs:
+            for w in d.batch_isend_irecv(reqs):
+                w.wait()
+        for recv in recvs:
+            parts.append(recv.numpy())
+        return np.concatenate(parts) if parts else np.zeros(0)
+
+    def apply_A(self, x):
+        from .sparse import spmv
+        x = np.asarray(x, dtype=np.float64)
+        x_halo = self._exchange(x) if self.comm.size > 1 else np.zeros(0)
+        y = spmv(self.A_ff, x)
+        if self.A_fh.ncols:
+            y = y + spmv(self.A_fh, x_halo)
+        return y
+
+    def apply_M(self, x):
+        if self.M is None:
+            return np.array(x, dtype=np.float64, copy=True)
+        return self.M.apply(x)
+
+    def fused_dots(self, pairs, overlapped=False):
+        import torch
+        partials = [float(np.dot(u, v)) for u, v in pairs]
+        self.comm.reductions += 1
+        if self.comm.size == 1:
+            return _Token(partials)
+        mine = torch.tensor(partials, dtype=torch.float64)
+        allv = torch.empty(len(partials) * self.comm.size, dtype=torch.float64)
+        self.comm.dist.all_gather_into_tensor(allv, mine, group=self.comm.group)
+        rows = allv.view(self.comm.size, len(partials)).tolist()
+        return _Token(_tree_sum_rows(rows))
+
+    def log_compute(self, label):
+        pass
+
+    def poll_faults(self, iteration):
+        pass
+
+    # -- device path used by krylov.solve
+    def local_system(self, b):
+        """LocalRankSystem with extended columns [halo_lo | owned | halo_hi]."""
+        import torch
+        from .sparse import CsrMatrix, as_device
+        n = self.n
+        nbrs = [r for r, _ in self.part.neighbors[self.rank]]
+        halo_sizes = [len(s) for _, s in self.part.neighbors[self.rank]]
+        hlo = halo_sizes[nbrs.index(self.rank - 1)] if (self.rank - 1) in nbrs else 0
+        hhi = halo_sizes[nbrs.index(self.rank + 1)] if (self.rank + 1) in nbrs else 0
+        ff, fh = self.A_ff, self.A_fh
+        rows_ff = np.repeat(np.arange(n), np.diff(ff.row_offsets))
+        rows_fh = np.repeat(np.arange(n), np.diff(fh.row_offsets)) if fh.ncols else \
+            np.zeros(0, dtype=np.int64)
+        cfh = np.asarray(fh.col_indices, dtype=np.int64) if fh.ncols else np.zeros(0, np.int64)
+        cfh = np.where(cfh < hlo, cfh, cfh + n)
+        A_ext = CsrMatrix.from_coo(n, hlo + n + hhi, np.concatenate([rows_ff, rows_fh]),
+                                   np.concatenate([np.asarray(ff.col_indices) + hlo, cfh]),
+                                   np.concatenate([ff.values, fh.values if fh.ncols
+                                                   else np.zeros(0)]))
+        M_ext = None
+        if self.M is not None:
+            Mm = getattr(self.M, "M", None)
+            if Mm is None:
+                raise NotImplementedError("device multi-rank solve needs a sparse-matrix "
+                                          "preconditioner (or None)")
+            Mm = Mm.to_host() if hasattr(Mm, "to_host") else Mm
+            rows_m = np.repeat(np.arange(n), np.diff(Mm.row_offsets))
+            M_ext = as_device(CsrMatrix.from_coo(n, hlo + n + hhi, rows_m,
+                                                 np.asarray(Mm.col_indices) + hlo, Mm.values))
+        bd = b if isinstance(b, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(b, dtype=np.float64))
+        return LocalRankSystem(n, hlo, hhi, as_device(A_ext), M_ext, bd.cuda().double())

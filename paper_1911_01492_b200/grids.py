@@ -160,3 +160,75 @@ def make_rhs(grid, A, mode: str = "ones", seed: int = 0):
     if mode == "random":
         return np.random.default_rng(seed).standard_normal(n)
     raise ValueError(f"unknown rhs mode {mode!r}")
+
+
+# ---------------------------------------------------------------- partition (grids.py:48-158)
+@dataclass
+class Partition:
+    """Strip partition: per-rank owned index sets, halos and neighbour map
+    (grids.py:48-64)."""
+
+    num_ranks: int
+    owned: list            # rank -> owned global indices
+    halo: list             # rank -> halo global indices
+    neighbors: list        # rank -> [(neighbour rank, shared global indices)]
+    row_ranges: list       # rank -> (first grid row, last grid row + 1)
+
+    def rank_of(self, index: int) -> int:
+        for r, (lo, hi) in enumerate(self.row_ranges):
+            if self.owned[r].size and self.owned[r][0] <= index <= self.owned[r][-1]:
+                return r
+        raise KeyError(index)
+
+
+def partition_1d_strips(grid: StructuredGrid, p: int) -> Partition:
+    """p contiguous strips of grid rows along y, heights differing by at most
+    one, one halo line per internal interface (grids.py:99-139)."""
+    from .errors import InvalidPartitionError
+    if p < 1:
+        raise InvalidPartitionError("need at least one rank")
+    if p > grid.ny:
+        raise InvalidPartitionError(f"cannot split {grid.ny} grid rows into {p} strips")
+    base, extra = divmod(grid.ny, p)
+    row_ranges, start = [], 0
+    for r in range(p):
+        height = base + (1 if r < extra else 0)
+        row_ranges.append((start, start + height))
+        start += height
+
+    def line(iy):
+        return np.arange(grid.index(0, iy), grid.index(0, iy) + grid.nx, dtype=np.int64)
+
+    owned, halo, neighbors = [], [], []
+    for r, (lo, hi) in enumerate(row_ranges):
+        owned.append(np.arange(grid.index(0, lo), grid.index(0, hi), dtype=np.int64))
+        parts, nbrs = [], []
+        if r > 0:
+            shared = line(lo - 1)
+            parts.append(shared)
+            nbrs.append((r - 1, shared))
+        if r < p - 1:
+            shared = line(hi)
+            parts.append(shared)
+            nbrs.append((r + 1, shared))
+        halo.append(np.concatenate(parts) if parts else np.empty(0, dtype=np.int64))
+        neighbors.append(nbrs)
+    return Partition(p, owned, halo, neighbors, row_ranges)
+
+
+def extract_local_system(A, part: Partition, rank: int):
+    """(A_FF, A_FH): owned principal block and halo couplings, columns of A_FH
+    ordered like part.halo[rank] (grids.py:142-158)."""
+    from .errors import InvalidPartitionError
+    if rank >= part.num_ranks:
+        raise InvalidPartitionError(f"rank {rank} out of range")
+    if isinstance(A, DeviceCsr):
+        A = A.to_host()
+    owned, halo = part.owned[rank], part.halo[rank]
+    a_ff = A.submatrix(owned, owned)
+    if len(halo):
+        a_fh = A.submatrix(owned, halo)
+    else:
+        a_fh = CsrMatrix(len(owned), 0, np.zeros(len(owned) + 1, dtype=np.int64),
+                         np.empty(0, dtype=np.int64), np.empty(0))
+    return a_ff, a_fh

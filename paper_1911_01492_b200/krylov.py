@@ -441,6 +441,20 @@ class DeviceCGV:
             pass
 
 
+def _solve_rank(system, b, cfg, x0, callback, torch):
+    from .distributed import DistributedPCG, GpuBackend
+    if cfg.variant != "classic" or x0 is not None or callback is not None:
+        raise NotImplementedError("the device multi-rank solve runs classic PCG from x0 = 0 "
+                                  "without callbacks")
+    on_device = isinstance(b, torch.Tensor) and b.is_cuda
+    local = system.local_system(b)
+    x, rec = DistributedPCG(local, system.comm, GpuBackend(), tol=cfg.tol,
+                            maxit=cfg.maxit).solve()
+    if not cfg.record_history:
+        rec.residual_norms, rec.reductions_cum, rec.overlapped_cum = [], [], []
+    return (x if on_device else x.cpu().numpy()), rec
+
+
 def _solve_variant(system, bd, cfg, x0d, callback, on_device):
     """krylov.py:235-248 for the non-classic variants, on the device (K10)."""
     solver = DeviceCGV(cfg.variant, system.device_A, system.device_M(), cfg.tol, cfg.maxit)
@@ -512,6 +526,9 @@ def solve(system, b, cfg: SolverConfig, x0=None, callback=None):
     solver then syncs every iteration and exposes host copies of x, r, p, z).
     """
     torch = _require_cuda()
+    from .distributed import RankSystem
+    if isinstance(system, RankSystem):       # device multi-rank PCG (krylov.py:196-232 path)
+        return _solve_rank(system, b, cfg, x0, callback, torch)
     if isinstance(system, (CsrMatrix, DeviceCsr)) or (
             hasattr(system, "row_offsets") and not hasattr(system, "apply_A")):
         system = LocalSystem(system)

@@ -87,6 +87,27 @@ def _worker(rank, world, port, case, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1911_01492_b200.grids import fd5_stencil
+        if case == "rank_system":
+            # the reference multi-rank API: partition_1d_strips + extract_local_system
+            # + RankSystem (krylov.py:196-232) driving solve, CLI block-local SPAI
+            grid = pb.StructuredGrid(32, 32)
+            A = pb.assemble_poisson(grid)
+            b = pb.make_rhs(grid, A, "ones")
+            part = pb.partition_1d_strips(grid, world)
+            A_ff, A_fh = pb.extract_local_system(A, part, rank)
+            P = pb.make_spai1_factory()(A_ff)
+            rs = pb.RankSystem(A_ff, A_fh, part, rank, M=P)
+            own = part.owned[rank]
+            # protocol: apply_A == global rows, fused_dots == global dots
+            v = np.linspace(-1.0, 2.0, A.nrows)
+            yA = rs.apply_A(v[own])
+            yg = pb.spmv(A, v)[own]
+            dots = rs.fused_dots([(v[own], v[own])]).get()
+            x, rec = pb.solve(rs, b[own], pb.SolverConfig(tol=1e-8, maxit=2000))
+            q.put((rank, int(own[0]), int(own[-1]) + 1, x, rec.iterations,
+                   list(rec.residual_norms), float(np.max(np.abs(yA - yg))),
+                   abs(dots[0] - float(v @ v))))
+            return
         if case == "q1_global":
             dims = (20, 18, 16)
             part = SlabPartition(dims[-1], dims[0] * dims[1], world)
@@ -129,6 +150,25 @@ def test_two_ranks_global_spai_is_rank_invariant():
     for _, r0, r1, xr, *_ in out:
         x[r0:r1] = xr
     assert np.max(np.abs(x - x1.cpu().numpy())) <= 1e-7
+
+
+def test_reference_rank_system_api_matches_reference(golden):
+    """partition_1d_strips / extract_local_system / RankSystem + solve on two
+    ranks reproduce the reference's own 2-rank run (cli.py:234-253)."""
+    out = _run(2, "rank_system")
+    for o in out:
+        assert o[6] <= 1e-12 and o[7] <= 1e-9
+    assert abs(out[0][4] - int(golden["multirank/fd5_32x32/2/its"])) <= 1
+    ref = golden["multirank/fd5_32x32/2/hist"]
+    h = np.array(out[0][5])
+    m = min(len(h), len(ref))
+    head = ref[:m] > 1e-6 * ref[0]
+    assert np.max((np.abs(h[:m] - ref[:m]) / ref[:m])[head]) <= 1e-8
+    x = np.zeros(32 * 32)
+    for _, r0, r1, xr, *_ in out:
+        x[r0:r1] = xr
+    xr = golden["multirank/fd5_32x32/2/x"]
+    assert np.max(np.abs(x - xr)) <= 1e-6 * np.max(np.abs(xr))
 
 
 def test_two_ranks_block_local_matches_reference(golden):

@@ -115,3 +115,32 @@ def test_submatrix_matches_row_loop():
     assert np.array_equal(B.row_offsets, R.row_offsets)
     assert np.array_equal(B.col_indices, R.col_indices)
     assert np.array_equal(B.values, R.values)
+
+
+def test_partition_and_local_system_match_reference_rules():
+    """grids.py:99-158: strip heights, halos, neighbour lists and the
+    [A_FF | A_FH] split reproduce the global rows."""
+    import paper_1911_01492_b200 as pb
+    from paper_1911_01492_b200.grids import extract_local_system, partition_1d_strips
+    grid = pb.StructuredGrid(7, 10)
+    n = grid.n
+    rows = np.concatenate([np.arange(n)] + [np.arange(n - d) for d in (1, 7)]
+                          + [np.arange(d, n) for d in (1, 7)])
+    cols = np.concatenate([np.arange(n)] + [np.arange(d, n) for d in (1, 7)]
+                          + [np.arange(n - d) for d in (1, 7)])
+    A = pb.CsrMatrix.from_coo(n, n, rows, cols, np.arange(len(rows), dtype=np.float64) + 1.0)
+    for p in (1, 2, 3, 4):
+        part = partition_1d_strips(grid, p)
+        heights = [hi - lo for lo, hi in part.row_ranges]
+        assert sum(heights) == grid.ny and max(heights) - min(heights) <= 1
+        assert heights == sorted(heights, reverse=True)
+        dense = A.to_dense()
+        for r in range(p):
+            own, halo = part.owned[r], part.halo[r]
+            A_ff, A_fh = extract_local_system(A, part, r)
+            assert np.array_equal(A_ff.to_dense(), dense[np.ix_(own, own)])
+            if len(halo):
+                assert np.array_equal(A_fh.to_dense(), dense[np.ix_(own, halo)])
+            assert [nb for nb, _ in part.neighbors[r]] == [q for q in (r - 1, r + 1) if 0 <= q < p]
+    with pytest.raises(pb.InvalidPartitionError):
+        partition_1d_strips(grid, 11)
