@@ -18,7 +18,7 @@ from .sparse import (CsrMatrix, DeviceCsr, as_device, read_matrix_market, read_v
 from .grids import (Anisotropy, Partition, StructuredGrid, assemble_poisson, assemble_q1,
                     extract_local_system, fd5_stencil, make_rhs, partition_1d_strips,
                     q1_device, q1_stencil, stencil_device)
-from .distributed import RankSystem
+from .distributed import RankSystem, fused_allreduce, halo_exchange
 from .precond import (IdentityPreconditioner, JacobiPreconditioner,
                       Preconditioner, SparseMatrixPreconditioner, SpaiStats,
                       drop_exact_zeros, jacobi, make_spai1_factory,
@@ -29,7 +29,7 @@ from .block import (GRAM_MODES, GramMatrix, MultiVector, axpy, block_solve, copy
 from .multigrid import (Hierarchy, MultigridPreconditioner, build_hierarchy, prolongate_full,
                         restrict_full)
 from .krylov import (ConvergenceRecord, DeviceKrylov, DevicePCG, KrylovState,
-                     LocalSystem, SolverConfig, VARIANTS, bicgstab,
+                     LocalSystem, SolverConfig, VARIANTS, bicgstab, pipelined_consistency_check,
                      fused_dots_device, memory_accounting, reduction_rate,
                      richardson, solve)
 

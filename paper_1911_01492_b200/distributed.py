@@ -482,7 +482,7 @@ def _symmetric_range(A, c0, c1):
 # ------------------------------------------------------------------ reference RankSystem
 class _Token:
     def __init__(self, vals):
-        self._vals = list(vals)
+        self._vals = vals
 
     def ready(self):
         return True
@@ -612,3 +612,31 @@ class RankSystem:
         bd = b if isinstance(b, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(b, dtype=np.float64))
         return LocalRankSystem(n, hlo, hhi, as_device(A_ext), M_ext, bd.cuda().double())
+
+
+def fused_allreduce(comm, values, overlapped=False, rank=None):
+    """Elementwise global sum of a short list, summed in ascending-rank
+    pairwise order (commsim.py:578-585, 336-347) over torch.distributed;
+    returns a completed token (get() / valid())."""
+    import torch
+    comm = comm if comm is not None else TorchComm()
+    comm.reductions += 1
+    vals = [float(v) for v in values]
+    if comm.size == 1:
+        return _Token(vals)
+    mine = torch.tensor(vals, dtype=torch.float64)
+    allv = torch.empty(len(vals) * comm.size, dtype=torch.float64)
+    comm.dist.all_gather_into_tensor(allv, mine, group=comm.group)
+    return _Token(_tree_sum_rows(allv.view(comm.size, len(vals)).tolist()))
+
+
+def halo_exchange(comm, part, x, rank=None):
+    """This rank's halo values, ordered like part.halo[rank]
+    (commsim.py:588-596) over torch.distributed; returns a completed token."""
+    comm = comm if comm is not None else TorchComm()
+    rank = comm.rank if rank is None else rank
+    rs = RankSystem.__new__(RankSystem)
+    rs.part, rs.rank, rs.comm = part, rank, comm
+    rs.n = len(part.owned[rank])
+    return _Token(rs._exchange(np.asarray(x, dtype=np.float64)) if comm.size > 1
+                  else np.zeros(0))

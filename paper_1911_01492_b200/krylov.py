@@ -336,6 +336,22 @@ class DevicePCG:
             pass
 
 
+def pipelined_consistency_check(state: KrylovState, A, M=None):
+    """Maximum relative drift of the pipelined recurrences z = M r, w = A z
+    against fresh recomputation (krylov.py:538-549)."""
+    from .sparse import spmv
+    if state.variant != "pipelined":
+        raise ValueError("consistency check applies to the pipelined variant")
+    r = np.asarray(state.r, dtype=np.float64)
+    z_ref = M.apply(r) if M is not None else r.copy()
+    w_ref = spmv(A, np.asarray(state.z, dtype=np.float64))
+    drift = 0.0
+    for have, want in ((state.z, z_ref), (state.w, w_ref)):
+        scale = max(float(np.linalg.norm(want)), 1e-300)
+        drift = max(drift, float(np.linalg.norm(np.asarray(have) - np.asarray(want))) / scale)
+    return drift
+
+
 _CGV_CODES = {"chronopoulos_gear": 1, "gropp": 2, "pipelined": 3}
 # the reference's KrylovState buffers per variant (krylov.py:33-38)
 _CGV_STATE = {"chronopoulos_gear": ("x", "r", "u", "w", "p", "q"),

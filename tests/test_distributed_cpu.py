@@ -97,3 +97,47 @@ def test_two_rank_block_local_matches_reference(golden, world):
     assert np.max(np.abs(x - xref)) <= 1e-6 * np.max(np.abs(xref))
     assert out[0][6] == 2 * it                # two fused reductions per iteration
     assert out[0][7] == [2 * (i + 1) for i in range(it)]
+
+
+def _comm_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, REPO)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1911_01492_b200.distributed import fused_allreduce, halo_exchange
+        from paper_1911_01492_b200.grids import StructuredGrid, partition_1d_strips
+        grid = StructuredGrid(6, 9)
+        part = partition_1d_strips(grid, world)
+        g = np.arange(grid.n, dtype=np.float64) * 1.5 + 0.25
+        x_local = g[part.owned[rank]]
+        halo = halo_exchange(TorchComm(), part, x_local, rank).get()
+        vals = [0.1 * (rank + 1), 1e16 if rank == 0 else 1.0, -1e16 if rank == 1 else 3.0]
+        red = fused_allreduce(TorchComm(), vals).get()
+        q.put((rank, np.asarray(halo), np.asarray(part.halo[rank]), g, red))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_and_fused_allreduce_semantics(world):
+    """commsim.py:578-596: halo values ordered like part.halo[rank]; the sum
+    is the ascending-rank pairwise tree (commsim.py:336-347)."""
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=300) for _ in range(world)), key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    per_rank = [[0.1 * (r + 1), 1e16 if r == 0 else 1.0, -1e16 if r == 1 else 3.0]
+                for r in range(world)]
+    want = [oracle.tree_sum([np.array([pr[k]]) for pr in per_rank])[0] for k in range(3)]
+    for rank, halo, hidx, g, red in out:
+        assert np.array_equal(halo, g[hidx])
+        assert red == want
