@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libspaib200.so")
+LIB_PATH = os.environ.get("SPAI_LIB") or os.path.join(HERE, "_lib", "libspaib200.so")
 
 SPAI_OK = 0
 SPAI_E_RANK_DEFICIENT = 1

@@ -9,13 +9,17 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_lib")
-OBJ_DIR = os.path.join(HERE, "_lib", "obj")
+# experiment builds: SPAI_BUILD_TAG=<tag> SPAI_BUILD_DEFINES="NAME=VAL ..." put a
+# variant library in _lib/variants/<tag>/ (load it with SPAI_LIB=<path>)
+_TAG = os.environ.get("SPAI_BUILD_TAG", "")
+OUT_DIR = os.path.join(HERE, "_lib", "variants", _TAG) if _TAG else os.path.join(HERE, "_lib")
+OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libspaib200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-extended-lambda",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+FLAGS += [f"-D{d}" for d in os.environ.get("SPAI_BUILD_DEFINES", "").split()]
 
 
 def sources():

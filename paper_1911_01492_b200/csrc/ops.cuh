@@ -23,7 +23,11 @@ struct SellOp {
 };
 template <int WM>
 struct SymOp {
+#ifdef SPAI_SSELL_MINB
+  static constexpr int kMinBlocks = SPAI_SSELL_MINB;
+#else
   static constexpr int kMinBlocks = 4;
+#endif
   SymSell m;
   template <class XF>
   __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {

@@ -47,6 +47,10 @@ __device__ __forceinline__ int32_t ssell_lane_offset(const SymSell& A, int lane)
 // every offset and mirrored address is a kernel-parameter constant, loads go
 // out in batches of kSymBatch values + gathers.
 constexpr int kSymBatch = 7;
+#ifndef SPAI_SSELL_UPPER_BATCH
+#define SPAI_SSELL_UPPER_BATCH 7
+#endif
+constexpr int kSymUpperBatch = SPAI_SSELL_UPPER_BATCH;
 
 template <int W, bool SMEM = false, class XF>
 __device__ __forceinline__ double ssell_row_fixed(const SymSell& A, const double* __restrict__ up,
@@ -57,16 +61,16 @@ __device__ __forceinline__ double ssell_row_fixed(const SymSell& A, const double
   const double* __restrict__ mb = SMEM ? mirror_base : up;
   double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-  for (int kb = 0; kb < W; kb += kSymBatch) {
-    double v[kSymBatch], x[kSymBatch];
+  for (int kb = 0; kb < W; kb += kSymUpperBatch) {
+    double v[kSymUpperBatch], x[kSymUpperBatch];
 #pragma unroll
-    for (int u = 0; u < kSymBatch; ++u)
+    for (int u = 0; u < kSymUpperBatch; ++u)
       if (kb + u < W) {
         v[u] = SMEM ? up[(kb + u) * kSell] : __ldg(up + (kb + u) * kSell);
         x[u] = xf(i + A.g[kb + u]);
       }
 #pragma unroll
-    for (int u = 0; u < kSymBatch; ++u)
+    for (int u = 0; u < kSymUpperBatch; ++u)
       if (kb + u < W) a0 = fma(v[u], x[u], a0);
   }
 #pragma unroll
