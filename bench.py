@@ -450,6 +450,10 @@ def run_distributed(args, world, rank, local):
     from paper_1911_01492_b200.distributed import (DistributedPCG, GpuBackend, RankSetup,
                                                    SlabPartition, TorchComm)
 
+    # one collective on every rank before the first point-to-point halo
+    # (batched NCCL send/recv needs an initialised communicator)
+    dist.barrier()
+
     N = args.grid
     dims = (N, N, N)
     dev = torch.device("cuda", local)
