@@ -208,11 +208,12 @@ int spai_ssell_offsets(int64_t n, const int64_t* rowptr, const int32_t* colidx,
                        int32_t* g_out, int* w, void* stream);
 /* values needed for U: 32 * ceil(n / 32) * w                               */
 size_t spai_ssell_vals_count(int64_t n, int w);
-/* Synchronous: fills U and checks every strictly-lower entry against its
- * mirror bit for bit (*is_symmetric).  The pattern must be structurally
- * symmetric (spai_structure_is_symmetric).                                */
+/* Synchronous: fills U and (verify != 0) checks every strictly-lower entry
+ * against its mirror bit for bit (*is_symmetric); verify = 0 trusts a matrix
+ * symmetric by construction.  The pattern must be structurally symmetric
+ * (spai_structure_is_symmetric).                                           */
 int spai_ssell_fill(int64_t n, const int64_t* rowptr, const int32_t* colidx,
-                    const double* vals, const int32_t* g, int w, double* U,
+                    const double* vals, const int32_t* g, int w, double* U, int verify,
                     int* is_symmetric, void* stream);
 int spai_ssell_spmv(int64_t n, const int32_t* g, int w, const double* U,
                     const double* x, double* y, void* stream);

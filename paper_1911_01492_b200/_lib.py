@@ -95,7 +95,7 @@ _SIGS = {
     "spai_sell_spmv_tma": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "spai_ssell_offsets": (_i32, [_i64, _vp, _vp, _vp, C.POINTER(_i32), _vp]),
     "spai_ssell_vals_count": (_sz, [_i64, _i32]),
-    "spai_ssell_fill": (_i32, [_i64, _vp, _vp, _vp, _vp, _i32, _vp, C.POINTER(_i32), _vp]),
+    "spai_ssell_fill": (_i32, [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, C.POINTER(_i32), _vp]),
     "spai_ssell_spmv": (_i32, [_i64, _vp, _i32, _vp, _vp, _vp, _vp]),
     "spai_ssell_spmv_tma": (_i32, [_i64, _vp, _i32, _vp, _vp, _vp, _vp]),
     "spai_pcg_create_sym": (_i32, [C.POINTER(_vp), _i64, _vp, _i32, _vp, _vp, _dbl, _i64, _vp,

@@ -201,7 +201,7 @@ extern "C" size_t spai_ssell_vals_count(int64_t n, int w) {
 
 extern "C" int spai_ssell_fill(int64_t n, const int64_t* rowptr, const int32_t* colidx,
                                const double* vals, const int32_t* g, int w, double* U,
-                               int* is_symmetric, void* stream) {
+                               int verify, int* is_symmetric, void* stream) {
   *is_symmetric = 0;
   SymSell A;
   if (!make_symsell(g, w, U, n, &A)) { set_error("ssell: bad offset table"); return SPAI_E_ARG; }
@@ -213,8 +213,10 @@ extern "C" int spai_ssell_fill(int64_t n, const int64_t* rowptr, const int32_t* 
   const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 16));
   ssell_fill_kernel<<<b, 256, 0, s>>>(n, rowptr, colidx, vals, A, U, bad);
   SPAI_LAUNCH_CHECK("ssell_fill_kernel");
-  ssell_verify_kernel<<<b, 256, 0, s>>>(n, rowptr, colidx, vals, A, bad);
-  SPAI_LAUNCH_CHECK("ssell_verify_kernel");
+  if (verify) {
+    ssell_verify_kernel<<<b, 256, 0, s>>>(n, rowptr, colidx, vals, A, bad);
+    SPAI_LAUNCH_CHECK("ssell_verify_kernel");
+  }
   int h = 1;
   SPAI_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));

@@ -177,12 +177,17 @@ def spai1_symmetric_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
     if not A.structurally_symmetric():
         raise DimensionMismatchError(
             "symmetrised SPAI(1) needs a structurally symmetric pattern")
+    # the solve will want A's half storage anyway; building it first also
+    # certifies A = A^T bit for bit, so the CSC values alias A's values
+    A.ssell_values()
     m_csc = spai1_columns_device(A, stats)
     _, _, csc2csr = A.csc()
     vals = torch.empty_like(m_csc)
     _lib.check(_lib.load().spai_symmetrize(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals),
                                            stream_handle()), "spai_symmetrize")
-    return A.with_values(vals)
+    S = A.with_values(vals)
+    S.symmetric_by_construction = True     # 0.5 (m_p + m_p^T): bit-symmetric
+    return S
 
 
 def spai1(A) -> CsrMatrix:

@@ -270,6 +270,9 @@ class DeviceCsr:
     def csc_values(self):
         """A's values in CSC order (cached); aliases `vals` when A is
         numerically symmetric on a symmetric pattern (no copy kept)."""
+        if self._cscval is None and isinstance(self._ssell_vals, _torch().Tensor) and \
+                self.csc()[0] is self.rowptr:
+            self._cscval = self.vals          # bit-symmetric (half-storage check passed)
         if self._cscval is None:
             torch = _require_cuda()
             _, _, csc2csr = self.csc()
@@ -420,9 +423,10 @@ class DeviceCsr:
                 U = torch.empty(max(cnt, 1), dtype=torch.float64, device=self.vals.device)
                 garr = (C.c_int32 * len(g))(*g)
                 ok = C.c_int(0)
+                verify = 0 if getattr(self, "symmetric_by_construction", False) else 1
                 _lib.check(lib.spai_ssell_fill(self.nrows, ptr(self.rowptr), ptr(self.colidx),
                                                ptr(self.vals), C.cast(garr, C.c_void_p), len(g),
-                                               ptr(U), C.byref(ok), stream_handle()),
+                                               ptr(U), verify, C.byref(ok), stream_handle()),
                            "spai_ssell_fill")
                 self._ssell_vals = U if ok.value else False
         return self._ssell_vals if self._ssell_vals is not False else None
