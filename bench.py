@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--grid", type=int, default=400, help="grid points per axis")
+    ap.add_argument("--variant", default="classic",
+                    choices=["classic", "chronopoulos_gear", "pipelined"],
+                    help="PCG variant (krylov.py:348-535); the headline is classic")
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=20000)
     ap.add_argument("--no-e2e", action="store_true")
@@ -250,7 +253,7 @@ def run_ours(args):
         n, nnz = A.nrows, A.nnz
         b = A.matvec(torch.ones(n, dtype=torch.float64, device=dev))
     stream.synchronize()
-    cfg = pb.SolverConfig(tol=args.tol, maxit=args.maxit)
+    cfg = pb.SolverConfig(tol=args.tol, maxit=args.maxit, variant=args.variant)
     launches = {"n": 0}
 
     def step(Adev, bdev):
@@ -409,7 +412,7 @@ def run_ours(args):
             "scaling": "strong" if world > 1 else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"configs[2]: 3D Q1 Poisson {N}^3 ({n} DOF, nnz {nnz}), "
-                                   f"SPAI(1)+CG, b=A*1, x0=0, tol {args.tol}",
+                                   f"SPAI(1)+CG ({args.variant}), b=A*1, x0=0, tol {args.tol}",
                        "n_dof": n, "nnz": nnz, "iterations": its,
                        "l2": "inputs (21 GB matrix) far larger than the 126 MB L2",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
@@ -428,7 +431,9 @@ def run_ours(args):
                          "algorithmic_bytes_per_iteration": b_it,
                          "csr_int32_bytes_per_iteration": b_it_csr,
                          "operator_format": fmt,
-                         "stored_values_per_operator": nvals},
+                         "stored_values_per_operator": nvals,
+                         "variant": args.variant + ("" if args.variant == "classic" else
+                                                    " (bytes model is the classic one)")},
             "clocks": clocks,
             "gpu_launches": gpu_launches,
             "e2e": e2e,
@@ -447,7 +452,8 @@ def run_distributed(args, world, rank, local):
     import torch.distributed as dist
 
     import paper_1911_01492_b200 as pb
-    from paper_1911_01492_b200.distributed import (DistributedPCG, GpuBackend, RankSetup,
+    from paper_1911_01492_b200.distributed import (DistributedCGV, DistributedPCG, GpuBackend,
+                                                   RankSetup,
                                                    SlabPartition, TorchComm)
 
     # one collective on every rank before the first point-to-point halo
@@ -472,7 +478,12 @@ def run_distributed(args, world, rank, local):
         e0.record(stream)
         M = rs.preconditioner()
         e1.record(stream)
-        solver = DistributedPCG(rs.system(M), comm, be, tol=args.tol, maxit=args.maxit, chunk=32)
+        if args.variant == "classic":
+            solver = DistributedPCG(rs.system(M), comm, be, tol=args.tol, maxit=args.maxit,
+                                    chunk=32)
+        else:
+            solver = DistributedCGV(args.variant, rs.system(M), comm, be, tol=args.tol,
+                                    maxit=args.maxit, chunk=32)
         x, rec = solver.solve()
         e2.record(stream)
         e2.synchronize()
@@ -541,7 +552,8 @@ def run_distributed(args, world, rank, local):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_s / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"configs[2]: 3D Q1 Poisson {N}^3 ({n} DOF), SPAI(1)+CG, "
+            "config": {"workload": f"configs[2]: 3D Q1 Poisson {N}^3 ({n} DOF), "
+                                   f"SPAI(1)+CG ({args.variant}), "
                                    f"b=A*1, x0=0, tol {args.tol}, z-slab partition",
                        "n_dof": n, "iterations": its,
                        "parallelism": f"rows x{world} ({dist.get_backend()})",

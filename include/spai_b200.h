@@ -342,6 +342,33 @@ int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext, const int
                        const double* U, const double* xext, int64_t own_off, double* y,
                        const double* raux, void* partials_ws, double* out, const void* scal,
                        void* stream);
+/* same two entries with an explicit device status word (any solver's), and
+ * modes 5 ([(r,u),(w,u),(r,r)] with u = x, w = y, r = raux: Chronopoulos-
+ * Gear) and 6 ([(p,r),(p,q),(r,r)] with p = x, q = y: pipelined setup)     */
+int spai_dist_spmv_st(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
+                      const int64_t* cdesc, const int32_t* cols, const double* vals,
+                      const double* xext, int64_t own_off, double* y, const double* raux,
+                      void* partials_ws, double* out, const int* status, void* stream);
+int spai_dist_spmv_sym_st(int mode, int64_t n, int64_t r0, int64_t n_ext, const int32_t* g,
+                          int w, const double* U, const double* xext, int64_t own_off,
+                          double* y, const double* raux, void* partials_ws, double* out,
+                          const int* status, void* stream);
+/* Row-partitioned Chronopoulos-Gear / pipelined CG (DistributedCGV): the
+ * scalar state is a K10 VScal; variant 1 = chronopoulos_gear, 3 = pipelined */
+size_t spai_dcgv_scal_bytes(void);
+int spai_dcgv_scal_init(void* scal, double tol, int64_t maxit, void* stream);
+const int* spai_dcgv_status_ptr(const void* scal);
+int spai_dcgv_read(const void* scal, int64_t* state, double* norms, void* stream);
+int spai_dcgv_cg_update(int64_t n, double* x, double* r, double* p, double* q, const double* u,
+                        const double* w, const void* scal, void* stream);
+int spai_dcgv_pipe_update(int64_t n, double* x, double* r, double* p, double* q, double* z,
+                          double* w, double* s, double* t, const double* u, const double* v,
+                          void* partials_ws, double* out, const void* scal, void* stream);
+/* gathered[rank * 3 + k] -> ascending-rank tree sum -> the variant's loop
+ * head (count_issue: a new overlapped reduction was issued; count_body: an
+ * iteration body completed)                                                */
+int spai_dcgv_head(int variant, int nranks, const double* gathered, void* scal, double* hist,
+                   int count_issue, int count_body, void* stream);
 int spai_dist_update_p(int64_t n, double* p, const double* z, const void* scal,
                        void* stream);
 int spai_dist_update_xr(int64_t n, double* x, double* r, const double* p,

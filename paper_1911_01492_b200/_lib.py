@@ -73,6 +73,18 @@ _SIGS = {
                               _vp, _vp]),
     "spai_dist_spmv_sym": (_i32, [_i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i64, _vp, _vp,
                                   _vp, _vp, _vp, _vp]),
+    "spai_dist_spmv_st": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp,
+                                 _vp, _vp, _vp]),
+    "spai_dist_spmv_sym_st": (_i32, [_i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i64, _vp, _vp,
+                                     _vp, _vp, _vp, _vp]),
+    "spai_dcgv_scal_bytes": (_sz, []),
+    "spai_dcgv_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),
+    "spai_dcgv_status_ptr": (_vp, [_vp]),
+    "spai_dcgv_read": (_i32, [_vp, _vp, _vp, _vp]),
+    "spai_dcgv_cg_update": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dcgv_pipe_update": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     _vp, _vp, _vp]),
+    "spai_dcgv_head": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
     "spai_dist_update_p": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_dist_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_dist_reduce_step": (_i32, [_i32, _vp, _i32, _i32, _vp, _vp, _vp]),

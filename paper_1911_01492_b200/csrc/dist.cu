@@ -32,9 +32,9 @@ __global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
 dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
                  const double* __restrict__ xext, int64_t own_off, double* __restrict__ y,
                  const double* __restrict__ raux, double* partials, unsigned int* ticket,
-                 double* out, const DistScal* sc) {
-  if (MODE != 0 && sc->status != dRunning) return;
-  constexpr int K = MODE == 1 ? 3 : (MODE == 2 ? 1 : 2);
+                 double* out, const int* status) {
+  if (MODE != 0 && *status != dRunning) return;
+  constexpr int K = (MODE == 1 || MODE >= 5) ? 3 : (MODE == 2 ? 1 : 2);
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
@@ -57,6 +57,16 @@ dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
         acc[2] = fma(ri, ri, acc[2]);
       } else if (MODE == 2) {
         acc[0] = fma(xi, v, acc[0]);
+      } else if (MODE == 5) {            // Chronopoulos-Gear: w = A u, [(r,u),(w,u),(r,r)]
+        const double ri = raux[i];
+        acc[0] = fma(ri, xi, acc[0]);
+        acc[1] = fma(v, xi, acc[1]);
+        acc[2] = fma(ri, ri, acc[2]);
+      } else if (MODE == 6) {            // pipelined setup: q = A p, [(p,r),(p,q),(r,r)]
+        const double ri = raux[i];
+        acc[0] = fma(xi, ri, acc[0]);
+        acc[1] = fma(xi, v, acc[1]);
+        acc[2] = fma(ri, ri, acc[2]);
       } else if (MODE >= 3) {
         acc[0] = fma(v, xi, acc[0]);
         acc[1] = fma(xi, xi, acc[1]);
@@ -158,13 +168,15 @@ template <class OP>
 static int dist_launch(int mode, unsigned b, int64_t n, int64_t s0, int64_t s1, int64_t r0,
                        const OP& A, const double* xext, int64_t own_off, double* y,
                        const double* raux, double* part, unsigned int* ticket, double* out,
-                       const DistScal* sc, cudaStream_t s) {
+                       const int* sc, cudaStream_t s) {
   switch (mode) {
     case 0: dist_spmv_kernel<0, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
     case 1: dist_spmv_kernel<1, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
     case 2: dist_spmv_kernel<2, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
     case 3: dist_spmv_kernel<3, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
     case 4: dist_spmv_kernel<4, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 5: dist_spmv_kernel<5, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 6: dist_spmv_kernel<6, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
     default: set_error("bad dist_spmv mode %d", mode); return SPAI_E_ARG;
   }
   SPAI_LAUNCH_CHECK("dist_spmv_kernel");
@@ -206,11 +218,11 @@ extern "C" size_t spai_dist_partials_bytes(void) {
   return 256 + (size_t)num_sms() * 32 * 3 * sizeof(double);
 }
 
-extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
-                              const int64_t* cdesc, const int32_t* cols,
-                              const double* vals, const double* xext, int64_t own_off, double* y,
-                              const double* raux, void* partials_ws, double* out,
-                              const void* scal, void* stream) {
+extern "C" int spai_dist_spmv_st(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
+                                 const int64_t* cdesc, const int32_t* cols,
+                                 const double* vals, const double* xext, int64_t own_off,
+                                 double* y, const double* raux, void* partials_ws, double* out,
+                                 const int* status, void* stream) {
   const int64_t ns = (n + kSell - 1) / kSell;
   if (ns == 0) {
     if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
@@ -223,16 +235,25 @@ extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t*
   double* part = (double*)((char*)partials_ws + 256);
   const SellOp A{Sell{sliceptr, cdesc, cols, vals, ncols}};
   return dist_launch(mode, b, n, 0, ns, 0, A, xext, own_off, y, raux, part, ticket, out,
-                     (const DistScal*)scal, (cudaStream_t)stream);
+                     status, (cudaStream_t)stream);
+}
+
+extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
+                              const int64_t* cdesc, const int32_t* cols,
+                              const double* vals, const double* xext, int64_t own_off, double* y,
+                              const double* raux, void* partials_ws, double* out,
+                              const void* scal, void* stream) {
+  return spai_dist_spmv_st(mode, n, ncols, sliceptr, cdesc, cols, vals, xext, own_off, y, raux,
+                           partials_ws, out, &((const DistScal*)scal)->status, stream);
 }
 
 // Same on the half-storage extended principal submatrix (n_ext rows; the
 // owned rows are [r0, r0 + n)).
-extern "C" int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext,
-                                  const int32_t* g, int w, const double* U, const double* xext,
-                                  int64_t own_off, double* y, const double* raux,
-                                  void* partials_ws, double* out, const void* scal,
-                                  void* stream) {
+extern "C" int spai_dist_spmv_sym_st(int mode, int64_t n, int64_t r0, int64_t n_ext,
+                                     const int32_t* g, int w, const double* U,
+                                     const double* xext, int64_t own_off, double* y,
+                                     const double* raux, void* partials_ws, double* out,
+                                     const int* status, void* stream) {
   if (n == 0) {
     if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
     return SPAI_OK;
@@ -248,9 +269,18 @@ extern "C" int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext
     const unsigned b = std::max(1u, std::min(ssell_blocks((const void*)dist_spmv_kernel<1, SymOp<WM>>, s1 - s0),
                                              (unsigned)num_sms() * 32));
     st = dist_launch(mode, b, n, s0, s1, r0, op, xext, own_off, y, raux, part, ticket, out,
-                     (const DistScal*)scal, (cudaStream_t)stream);
+                     status, (cudaStream_t)stream);
   });
   return st;
+}
+
+extern "C" int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext,
+                                  const int32_t* g, int w, const double* U, const double* xext,
+                                  int64_t own_off, double* y, const double* raux,
+                                  void* partials_ws, double* out, const void* scal,
+                                  void* stream) {
+  return spai_dist_spmv_sym_st(mode, n, r0, n_ext, g, w, U, xext, own_off, y, raux, partials_ws,
+                               out, &((const DistScal*)scal)->status, stream);
 }
 
 extern "C" int spai_dist_update_p(int64_t n, double* p, const double* z, const void* scal,

@@ -590,3 +590,173 @@ extern "C" int spai_cgv_destroy(spai_cgv* s) {
   delete s;
   return SPAI_OK;
 }
+
+
+// ---------------------------------------------------------------- multi-rank
+// Row-partitioned variants (DistributedCGV, distributed.py): the vector
+// kernels below run on the owned rows; the SpMVs are the dist_spmv kernels
+// on extended vectors (halo refreshed before each); the reductions are
+// per-rank partials -> all-gather -> dcgv_head (commsim's ascending-rank
+// pairwise tree, then the variant's loop head).  For the pipelined variant
+// the all-gather is left in flight behind the two SpMVs and waited for only
+// before the head: the overlapped reduction of krylov.py:461-535.
+namespace spai {
+
+// Chronopoulos-Gear C1 on owned vectors
+__global__ void __launch_bounds__(kSpmvThreads)
+dcgv_cg_update(int64_t n, double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
+               double* __restrict__ q, const double* __restrict__ u, const double* __restrict__ w,
+               const VScal* sc) {
+  if (!vrun(sc)) return;
+  const double a = sc->alpha, b = sc->beta;
+  vloop(n, [&](int64_t i) {
+    const double pi = addm(u[i], b, p[i]);
+    const double qi = addm(w[i], b, q[i]);
+    p[i] = pi;
+    q[i] = qi;
+    x[i] = addm(x[i], a, pi);
+    r[i] = subm(r[i], a, qi);
+  });
+}
+
+// pipelined Q1 on owned vectors; partial dots [(z,r),(z,w),(r,r)] -> out
+__global__ void __launch_bounds__(kSpmvThreads)
+dcgv_pipe_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                 double* __restrict__ p, double* __restrict__ q, double* __restrict__ z,
+                 double* __restrict__ w, double* __restrict__ s, double* __restrict__ t,
+                 const double* __restrict__ u, const double* __restrict__ v, double* partials,
+                 unsigned int* ticket, double* out, const VScal* sc) {
+  if (!vrun(sc)) return;
+  const bool recombine = sc->it >= 2;
+  const double c = sc->ratio, l = sc->lam;
+  double acc[3] = {0.0, 0.0, 0.0};
+  vloop(n, [&](int64_t i) {
+    double pi = p[i], qi = q[i], si = s[i], ti = t[i];
+    if (recombine) {
+      pi = addm(z[i], c, pi);
+      qi = addm(w[i], c, qi);
+      si = addm(v[i], c, si);
+      ti = addm(u[i], c, ti);
+      p[i] = pi;
+      q[i] = qi;
+      s[i] = si;
+      t[i] = ti;
+    }
+    x[i] = addm(x[i], l, pi);
+    const double ri = subm(r[i], l, qi);
+    const double zi = subm(z[i], l, si);
+    const double wi = subm(w[i], l, ti);
+    r[i] = ri;
+    z[i] = zi;
+    w[i] = wi;
+    acc[0] = fma(zi, ri, acc[0]);
+    acc[1] = fma(zi, wi, acc[1]);
+    acc[2] = fma(ri, ri, acc[2]);
+  });
+  grid_finalize<3>(acc, partials, ticket, [&](double (&tot)[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out[k] = tot[k];
+  });
+}
+
+// gathered[rank * 3 + k] -> tree sum -> the variant's loop head
+__global__ void dcgv_head(int variant, int nranks, const double* __restrict__ gathered,
+                          VScal* sc, double* hist, int count_issue, int count_body) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (!vrun(sc)) return;
+  double tot[3];
+  for (int k = 0; k < 3; ++k) {
+    double buf[64];
+    int m = nranks;
+    for (int r = 0; r < m; ++r) buf[r] = gathered[r * 3 + k];
+    while (m > 1) {                        // ((a+b)+(c+d))...: commsim.py:336-347
+      int o = 0;
+      for (int i = 0; i < m; i += 2) buf[o++] = (i + 1 < m) ? buf[i] + buf[i + 1] : buf[i];
+      m = o;
+    }
+    tot[k] = buf[0];
+  }
+  if (count_body) sc->done += 1;
+  if (variant == kVarCG) {
+    cg_head(sc, hist, tot[0], tot[1], tot[2]);
+  } else {
+    if (count_issue) { sc->red += 1; sc->ovl += 1; }
+    pipe_head(sc, hist, tot[0], tot[1], tot[2]);
+  }
+}
+
+}  // namespace spai
+
+extern "C" size_t spai_dcgv_scal_bytes(void) { return sizeof(VScal); }
+
+extern "C" int spai_dcgv_scal_init(void* scal, double tol, int64_t maxit, void* stream) {
+  VScal h{};
+  h.tol = tol;
+  h.maxit = maxit;
+  h.norm = INFINITY;
+  h.norm0 = NAN;
+  SPAI_CUDA(cudaMemcpyAsync(scal, &h, sizeof(h), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  SPAI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return SPAI_OK;
+}
+
+// device address of the status word (for the dist_spmv kernels)
+extern "C" const int* spai_dcgv_status_ptr(const void* scal) {
+  return &((const VScal*)scal)->status;
+}
+
+extern "C" int spai_dcgv_read(const void* scal, int64_t* state, double* norms, void* stream) {
+  VScal h;
+  SPAI_CUDA(cudaMemcpyAsync(&h, scal, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  SPAI_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  state[0] = h.status;
+  state[1] = h.it;
+  state[2] = h.nnotes;
+  state[3] = h.red;
+  state[4] = h.ovl;
+  state[5] = h.done;
+  state[6] = h.div_kind;
+  norms[0] = h.norm0;
+  norms[1] = h.norm;
+  norms[2] = h.aux;
+  return SPAI_OK;
+}
+
+extern "C" int spai_dcgv_cg_update(int64_t n, double* x, double* r, double* p, double* q,
+                                   const double* u, const double* w, const void* scal,
+                                   void* stream) {
+  if (n == 0) return SPAI_OK;
+  const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 8));
+  dcgv_cg_update<<<b, kSpmvThreads, 0, (cudaStream_t)stream>>>(n, x, r, p, q, u, w, (const VScal*)scal);
+  SPAI_LAUNCH_CHECK("dcgv_cg_update");
+  return SPAI_OK;
+}
+
+extern "C" int spai_dcgv_pipe_update(int64_t n, double* x, double* r, double* p, double* q,
+                                     double* z, double* w, double* s, double* t, const double* u,
+                                     const double* v, void* partials_ws, double* out,
+                                     const void* scal, void* stream) {
+  if (n == 0) {
+    SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
+    return SPAI_OK;
+  }
+  const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 8));
+  unsigned int* ticket = (unsigned int*)partials_ws;
+  double* part = (double*)((char*)partials_ws + 256);
+  dcgv_pipe_update<<<b, kSpmvThreads, 0, (cudaStream_t)stream>>>(n, x, r, p, q, z, w, s, t, u, v,
+                                                                 part, ticket, out, (const VScal*)scal);
+  SPAI_LAUNCH_CHECK("dcgv_pipe_update");
+  return SPAI_OK;
+}
+
+extern "C" int spai_dcgv_head(int variant, int nranks, const double* gathered, void* scal,
+                              double* hist, int count_issue, int count_body, void* stream) {
+  if (nranks < 1 || nranks > 64 || (variant != kVarCG && variant != kVarPipe)) {
+    set_error("dcgv_head: bad arguments");
+    return SPAI_E_ARG;
+  }
+  dcgv_head<<<1, 32, 0, (cudaStream_t)stream>>>(variant, nranks, gathered, (VScal*)scal, hist,
+                                                count_issue, count_body);
+  SPAI_LAUNCH_CHECK("dcgv_head");
+  return SPAI_OK;
+}

@@ -101,6 +101,15 @@ class TorchComm:
             return
         self.dist.all_gather_into_tensor(gathered, out, group=self.group)
 
+    def allgather_async(self, out, gathered):
+        """Start the all-gather; returns an object whose wait() completes it
+        (NCCL: the reduction overlaps the kernels enqueued in between)."""
+        if self.size == 1 or self.stage:
+            self.allgather(out, gathered)
+            return _Done()
+        self.reductions += 1
+        return self.dist.all_gather_into_tensor(gathered, out, group=self.group, async_op=True)
+
     def halo(self, xext, own_off: int, n_own: int, hlo: int, hhi: int):
         """Fill xext[:hlo] from rank-1's last rows, xext[own_off+n_own:] from rank+1."""
         if self.size == 1:
@@ -127,6 +136,11 @@ class TorchComm:
         if ops:
             for w in d.batch_isend_irecv(ops):
                 w.wait()
+
+
+class _Done:
+    def wait(self):
+        return True
 
 
 # ------------------------------------------------------------------ local system
@@ -223,6 +237,21 @@ class GpuBackend:
                                            _p(cols), _p(vals), _p(xext), own_off, _p(y),
                                            _p(raux), _p(ws), _p(out), _p(scal), self._s()),
                    "spai_dist_spmv")
+
+    def spmv_st(self, mode, M, xext, own_off, y, raux, ws, out, status):
+        """dist SpMV with an explicit device status word (any solver)."""
+        if isinstance(M, SymExtOperator):
+            _lib.check(self.lib.spai_dist_spmv_sym_st(
+                mode, M.n_own, M.r0, M.n_ext, C.cast(M.garr, C.c_void_p), len(M.g), _p(M.U),
+                _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out), C.c_void_p(status),
+                self._s()), "spai_dist_spmv_sym_st")
+            return
+        sliceptr, cdesc, cols = M.sell()
+        vals = M.sell_values()
+        _lib.check(self.lib.spai_dist_spmv_st(mode, M.nrows, M.ncols, _p(sliceptr), _p(cdesc),
+                                              _p(cols), _p(vals), _p(xext), own_off, _p(y),
+                                              _p(raux), _p(ws), _p(out), C.c_void_p(status),
+                                              self._s()), "spai_dist_spmv_st")
 
     def update_p(self, p_own, z, scal):
         _lib.check(self.lib.spai_dist_update_p(z.numel(), _p(p_own), _p(z), _p(scal), self._s()),
@@ -333,6 +362,159 @@ class DistributedPCG:
         rec.total_reductions = 2 * noted + (1 if early else 0)
         rec.launched_iterations = self.launched
         return self.x, rec
+
+
+class DistributedCGV:
+    """Row-partitioned Chronopoulos-Gear or pipelined CG (krylov.py:348-399,
+    461-535) with the reference's record semantics.  Each reduction is the
+    per-rank partials -> all-gather -> on-device ascending-rank tree sum and
+    loop head (spai_dcgv_head); the pipelined variant leaves the all-gather
+    in flight behind its two SpMVs (the overlapped reduction)."""
+
+    _CODES = {"chronopoulos_gear": 1, "pipelined": 3}
+
+    def __init__(self, variant, system: LocalRankSystem, comm, backend, tol=1e-8, maxit=1000,
+                 chunk=16):
+        if variant not in self._CODES:
+            raise ValueError(f"distributed variants: {sorted(self._CODES)}")
+        import torch
+        self.variant, self.code = variant, self._CODES[variant]
+        self.sys, self.comm, self.be = system, comm, backend
+        self.tol, self.maxit, self.chunk = tol, int(maxit), int(chunk)
+        be = backend
+        n, ne = system.n_own, system.n_ext
+        names_ext = ("r", "u") if variant == "chronopoulos_gear" else ("r", "p", "q", "s", "w", "v")
+        names_own = ("x", "p", "q", "w") if variant == "chronopoulos_gear" else ("x", "z", "t", "u")
+        self.v = {k: be.zeros(ne) for k in names_ext}
+        for k in names_own:
+            self.v[k] = be.zeros(n)
+        self.out = be.zeros(3)
+        self.gathered = be.zeros(3 * comm.size)
+        self.hist = be.zeros(3 * self.maxit)
+        self.ws = be.partials()
+        self.scal = torch.empty(be.lib.spai_dcgv_scal_bytes(), dtype=torch.uint8, device=be.dev)
+        _lib.check(be.lib.spai_dcgv_scal_init(_p(self.scal), float(tol), self.maxit, be._s()),
+                   "spai_dcgv_scal_init")
+        self.status = be.lib.spai_dcgv_status_ptr(_p(self.scal))
+        self.launched = 0
+
+    def _own(self, name):
+        t = self.v[name]
+        if t.numel() == self.sys.n_own:
+            return t
+        return t[self.sys.hlo:self.sys.hlo + self.sys.n_own]
+
+    def _halo(self, name):
+        s = self.sys
+        self.comm.halo(self.v[name], s.hlo, s.n_own, s.hlo, s.hhi)
+
+    def _apply(self, op, src, dst, mode=0, raux=None):
+        """dst(owned) = op src_ext (after the halo of src); op None = identity."""
+        s = self.sys
+        if op is None:
+            self._own(dst).copy_(self._own(src))
+            return
+        self.be.spmv_st(mode, op, self.v[src], s.hlo, self._own(dst), raux, self.ws, self.out,
+                        self.status)
+
+    def _head(self, count_issue, count_body):
+        _lib.check(self.be.lib.spai_dcgv_head(self.code, self.comm.size, _p(self.gathered),
+                                              _p(self.scal), _p(self.hist), count_issue,
+                                              count_body, self.be._s()), "spai_dcgv_head")
+
+    def start(self):
+        s = self.sys
+        A, M = s.A_op or s.A, s.M_op or s.M
+        self._own("r").copy_(s.b)
+        if self.variant == "chronopoulos_gear":
+            self._halo("r")
+            self._apply(M, "r", "u")
+            self._halo("u")
+            self._apply(A, "u", "w", 5, self._own("r"))
+            self.comm.allgather(self.out, self.gathered)
+            self._head(0, 0)
+        else:
+            self._halo("r")
+            self._apply(M, "r", "p")
+            self._halo("p")
+            self._apply(A, "p", "q", 6, self._own("r"))
+            self.comm.allgather(self.out, self.gathered)
+            self._head(1, 0)
+            self._halo("q")
+            self._apply(M, "q", "s")
+            self._halo("s")
+            self._apply(A, "s", "t")
+            self._own("z").copy_(self._own("p"))
+            self._own("w").copy_(self._own("q"))
+
+    def iteration(self):
+        s, be = self.sys, self.be
+        A, M = s.A_op or s.A, s.M_op or s.M
+        o = self._own
+        if self.variant == "chronopoulos_gear":
+            _lib.check(be.lib.spai_dcgv_cg_update(s.n_own, _p(o("x")), _p(o("r")), _p(o("p")),
+                                                  _p(o("q")), _p(o("u")), _p(o("w")),
+                                                  _p(self.scal), be._s()), "spai_dcgv_cg_update")
+            self._halo("r")
+            self._apply(M, "r", "u")
+            self._halo("u")
+            self._apply(A, "u", "w", 5, o("r"))
+            self.comm.allgather(self.out, self.gathered)
+            self._head(0, 1)
+        else:
+            _lib.check(be.lib.spai_dcgv_pipe_update(
+                s.n_own, _p(o("x")), _p(o("r")), _p(o("p")), _p(o("q")), _p(o("z")), _p(o("w")),
+                _p(o("s")), _p(o("t")), _p(o("u")), _p(o("v")), _p(self.ws), _p(self.out),
+                _p(self.scal), be._s()), "spai_dcgv_pipe_update")
+            pending = self.comm.allgather_async(self.out, self.gathered)
+            self._halo("w")
+            self._apply(M, "w", "v")
+            self._halo("v")
+            self._apply(A, "v", "u")
+            pending.wait()
+            self._head(1, 1)
+        self.launched += 1
+
+    def read(self):
+        state = np.zeros(7, dtype=np.int64)
+        norms = np.zeros(3)
+        _lib.check(self.be.lib.spai_dcgv_read(_p(self.scal), state.ctypes.data, norms.ctypes.data,
+                                              self.be._s()), "spai_dcgv_read")
+        keys = ("status", "it", "notes", "red", "ovl", "done", "div_kind")
+        d = {k: int(v) for k, v in zip(keys, state)}
+        d.update(norm0=float(norms[0]), norm=float(norms[1]), aux=float(norms[2]))
+        return d
+
+    def solve(self):
+        """Returns (x_owned, ConvergenceRecord) with the reference's semantics."""
+        from .krylov import _CGV_BREAKDOWN, _EXTRA_OPS, memory_accounting
+        self.start()
+        st = self.read()
+        while st["status"] == 0:
+            for _ in range(self.chunk):
+                self.iteration()
+            st = self.read()
+        if st["status"] == 3:
+            raise BreakdownError(_CGV_BREAKDOWN[self.variant].format(st["aux"]))
+        if st["status"] == 4:
+            raise DivergenceError("non-finite residual norm" if st["div_kind"] == 2
+                                  else "non-finite value in solver recurrence")
+        rec = ConvergenceRecord(variant=self.variant,
+                                vector_memory_units=memory_accounting(self.variant),
+                                extra_vector_ops_units=_EXTRA_OPS[self.variant])
+        k, m = st["notes"], self.maxit
+        h = self.hist.cpu().numpy()
+        rec.residual_norms = [float(v) for v in h[:k]]
+        rec.reductions_cum = [int(v) for v in h[m:m + k]]
+        rec.overlapped_cum = [int(v) for v in h[2 * m:2 * m + k]]
+        rec.initial_residual = st["norm0"]
+        rec.iterations = st["it"]
+        rec.converged = st["status"] == 1
+        rec.final_residual = st["norm"]
+        rec.total_reductions = st["red"]
+        rec.total_overlapped = st["ovl"]
+        rec.launched_iterations = self.launched
+        return self._own("x"), rec
 
 
 # ------------------------------------------------------------------ local operators

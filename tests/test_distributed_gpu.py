@@ -19,8 +19,8 @@ import torch.distributed as dist            # noqa: E402
 import torch.multiprocessing as mp          # noqa: E402
 
 import paper_1911_01492_b200 as pb          # noqa: E402
-from paper_1911_01492_b200.distributed import (DistributedPCG, GpuBackend,  # noqa: E402
-                                               SlabPartition, TorchComm,
+from paper_1911_01492_b200.distributed import (DistributedCGV, DistributedPCG,  # noqa: E402
+                                               GpuBackend, SlabPartition, TorchComm,
                                                q1_rank_system, stencil_rank_system)
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -108,6 +108,17 @@ def _worker(rank, world, port, case, q):
                    list(rec.residual_norms), float(np.max(np.abs(yA - yg))),
                    abs(dots[0] - float(v @ v))))
             return
+        if case.startswith("variant_"):
+            variant = case[len("variant_"):]
+            dims = (20, 18, 16)
+            part = SlabPartition(dims[-1], dims[0] * dims[1], world)
+            sysr = q1_rank_system(dims, part, rank, "global")
+            x, rec = DistributedCGV(variant, sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                                    maxit=2000).solve()
+            r0, r1 = part.rows(rank)
+            q.put((rank, r0, r1, x.cpu().numpy(), rec.iterations, list(rec.residual_norms),
+                   rec.reductions_cum, rec.overlapped_cum, rec.total_reductions))
+            return
         if case == "q1_global":
             dims = (20, 18, 16)
             part = SlabPartition(dims[-1], dims[0] * dims[1], world)
@@ -169,6 +180,39 @@ def test_reference_rank_system_api_matches_reference(golden):
         x[r0:r1] = xr
     xr = golden["multirank/fd5_32x32/2/x"]
     assert np.max(np.abs(x - xr)) <= 1e-6 * np.max(np.abs(xr))
+
+
+@pytest.mark.parametrize("variant", ["chronopoulos_gear", "pipelined"])
+def test_distributed_variants_match_single_gpu(variant):
+    """Row-partitioned Chronopoulos-Gear / pipelined CG (1 rank, and 2 ranks
+    over gloo) against the single-GPU K10 solve: same iterations, histories
+    and reduction / overlap accounting."""
+    dims = (20, 18, 16)
+    A = pb.q1_device(dims)
+    S = pb.spai1_symmetric_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    x1, rec1 = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                        pb.SolverConfig(variant=variant, tol=1e-10, maxit=2000))
+    h1 = np.array(rec1.residual_norms)
+    part = SlabPartition(dims[-1], dims[0] * dims[1], 1)
+    sysr = q1_rank_system(dims, part, 0)
+    x, rec = DistributedCGV(variant, sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                            maxit=2000).solve()
+    assert rec.iterations == rec1.iterations
+    assert rec.reductions_cum == rec1.reductions_cum
+    assert rec.overlapped_cum == rec1.overlapped_cum
+    h = np.array(rec.residual_norms)
+    assert np.all(np.abs(h - h1) <= 1e-9 * h1 + 1e-14 * rec1.initial_residual)
+    assert float((x - x1).abs().max()) <= 1e-8
+    out = _run(2, f"variant_{variant}")
+    assert {o[4] for o in out} == {rec1.iterations}
+    assert out[0][6] == rec1.reductions_cum and out[0][7] == rec1.overlapped_cum
+    h2 = np.array(out[0][5])
+    assert np.all(np.abs(h2 - h1) <= 1e-8 * h1 + 1e-14 * rec1.initial_residual)
+    xs = np.zeros(x1.numel())
+    for _, r0, r1, xr, *_ in out:
+        xs[r0:r1] = xr
+    assert np.max(np.abs(xs - x1.cpu().numpy())) <= 1e-7
 
 
 def test_two_ranks_block_local_matches_reference(golden):
