@@ -308,6 +308,11 @@ int spai_ksolver_create(spai_ksolver** out, int kind, int64_t n, const int64_t* 
                         const int32_t* m_cols, const double* M_vals, double tol,
                         int use_tol, double relax, int64_t maxit, void* ws,
                         size_t ws_bytes, void* stream);
+/* Switch A (and M when M_U != NULL, same pattern as A) to the symmetric
+ * half-storage SELL operators (K5c) built with spai_ssell_fill on offsets g[w];
+ * call after create, before start (products equal the SELL path to rounding). */
+int spai_ksolver_set_symmetric(spai_ksolver* s, const int32_t* g, int w, const double* A_U,
+                               const double* M_U);
 int spai_ksolver_start(spai_ksolver* s, const double* b);
 int spai_ksolver_advance(spai_ksolver* s, int64_t iters);
 int spai_ksolver_poll(spai_ksolver* s, int* status, int64_t* iterations, double* norm0,

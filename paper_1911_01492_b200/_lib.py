@@ -57,6 +57,7 @@ _SIGS = {
     "spai_ksolver_workspace_bytes": (_sz, [_i64, _i64]),
     "spai_ksolver_create": (_i32, [C.POINTER(_vp), _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                    _vp, _dbl, _i32, _dbl, _i64, _vp, _sz, _vp]),
+    "spai_ksolver_set_symmetric": (_i32, [_vp, _vp, _i32, _vp, _vp]),
     "spai_ksolver_start": (_i32, [_vp, _vp]),
     "spai_ksolver_advance": (_i32, [_vp, _i64]),
     "spai_ksolver_poll": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),

@@ -11,8 +11,7 @@
 //   B7 x += alpha ph + omega sh, r = s - omega t, [(r^,r),(r,r)] -> rho, norm
 // Richardson iteration (2 kernels, 1 reduction):
 //   R1 x += omega M r                      R2 r = b - A x, [(r,r)] -> norm
-#include "sell.cuh"
-#include "spmv_core.cuh"
+#include "ops.cuh"
 
 namespace spai {
 
@@ -46,9 +45,9 @@ __global__ void bicg_b1(int64_t n, KVecs v, const KScal* sc) {
 }
 
 // y = M x (or copy when no M)
-template <bool HAS_M>
-__global__ void __launch_bounds__(kSpmvThreads)
-k_apply_m(int64_t n, int64_t nslices, Sell M, const double* __restrict__ x, double* __restrict__ y,
+template <bool HAS_M, class OPM>
+__global__ void __launch_bounds__(kSpmvThreads, OPM::kMinBlocks)
+k_apply_m(int64_t n, int64_t nslices, OPM M, const double* __restrict__ x, double* __restrict__ y,
           const KScal* sc) {
   if (!krun(sc)) return;
   const int lane = threadIdx.x & 31;
@@ -56,22 +55,23 @@ k_apply_m(int64_t n, int64_t nslices, Sell M, const double* __restrict__ x, doub
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   for (int64_t s = w0; s < nslices; s += nw) {
     double acc = 0.0;
-    if (HAS_M) acc = sell_row(M, s, lane, [&](int32_t j) { return __ldg(x + j); });
+    if (HAS_M) acc = M.row(s, lane, [&](int32_t j) { return __ldg(x + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) y[i] = HAS_M ? acc : x[i];
   }
 }
 
 // B3: v = A ph, [(rh, v)] -> alpha
-__global__ void __launch_bounds__(kSpmvThreads)
-bicg_b3(int64_t n, int64_t nslices, Sell A, KVecs v, KScal* sc) {
+template <class OPA>
+__global__ void __launch_bounds__(kSpmvThreads, OPA::kMinBlocks)
+bicg_b3(int64_t n, int64_t nslices, OPA A, KVecs v, KScal* sc) {
   if (!krun(sc)) return;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   double acc[1] = {0.0};
   for (int64_t s = w0; s < nslices; s += nw) {
-    const double y = sell_row(A, s, lane, [&](int32_t j) { return __ldg(v.ph + j); });
+    const double y = A.row(s, lane, [&](int32_t j) { return __ldg(v.ph + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) { v.v[i] = y; acc[0] = fma(v.rh[i], y, acc[0]); }
   }
@@ -91,15 +91,16 @@ __global__ void bicg_b4(int64_t n, KVecs v, const KScal* sc) {
 }
 
 // B6: t = A sh, [(t,s),(t,t)] -> omega
-__global__ void __launch_bounds__(kSpmvThreads)
-bicg_b6(int64_t n, int64_t nslices, Sell A, KVecs v, KScal* sc) {
+template <class OPA>
+__global__ void __launch_bounds__(kSpmvThreads, OPA::kMinBlocks)
+bicg_b6(int64_t n, int64_t nslices, OPA A, KVecs v, KScal* sc) {
   if (!krun(sc)) return;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   double acc[2] = {0.0, 0.0};
   for (int64_t s = w0; s < nslices; s += nw) {
-    const double y = sell_row(A, s, lane, [&](int32_t j) { return __ldg(v.sh + j); });
+    const double y = A.row(s, lane, [&](int32_t j) { return __ldg(v.sh + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) {
       v.t[i] = y;
@@ -146,9 +147,9 @@ bicg_b7(int64_t n, KVecs v, KScal* sc) {
 }
 
 // Richardson R1: x += omega * (M r)
-template <bool HAS_M>
-__global__ void __launch_bounds__(kSpmvThreads)
-rich_r1(int64_t n, int64_t nslices, Sell M, KVecs v, const KScal* sc) {
+template <bool HAS_M, class OPM>
+__global__ void __launch_bounds__(kSpmvThreads, OPM::kMinBlocks)
+rich_r1(int64_t n, int64_t nslices, OPM M, KVecs v, const KScal* sc) {
   if (!krun(sc)) return;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
@@ -156,22 +157,23 @@ rich_r1(int64_t n, int64_t nslices, Sell M, KVecs v, const KScal* sc) {
   const double om = sc->relax;
   for (int64_t s = w0; s < nslices; s += nw) {
     double z = 0.0;
-    if (HAS_M) z = sell_row(M, s, lane, [&](int32_t j) { return __ldg(v.r + j); });
+    if (HAS_M) z = M.row(s, lane, [&](int32_t j) { return __ldg(v.r + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) v.x[i] = v.x[i] + om * (HAS_M ? z : v.r[i]);
   }
 }
 
 // Richardson R2: r = b - A x, [(r,r)]
-__global__ void __launch_bounds__(kSpmvThreads)
-rich_r2(int64_t n, int64_t nslices, Sell A, KVecs v, KScal* sc) {
+template <class OPA>
+__global__ void __launch_bounds__(kSpmvThreads, OPA::kMinBlocks)
+rich_r2(int64_t n, int64_t nslices, OPA A, KVecs v, KScal* sc) {
   if (!krun(sc)) return;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
   double acc[1] = {0.0};
   for (int64_t s = w0; s < nslices; s += nw) {
-    const double ax = sell_row(A, s, lane, [&](int32_t j) { return __ldg(v.x + j); });
+    const double ax = A.row(s, lane, [&](int32_t j) { return __ldg(v.x + j); });
     const int64_t i = s * kSell + lane;
     if (i < n) {
       const double ri = v.b[i] - ax;
@@ -217,6 +219,8 @@ k_start(int64_t n, KVecs v, KScal* sc, int bicg) {
 }
 
 unsigned sell_blocks(const void* kern, int64_t nslices);
+unsigned ssell_blocks(const void* kern, int64_t nslices);
+bool make_symsell(const int32_t* g, int w, const double* U, int64_t n, SymSell* out);
 
 }  // namespace spai
 
@@ -226,6 +230,8 @@ struct spai_ksolver {
   int kind = 0;                 // 1 BiCGStab, 2 Richardson
   int64_t n = 0, nslices = 0;
   Sell A{}, M{};
+  bool symA = false, symM = false;   // half-storage operators (spai_ksolver_set_symmetric)
+  SymSell As{}, Ms{};
   bool hasM = false;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -264,7 +270,7 @@ extern "C" int spai_ksolver_create(spai_ksolver** out, int kind, int64_t n, cons
     if (e != cudaSuccess) { delete s; return cuda_fail(e, "cudaStreamCreate"); }
     s->own_stream = true;
   }
-  s->bs = sell_blocks((const void*)bicg_b3, s->nslices);
+  s->bs = sell_blocks((const void*)bicg_b3<SellOp>, s->nslices);
   s->bs = std::min<unsigned>(s->bs, (unsigned)num_sms() * 32);
   s->bv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kSpmvThreads - 1) / kSpmvThreads, num_sms() * 8));
   char* p = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -283,23 +289,41 @@ extern "C" int spai_ksolver_create(spai_ksolver** out, int kind, int64_t n, cons
   return SPAI_OK;
 }
 
-static int kiter(spai_ksolver* s) {
+template <class OPA, class OPM>
+static void kiter_ops(spai_ksolver* s, const OPA& A, const OPM& M) {
   cudaStream_t st = s->stream;
   const int64_t n = s->n, ns = s->nslices;
   if (s->kind == 1) {
     bicg_b1<<<s->bv, 256, 0, st>>>(n, s->v, s->sc);
-    if (s->hasM) k_apply_m<true><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->M, s->v.p, s->v.ph, s->sc);
-    else k_apply_m<false><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->M, s->v.p, s->v.ph, s->sc);
-    bicg_b3<<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->A, s->v, s->sc);
+    if (s->hasM) k_apply_m<true><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, M, s->v.p, s->v.ph, s->sc);
+    else k_apply_m<false><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, M, s->v.p, s->v.ph, s->sc);
+    bicg_b3<<<s->bs, kSpmvThreads, 0, st>>>(n, ns, A, s->v, s->sc);
     bicg_b4<<<s->bv, 256, 0, st>>>(n, s->v, s->sc);
-    if (s->hasM) k_apply_m<true><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->M, s->v.s, s->v.sh, s->sc);
-    else k_apply_m<false><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->M, s->v.s, s->v.sh, s->sc);
-    bicg_b6<<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->A, s->v, s->sc);
+    if (s->hasM) k_apply_m<true><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, M, s->v.s, s->v.sh, s->sc);
+    else k_apply_m<false><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, M, s->v.s, s->v.sh, s->sc);
+    bicg_b6<<<s->bs, kSpmvThreads, 0, st>>>(n, ns, A, s->v, s->sc);
     bicg_b7<<<s->bs, kSpmvThreads, 0, st>>>(n, s->v, s->sc);
   } else {
-    if (s->hasM) rich_r1<true><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->M, s->v, s->sc);
-    else rich_r1<false><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->M, s->v, s->sc);
-    rich_r2<<<s->bs, kSpmvThreads, 0, st>>>(n, ns, s->A, s->v, s->sc);
+    if (s->hasM) rich_r1<true><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, M, s->v, s->sc);
+    else rich_r1<false><<<s->bs, kSpmvThreads, 0, st>>>(n, ns, M, s->v, s->sc);
+    rich_r2<<<s->bs, kSpmvThreads, 0, st>>>(n, ns, A, s->v, s->sc);
+  }
+}
+
+template <class OPA>
+static void kiter_m(spai_ksolver* s, const OPA& A) {
+  if (s->symM) {
+    SPAI_SSELL_DISPATCH(s->Ms.w, kiter_ops(s, A, SymOp<WM>{s->Ms}));
+  } else {
+    kiter_ops(s, A, SellOp{s->M});
+  }
+}
+
+static int kiter(spai_ksolver* s) {
+  if (s->symA) {
+    SPAI_SSELL_DISPATCH(s->As.w, kiter_m(s, SymOp<WM>{s->As}));
+  } else {
+    kiter_m(s, SellOp{s->A});
   }
   SPAI_LAUNCH_CHECK("ksolver iteration");
   return SPAI_OK;
@@ -370,5 +394,24 @@ extern "C" int spai_ksolver_destroy(spai_ksolver* s) {
   if (s->own_stream) cudaStreamDestroy(s->stream);
   delete s->host_init;
   delete s;
+  return SPAI_OK;
+}
+
+// Switch A (and M when M_U != NULL) to half-storage operators (K5c, offset
+// table g): same iteration, fewer matrix bytes; A's SELL-32 layout given at
+// create time is then unused.
+extern "C" int spai_ksolver_set_symmetric(spai_ksolver* s, const int32_t* g, int w,
+                                          const double* A_U, const double* M_U) {
+  if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
+  if (A_U) {
+    if (!make_symsell(g, w, A_U, s->n, &s->As)) { set_error("ksolver: bad offset table"); return SPAI_E_ARG; }
+    s->symA = true;
+    // one resident wave (the mirrored reads rely on the slices in flight)
+    SPAI_SSELL_DISPATCH(w, s->bs = std::min(s->bs, ssell_blocks((const void*)bicg_b3<SymOp<WM>>, s->nslices)));
+  }
+  if (M_U) {
+    if (!make_symsell(g, w, M_U, s->n, &s->Ms)) { set_error("ksolver: bad offset table"); return SPAI_E_ARG; }
+    s->symM = true;
+  }
   return SPAI_OK;
 }

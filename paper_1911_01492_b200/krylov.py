@@ -638,7 +638,7 @@ class DeviceKrylov:
     """Owner of a native `spai_ksolver` (K9): kind 1 BiCGStab, kind 2 Richardson."""
 
     def __init__(self, kind, A: DeviceCsr, M: DeviceCsr | None, tol, maxit, relax=1.0,
-                 use_tol=True):
+                 use_tol=True, symmetric=None):
         torch = _require_cuda()
         self.lib = _lib.load()
         self.n, self.maxit, self.kind = A.nrows, int(maxit), kind
@@ -662,6 +662,20 @@ class DeviceKrylov:
             "spai_ksolver_create")
         self.h = h
         self.launched = 0
+        self.operator_format = "sell"
+        # half storage (K5c) when A is bit-symmetric; M too when it shares A's pattern
+        g = A.ssell_offsets() if symmetric is not False else None
+        a_u = A.ssell_values() if g else None
+        if a_u is not None:
+            m_u = None
+            if M is not None and M._pat is A._pat:
+                m_u = M.ssell_values()
+            garr = (C.c_int32 * len(g))(*g)
+            _lib.check(self.lib.spai_ksolver_set_symmetric(
+                self.h, C.cast(garr, C.c_void_p), len(g), ptr(a_u),
+                ptr(m_u) if m_u is not None else z), "spai_ksolver_set_symmetric")
+            self._keep += (a_u, m_u)
+            self.operator_format = "ssell" if (M is None or m_u is not None) else "ssell+sell"
 
     def run(self, b, chunk=32):
         _lib.check(self.lib.spai_ksolver_start(self.h, ptr(b)), "spai_ksolver_start")
@@ -733,6 +747,7 @@ def _krylov_run(kind, system, b, tol, maxit, relax=1.0, use_tol=True):
         rec.overlapped_cum = [0] * it
         rec.final_residual = norm if it > 0 else norm0
         rec.launched_iterations = s.launched
+        rec.operator_format = s.operator_format
         x = s.x()
         return (x if on_device else x.cpu().numpy()), rec
     finally:

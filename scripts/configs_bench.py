@@ -41,7 +41,8 @@ def main():
             (x, rec), t = timed(lambda: pb.bicgstab(pb.LocalSystem(A, M), b, tol=1e-8, maxit=5000))
             out[name] = {"n": A.nrows, "spai_s": t_m, "cols_per_s": A.nrows / t_m, "solve_s": t,
                          "its": rec.iterations, "converged": rec.converged,
-                         "ms_per_it": t / max(rec.iterations, 1) * 1e3}
+                         "ms_per_it": t / max(rec.iterations, 1) * 1e3,
+                         "operator_format": getattr(rec, "operator_format", None)}
             print(name, json.dumps(out[name]), flush=True)
             del A, M, b, x
     print(json.dumps(out))

@@ -590,3 +590,45 @@ def test_richardson_matches_oracle_fixed_sweeps():
                           maxit=5000, tol=1e-3)
     _, rrt = oracle.richardson(_ocsr(A), _ocsr(M), b, omega=1.0, maxit=5000, tol=1e-3)
     assert rt.converged and abs(rt.iterations - rrt.iterations) <= 1
+
+
+@pytest.mark.parametrize("kind", [1, 2])
+def test_ksolver_half_storage_matches_sell(kind):
+    """K9 on the symmetric half-storage operators (A and the symmetric SPAI on
+    A's pattern) against the SELL operators and the oracle."""
+    from paper_1911_01492_b200.krylov import DeviceKrylov
+    dims = (96, 80)
+    A = pb.q1_device(dims, eps=(1.0, 0.1))
+    S = pb.spai1_symmetric_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    maxit = 400 if kind == 1 else 60
+    hists, xs = {}, {}
+    for sym in (None, False):
+        s = DeviceKrylov(kind, A, S, 1e-10, maxit, 1.0, kind == 1, symmetric=sym)
+        assert s.operator_format == ("ssell" if sym is None else "sell")
+        if sym is None:    # A alone on half storage, M kept in SELL
+            s2 = DeviceKrylov(kind, A, pb.spai1_device(A), 1e-10, 2, 1.0, True)
+            assert s2.operator_format == "ssell+sell"
+            s2.close()
+        st = s.run(b)
+        assert st[0] in (1, 2)
+        hists[sym] = s.history(st[1])
+        xs[sym] = s.x().cpu().numpy()
+        s.close()
+    h, hs = hists[None], hists[False]
+    # BiCGStab amplifies the rounding differences of the two summation orders
+    # (see test_bicgstab_matches_oracle): tight on the first iterations only
+    assert abs(len(h) - len(hs)) <= (3 if kind == 1 else 0)
+    k = 4 if kind == 1 else len(h)
+    assert np.max(np.abs(h[:k] - hs[:k]) / hs[:k]) <= (1e-10 if kind == 1 else 1e-12)
+    Ah, Sh = A.to_host(), S.to_host()
+    bh = b.cpu().numpy()
+    if kind == 1:
+        _, rr = oracle.bicgstab_right(_ocsr(Ah), _ocsr(Sh), bh, tol=1e-10, maxit=maxit)
+        assert abs(rr.iterations - len(h)) <= 3
+        assert np.max(np.abs(xs[None] - 1.0)) <= 1e-7
+    else:
+        xr, rr = oracle.richardson(_ocsr(Ah), _ocsr(Sh), bh, omega=1.0, maxit=maxit)
+        assert np.max(np.abs(h - np.array(rr.residual_norms)) / np.array(rr.residual_norms)) \
+            <= HIST_TOL
+        assert np.max(np.abs(xs[None] - xr)) <= 1e-10 * np.max(np.abs(xr))
