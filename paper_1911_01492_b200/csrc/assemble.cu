@@ -843,6 +843,64 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
   }
 }
 
+// Product program of a plan (plan.cuh): G entries accumulated round by round
+// from the staged values (two accumulators for the two steps of a pair).
+// Software-pipelined: the 8-byte op pairs are prefetched one group of kOpAhead
+// pairs ahead into registers, each group's shared-memory operands are loaded
+// before its FMAs, and the next round's destination / length are read one
+// round early -- the plan lives in global memory (L1-resident) and the
+// load-to-use distance of the plain loop stalled the warps on it.
+constexpr int kOpAhead = 4;
+__device__ __forceinline__ void product_program(const uint32_t* __restrict__ P, int lane,
+                                                const double* lval, double* G) {
+  const uint2* ops = reinterpret_cast<const uint2*>(P + kPO_ops) + lane;
+  const uint16_t* rdst = reinterpret_cast<const uint16_t*>(P + kPO_rdst) + lane;
+  const unsigned char* lv = reinterpret_cast<const unsigned char*>(lval);
+  const int npairs = (int)P[kPH_nsteps] >> 1;
+  int r = 0, rend = (int)(P[kPO_rlen] >> 1);
+  uint32_t rlen_next = P[kPO_rlen + 1];
+  uint16_t dcur = rdst[0], dnext = rdst[32];
+  double s0 = 0.0, s1 = 0.0;
+  uint2 ring[kOpAhead];
+#pragma unroll
+  for (int i = 0; i < kOpAhead; ++i) ring[i] = i < npairs ? ops[i * 32] : make_uint2(0u, 0u);
+  for (int p0 = 0; p0 < npairs; p0 += kOpAhead) {
+    double a[kOpAhead][4];
+#pragma unroll
+    for (int i = 0; i < kOpAhead; ++i) {
+      const int p = p0 + i;
+      const uint2 oo = ring[i];
+      if (p < npairs) {
+        a[i][0] = *reinterpret_cast<const double*>(lv + (oo.x & 0xFFFFu));
+        a[i][1] = *reinterpret_cast<const double*>(lv + (oo.x >> 16));
+        a[i][2] = *reinterpret_cast<const double*>(lv + (oo.y & 0xFFFFu));
+        a[i][3] = *reinterpret_cast<const double*>(lv + (oo.y >> 16));
+      }
+      if (p + kOpAhead < npairs) ring[i] = ops[(p + kOpAhead) * 32];
+    }
+#pragma unroll
+    for (int i = 0; i < kOpAhead; ++i) {
+      const int p = p0 + i;
+      if (p < npairs) {
+        s0 = fma(a[i][0], a[i][1], s0);
+        s1 = fma(a[i][2], a[i][3], s1);
+        if (p + 1 == rend) {
+          if (dcur != 0xFFFFu) G[dcur] = s0 + s1;
+          s0 = 0.0;
+          s1 = 0.0;
+          ++r;
+          rend += (int)(rlen_next >> 1);
+          dcur = dnext;
+          if (p + 1 < npairs) {          // prefetch the round after next
+            dnext = rdst[(r + 1) * 32];
+            rlen_next = P[kPO_rlen + r + 1];
+          }
+        }
+      }
+    }
+  }
+}
+
 // (C) numeric replay: gather values, verify the relative pattern, run the
 // product program, register Cholesky, solve.  Mismatches -> direct list.
 template <int NJ, int CAPL>
@@ -910,30 +968,7 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
     // product program in rounds (plan.cuh): every lane accumulates one G entry
     // per round (rounds have even length: two accumulators for even / odd
     // steps); one flat loop so the op loads run ahead across rounds
-    {
-      const uint2* ops = reinterpret_cast<const uint2*>(P + kPO_ops) + lane;
-      const uint16_t* rdst = reinterpret_cast<const uint16_t*>(P + kPO_rdst) + lane;
-      const unsigned char* lv = reinterpret_cast<const unsigned char*>(lval);
-      int r = 0, rend = (int)P[kPO_rlen];
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll 2
-      for (int t = 0; t < nsteps; t += 2) {
-        const uint2 oo = ops[(t >> 1) * 32];     // steps t, t + 1 in one 8-byte load
-        const uint32_t o0 = oo.x, o1 = oo.y;
-        s0 = fma(*reinterpret_cast<const double*>(lv + (o0 & 0xFFFFu)),
-                 *reinterpret_cast<const double*>(lv + (o0 >> 16)), s0);
-        s1 = fma(*reinterpret_cast<const double*>(lv + (o1 & 0xFFFFu)),
-                 *reinterpret_cast<const double*>(lv + (o1 >> 16)), s1);
-        if (t + 2 == rend) {
-          const uint16_t d = rdst[r * 32];
-          if (d != 0xFFFFu) G[d] = s0 + s1;
-          s0 = 0.0;
-          s1 = 0.0;
-          ++r;
-          rend += (int)P[kPO_rlen + r];
-        }
-      }
-    }
+    product_program(P, lane, lval, G);
     __syncwarp();
     double y = 0.0;
     if (lane < nj) {
@@ -953,7 +988,10 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
 // dead once the product program and the right-hand side have read it), so
 // the gather latency overlaps arithmetic instead of stalling the warp.
 __device__ __forceinline__ void cp_async_8(void* sdst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+  // no "memory" clobber: the gathers may be batched with the surrounding
+  // loads; ordering against lval's readers comes from the __syncwarp before
+  // the gather and cp_async_wait_all (which clobbers memory) after it
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(sdst)), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_commit_all() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
@@ -1013,6 +1051,7 @@ plan_replay_pipe_kernel(int64_t n, const double* __restrict__ vals,
     if (lane < nj) lsrc[lane] = clo - (int64_t)P[kPO_loff + lane];
     __syncwarp();
     const uint8_t* listid = reinterpret_cast<const uint8_t*>(P + kPO_listid);
+#pragma unroll 4
     for (int e = lane; e < total; e += 32) {
       const int64_t q = lsrc[listid[e]] + e;
       cp_async_8(lval + e, cscval ? cscval + q : vals + csc2csr[q]);
@@ -1031,35 +1070,12 @@ plan_replay_pipe_kernel(int64_t n, const double* __restrict__ vals,
       continue;
     }
     const uint32_t* P = cur.P;
-    const int nj = (int)P[kPH_nj], total = (int)P[kPH_total], nsteps = (int)P[kPH_nsteps];
+    const int nj = (int)P[kPH_nj], total = (int)P[kPH_total];
     cp_async_wait_all();
     if (lane == 0) lval[total] = 0.0;     // zero slot read by the padding ops
     for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
     __syncwarp();
-    {
-      const uint2* ops = reinterpret_cast<const uint2*>(P + kPO_ops) + lane;
-      const uint16_t* rdst = reinterpret_cast<const uint16_t*>(P + kPO_rdst) + lane;
-      const unsigned char* lv = reinterpret_cast<const unsigned char*>(lval);
-      int r = 0, rend = (int)P[kPO_rlen];
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll 2
-      for (int t = 0; t < nsteps; t += 2) {
-        const uint2 oo = ops[(t >> 1) * 32];
-        const uint32_t o0 = oo.x, o1 = oo.y;
-        s0 = fma(*reinterpret_cast<const double*>(lv + (o0 & 0xFFFFu)),
-                 *reinterpret_cast<const double*>(lv + (o0 >> 16)), s0);
-        s1 = fma(*reinterpret_cast<const double*>(lv + (o1 & 0xFFFFu)),
-                 *reinterpret_cast<const double*>(lv + (o1 >> 16)), s1);
-        if (t + 2 == rend) {
-          const uint16_t d = rdst[r * 32];
-          if (d != 0xFFFFu) G[d] = s0 + s1;
-          s0 = 0.0;
-          s1 = 0.0;
-          ++r;
-          rend += (int)P[kPO_rlen + r];
-        }
-      }
-    }
+    product_program(P, lane, lval, G);
     __syncwarp();
     double y = 0.0;
     if (lane < nj) {
