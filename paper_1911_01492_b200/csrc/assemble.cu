@@ -531,10 +531,13 @@ __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int
     for (int l = 0; l < NJ; ++l) if (l <= lane) G[ti + l] = g[l];
   }
   __syncwarp();
-  for (int j = nj - 1; j >= 0; --j) {
+  // backward: L^T m = y, unrolled so the L loads run ahead of the shuffle chain
+  // (rows j >= nj are identity padding: L not stored, m_j = 0)
+#pragma unroll
+  for (int j = NJ - 1; j >= 0; --j) {
+    const double lj = (lane < j && j < nj) ? G[tri(j) + lane] : 0.0;
     const double mj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
-    if (lane == j) y = mj;
-    else if (lane < j) y = fma(-G[tri(j) + lane], mj, y);
+    y = lane == j ? mj : fma(-lj, mj, y);
   }
   return true;
 }
@@ -1050,11 +1053,26 @@ plan_replay_pipe_kernel(int64_t n, const double* __restrict__ vals,
     }
     if (lane < nj) lsrc[lane] = clo - (int64_t)P[kPO_loff + lane];
     __syncwarp();
-    const uint8_t* listid = reinterpret_cast<const uint8_t*>(P + kPO_listid);
-#pragma unroll 4
-    for (int e = lane; e < total; e += 32) {
-      const int64_t q = lsrc[listid[e]] + e;
-      cp_async_8(lval + e, cscval ? cscval + q : vals + csc2csr[q]);
+    // four consecutive entries per lane: one 32-bit load of their list ids
+    const uint32_t* listid4 = P + kPO_listid;
+    if (cscval) {
+      for (int e4 = lane; 4 * e4 < total; e4 += 32) {
+        const uint32_t ids = listid4[e4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = 4 * e4 + u;
+          if (e < total) cp_async_8(lval + e, cscval + lsrc[(ids >> (8 * u)) & 255u] + e);
+        }
+      }
+    } else {
+      for (int e4 = lane; 4 * e4 < total; e4 += 32) {
+        const uint32_t ids = listid4[e4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = 4 * e4 + u;
+          if (e < total) cp_async_8(lval + e, vals + csc2csr[lsrc[(ids >> (8 * u)) & 255u] + e]);
+        }
+      }
     }
     c.jlo = jlo;
     c.P = P;
