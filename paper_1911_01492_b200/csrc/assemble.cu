@@ -486,30 +486,38 @@ __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int
   const double gdiag = lane < nj ? G[ti + lane] : 1.0;
   if (lane >= nj) y = 0.0;
   double myinv = 0.0, myd = 1.0;
+  // Look-ahead: lane j+1 owns L(j+1, j) = its lij, so it forms the next pivot
+  // g[j+1] - lij^2 itself (bit-identical to its update below) and the next
+  // rsqrt starts before the shared-memory broadcast of column j completes.
+  // colbuf is double-buffered: one warp barrier per pivot.
+  double d = __shfl_sync(0xffffffffu, g[0], 0);
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
-    const double d = __shfl_sync(0xffffffffu, g[j], j);
     const double inv = rsqrt(d);
     const double lij = lane > j ? g[j] * inv : 0.0;
-    colbuf[lane] = lij;
+    double dnext = 0.0;
+    if (j + 1 < NJ) dnext = __shfl_sync(0xffffffffu, fma(-lij, lij, g[j + 1]), j + 1);
+    double* cb = colbuf + 32 * (j & 1);
+    cb[lane] = lij;
     __syncwarp();
     if (lane == j) { g[j] = d * inv; myinv = inv; myd = d; }
     else if (lane > j) g[j] = lij;
     if ((j + 1) & 1) {                 // odd start: one scalar, then aligned pairs
-      if (j + 1 < NJ) g[j + 1] = fma(-lij, colbuf[j + 1], g[j + 1]);
+      if (j + 1 < NJ) g[j + 1] = fma(-lij, cb[j + 1], g[j + 1]);
     }
 #pragma unroll
     for (int l = (j + 2) & ~1; l < NJ; l += 2) {
       if (l + 1 < NJ) {
-        const double2 c2 = *reinterpret_cast<const double2*>(colbuf + l);
+        const double2 c2 = *reinterpret_cast<const double2*>(cb + l);
         g[l] = fma(-lij, c2.x, g[l]);
         g[l + 1] = fma(-lij, c2.y, g[l + 1]);
       } else {
-        g[l] = fma(-lij, colbuf[l], g[l]);
+        g[l] = fma(-lij, cb[l], g[l]);
       }
     }
-    __syncwarp();
+    d = dnext;
   }
+  __syncwarp();
   // pivot tests after the fact: d_j > 1e-4 G_jj and the rank guard on L_jj = sqrt(d_j)
   const bool bad = lane < nj && !(myd > kFlagPivot * gdiag);
   double dmin = lane < nj ? myd : 1e300, dmax = lane < nj ? myd : 0.0;
@@ -911,7 +919,7 @@ struct ReplaySmem {
   static constexpr size_t off_lval = 0;                          // values + zero slot 1023
   static constexpr size_t off_G = (((size_t)(CAPL + 1) * 8) + 15) & ~(size_t)15;
   static constexpr size_t off_col = (off_G + (size_t)tri(NJ) * 8 + 15) & ~(size_t)15;
-  static constexpr size_t off_lsrc = off_col + 32 * 8;
+  static constexpr size_t off_lsrc = off_col + 64 * 8;     // colbuf: 2 x 32 doubles
   static constexpr size_t bytes = (off_lsrc + (size_t)NJ * 8 + 15) & ~(size_t)15;
 };
 
