@@ -470,6 +470,15 @@ spai_qr_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscp
 }
 
 // ---------------------------------------------------------------- plan path
+// G's packed lower triangle over all NJ rows: zero, with unit diagonal on the
+// padding rows nj..NJ-1 (the product program then fills rows < nj)
+template <int NJ>
+__device__ __forceinline__ void g_init(double* G, int nj, int lane) {
+  for (int i = lane; i < tri(NJ); i += 32) G[i] = 0.0;
+  __syncwarp();
+  if (lane >= nj && lane < NJ) G[tri(lane) + lane] = 1.0;
+}
+
 // Register Cholesky of the packed G in smem, padded to NJ with identity rows
 // (no per-element predicates): lane i keeps row i of the lower factor in
 // registers; column j of L is broadcast through a 32-entry smem buffer
@@ -478,11 +487,14 @@ spai_qr_kernel(const double* __restrict__ vals, const int64_t* __restrict__ cscp
 template <int NJ>
 __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int nj, int lane,
                                                   double& y) {
-  const int ti = tri(lane);
+  // G (packed lower, NJ rows, identity padding from g_init) row by row: lane i
+  // reads tri(i) + l for every l -- the entries right of the diagonal belong
+  // to later rows and never reach a lower-triangle result (lanes >= NJ read
+  // row NJ - 1 and are ignored)
+  const int ti = tri(lane < NJ ? lane : NJ - 1);
   double g[NJ];
 #pragma unroll
-  for (int l = 0; l < NJ; ++l)
-    g[l] = lane < nj ? (l <= lane ? G[ti + l] : 0.0) : (l == lane ? 1.0 : 0.0);
+  for (int l = 0; l < NJ; ++l) g[l] = G[ti + l];
   const double gdiag = lane < nj ? G[ti + lane] : 1.0;
   if (lane >= nj) y = 0.0;
   double myinv = 0.0, myd = 1.0;
@@ -974,7 +986,7 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
       lval[e] = cscval ? cscval[q] : vals[csc2csr[q]];
     }
     if (lane == 0) lval[total] = 0.0;     // zero slot read by the padding ops
-    for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
+    g_init<NJ>(G, nj, lane);
     __syncwarp();
     // product program in rounds (plan.cuh): every lane accumulates one G entry
     // per round (rounds have even length: two accumulators for even / odd
@@ -1099,7 +1111,7 @@ plan_replay_pipe_kernel(int64_t n, const double* __restrict__ vals,
     const int nj = (int)P[kPH_nj], total = (int)P[kPH_total];
     cp_async_wait_all();
     if (lane == 0) lval[total] = 0.0;     // zero slot read by the padding ops
-    for (int i = lane; i < tri(nj); i += 32) G[i] = 0.0;
+    g_init<NJ>(G, nj, lane);
     __syncwarp();
     product_program(P, lane, lval, G);
     __syncwarp();
