@@ -673,11 +673,81 @@ struct BuildSmem {
   int32_t loff[kPlanNJ + 1];
   int32_t loads[32];
   int64_t lsrc[kPlanNJ];
+  // bank-aware step order of a round (reorder_round)
+  uint32_t cand[32][33];
+  uint32_t used[32];
+  int32_t ocnt[64];              // [operand][half-warp][bank class]
+  uint16_t oaddr[64][2];
 };
+
+// Shared-memory bank classes of the product program's operand loads: an
+// 8-byte load is served per half-warp, one wavefront per distinct double in
+// the most loaded of the 16 bank pairs (element index mod 16).  The table
+// remembers two addresses per class (same address = broadcast, free).
+__device__ __forceinline__ int occ_cost(const BuildSmem& S, int idx, int addr) {
+  const int n = S.ocnt[idx];
+  return (n > 0 && S.oaddr[idx][0] == addr) || (n > 1 && S.oaddr[idx][1] == addr) ? 0 : n;
+}
+__device__ __forceinline__ void occ_add(BuildSmem& S, int idx, int addr) {
+  const int n = S.ocnt[idx];
+  if ((n > 0 && S.oaddr[idx][0] == addr) || (n > 1 && S.oaddr[idx][1] == addr)) return;
+  if (n < 2) S.oaddr[idx][n] = (uint16_t)addr;
+  S.ocnt[idx] = n + 1;
+}
+
+// Reorder the steps of one round (each lane's products are summed in any
+// order) so that every step's two operand loads spread over the bank
+// classes: greedy per step, lanes in order, each taking the remaining product
+// (and operand orientation) that adds the fewest conflicts in its half-warp.
+// The two half-warps are independent: lanes 0-15 schedule op lanes 0-15,
+// lanes 16-31 op lanes 16-31, each lane scoring two candidate products.
+__device__ void reorder_round(BuildSmem& S, uint32_t* ops, int t0, int len, int lane) {
+  for (int s = 0; s < len; ++s) S.cand[lane][s] = ops[op_index(t0 + s, lane)];
+  S.used[lane] = 0u;
+  const int h = lane & 16;                       // half-warp base (op lanes and table)
+  const int c = lane & 15;
+  const unsigned hmask = h ? 0xFFFF0000u : 0x0000FFFFu;
+  __syncwarp();
+  for (int t = 0; t < len; ++t) {
+    S.ocnt[lane] = 0;
+    S.ocnt[lane + 32] = 0;
+    __syncwarp();
+    for (int q = 0; q < 16; ++q) {
+      const int l = h + q;
+      const uint32_t used = S.used[l];
+      unsigned best = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int s = c + 16 * k;
+        if (s < len && !((used >> s) & 1u)) {
+          const uint32_t op = S.cand[l][s];
+          const int a = (int)((op & 0xFFFFu) >> 3), b = (int)(op >> 19);
+          const int cab = occ_cost(S, h + (a & 15), a) + occ_cost(S, 32 + h + (b & 15), b);
+          const int cba = occ_cost(S, h + (b & 15), b) + occ_cost(S, 32 + h + (a & 15), a);
+          const unsigned v = cab <= cba ? ((unsigned)cab << 8) | (unsigned)(s << 1)
+                                        : ((unsigned)cba << 8) | (unsigned)(s << 1) | 1u;
+          best = min(best, v);
+        }
+      }
+      best = __reduce_min_sync(hmask, best);
+      if (c == 0) {
+        const int s = (int)(best >> 1) & 127;
+        uint32_t op = S.cand[l][s];
+        if (best & 1u) op = (op >> 16) | (op << 16);
+        S.used[l] = used | (1u << s);
+        ops[op_index(t0 + t, l)] = op;
+        const int a = (int)((op & 0xFFFFu) >> 3), b = (int)(op >> 19);
+        occ_add(S, h + (a & 15), a);
+        occ_add(S, 32 + h + (b & 15), b);
+      }
+      __syncwarp();
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kBuildWarps * 32)
 plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict__ cscrow,
-                  PlanWs pw) {
+                  PlanWs pw, bool reorder) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   BuildSmem& S = reinterpret_cast<BuildSmem*>(smem_raw)[w];
@@ -846,6 +916,8 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
         // padding: 0 * 0 from the zero slot lval[total]
         for (; step < len && t0 + step < kPlanSteps; ++step)
           ops[op_index(t0 + step, lane)] = op_pack(total, total);
+        __syncwarp();
+        if (reorder && t0 + len <= kPlanSteps) reorder_round(S, ops, t0, len, lane);
         t0 += len;
       }
       ok = t0 <= kPlanSteps;
@@ -1250,8 +1322,12 @@ static int assemble_all(int64_t c0, int64_t n, const double* vals, const int64_t
     SPAI_CUDA(cudaStreamSynchronize(s));
     if (np > 0 && np <= kMaxPlans && (int64_t)np * 4 <= ncols) {
       const size_t bsm = sizeof(BuildSmem) * kBuildWarps;
+      // bank-aware step order: ~1 ms of plan building, worth it for large ranges
+      static int reorder_env = -1;
+      if (reorder_env < 0) { const char* e = getenv("SPAI_PLAN_REORDER"); reorder_env = e ? atoi(e) : 2; }
+      const bool reorder = reorder_env == 1 || (reorder_env == 2 && ncols >= (int64_t)1 << 22);
       SPAI_CUDA(cudaFuncSetAttribute(plan_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-      plan_build_kernel<<<kPlanTable / kBuildWarps / 8, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw);
+      plan_build_kernel<<<kPlanTable / kBuildWarps, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw, reorder);
       SPAI_LAUNCH_CHECK("plan_build_kernel");
       constexpr int RNJ = NJ;
       static int cfg = -1;
