@@ -779,7 +779,7 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
     for (int a = 0; a < nj; ++a)
       for (int t = lane; t < S.loff[a + 1] - S.loff[a]; t += 32) {
         S.lrow[S.loff[a] + t] = cscrow[S.lsrc[a] + t];
-        reinterpret_cast<uint8_t*>(P + kPO_listid)[S.loff[a] + t] = (uint8_t)a;
+        reinterpret_cast<uint8_t*>(P + kPO_listid)[listid_pos(S.loff[a] + t)] = (uint8_t)a;
       }
     __syncwarp();
     if (lane < nj) {
@@ -1054,7 +1054,7 @@ plan_replay_kernel(int64_t n, const double* __restrict__ vals, const int64_t* __
     __syncwarp();
     const uint8_t* listid = reinterpret_cast<const uint8_t*>(P + kPO_listid);
     for (int e = lane; e < total; e += 32) {
-      const int64_t q = lsrc[listid[e]] + e;
+      const int64_t q = lsrc[listid[listid_pos(e)]] + e;
       lval[e] = cscval ? cscval[q] : vals[csc2csr[q]];
     }
     if (lane == 0) lval[total] = 0.0;     // zero slot read by the padding ops
@@ -1145,23 +1145,24 @@ plan_replay_pipe_kernel(int64_t n, const double* __restrict__ vals,
     }
     if (lane < nj) lsrc[lane] = clo - (int64_t)P[kPO_loff + lane];
     __syncwarp();
-    // four consecutive entries per lane: one 32-bit load of their list ids
+    // one 32-bit load of list ids per lane covers entries base + lane + 32 u
+    // (listid_pos); consecutive lanes fill consecutive doubles (no conflicts)
     const uint32_t* listid4 = P + kPO_listid;
     if (cscval) {
-      for (int e4 = lane; 4 * e4 < total; e4 += 32) {
-        const uint32_t ids = listid4[e4];
+      for (int base = 0; base < total; base += 128) {
+        const uint32_t ids = listid4[(base >> 2) + lane];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int e = 4 * e4 + u;
+          const int e = base + 32 * u + lane;
           if (e < total) cp_async_8(lval + e, cscval + lsrc[(ids >> (8 * u)) & 255u] + e);
         }
       }
     } else {
-      for (int e4 = lane; 4 * e4 < total; e4 += 32) {
-        const uint32_t ids = listid4[e4];
+      for (int base = 0; base < total; base += 128) {
+        const uint32_t ids = listid4[(base >> 2) + lane];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int e = 4 * e4 + u;
+          const int e = base + 32 * u + lane;
           if (e < total) cp_async_8(lval + e, vals + csc2csr[lsrc[(ids >> (8 * u)) & 255u] + e]);
         }
       }

@@ -7,7 +7,9 @@
 // all index work: I_k, local ranks, the sparse overlap structure of
 // G = (A^T A)[J,J] and the position of e_k.  A plan stores that once:
 //   - jrel[a] = J_a - k, jcls[a] = class of column J_a  (exact match key)
-//   - loff[nj+1], listid[e]
+//   - loff[nj+1], listid[e] (list of entry e; byte listid_pos(e): each group
+//     of 128 entries is stored lane-interleaved, so lane L's 32-bit word holds
+//     entries L, L+32, L+64, L+96 of the group)
 //   - rhsidx[a]                          (entry holding A[k, J_a], or -1)
 //   - product program in "rounds": the G entries with a nonzero overlap are
 //     sorted by overlap length and dealt 32 per round (one per lane); round r
@@ -52,6 +54,10 @@ constexpr int kPlanWords = ((kPO_ops + 32 * kPlanSteps) + 31) & ~31;
 // steps t and t + 1 of a lane are adjacent words (one 8-byte load per pair)
 __host__ __device__ __forceinline__ int op_index(int t, int lane) {
   return (t >> 1) * 64 + lane * 2 + (t & 1);
+}
+
+__host__ __device__ __forceinline__ int listid_pos(int e) {
+  return (e & ~127) | ((e & 31) << 2) | ((e >> 5) & 3);
 }
 
 __device__ __forceinline__ uint32_t op_pack(int ea, int eb) {   // byte offsets of two doubles
