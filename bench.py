@@ -9,7 +9,8 @@ One step = the whole hot path on inputs already in HBM:
 value = n_dof * iterations / step time  ("DOF*it/s", setup included).
 Per-phase numbers (assembly cols/s, solve DOF*it/s, SpMV GB/s) ride along.
 `e2e` repeats the step through the public API with the matrix and b in
-pinned HOST memory (H2D inside the timed region) and x read back to host.
+pinned HOST memory (H2D inside the timed region: spai1_symmetric_from_host
+streams the values in row blocks while the assembly runs) and x read back.
 
 --impl reference times the unmodified reference (ftkrylov from
 baseline/_ref; CLI spai1 factory + solve) on a bounded sample of the same
@@ -370,9 +371,6 @@ def run_ours(args):
             h_vals = A.vals.cpu().pin_memory()
             h_b = b.cpu().pin_memory()
             h_x = torch.empty(n, dtype=torch.float64).pin_memory()
-            d_rowptr = torch.empty_like(A.rowptr)
-            d_colidx = torch.empty_like(A.colidx)
-            d_vals = torch.empty_like(A.vals)
             d_b = torch.empty_like(b)
             barrier()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -380,14 +378,15 @@ def run_ours(args):
             e_work = 0
             reps = max(1, min(args.steps, 3))
             for _ in range(reps):
-                d_rowptr.copy_(h_rowptr, non_blocking=True)
-                d_colidx.copy_(h_colidx, non_blocking=True)
-                d_vals.copy_(h_vals, non_blocking=True)
+                # public API from host buffers: the value upload overlaps the
+                # assembly (spai1_symmetric_from_host), then b and the solve
+                Ad, S_e = pb.spai1_symmetric_from_host(h_rowptr, h_colidx, h_vals)
                 d_b.copy_(h_b, non_blocking=True)
-                Ad = DeviceCsr(n, n, d_rowptr, d_colidx, d_vals)
-                _, _, rec_e, x_e = step(Ad, d_b)
+                x_e, rec_e = pb.solve(pb.LocalSystem(Ad, pb.SparseMatrixPreconditioner(S_e)),
+                                      d_b, cfg)
                 h_x.copy_(x_e, non_blocking=True)
                 e_work += n * rec_e.iterations
+                del Ad, S_e
             ev[1].record(stream)
             ev[1].synchronize()
             e_t = ev[0].elapsed_time(ev[1]) / 1e3

@@ -118,6 +118,25 @@ int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr,
                         const int64_t* csc2csr, const double* cscval, int64_t c0,
                         int64_t c1, double* m_csc, void* ws, size_t ws_bytes,
                         int64_t* bad_col, int64_t* n_fallback, void* stream);
+/* The same assembly in three phases, so the value upload can overlap the
+ * numeric work (spai1_symmetric_from_host): begin needs the pattern only
+ * (longest column -> *hmax, classes, signatures of [c0, c1), plans ->
+ * *plans); columns assembles [c0, c1) within the begun range and needs the
+ * values of those columns' stencils (any number of calls, stream-ordered);
+ * end finishes the leftover columns (QR / merge fallbacks) and reports the
+ * first error as spai_assemble does.  spai_assemble_range = begin + one
+ * columns call + end.                                                     */
+int spai_assemble_begin(int64_t n, const int64_t* cscptr, const int32_t* cscrow, int64_t c0,
+                        int64_t c1, void* ws, size_t ws_bytes, int* hmax, int* plans,
+                        void* stream);
+int spai_assemble_columns(int64_t n, const double* vals, const int64_t* cscptr,
+                          const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
+                          int64_t c0, int64_t c1, double* m_csc, void* ws, size_t ws_bytes,
+                          int hmax, int plans, void* stream);
+int spai_assemble_end(int64_t n, const double* vals, const int64_t* cscptr,
+                      const int32_t* cscrow, const int64_t* csc2csr, double* m_csc, void* ws,
+                      size_t ws_bytes, int hmax, int plans, int64_t* bad_col,
+                      int64_t* n_fallback, void* stream);
 /* Toggle the symbolic-plan replay (default on; env SPAI_NO_PLANS=1 disables):
  * columns with identical relative structure share one precomputed plan.   */
 int spai_set_assembly_plans(int enable);

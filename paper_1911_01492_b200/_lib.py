@@ -54,6 +54,12 @@ _SIGS = {
     "spai_set_assembly_plans": (_i32, [_i32]),
     "spai_assemble_range": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp,
                                    _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "spai_assemble_begin": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _sz, C.POINTER(_i32),
+                                   C.POINTER(_i32), _vp]),
+    "spai_assemble_columns": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _sz,
+                                     _i32, _i32, _vp]),
+    "spai_assemble_end": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _i32, _i32,
+                                 C.POINTER(_i64), C.POINTER(_i64), _vp]),
     "spai_ksolver_workspace_bytes": (_sz, [_i64, _i64]),
     "spai_ksolver_create": (_i32, [C.POINTER(_vp), _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                    _vp, _dbl, _i32, _dbl, _i64, _vp, _sz, _vp]),

@@ -1298,63 +1298,129 @@ extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
          align256((size_t)kMaxPlans * kPlanWords * sizeof(uint32_t));
 }
 
-template <int NJ, int CAPL, int MW, int WARPS>
-static int assemble_all(int64_t c0, int64_t n, const double* vals, const int64_t* cscptr,
-                        const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
-                        double* m_csc, AsmWs ws, PlanWs pw, int32_t* direct, int* ndirect,
-                        bool use_plans, cudaStream_t s) {
-  // columns [c0, n) are assembled (n is the end of the range here)
-  int nd = 0;
-  const int64_t ncols = n - c0;
-  if (use_plans) {
-    SPAI_CUDA(cudaMemsetAsync(pw.keys, 0, (size_t)kPlanTable * 8, s));
-    SPAI_CUDA(cudaMemsetAsync(pw.ckeys, 0, (size_t)kClassTable * 8, s));
-    SPAI_CUDA(cudaMemsetAsync(pw.crep, 0xFF, (size_t)kClassTable * 4, s));
-    SPAI_CUDA(cudaMemsetAsync(pw.nclass, 0, 4, s));
-    // classes of every column referenced by the range (all columns: cheap)
-    class_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((pw.ntot * 32 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
-        pw.ntot, cscptr, cscrow, pw);
-    SPAI_LAUNCH_CHECK("class_kernel");
-    plan_sig_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ncols * 32 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
-        n, cscptr, cscrow, pw, c0);
-    SPAI_LAUNCH_CHECK("plan_sig_kernel");
-    int np = 0;
-    SPAI_CUDA(cudaMemcpyAsync(&np, pw.nplans, 4, cudaMemcpyDeviceToHost, s));
-    SPAI_CUDA(cudaStreamSynchronize(s));
-    if (np > 0 && np <= kMaxPlans && (int64_t)np * 4 <= ncols) {
-      const size_t bsm = sizeof(BuildSmem) * kBuildWarps;
-      // bank-aware step order: ~1 ms of plan building, worth it for large ranges
-      static int reorder_env = -1;
-      if (reorder_env < 0) { const char* e = getenv("SPAI_PLAN_REORDER"); reorder_env = e ? atoi(e) : 2; }
-      const bool reorder = reorder_env == 1 || (reorder_env == 2 && ncols >= (int64_t)1 << 22);
-      SPAI_CUDA(cudaFuncSetAttribute(plan_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-      plan_build_kernel<<<kPlanTable / kBuildWarps, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw, reorder);
-      SPAI_LAUNCH_CHECK("plan_build_kernel");
-      constexpr int RNJ = NJ;
-      static int cfg = -1;
-      if (cfg < 0) { const char* e = getenv("SPAI_REPLAY_CFG"); cfg = e ? atoi(e) : 3; }
-      int st = cfg == 0
-          ? launch_replay<RNJ, CAPL, 8, 2>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
-                                           direct, ndirect, c0, s)
-          : cfg == 2
-          ? launch_replay<RNJ, CAPL, 4, 5, true>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc,
-                                                 ws, pw, direct, ndirect, c0, s)
-          : cfg == 3
-          ? launch_replay<RNJ, CAPL, 8, 2, true>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc,
-                                                 ws, pw, direct, ndirect, c0, s)
-          : launch_replay<RNJ, CAPL, 4, 5>(n, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
-                                           direct, ndirect, c0, s);
-      if (st) return st;
-      SPAI_CUDA(cudaMemcpyAsync(&nd, ndirect, 4, cudaMemcpyDeviceToHost, s));
-      SPAI_CUDA(cudaStreamSynchronize(s));
-      if (nd == 0) return SPAI_OK;
-      return launch_hash<NJ, CAPL, MW, WARPS>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, direct,
-                                              ndirect, nd, 0, s);
-    }
-  }
-  return launch_hash<NJ, CAPL, MW, WARPS>(n, vals, cscptr, cscrow, csc2csr, m_csc, ws, nullptr,
-                                          nullptr, ncols, c0, s);
+// Assembly in three phases, so a caller can overlap the value upload with the
+// numeric work (precond.spai1_symmetric_from_host): begin (pattern only:
+// longest column, classes, signatures, plans), columns (any number of column
+// ranges, values needed for their stencil), end (leftover columns, merges, QR
+// fallback, error report).  spai_assemble_range = begin + columns + end.
+struct AsmCtx {
+  AsmWs ws;
+  PlanWs pw;
+  int* maxlen;
+  int* ndirect;
+  int32_t* direct;
+  unsigned char* hdr;
+};
+
+static AsmCtx carve_ws(void* wsp, int64_t n) {
+  AsmCtx c;
+  unsigned char* b = (unsigned char*)(((uintptr_t)wsp + 255) & ~(uintptr_t)255);
+  c.hdr = b;
+  c.ws.err = (unsigned long long*)b;
+  c.ws.nmerge = (int*)(b + 8);
+  c.ws.nqr = (int*)(b + 12);
+  c.maxlen = (int*)(b + 16);
+  c.ndirect = (int*)(b + 20);
+  c.pw.nplans = (int*)(b + 24);
+  c.pw.nbuilt = (int*)(b + 28);
+  c.pw.nclass = (int*)(b + 32);
+  c.pw.ntot = n;
+  unsigned char* p = b + 256;
+  const size_t lb = align256((size_t)n * sizeof(int32_t));
+  c.ws.merge_list = (int32_t*)p; p += lb;
+  c.ws.qr_list = (int32_t*)p; p += lb;
+  c.direct = (int32_t*)p; p += lb;
+  c.pw.plan_slot = (int32_t*)p; p += lb;
+  c.pw.col_class = (int32_t*)p; p += lb;
+  c.pw.ckeys = (unsigned long long*)p;
+  c.pw.crep = (int32_t*)(p + (size_t)kClassTable * 8);
+  p += align256((size_t)kClassTable * 12);
+  c.pw.keys = (unsigned long long*)p;
+  c.pw.rep = (int32_t*)(p + (size_t)kPlanTable * 8);
+  c.pw.slot_plan = (int32_t*)(p + (size_t)kPlanTable * 12);
+  p += align256((size_t)kPlanTable * 16);
+  c.pw.plans = (uint32_t*)p;
+  return c;
 }
+
+// phase 1 with plans: classes of all columns, signatures of [c0, c1), plan
+// build.  Returns true when the plans are usable for the range.
+static bool build_plans(int64_t c0, int64_t c1, const int64_t* cscptr, const int32_t* cscrow,
+                        PlanWs pw, cudaStream_t s, int* st) {
+  *st = SPAI_OK;
+  const int64_t ncols = c1 - c0;
+  auto fail = [&](int e) { *st = e; return false; };
+  if (cudaMemsetAsync(pw.keys, 0, (size_t)kPlanTable * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(pw.ckeys, 0, (size_t)kClassTable * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(pw.crep, 0xFF, (size_t)kClassTable * 4, s) != cudaSuccess ||
+      cudaMemsetAsync(pw.nclass, 0, 4, s) != cudaSuccess) {
+    set_error("cuda: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(SPAI_E_CUDA);
+  }
+  // classes of every column referenced by the range (all columns: cheap)
+  class_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((pw.ntot * 32 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
+      pw.ntot, cscptr, cscrow, pw);
+  plan_sig_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ncols * 32 + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
+      c1, cscptr, cscrow, pw, c0);
+  int np = 0;
+  if (cudaMemcpyAsync(&np, pw.nplans, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess) {
+    set_error("cuda: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(SPAI_E_CUDA);
+  }
+  if (!(np > 0 && np <= kMaxPlans && (int64_t)np * 4 <= ncols)) return false;
+  const size_t bsm = sizeof(BuildSmem) * kBuildWarps;
+  // bank-aware step order: ~1-2 ms of plan building, worth it for large ranges
+  static int reorder_env = -1;
+  if (reorder_env < 0) { const char* e = getenv("SPAI_PLAN_REORDER"); reorder_env = e ? atoi(e) : 2; }
+  const bool reorder = reorder_env == 1 || (reorder_env == 2 && ncols >= (int64_t)1 << 22);
+  cudaFuncSetAttribute(plan_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+  plan_build_kernel<<<kPlanTable / kBuildWarps, kBuildWarps * 32, bsm, s>>>(cscptr, cscrow, pw, reorder);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_error("plan_build_kernel: %s", cudaGetErrorString(e)); return fail(SPAI_E_CUDA); }
+  return true;
+}
+
+template <int NJ, int CAPL, int MW, int WARPS>
+static int columns_impl(int64_t c0, int64_t c1, const double* vals, const int64_t* cscptr,
+                        const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
+                        double* m_csc, const AsmCtx& c, bool plans, cudaStream_t s) {
+  if (c1 <= c0) return SPAI_OK;
+  if (!plans)
+    return launch_hash<NJ, CAPL, MW, WARPS>(c1, vals, cscptr, cscrow, csc2csr, m_csc, c.ws,
+                                            nullptr, nullptr, c1 - c0, c0, s);
+  static int cfg = -1;
+  if (cfg < 0) { const char* e = getenv("SPAI_REPLAY_CFG"); cfg = e ? atoi(e) : 3; }
+  const AsmWs ws = c.ws;
+  const PlanWs pw = c.pw;
+  return cfg == 0
+      ? launch_replay<NJ, CAPL, 8, 2>(c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
+                                      c.direct, c.ndirect, c0, s)
+      : cfg == 2
+      ? launch_replay<NJ, CAPL, 4, 5, true>(c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws,
+                                            pw, c.direct, c.ndirect, c0, s)
+      : cfg == 3
+      ? launch_replay<NJ, CAPL, 8, 2, true>(c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws,
+                                            pw, c.direct, c.ndirect, c0, s)
+      : launch_replay<NJ, CAPL, 4, 5>(c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw,
+                                      c.direct, c.ndirect, c0, s);
+}
+
+template <int NJ, int CAPL, int MW, int WARPS>
+static int leftovers_impl(int64_t n, const double* vals, const int64_t* cscptr,
+                          const int32_t* cscrow, const int64_t* csc2csr, double* m_csc,
+                          const AsmCtx& c, cudaStream_t s) {
+  int nd = 0;
+  SPAI_CUDA(cudaMemcpyAsync(&nd, c.ndirect, 4, cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaStreamSynchronize(s));
+  if (nd == 0) return SPAI_OK;
+  return launch_hash<NJ, CAPL, MW, WARPS>(n, vals, cscptr, cscrow, csc2csr, m_csc, c.ws, c.direct,
+                                          c.ndirect, nd, 0, s);
+}
+
+#define SPAI_ASM_DISPATCH(HMAX, CALL)                                   \
+  ((HMAX) <= 8 ? CALL(8, 64, 4, 8) : (HMAX) <= 16 ? CALL(16, 256, 4, 8) \
+   : (HMAX) <= 28 ? CALL(28, 784, 4, 8) : CALL(32, 1024, 8, 4))
 
 }  // namespace spai
 
@@ -1367,87 +1433,87 @@ extern "C" int spai_set_assembly_plans(int enable) {
   return SPAI_OK;
 }
 
-extern "C" int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr,
-                                   const int32_t* colidx, const double* vals,
-                                   const int64_t* cscptr, const int32_t* cscrow,
-                                   const int64_t* csc2csr, const double* cscval_in,
-                                   int64_t c0, int64_t c1, double* m_csc, void* wsp,
-                                   size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
-                                   void* stream) {
-  (void)rowptr; (void)colidx; (void)nnz;
-  if (c0 < 0 || c1 > n || c0 > c1) { set_error("bad column range [%lld, %lld)", (long long)c0, (long long)c1); return SPAI_E_ARG; }
-  cudaStream_t s = (cudaStream_t)stream;
+extern "C" int spai_assemble_begin(int64_t n, const int64_t* cscptr, const int32_t* cscrow,
+                                   int64_t c0, int64_t c1, void* wsp, size_t ws_bytes,
+                                   int* hmax_out, int* plans_out, void* stream) {
+  if (!hmax_out || !plans_out || c0 < 0 || c1 > n || c0 > c1) { set_error("spai_assemble_begin: bad arguments"); return SPAI_E_ARG; }
   if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
-  if (bad_col) *bad_col = -1;
-  if (n_fallback) *n_fallback = 0;
-  if (c1 == c0) return SPAI_OK;
+  cudaStream_t s = (cudaStream_t)stream;
   if (g_use_plans < 0) {
     const char* e = getenv("SPAI_NO_PLANS");
     g_use_plans = (e && *e && *e != '0') ? 0 : 1;
   }
-  AsmWs ws;
-  PlanWs pw;
-  unsigned char* b = (unsigned char*)(((uintptr_t)wsp + 255) & ~(uintptr_t)255);
-  ws.err = (unsigned long long*)b;
-  ws.nmerge = (int*)(b + 8);
-  ws.nqr = (int*)(b + 12);
-  int* maxlen = (int*)(b + 16);
-  int* ndirect = (int*)(b + 20);
-  pw.nplans = (int*)(b + 24);
-  pw.nbuilt = (int*)(b + 28);
-  pw.nclass = (int*)(b + 32);
-  pw.ntot = n;
-  unsigned char* p = b + 256;
-  const size_t lb = align256((size_t)n * sizeof(int32_t));
-  ws.merge_list = (int32_t*)p; p += lb;
-  ws.qr_list = (int32_t*)p; p += lb;
-  int32_t* direct = (int32_t*)p; p += lb;
-  pw.plan_slot = (int32_t*)p; p += lb;
-  pw.col_class = (int32_t*)p; p += lb;
-  pw.ckeys = (unsigned long long*)p;
-  pw.crep = (int32_t*)(p + (size_t)kClassTable * 8);
-  p += align256((size_t)kClassTable * 12);
-  pw.keys = (unsigned long long*)p;
-  pw.rep = (int32_t*)(p + (size_t)kPlanTable * 8);
-  pw.slot_plan = (int32_t*)(p + (size_t)kPlanTable * 12);
-  p += align256((size_t)kPlanTable * 16);
-  pw.plans = (uint32_t*)p;
+  const AsmCtx c = carve_ws(wsp, n);
   static const unsigned long long init_err = ~0ull;
-  SPAI_CUDA(cudaMemsetAsync(b + 8, 0, 32, s));
-  SPAI_CUDA(cudaMemcpyAsync(ws.err, &init_err, 8, cudaMemcpyHostToDevice, s));
-  maxlen_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8), 256, 0, s>>>(n, cscptr, maxlen);
+  SPAI_CUDA(cudaMemsetAsync(c.hdr + 8, 0, 32, s));
+  SPAI_CUDA(cudaMemcpyAsync(c.ws.err, &init_err, 8, cudaMemcpyHostToDevice, s));
+  *hmax_out = 0;
+  *plans_out = 0;
+  if (n == 0) return SPAI_OK;
+  maxlen_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 8), 256, 0, s>>>(n, cscptr, c.maxlen);
   SPAI_LAUNCH_CHECK("maxlen_kernel");
   int hmax = 0;
-  SPAI_CUDA(cudaMemcpyAsync(&hmax, maxlen, 4, cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaMemcpyAsync(&hmax, c.maxlen, 4, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
-  const double* cscval = cscval_in;   // NULL: values gathered through csc2csr
-  const bool plans = g_use_plans == 1;
-  int st;
-  if (hmax <= 8)       st = assemble_all<8, 64, 4, 8>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
-  else if (hmax <= 16) st = assemble_all<16, 256, 4, 8>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
-  else if (hmax <= 28) st = assemble_all<28, 784, 4, 8>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
-  else                 st = assemble_all<32, 1024, 8, 4>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, ws, pw, direct, ndirect, plans, s);
-  if (st) return st;
+  *hmax_out = hmax;
+  if (g_use_plans == 1 && c1 > c0) {
+    int st = SPAI_OK;
+    *plans_out = build_plans(c0, c1, cscptr, cscrow, c.pw, s, &st) ? 1 : 0;
+    if (st) return st;
+  }
+  return SPAI_OK;
+}
+
+extern "C" int spai_assemble_columns(int64_t n, const double* vals, const int64_t* cscptr,
+                                     const int32_t* cscrow, const int64_t* csc2csr,
+                                     const double* cscval, int64_t c0, int64_t c1,
+                                     double* m_csc, void* wsp, size_t ws_bytes, int hmax,
+                                     int plans, void* stream) {
+  if (c0 < 0 || c1 > n || c0 > c1) { set_error("bad column range [%lld, %lld)", (long long)c0, (long long)c1); return SPAI_E_ARG; }
+  if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
+  const AsmCtx c = carve_ws(wsp, n);
+  cudaStream_t s = (cudaStream_t)stream;
+#define SPAI_COLS(A, B, C_, D) columns_impl<A, B, C_, D>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, c, plans != 0, s)
+  return SPAI_ASM_DISPATCH(hmax, SPAI_COLS);
+#undef SPAI_COLS
+}
+
+extern "C" int spai_assemble_end(int64_t n, const double* vals, const int64_t* cscptr,
+                                 const int32_t* cscrow, const int64_t* csc2csr, double* m_csc,
+                                 void* wsp, size_t ws_bytes, int hmax, int plans,
+                                 int64_t* bad_col, int64_t* n_fallback, void* stream) {
+  if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
+  if (bad_col) *bad_col = -1;
+  if (n_fallback) *n_fallback = 0;
+  if (n == 0) return SPAI_OK;
+  const AsmCtx c = carve_ws(wsp, n);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (plans) {
+#define SPAI_LEFT(A, B, C_, D) leftovers_impl<A, B, C_, D>(n, vals, cscptr, cscrow, csc2csr, m_csc, c, s)
+    const int st = SPAI_ASM_DISPATCH(hmax, SPAI_LEFT);
+#undef SPAI_LEFT
+    if (st) return st;
+  }
   int counts[2] = {0, 0};
-  SPAI_CUDA(cudaMemcpyAsync(counts, ws.nmerge, 8, cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaMemcpyAsync(counts, c.ws.nmerge, 8, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
   if (counts[0] > 0) {
     const size_t smem = kMergeWarpBytes * kMergeWarps;
     SPAI_CUDA(cudaFuncSetAttribute(gram_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int blocks = std::min((counts[0] + kMergeWarps - 1) / kMergeWarps, num_sms() * 4);
-    gram_merge_kernel<<<blocks, kMergeWarps * 32, smem, s>>>(vals, cscptr, cscrow, csc2csr, m_csc, ws);
+    gram_merge_kernel<<<blocks, kMergeWarps * 32, smem, s>>>(vals, cscptr, cscrow, csc2csr, m_csc, c.ws);
     SPAI_LAUNCH_CHECK("gram_merge_kernel");
-    SPAI_CUDA(cudaMemcpyAsync(counts, ws.nmerge, 8, cudaMemcpyDeviceToHost, s));
+    SPAI_CUDA(cudaMemcpyAsync(counts, c.ws.nmerge, 8, cudaMemcpyDeviceToHost, s));
     SPAI_CUDA(cudaStreamSynchronize(s));
   }
   if (counts[1] > 0) {
     SPAI_CUDA(cudaFuncSetAttribute(spai_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrSmem));
     const int blocks = std::min(counts[1], num_sms());
-    spai_qr_kernel<<<blocks, kQrThreads, kQrSmem, s>>>(vals, cscptr, cscrow, csc2csr, m_csc, ws);
+    spai_qr_kernel<<<blocks, kQrThreads, kQrSmem, s>>>(vals, cscptr, cscrow, csc2csr, m_csc, c.ws);
     SPAI_LAUNCH_CHECK("spai_qr_kernel");
   }
   unsigned long long herr = 0;
-  SPAI_CUDA(cudaMemcpyAsync(&herr, ws.err, 8, cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaMemcpyAsync(&herr, c.ws.err, 8, cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
   if (n_fallback) *n_fallback = ((int64_t)counts[0] << 32) | (int64_t)counts[1];
   if (herr != ~0ull) {
@@ -1461,6 +1527,29 @@ extern "C" int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr
     return SPAI_E_UNSUPPORTED;
   }
   return SPAI_OK;
+}
+
+extern "C" int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr,
+                                   const int32_t* colidx, const double* vals,
+                                   const int64_t* cscptr, const int32_t* cscrow,
+                                   const int64_t* csc2csr, const double* cscval,
+                                   int64_t c0, int64_t c1, double* m_csc, void* wsp,
+                                   size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
+                                   void* stream) {
+  (void)rowptr; (void)colidx; (void)nnz;
+  if (c0 < 0 || c1 > n || c0 > c1) { set_error("bad column range [%lld, %lld)", (long long)c0, (long long)c1); return SPAI_E_ARG; }
+  if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
+  if (bad_col) *bad_col = -1;
+  if (n_fallback) *n_fallback = 0;
+  if (c1 == c0) return SPAI_OK;
+  int hmax = 0, plans = 0;
+  int st = spai_assemble_begin(n, cscptr, cscrow, c0, c1, wsp, ws_bytes, &hmax, &plans, stream);
+  if (st) return st;
+  st = spai_assemble_columns(n, vals, cscptr, cscrow, csc2csr, cscval, c0, c1, m_csc, wsp,
+                             ws_bytes, hmax, plans, stream);
+  if (st) return st;
+  return spai_assemble_end(n, vals, cscptr, cscrow, csc2csr, m_csc, wsp, ws_bytes, hmax, plans,
+                           bad_col, n_fallback, stream);
 }
 
 extern "C" int spai_assemble(int64_t n, int64_t nnz, const int64_t* rowptr,

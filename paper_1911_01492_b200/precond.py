@@ -190,6 +190,109 @@ def spai1_symmetric_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
     return S
 
 
+def spai1_symmetric_from_host(rowptr, colidx, vals, nchunks: int = 8,
+                              stats: SpaiStats | None = None):
+    """Upload a host CSR matrix and build 0.5*(M + M^T) with the value upload
+    overlapped with the assembly; returns (A on the device, S).
+
+    The pattern (rowptr int64, colidx int32; pinned torch tensors give async
+    copies) goes first; while the values stream in `nchunks` row blocks on a
+    copy stream, the pattern-only phase runs (transpose, symmetry check,
+    classes, signatures, plans -- `spai_assemble_begin`), then every column
+    block is assembled as soon as the rows within the matrix bandwidth of it
+    have arrived (`spai_assemble_columns`; one column's least-squares problem
+    reads the values of its stencil columns only).  The values are trusted to
+    be symmetric (CSC values = CSR values) during the overlap and certified
+    afterwards by the half-storage check; a matrix that fails it is assembled
+    again through the CSC gather.  Same S as `spai1_symmetric_device`."""
+    torch = _require_cuda()
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def host(t, dtype):
+        if isinstance(t, torch.Tensor):
+            return t if t.dtype == dtype else t.to(dtype)
+        return torch.from_numpy(np.ascontiguousarray(t)).to(dtype)
+
+    h_rowptr, h_colidx, h_vals = host(rowptr, torch.int64), host(colidx, torch.int32), \
+        host(vals, torch.float64)
+    n = h_rowptr.numel() - 1
+    nnz = h_colidx.numel()
+    if n <= 0 or h_vals.numel() != nnz:
+        raise DimensionMismatchError("spai1_symmetric_from_host: inconsistent CSR arrays")
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    d_rowptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    d_colidx = torch.empty(nnz, dtype=torch.int32, device=dev)
+    d_vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    rows = np.linspace(0, n, max(1, int(nchunks)) + 1).astype(np.int64)
+    offs = h_rowptr[torch.from_numpy(rows)].numpy()
+    events = []
+    copy.wait_stream(comp)                       # the buffers were allocated on comp
+    with torch.cuda.stream(copy):
+        d_rowptr.copy_(h_rowptr, non_blocking=True)
+        d_colidx.copy_(h_colidx, non_blocking=True)
+        e_pat = torch.cuda.Event()
+        e_pat.record(copy)
+        for i in range(len(rows) - 1):
+            if offs[i + 1] > offs[i]:
+                d_vals[offs[i]:offs[i + 1]].copy_(h_vals[offs[i]:offs[i + 1]], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            events.append(ev)
+    comp.wait_event(e_pat)
+    A = DeviceCsr(n, n, d_rowptr, d_colidx, d_vals)
+    for t in (d_rowptr, d_colidx, d_vals):
+        t.record_stream(copy)
+    if not A.structurally_symmetric():
+        comp.wait_event(events[-1])
+        raise DimensionMismatchError(
+            "symmetrised SPAI(1) needs a structurally symmetric pattern")
+    g = A.ssell_offsets()
+    bw = int(max(g)) if g else n                 # no bandwidth bound: wait for everything
+    cscptr, cscrow, csc2csr = A.csc()
+    m_csc = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    wsb = lib.spai_assemble_workspace_bytes(n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    hmax, plans = C.c_int(0), C.c_int(0)
+    s = stream_handle()
+    _lib.check(lib.spai_assemble_begin(n, ptr(cscptr), ptr(cscrow), 0, n, ptr(ws), wsb,
+                                       C.byref(hmax), C.byref(plans), s), "spai_assemble_begin")
+    waited = -1
+    for j in range(len(rows) - 1):
+        need = min(n, int(rows[j + 1]) + bw) - 1          # last row this block reads
+        k = int(np.searchsorted(rows, need, side="right")) - 1
+        k = min(max(k, 0), len(events) - 1)
+        if k > waited:
+            comp.wait_event(events[k])
+            waited = k
+        _lib.check(lib.spai_assemble_columns(n, ptr(d_vals), ptr(cscptr), ptr(cscrow),
+                                             ptr(csc2csr), ptr(d_vals), int(rows[j]),
+                                             int(rows[j + 1]), ptr(m_csc), ptr(ws), wsb,
+                                             hmax.value, plans.value, s),
+                   "spai_assemble_columns")
+    comp.wait_event(events[-1])
+    bad, nfb = C.c_int64(-1), C.c_int64(0)
+    st = lib.spai_assemble_end(n, ptr(d_vals), ptr(cscptr), ptr(cscrow), ptr(csc2csr),
+                               ptr(m_csc), ptr(ws), wsb, hmax.value, plans.value, C.byref(bad),
+                               C.byref(nfb), s)
+    _lib.check(st, "spai_assemble_end")
+    if st != _lib.SPAI_OK:
+        _raise_assembly(st, bad.value)
+    sym_values = A.ssell_values() is not None if g else A.csc_values() is A.vals
+    if not sym_values:
+        # not bit-symmetric: the overlapped pass read CSR values as CSC values
+        m_csc = spai1_columns_device(A, stats)
+    elif stats is not None:
+        stats.n_merge = nfb.value >> 32
+        stats.n_fallback = nfb.value & 0xFFFFFFFF
+    sv = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    _lib.check(lib.spai_symmetrize(nnz, ptr(csc2csr), ptr(m_csc), ptr(sv), s), "spai_symmetrize")
+    S = A.with_values(sv[:nnz])
+    S.symmetric_by_construction = True
+    return A, S
+
+
 def spai1(A) -> CsrMatrix:
     """Sparse approximate inverse on the pattern of A (precond.py:175-199).
 

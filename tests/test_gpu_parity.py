@@ -632,3 +632,23 @@ def test_ksolver_half_storage_matches_sell(kind):
         assert np.max(np.abs(h - np.array(rr.residual_norms)) / np.array(rr.residual_norms)) \
             <= HIST_TOL
         assert np.max(np.abs(xs[None] - xr)) <= 1e-10 * np.max(np.abs(xr))
+
+
+@pytest.mark.parametrize("dims,conv,nchunks", [((40, 36, 30), None, 8), ((50, 47), None, 3),
+                                                ((24, 20, 18), (1.0, 0.5, 0.25), 5)])
+def test_spai1_symmetric_from_host_matches_device_path(dims, conv, nchunks):
+    """Overlapped upload + phased assembly (begin / columns / end) gives the
+    same S, bit for bit, as the resident path; a numerically nonsymmetric
+    matrix (convection) takes the recompute branch."""
+    A = pb.q1_device(dims, conv=conv)
+    ref = pb.spai1_symmetric_device(pb.sparse.DeviceCsr(A.nrows, A.ncols, A.rowptr, A.colidx,
+                                                        A.vals))
+    h = (A.rowptr.cpu().pin_memory(), A.colidx.cpu().pin_memory(), A.vals.cpu().pin_memory())
+    Ad, S = pb.spai1_symmetric_from_host(*h, nchunks=nchunks)
+    torch.cuda.synchronize()
+    assert torch.equal(Ad.vals, A.vals) and torch.equal(Ad.colidx, A.colidx)
+    assert torch.equal(S.vals, ref.vals)
+    # numpy inputs (pageable) as well
+    _, S2 = pb.spai1_symmetric_from_host(A.rowptr.cpu().numpy(), A.colidx.cpu().numpy(),
+                                         A.vals.cpu().numpy(), nchunks=2)
+    assert torch.equal(S2.vals, ref.vals)
