@@ -476,6 +476,22 @@ int spai_coo_to_csr(int64_t nrows, int64_t count, const int64_t* rows, const int
 int spai_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* rowptr,
                   const int64_t* colidx, const double* vals, int nthreads);
 int spai_vec_write(const char* path, int64_t n, const double* x);
+
+/* ------------------------------------------------------------------ backup codec
+ * Accuracy-bounded backup payload (replaces resilience.py:126-169
+ * `_quantize` / `_dequantize`; host pointers, byte-identical format).  The
+ * predictor runs through the previously decoded value, one sequential
+ * recurrence per vector; spai_quantize_many encodes independent vectors
+ * (e.g. every rank's owned segment) on `threads` host threads (<= 0: all).
+ * bound = the largest payload for n entries.                               */
+size_t spai_quantize_bound(int64_t n);
+int spai_quantize(const double* x, int64_t n, double tau, uint8_t* out, size_t cap,
+                  size_t* len);
+int spai_quantize_many(int count, const double* const* xs, const int64_t* ns,
+                       const double* taus, uint8_t* const* outs, const size_t* caps,
+                       size_t* lens, int threads);
+int spai_dequantize_header(const uint8_t* payload, size_t len, int64_t* n, double* tau);
+int spai_dequantize(const uint8_t* payload, size_t len, double* out, int64_t n);
 int spai_vec_read(const char* path, double* x, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus

@@ -28,6 +28,8 @@ from .block import (GRAM_MODES, GramMatrix, MultiVector, axpy, block_solve, copy
                     norm2, scale, spmm_multi)
 from .multigrid import (Hierarchy, MultigridPreconditioner, build_hierarchy, prolongate_full,
                         restrict_full)
+from .codec import (CODEC_KINDS, BackupSnapshot, Codec, CodecError, decode, dequantize, encode,
+                    encode_many, quantize)
 from .krylov import (ConvergenceRecord, DeviceKrylov, DevicePCG, KrylovState,
                      LocalSystem, SolverConfig, VARIANTS, bicgstab, pipelined_consistency_check,
                      fused_dots_device, memory_accounting, reduction_rate,

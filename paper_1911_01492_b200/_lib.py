@@ -163,6 +163,11 @@ _SIGS = {
     "spai_coo_to_csr": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
     "spai_mm_write": (_i32, [C.c_char_p, _i64, _i64, _vp, _vp, _vp, _i32]),
     "spai_vec_write": (_i32, [C.c_char_p, _i64, _vp]),
+    "spai_quantize_bound": (_sz, [_i64]),
+    "spai_quantize": (_i32, [_vp, _i64, _dbl, _vp, _sz, C.POINTER(_sz)]),
+    "spai_quantize_many": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
+    "spai_dequantize_header": (_i32, [_vp, _sz, C.POINTER(_i64), C.POINTER(_dbl)]),
+    "spai_dequantize": (_i32, [_vp, _sz, _vp, _i64]),
     "spai_vec_read": (_i32, [C.c_char_p, _vp, _i64, C.POINTER(_i64)]),
 }
 

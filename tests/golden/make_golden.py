@@ -180,6 +180,34 @@ def multirank_cases():
     return out
 
 
+def codec_cases():
+    """resilience.py:126-199: accuracy-bounded payloads of the reference codec."""
+    from ftkrylov import resilience as rs
+    rng = np.random.default_rng(21)
+    smooth = 3.0 * np.sin(np.linspace(0.0, 20.0, 1000))
+    jumps = np.array([0.0, 1e20, -1e20, 1e308, 5.0, 5.0 + 1e-7, -1e308, 1e-300, 0.0, 7.25,
+                      2.0 ** 60, -3.5, 1e15, 1e15 + 1.0])
+    ties = np.array([0.5, 1.5, 2.5, -0.5, -1.5, 3.0, 2.0, 0.0, 1.0])
+    cases = {
+        "smooth": (smooth, rs.Codec("accuracy_bounded", tau=1e-6), None),
+        "random": (rng.standard_normal(500), rs.Codec("accuracy_bounded", tau=1e-3), None),
+        "jumps": (jumps, rs.Codec("accuracy_bounded", tau=1e-6), None),
+        "ties": (ties, rs.Codec("accuracy_bounded", tau=0.5), None),
+        "adaptive": (rng.standard_normal(300) * 1e-3, rs.Codec("adaptive_accuracy", c=0.1),
+                     1e-4),
+        "empty": (np.zeros(0), rs.Codec("accuracy_bounded", tau=1e-6), None),
+    }
+    out = {}
+    for name, (x, codec, rn) in cases.items():
+        snap = rs.encode(codec, x, residual_norm=rn)
+        out[name] = dict(x=x, kind=np.array(codec.kind), tau=np.array(codec.tau),
+                         c=np.array(codec.c), rn=np.array(-1.0 if rn is None else rn),
+                         tau_used=np.array(snap.tau_used),
+                         payload=np.frombuffer(snap.payload, dtype=np.uint8),
+                         decoded=rs.decode(snap))
+    return out
+
+
 def main():
     data = {}
     for name, A in spai_cases().items():
@@ -257,6 +285,10 @@ def main():
         data[f"multirank/fd5_32x32/{ranks}/its"] = np.array(d["its"])
         data[f"multirank/fd5_32x32/{ranks}/x"] = d["x"]
         print(f"multirank {ranks}: its={d['its']}")
+    for name, d in codec_cases().items():
+        for k, v in d.items():
+            data[f"codec/{name}/{k}"] = v
+        print(f"codec {name}: {d['payload'].size} bytes")
     # FactorBreakdownError case (precond.py:192-194)
     A = fk.CsrMatrix.from_dense(np.array([[1.0, 1.0, 0.0],
                                           [1.0, 1.0, 0.0],

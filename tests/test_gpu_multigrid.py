@@ -131,3 +131,21 @@ def test_mg_pcg_large_2d_anisotropic_properties():
     res = b - A.matvec(x)
     assert float(torch.linalg.norm(res)) <= 1e-7 * float(torch.linalg.norm(b))
     assert float((x - 1.0).abs().max()) <= 1e-5
+
+
+def test_hierarchical_backup_codec_round_trip():
+    """resilience.py:181-185,208-212: the hierarchical codec keeps the level-l
+    restriction and decodes by prolongation (transfers on the GPU)."""
+    nx, ny, levels = 16, 16, 3
+    H = pb.build_hierarchy(pb.StructuredGrid(nx, ny), levels)
+    h = omg.build_hierarchy(nx, ny, levels)
+    x = np.random.default_rng(4).standard_normal(nx * ny)
+    codec = pb.Codec("hierarchical", level=2, hierarchy=H)
+    snap = pb.encode(codec, x, source_rank=1, iteration=3)
+    nc = omg.restrict_full(h, x, 2).size
+    assert snap.payload_len == 16 + 8 * nc and snap.level == 2 and snap.tau_used == float("inf")
+    y = pb.decode(snap)
+    ref = omg.prolongate_full(h, omg.restrict_full(h, x, 2), 2)
+    assert np.allclose(y, ref, rtol=1e-15, atol=1e-15)
+    with pytest.raises(pb.CodecError, match="no level"):
+        pb.Codec("hierarchical", level=3, hierarchy=H)
