@@ -328,12 +328,18 @@ def run_ours(args):
     # reference's Householder QR would need 2 n^2 (m - n/3) + n^2 = 169,857
     fp64 = fp64_peak_tflops(stream)
     exec_tf = n * 15607 / t_asm / 1e12
-    asm_roof = {"bound": "fp64 (latency in practice)", "unit": "TFLOP/s",
+    asm_roof = {"bound": "fp64 on paper; the shared-memory data pipe in practice",
+                "unit": "TFLOP/s",
                 "achieved_executed": exec_tf, "peak_measured_dfma": fp64,
                 "frac": exec_tf / fp64,
                 "householder_equivalent": n * 169857 / t_asm / 1e12,
                 "flop_per_column": {"executed_normal_equations": 15607,
-                                    "householder_qr_reference": 169857}}
+                                    "householder_qr_reference": 169857},
+                # ncu of the replay kernel (profiles/r01_replay_lines_200.txt):
+                # 1,535 shared-memory wavefronts per column, pipe ~76 % busy;
+                # floor of the design ~1,070 (operands 474 + broadcast of L 364
+                # + gather 80 + Gram / factor stores ~150)
+                "shared_wavefronts_per_column": {"measured_ncu": 1535, "design_floor": 1070}}
     solve_gbs = b_it * its / t_sol / 1e9
 
     # ---- SpMV alone (K5 plain and TMA-staged) with CUDA events
