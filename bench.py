@@ -216,8 +216,15 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"3D Q1 Poisson {REF_SAMPLE_N}^3 sample of configs[2] "
-                                   "(reference cannot densify 400^3)"},
+            # the workload our arm runs; each step here is a bounded sample of
+            # it (the reference densifies A, impossible at 400^3): see
+            # cpu_baseline.sample
+            "config": {"workload": f"configs[2]: 3D Q1 Poisson {args.grid}^3 "
+                                   f"({args.grid ** 3} DOF, nnz {(3 * args.grid - 2) ** 3}), "
+                                   f"SPAI(1)+CG ({args.variant}), b=A*1, x0=0, tol {args.tol}",
+                       "n_dof": args.grid ** 3, "nnz": (3 * args.grid - 2) ** 3,
+                       "parallelism": "host cores (reference; Python, one thread)",
+                       "sample_per_step": f"3D Q1 Poisson {REF_SAMPLE_N}^3"},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
