@@ -652,3 +652,32 @@ def test_spai1_symmetric_from_host_matches_device_path(dims, conv, nchunks):
     _, S2 = pb.spai1_symmetric_from_host(A.rowptr.cpu().numpy(), A.colidx.cpu().numpy(),
                                          A.vals.cpu().numpy(), nchunks=2)
     assert torch.equal(S2.vals, ref.vals)
+
+
+def test_spai1_symmetric_from_host_irregular_and_errors():
+    """No half-storage layout (> 16 distinct offsets): no bandwidth bound, the
+    columns wait for every value block; a non-symmetric pattern raises like
+    spai1_symmetric_device."""
+    rng = np.random.default_rng(8)
+    n = 3000
+    r = rng.integers(0, n, 12000)
+    c = rng.integers(0, n, 12000)
+    keep = r != c
+    r, c = r[keep], c[keep]
+    v = rng.standard_normal(r.size) * 0.1
+    rows = np.concatenate([r, c, np.arange(n)])
+    cols = np.concatenate([c, r, np.arange(n)])
+    vals = np.concatenate([v, v, np.full(n, 8.0)])
+    key = rows * n + cols
+    _, first = np.unique(key, return_index=True)
+    A = pb.CsrMatrix.from_coo(n, n, rows[first], cols[first], vals[first])
+    dA = A.device()
+    assert dA.ssell_offsets() is None
+    ref = pb.spai1_symmetric_device(pb.sparse.DeviceCsr(n, n, dA.rowptr, dA.colidx, dA.vals))
+    _, S = pb.spai1_symmetric_from_host(A.row_offsets, A.col_indices.astype(np.int32), A.values,
+                                        nchunks=4)
+    assert torch.equal(S.vals, ref.vals)
+    B = pb.CsrMatrix.from_coo(3, 3, np.array([0, 0, 1, 2]), np.array([0, 1, 1, 2]),
+                              np.array([2.0, 1.0, 2.0, 2.0]))
+    with pytest.raises(pb.DimensionMismatchError):
+        pb.spai1_symmetric_from_host(B.row_offsets, B.col_indices.astype(np.int32), B.values)
