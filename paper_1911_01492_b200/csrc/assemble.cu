@@ -497,23 +497,31 @@ __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int
   for (int l = 0; l < NJ; ++l) g[l] = G[ti + l];
   const double gdiag = lane < nj ? G[ti + lane] : 1.0;
   if (lane >= nj) y = 0.0;
-  double myinv = 0.0, myd = 1.0;
+  double myinv = 0.0, myd = 1.0, yfin = 0.0;
   // Look-ahead: lane j+1 owns L(j+1, j) = its lij, so it forms the next pivot
   // g[j+1] - lij^2 itself (bit-identical to its update below) and the next
   // rsqrt starts before the shared-memory broadcast of column j completes.
   // colbuf is double-buffered: one warp barrier per pivot.
+  // No lane predicates on the elimination: a lane <= j computes garbage only
+  // in its own entries right of the diagonal, which no result reads (column j
+  // is read back from colbuf for rows > j only).  The forward substitution
+  // L y = rhs is fused the same way: every lane applies column j, and lane j
+  // keeps its final y_j (yfin) at its pivot.
   double d = __shfl_sync(0xffffffffu, g[0], 0);
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const double inv = rsqrt(d);
-    const double lij = lane > j ? g[j] * inv : 0.0;
+    const double lij = g[j] * inv;
     double dnext = 0.0;
     if (j + 1 < NJ) dnext = __shfl_sync(0xffffffffu, fma(-lij, lij, g[j + 1]), j + 1);
+    const double yj = __shfl_sync(0xffffffffu, y, j) * inv;
     double* cb = colbuf + 32 * (j & 1);
     cb[lane] = lij;
     __syncwarp();
-    if (lane == j) { g[j] = d * inv; myinv = inv; myd = d; }
-    else if (lane > j) g[j] = lij;
+    const bool piv = lane == j;
+    g[j] = piv ? d * inv : lij;
+    y = fma(-lij, yj, y);
+    if (piv) { myinv = inv; myd = d; yfin = yj; }
     if ((j + 1) & 1) {                 // odd start: one scalar, then aligned pairs
       if (j + 1 < NJ) g[j + 1] = fma(-lij, cb[j + 1], g[j + 1]);
     }
@@ -539,26 +547,26 @@ __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int
     dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   }
   if (__any_sync(0xffffffffu, bad) || !(sqrt(dmin) > kRankGuard * fmax(sqrt(dmax), 1.0))) return false;
-  // forward: L y = rhs
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const double yj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
-    y = lane == j ? yj : (lane > j ? fma(-g[j], yj, y) : y);
-  }
+  y = yfin;
   // store L (row i by lane i) for the backward solve L^T m = y
   if (lane < nj) {
 #pragma unroll
     for (int l = 0; l < NJ; ++l) if (l <= lane) G[ti + l] = g[l];
   }
   __syncwarp();
-  // backward: L^T m = y, unrolled so the L loads run ahead of the shuffle chain
-  // (rows j >= nj are identity padding: L not stored, m_j = 0)
+  // backward: L^T m = y, unrolled so the L loads run ahead of the shuffle
+  // chain; again every lane applies row j (garbage lands only in lanes >= j,
+  // whose m is final: lane j keeps it in mfin).  Rows j >= nj are the
+  // identity padding of g_init (m_j = 0, no coupling).
+  double mfin = 0.0;
 #pragma unroll
   for (int j = NJ - 1; j >= 0; --j) {
-    const double lj = (lane < j && j < nj) ? G[tri(j) + lane] : 0.0;
+    const double lj = G[tri(j) + lane];
     const double mj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
-    y = lane == j ? mj : fma(-lj, mj, y);
+    y = fma(-lj, mj, y);
+    if (lane == j) mfin = mj;
   }
+  y = mfin;
   return true;
 }
 
