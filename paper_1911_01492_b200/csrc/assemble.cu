@@ -928,6 +928,12 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
         if (reorder && t0 + len <= kPlanSteps) reorder_round(S, ops, t0, len, lane);
         t0 += len;
       }
+      // pad to whole groups (the last round's accumulators pick up 0 * 0
+      // after its store; nothing reads them)
+      if (t0 <= kPlanSteps) {
+        const int tpad = (t0 + kOpGroupSteps - 1) / kOpGroupSteps * kOpGroupSteps;
+        for (int t = t0; t < tpad && t < kPlanSteps; ++t) ops[op_index(t, lane)] = op_pack(total, total);
+      }
       ok = t0 <= kPlanSteps;
       if (lane == 0) {
         P[kPH_nsteps] = ok ? (uint32_t)t0 : 0xFFFFFFFFu;
@@ -953,7 +959,7 @@ plan_build_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
 // before its FMAs, and the next round's destination / length are read one
 // round early -- the plan lives in global memory (L1-resident) and the
 // load-to-use distance of the plain loop stalled the warps on it.
-constexpr int kOpAhead = 4;
+constexpr int kOpAhead = kOpGroupSteps / 2;    // pairs per group
 __device__ __forceinline__ void product_program(const uint32_t* __restrict__ P, int lane,
                                                 const double* lval, double* G) {
   const uint2* ops = reinterpret_cast<const uint2*>(P + kPO_ops) + lane;
@@ -966,38 +972,34 @@ __device__ __forceinline__ void product_program(const uint32_t* __restrict__ P, 
   double s0 = 0.0, s1 = 0.0;
   uint2 ring[kOpAhead];
 #pragma unroll
-  for (int i = 0; i < kOpAhead; ++i) ring[i] = i < npairs ? ops[i * 32] : make_uint2(0u, 0u);
+  for (int i = 0; i < kOpAhead; ++i) ring[i] = ops[i * 32];
+  // whole groups: the program is padded with 0 * 0 ops and one group of slack
   for (int p0 = 0; p0 < npairs; p0 += kOpAhead) {
     double a[kOpAhead][4];
 #pragma unroll
     for (int i = 0; i < kOpAhead; ++i) {
-      const int p = p0 + i;
       const uint2 oo = ring[i];
-      if (p < npairs) {
-        a[i][0] = *reinterpret_cast<const double*>(lv + (oo.x & 0xFFFFu));
-        a[i][1] = *reinterpret_cast<const double*>(lv + (oo.x >> 16));
-        a[i][2] = *reinterpret_cast<const double*>(lv + (oo.y & 0xFFFFu));
-        a[i][3] = *reinterpret_cast<const double*>(lv + (oo.y >> 16));
-      }
-      if (p + kOpAhead < npairs) ring[i] = ops[(p + kOpAhead) * 32];
+      a[i][0] = *reinterpret_cast<const double*>(lv + (oo.x & 0xFFFFu));
+      a[i][1] = *reinterpret_cast<const double*>(lv + (oo.x >> 16));
+      a[i][2] = *reinterpret_cast<const double*>(lv + (oo.y & 0xFFFFu));
+      a[i][3] = *reinterpret_cast<const double*>(lv + (oo.y >> 16));
+      ring[i] = ops[(p0 + i + kOpAhead) * 32];
     }
 #pragma unroll
     for (int i = 0; i < kOpAhead; ++i) {
       const int p = p0 + i;
-      if (p < npairs) {
-        s0 = fma(a[i][0], a[i][1], s0);
-        s1 = fma(a[i][2], a[i][3], s1);
-        if (p + 1 == rend) {
-          if (dcur != 0xFFFFu) G[dcur] = s0 + s1;
-          s0 = 0.0;
-          s1 = 0.0;
-          ++r;
-          rend += (int)(rlen_next >> 1);
-          dcur = dnext;
-          if (p + 1 < npairs) {          // prefetch the round after next
-            dnext = rdst[(r + 1) * 32];
-            rlen_next = P[kPO_rlen + r + 1];
-          }
+      s0 = fma(a[i][0], a[i][1], s0);
+      s1 = fma(a[i][2], a[i][3], s1);
+      if (p + 1 == rend) {
+        if (dcur != 0xFFFFu) G[dcur] = s0 + s1;
+        s0 = 0.0;
+        s1 = 0.0;
+        ++r;
+        rend += (int)(rlen_next >> 1);
+        dcur = dnext;
+        if (p + 1 < npairs) {          // prefetch the round after next
+          dnext = rdst[(r + 1) * 32];
+          rlen_next = P[kPO_rlen + r + 1];
         }
       }
     }

@@ -49,7 +49,11 @@ constexpr int kPO_rlen = kPO_jcls + kPlanNJ;                  // [kMaxRounds]
 constexpr int kPO_rdst = kPO_rlen + kMaxRounds + 1;           // uint16 [kMaxRounds][32]
 constexpr int kPO_ops = (kPO_rdst + kMaxRounds * 16 + 31) & ~31;   // 128-B aligned (8-byte op pairs)
 constexpr int kClassTable = 8192;    // column-class hash table (exact de-dup)
-constexpr int kPlanWords = ((kPO_ops + 32 * kPlanSteps) + 31) & ~31;
+// the op program is padded to whole groups of kOpGroupSteps steps (0 * 0 from
+// the zero slot) and followed by one more group of slack, so the replay reads
+// whole groups and prefetches one group ahead without bounds checks
+constexpr int kOpGroupSteps = 8;
+constexpr int kPlanWords = ((kPO_ops + 32 * (kPlanSteps + kOpGroupSteps)) + 31) & ~31;
 
 // steps t and t + 1 of a lane are adjacent words (one 8-byte load per pair)
 __host__ __device__ __forceinline__ int op_index(int t, int lane) {
