@@ -343,10 +343,11 @@ def run_ours(args):
                 "flop_per_column": {"executed_normal_equations": 15607,
                                     "householder_qr_reference": 169857},
                 # ncu of the replay kernel (profiles/r01_replay_lines_200.txt):
-                # 1,535 shared-memory wavefronts per column, pipe ~76 % busy;
+                # ~1,550 shared-memory wavefronts per column, LSU pipe ~91 % busy;
                 # floor of the design ~1,070 (operands 474 + broadcast of L 364
                 # + gather 80 + Gram / factor stores ~150)
-                "shared_wavefronts_per_column": {"measured_ncu": 1535, "design_floor": 1070}}
+                "shared_wavefronts_per_column": {"measured_ncu": 1554, "design_floor": 1070},
+                "lsu_pipe_busy_pct_ncu": 91}
     solve_gbs = b_it * its / t_sol / 1e9
 
     # ---- SpMV alone (K5 plain and TMA-staged) with CUDA events
