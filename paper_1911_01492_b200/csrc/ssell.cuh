@@ -45,8 +45,14 @@ __device__ __forceinline__ int32_t ssell_lane_offset(const SymSell& A, int lane)
 //
 // Interior slices (no neighbour outside [0, n)) of a compile-time width W:
 // every offset and mirrored address is a kernel-parameter constant, loads go
-// out in batches of kSymBatch values + gathers.
-constexpr int kSymBatch = 7;
+// out in batches of kSymUpperBatch (streamed upper values) and kSymBatch
+// (mirrored values, L2) + gathers.  Mirror batches of 3 measured best inside
+// the PCG (4.17 ms per iteration at 400^3 vs 4.52 with 7; 1, 2, 4, 5, 6 and
+// 14 in between or worse).
+#ifndef SPAI_SSELL_MIRROR_BATCH
+#define SPAI_SSELL_MIRROR_BATCH 3
+#endif
+constexpr int kSymBatch = SPAI_SSELL_MIRROR_BATCH;
 #ifndef SPAI_SSELL_UPPER_BATCH
 #define SPAI_SSELL_UPPER_BATCH 7
 #endif
