@@ -577,11 +577,20 @@ class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __res
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // the warp's last class (its exact pattern in registers): most columns
+  // repeat it, and then need no table probe and no representative compare
+  uint64_t last_h = 0;
+  int last_slot = -1, last_len = -1;
+  int32_t last_rel = 0;
   for (int64_t c = w0; c < n; c += nw) {
     const int64_t lo = cscptr[c];
     const int len = (int)(cscptr[c + 1] - lo);
     if (len > 32 || len == 0) { if (lane == 0) pw.col_class[c] = -1; continue; }
     const int32_t rel = lane < len ? cscrow[lo + lane] - (int32_t)c : 0;
+    if (len == last_len && __all_sync(0xffffffffu, lane >= len || rel == last_rel)) {
+      if (lane == 0) pw.col_class[c] = last_slot;
+      continue;
+    }
     uint64_t h = lane < len ? mix64(((uint64_t)(lane + 1) << 32) ^ (uint32_t)rel) : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
@@ -618,7 +627,9 @@ class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __res
       slot = (slot + 1) & (kClassTable - 1);
     }
     if (lane == 0) pw.col_class[c] = result;
+    if (result >= 0) { last_h = h; last_slot = result; last_len = len; last_rel = rel; }
   }
+  (void)last_h;
 }
 
 // (A) signature of every column: (nj, J_a - k, class(J_a)) -> plan-table slot
@@ -628,6 +639,8 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t last_h = 0;                         // the warp's last signature and its slot
+  int last_slot = -1;
   for (int64_t k = c0 + w0; k < n; k += nw) {
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
@@ -652,6 +665,10 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
     for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
     h = mix64(h ^ (uint64_t)nj);
     if (h == 0) h = 1;
+    if (h == last_h) {                         // the warp's last signature: same slot
+      if (lane == 0) pw.plan_slot[k] = last_slot;
+      continue;
+    }
     if (lane == 0) {
       int slot = (int)(h & (kPlanTable - 1));
       int found = -1;
@@ -663,7 +680,10 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
         slot = (slot + 1) & (kPlanTable - 1);
       }
       pw.plan_slot[k] = found;
+      last_slot = found;
     }
+    last_slot = __shfl_sync(0xffffffffu, last_slot, 0);
+    last_h = last_slot >= 0 ? h : 0;
   }
 }
 

@@ -52,7 +52,10 @@ constexpr int kClassTable = 8192;    // column-class hash table (exact de-dup)
 // the op program is padded to whole groups of kOpGroupSteps steps (0 * 0 from
 // the zero slot) and followed by one more group of slack, so the replay reads
 // whole groups and prefetches one group ahead without bounds checks
-constexpr int kOpGroupSteps = 8;
+#ifndef SPAI_OP_GROUP_STEPS
+#define SPAI_OP_GROUP_STEPS 8
+#endif
+constexpr int kOpGroupSteps = SPAI_OP_GROUP_STEPS;
 constexpr int kPlanWords = ((kPO_ops + 32 * (kPlanSteps + kOpGroupSteps)) + 31) & ~31;
 
 // steps t and t + 1 of a lane are adjacent words (one 8-byte load per pair)
