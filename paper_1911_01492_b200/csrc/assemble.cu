@@ -558,11 +558,14 @@ __device__ __forceinline__ bool chol_solve_padded(double* G, double* colbuf, int
   // chain; again every lane applies row j (garbage lands only in lanes >= j,
   // whose m is final: lane j keeps it in mfin).  Rows j >= nj are the
   // identity padding of g_init (m_j = 0, no coupling).
+  // every lane carries its y pre-scaled by its own 1 / L_ii, so the chain
+  // shuffles one value per step (m_j = y_j / L_jj)
   double mfin = 0.0;
+  y *= myinv;
 #pragma unroll
   for (int j = NJ - 1; j >= 0; --j) {
-    const double lj = G[tri(j) + lane];
-    const double mj = __shfl_sync(0xffffffffu, y, j) * __shfl_sync(0xffffffffu, myinv, j);
+    const double lj = G[tri(j) + lane] * myinv;
+    const double mj = __shfl_sync(0xffffffffu, y, j);
     y = fma(-lj, mj, y);
     if (lane == j) mfin = mj;
   }
