@@ -681,3 +681,40 @@ def test_spai1_symmetric_from_host_irregular_and_errors():
                               np.array([2.0, 1.0, 2.0, 2.0]))
     with pytest.raises(pb.DimensionMismatchError):
         pb.spai1_symmetric_from_host(B.row_offsets, B.col_indices.astype(np.int32), B.values)
+
+
+def test_phased_assembly_any_column_blocks():
+    """spai_assemble_begin / columns / end: the columns in blocks of any size
+    and order give the single-call result bit for bit (each column's problem
+    is independent); errors surface from `end` with the failing column."""
+    import ctypes as C
+    from paper_1911_01492_b200 import _lib
+    from paper_1911_01492_b200.sparse import ptr, stream_handle
+    lib = _lib.load()
+    A = pb.q1_device((30, 26, 22))
+    n = A.nrows
+    cscptr, cscrow, csc2csr = A.csc()
+    ref = pb.precond.spai1_columns_device(A)
+    wsb = lib.spai_assemble_workspace_bytes(n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    m = torch.full((A.nnz,), float("nan"), dtype=torch.float64, device="cuda")
+    hmax, plans = C.c_int(0), C.c_int(0)
+    s = stream_handle()
+    assert lib.spai_assemble_begin(n, ptr(cscptr), ptr(cscrow), 0, n, ptr(ws), wsb,
+                                   C.byref(hmax), C.byref(plans), s) == 0
+    assert hmax.value == 27 and plans.value == 1
+    cuts = sorted({0, n, 1, 777, 5000, 5001, n // 2, n - 3})
+    blocks = list(zip(cuts[:-1], cuts[1:]))
+    for c0, c1 in reversed(blocks):
+        assert lib.spai_assemble_columns(n, ptr(A.vals), ptr(cscptr), ptr(cscrow), ptr(csc2csr),
+                                         ptr(A.csc_values()), c0, c1, ptr(m), ptr(ws), wsb,
+                                         hmax.value, plans.value, s) == 0
+    bad, nfb = C.c_int64(-1), C.c_int64(0)
+    assert lib.spai_assemble_end(n, ptr(A.vals), ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(m),
+                                 ptr(ws), wsb, hmax.value, plans.value, C.byref(bad),
+                                 C.byref(nfb), s) == 0
+    assert torch.equal(m, ref)
+    # bad arguments are rejected
+    assert lib.spai_assemble_columns(n, ptr(A.vals), ptr(cscptr), ptr(cscrow), ptr(csc2csr),
+                                     ptr(A.csc_values()), 5, 2, ptr(m), ptr(ws), wsb,
+                                     hmax.value, plans.value, s) == _lib.SPAI_E_ARG
