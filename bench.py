@@ -273,10 +273,12 @@ def run_ours(args):
         x, rec = pb.solve(pb.LocalSystem(A2, pb.SparseMatrixPreconditioner(S)), bdev, cfg)
         e2.record(stream)
         e2.synchronize()
-        # per step: sym transpose, half-storage offsets + fill + verify of A,
-        # classes, signatures, plan build, replay, symmetrise, fill of S,
-        # PCG start (2) = 12 kernels, then 4 per launched PCG iteration
-        launches["n"] += 12 + 4 * _advanced(rec)
+        # per step (ncu launch list, profiles/r01_launches_400_final.txt):
+        # structure check, sym transpose, half-storage offsets + fill + verify
+        # of A, longest column, classes, signatures, plan build, replay,
+        # symmetrise, fill of S, PCG start (2) = 14 kernels, then 4 per
+        # launched PCG iteration
+        launches["n"] += 14 + 4 * _advanced(rec)
         return e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3, rec, x
 
     def barrier():
