@@ -681,6 +681,13 @@ def test_spai1_symmetric_from_host_irregular_and_errors():
                               np.array([2.0, 1.0, 2.0, 2.0]))
     with pytest.raises(pb.DimensionMismatchError):
         pb.spai1_symmetric_from_host(B.row_offsets, B.col_indices.astype(np.int32), B.values)
+    # fewer rows than value blocks
+    T = pb.CsrMatrix.from_dense(np.array([[4.0, -1.0, 0.0], [-1.0, 4.0, -1.0],
+                                          [0.0, -1.0, 4.0]]))
+    _, St = pb.spai1_symmetric_from_host(T.row_offsets, T.col_indices.astype(np.int32),
+                                         T.values, nchunks=8)
+    Sr = pb.spai1_symmetric_device(T.device())
+    assert torch.equal(St.vals, Sr.vals)
 
 
 def test_phased_assembly_any_column_blocks():
