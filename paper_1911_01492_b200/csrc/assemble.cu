@@ -707,6 +707,7 @@ struct BuildSmem {
   // bank-aware step order of a round (reorder_round)
   uint32_t cand[32][33];
   uint32_t used[32];
+  int32_t omax[4];               // [operand][half-warp]: the step's busiest class
   int32_t ocnt[64];              // [operand][half-warp][bank class]
   uint16_t oaddr[64][2];
 };
@@ -718,6 +719,10 @@ struct BuildSmem {
 __device__ __forceinline__ int occ_cost(const BuildSmem& S, int idx, int addr) {
   const int n = S.ocnt[idx];
   return (n > 0 && S.oaddr[idx][0] == addr) || (n > 1 && S.oaddr[idx][1] == addr) ? 0 : n;
+}
+__device__ __forceinline__ bool occ_has(const BuildSmem& S, int idx, int addr) {
+  const int n = S.ocnt[idx];
+  return (n > 0 && S.oaddr[idx][0] == addr) || (n > 1 && S.oaddr[idx][1] == addr);
 }
 __device__ __forceinline__ void occ_add(BuildSmem& S, int idx, int addr) {
   const int n = S.ocnt[idx];
@@ -742,6 +747,7 @@ __device__ void reorder_round(BuildSmem& S, uint32_t* ops, int t0, int len, int 
   for (int t = 0; t < len; ++t) {
     S.ocnt[lane] = 0;
     S.ocnt[lane + 32] = 0;
+    if (lane < 4) S.omax[lane] = 0;
     __syncwarp();
     for (int q = 0; q < 16; ++q) {
       const int l = h + q;
@@ -751,10 +757,15 @@ __device__ void reorder_round(BuildSmem& S, uint32_t* ops, int t0, int len, int 
       for (int k = 0; k < 2; ++k) {
         const int s = c + 16 * k;
         if (s < len && !((used >> s) & 1u)) {
+          // primary: how many of the two loads would raise their step's
+          // wavefront count (the busiest class); secondary: class load
           const uint32_t op = S.cand[l][s];
           const int a = (int)((op & 0xFFFFu) >> 3), b = (int)(op >> 19);
-          const int cab = occ_cost(S, h + (a & 15), a) + occ_cost(S, 32 + h + (b & 15), b);
-          const int cba = occ_cost(S, h + (b & 15), b) + occ_cost(S, 32 + h + (a & 15), a);
+          const int ma = S.omax[h >> 4], mb = S.omax[2 + (h >> 4)];
+          const int aa = occ_cost(S, h + (a & 15), a), bb = occ_cost(S, 32 + h + (b & 15), b);
+          const int ab = occ_cost(S, h + (b & 15), b), ba = occ_cost(S, 32 + h + (a & 15), a);
+          const int cab = ((aa >= ma && !occ_has(S, h + (a & 15), a)) + (bb >= mb && !occ_has(S, 32 + h + (b & 15), b))) * 64 + aa + bb;
+          const int cba = ((ab >= ma && !occ_has(S, h + (b & 15), b)) + (ba >= mb && !occ_has(S, 32 + h + (a & 15), a))) * 64 + ab + ba;
           const unsigned v = cab <= cba ? ((unsigned)cab << 8) | (unsigned)(s << 1)
                                         : ((unsigned)cba << 8) | (unsigned)(s << 1) | 1u;
           best = min(best, v);
@@ -770,6 +781,8 @@ __device__ void reorder_round(BuildSmem& S, uint32_t* ops, int t0, int len, int 
         const int a = (int)((op & 0xFFFFu) >> 3), b = (int)(op >> 19);
         occ_add(S, h + (a & 15), a);
         occ_add(S, 32 + h + (b & 15), b);
+        S.omax[h >> 4] = max(S.omax[h >> 4], S.ocnt[h + (a & 15)]);
+        S.omax[2 + (h >> 4)] = max(S.omax[2 + (h >> 4)], S.ocnt[32 + h + (b & 15)]);
       }
       __syncwarp();
     }
