@@ -1465,7 +1465,8 @@ static int leftovers_impl(int64_t n, const double* vals, const int64_t* cscptr,
 }
 
 #define SPAI_ASM_DISPATCH(HMAX, CALL)                                   \
-  ((HMAX) <= 8 ? CALL(8, 64, 4, 8) : (HMAX) <= 16 ? CALL(16, 256, 4, 8) \
+  ((HMAX) <= 8 ? CALL(8, 64, 4, 8) : (HMAX) <= 9 ? CALL(9, 128, 4, 8)   \
+   : (HMAX) <= 16 ? CALL(16, 256, 4, 8)                                 \
    : (HMAX) <= 27 ? CALL(27, 784, 4, 8)                                 \
    : (HMAX) <= 28 ? CALL(28, 784, 4, 8) : CALL(32, 1024, 8, 4))
 
