@@ -150,6 +150,20 @@ int spai_csc_to_csr_values(int64_t nnz, const int64_t* csc2csr,
  * spai_structure_is_symmetric).  s_csr may alias nothing.                 */
 int spai_symmetrize(int64_t nnz, const int64_t* csc2csr, const double* m_csc,
                     double* s_csr, void* stream);
+/* 0.5*(M + M^T) for a structurally NONsymmetric pattern (cli.py:189-194:
+ * the dense sum grows the pattern to pattern(M) u pattern(M^T) and
+ * from_dense(tol=0), sparse.py:78-81, drops exact zeros).  Inputs: M in CSR
+ * (rowptr/colidx/m_csr) and the same M in CSC (cscptr/cscrow/m_csc).
+ * count: srowptr[n+1] of S, *snnz (synchronous); fill: scol/sval[snnz].    */
+int spai_symmetrize_union_count(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                                const double* m_csr, const int64_t* cscptr,
+                                const int32_t* cscrow, const double* m_csc,
+                                int64_t* srowptr, int64_t* snnz, void* stream);
+int spai_symmetrize_union_fill(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                               const double* m_csr, const int64_t* cscptr,
+                               const int32_t* cscrow, const double* m_csc,
+                               const int64_t* srowptr, int32_t* scol, double* sval,
+                               void* stream);
 
 /* ------------------------------------------------------------------ K5
  * y = A x (replaces spmv, sparse.py:191-202, and
@@ -338,6 +352,9 @@ int spai_ksolver_poll(spai_ksolver* s, int* status, int64_t* iterations, double*
                       double* norm, int* breakdown_kind);
 int spai_ksolver_history(spai_ksolver* s, double* host_out, int64_t count);
 int spai_ksolver_x(spai_ksolver* s, double** x);
+/* Blocks of the fused reduction kernels (fixes the device summation order:
+ * oracle/devorder.c restates it for bit-level parity tests).               */
+int spai_ksolver_grid(spai_ksolver* s, int* blocks);
 int spai_ksolver_destroy(spai_ksolver* s);
 
 /* ------------------------------------------------------------------ K8 multi-GPU
@@ -352,6 +369,8 @@ int spai_ksolver_destroy(spai_ksolver* s);
  * runs the scalar recurrence (stage 1 after A p, stage 2 after M r).      */
 size_t spai_dist_scal_bytes(void);
 size_t spai_dist_partials_bytes(void);
+/* address of the status word inside a scal block (for the *_st entries)   */
+void* spai_dist_status_ptr(void* scal);
 int spai_dist_scal_init(void* scal, double tol, int64_t maxit, void* stream);
 int spai_dist_scal_read(const void* scal, int* status, int64_t* it, double* norm0,
                         double* norm, double* aux, void* stream);
@@ -377,6 +396,15 @@ int spai_dist_spmv_sym_st(int mode, int64_t n, int64_t r0, int64_t n_ext, const 
                           int w, const double* U, const double* xext, int64_t own_off,
                           double* y, const double* raux, void* partials_ws, double* out,
                           const int* status, void* stream);
+/* Block-local scope (the reference's RankSystem.apply_A, krylov.py:210-216):
+ * y = spmv(A_ff, x) + hadd with hadd = spmv(A_fh, x_halo) precomputed by the
+ * caller (spai_csr_spmv on the halo block), so each row is summed in the
+ * reference's two parts; the SELL operator holds A_ff only.               */
+int spai_dist_spmv_split_st(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
+                            const int64_t* cdesc, const int32_t* cols, const double* vals,
+                            const double* hadd, const double* xext, int64_t own_off,
+                            double* y, const double* raux, void* partials_ws, double* out,
+                            const int* status, void* stream);
 /* Row-partitioned Chronopoulos-Gear / pipelined CG (DistributedCGV): the
  * scalar state is a K10 VScal; variant 1 = chronopoulos_gear, 3 = pipelined */
 size_t spai_dcgv_scal_bytes(void);

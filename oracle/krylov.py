@@ -78,8 +78,14 @@ def _finite(*s):
             raise Divergence("non-finite value in solver recurrence")
 
 
-def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None):
-    """`krylov.py:301-345`. M is a CSR (applied by spmv) or None."""
+def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None, dot=None, matvec=None):
+    """`krylov.py:301-345`. M is a CSR (applied by spmv) or None.
+
+    `dot` / `matvec` replace np.dot / spmv (default: the reference's) -- used
+    by `rounding_sensitivity` to re-run the same algorithm in another
+    summation order."""
+    dot = np.dot if dot is None else dot
+    spmv = globals()["spmv"] if matvec is None else matvec
     apply_M = (lambda v: v.copy()) if M is None else (M if callable(M) else (lambda v: spmv(M, v)))
     rec = Record("classic")
     red = 0
@@ -107,14 +113,14 @@ def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None):
         q = spmv(A, p)
         red += 1
         if it == 1:
-            delta, rho, rr0 = (float(np.dot(p, q)), float(np.dot(p, r)),
-                               float(np.dot(r, r)))
+            delta, rho, rr0 = (float(dot(p, q)), float(dot(p, r)),
+                               float(dot(r, r)))
             norm0 = math.sqrt(rr0)
             rec.initial_residual = norm0
             if norm0 == 0.0:
                 return finish(x, 0.0, it, True)
         else:
-            delta = float(np.dot(p, q))
+            delta = float(dot(p, q))
         _finite(delta, rho)
         if delta <= 0.0:
             if rho == 0.0:
@@ -125,7 +131,7 @@ def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None):
         r = r - lam * q
         q = apply_M(r)
         red += 1
-        rho_new, rr = float(np.dot(q, r)), float(np.dot(r, r))
+        rho_new, rr = float(dot(q, r)), float(dot(r, r))
         _finite(rho_new, rr)
         norm = math.sqrt(rr)
         if not math.isfinite(norm):
@@ -136,6 +142,36 @@ def pcg_classic(A, M, b, tol=1e-8, maxit=1000, x0=None):
         rho = rho_new
     converged = norm0 is not None and norm <= tol * norm0
     return finish(x, norm, it, converged)
+
+
+def _spmv_reversed(A, x):
+    """spmv with every row summed right to left (another rounding order)."""
+    x = np.asarray(x, dtype=np.float64)
+    prod = (A.values * x[A.col_indices])
+    out = np.zeros(A.nrows)
+    lens = np.diff(A.row_offsets)
+    for k in range(int(lens.max()) if len(lens) else 0):
+        rows = np.flatnonzero(lens > k)
+        out[rows] += prod[A.row_offsets[rows + 1] - 1 - k]
+    return out
+
+
+def rounding_sensitivity(A, M, b, tol=1e-8, maxit=1000):
+    """How far `pcg_classic`'s residual history moves when only the rounding
+    order changes (exact dots via math.fsum; right-to-left row sums): the
+    max relative deviation per iteration.  A device run (fma chains, blocked
+    dots) cannot be held closer to the reference than this floor."""
+    import math as _m
+    _, r0 = pcg_classic(A, M, b, tol, maxit)
+    h0 = np.array(r0.residual_norms)
+    worst = 0.0
+    for kw in ({"dot": lambda a, c: _m.fsum(np.asarray(a) * np.asarray(c))},
+               {"matvec": _spmv_reversed}):
+        _, r1 = pcg_classic(A, M, b, tol, maxit, **kw)
+        h1 = np.array(r1.residual_norms)
+        m = min(len(h0), len(h1))
+        worst = max(worst, float(np.max(np.abs(h0[:m] - h1[:m]) / h0[:m])) if m else 0.0)
+    return worst
 
 
 class _Acc:

@@ -70,9 +70,11 @@ _SIGS = {
                                  C.POINTER(_dbl), C.POINTER(_i32)]),
     "spai_ksolver_history": (_i32, [_vp, _vp, _i64]),
     "spai_ksolver_x": (_i32, [_vp, C.POINTER(_vp)]),
+    "spai_ksolver_grid": (_i32, [_vp, C.POINTER(_i32)]),
     "spai_ksolver_destroy": (_i32, [_vp]),
     "spai_dist_scal_bytes": (_sz, []),
     "spai_dist_partials_bytes": (_sz, []),
+    "spai_dist_status_ptr": (_vp, [_vp]),
     "spai_dist_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),
     "spai_dist_scal_read": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),
                                    C.POINTER(_dbl), C.POINTER(_dbl), _vp]),
@@ -84,6 +86,8 @@ _SIGS = {
                                  _vp, _vp, _vp]),
     "spai_dist_spmv_sym_st": (_i32, [_i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i64, _vp, _vp,
                                      _vp, _vp, _vp, _vp]),
+    "spai_dist_spmv_split_st": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                                       _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_dcgv_scal_bytes": (_sz, []),
     "spai_dcgv_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),
     "spai_dcgv_status_ptr": (_vp, [_vp]),
@@ -97,6 +101,10 @@ _SIGS = {
     "spai_dist_reduce_step": (_i32, [_i32, _vp, _i32, _i32, _vp, _vp, _vp]),
     "spai_csc_to_csr_values": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_symmetrize": (_i32, [_i64, _vp, _vp, _vp, _vp]),
+    "spai_symmetrize_union_count": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                           C.POINTER(_i64), _vp]),
+    "spai_symmetrize_union_fill": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                          _vp]),
     "spai_csr_spmv": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_tile_count": (_i32, [_i64, _i64, C.POINTER(_i64)]),
     "spai_tile_rows": (_i32, [_i64, _vp, _i64, _vp, _vp, _vp]),

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
 dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
                  const double* __restrict__ xext, int64_t own_off, double* __restrict__ y,
                  const double* __restrict__ raux, double* partials, unsigned int* ticket,
-                 double* out, const int* status) {
+                 double* out, const int* status, const double* __restrict__ hadd) {
   if (MODE != 0 && *status != dRunning) return;
   constexpr int K = (MODE == 1 || MODE >= 5) ? 3 : (MODE == 2 ? 1 : 2);
   const int lane = threadIdx.x & 31;
@@ -49,6 +49,9 @@ dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
     if (i >= 0 && i < n) {
       const double xi = xo[i];
       if (MODE == 4) v = xi;
+      // block-local reference order: spmv(A_ff, x) + spmv(A_fh, x_halo),
+      // the second product precomputed into hadd (krylov.py:210-216)
+      if (hadd) v = v + hadd[i];
       y[i] = v;
       if (MODE == 1) {
         const double ri = raux[i];
@@ -87,7 +90,7 @@ __global__ void dist_update_p(int64_t n, double* __restrict__ p, const double* _
   const double beta = sc->beta;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], z[i]);
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));    // numpy z + beta * p (krylov.py:340)
 }
 
 // x += lambda p, r -= lambda q (owned parts)
@@ -98,8 +101,9 @@ __global__ void dist_update_xr(int64_t n, double* __restrict__ x, double* __rest
   const double lambda = sc->lambda;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    r[i] = fma(-lambda, q[i], r[i]);
-    x[i] = fma(lambda, p[i], x[i]);
+    // numpy x + lam * p, r - lam * q (krylov.py:332-333), separately rounded
+    r[i] = __dsub_rn(r[i], __dmul_rn(lambda, q[i]));
+    x[i] = __dadd_rn(x[i], __dmul_rn(lambda, p[i]));
   }
 }
 
@@ -168,15 +172,15 @@ template <class OP>
 static int dist_launch(int mode, unsigned b, int64_t n, int64_t s0, int64_t s1, int64_t r0,
                        const OP& A, const double* xext, int64_t own_off, double* y,
                        const double* raux, double* part, unsigned int* ticket, double* out,
-                       const int* sc, cudaStream_t s) {
+                       const int* sc, cudaStream_t s, const double* hadd = nullptr) {
   switch (mode) {
-    case 0: dist_spmv_kernel<0, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 1: dist_spmv_kernel<1, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 2: dist_spmv_kernel<2, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 3: dist_spmv_kernel<3, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 4: dist_spmv_kernel<4, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 5: dist_spmv_kernel<5, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
-    case 6: dist_spmv_kernel<6, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc); break;
+    case 0: dist_spmv_kernel<0, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 1: dist_spmv_kernel<1, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 2: dist_spmv_kernel<2, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 3: dist_spmv_kernel<3, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 4: dist_spmv_kernel<4, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 5: dist_spmv_kernel<5, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 6: dist_spmv_kernel<6, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
     default: set_error("bad dist_spmv mode %d", mode); return SPAI_E_ARG;
   }
   SPAI_LAUNCH_CHECK("dist_spmv_kernel");
@@ -214,6 +218,8 @@ extern "C" int spai_dist_scal_read(const void* scal, int* status, int64_t* it, d
   return SPAI_OK;
 }
 
+extern "C" void* spai_dist_status_ptr(void* scal) { return &((DistScal*)scal)->status; }
+
 extern "C" size_t spai_dist_partials_bytes(void) {
   return 256 + (size_t)num_sms() * 32 * 3 * sizeof(double);
 }
@@ -236,6 +242,30 @@ extern "C" int spai_dist_spmv_st(int mode, int64_t n, int64_t ncols, const int64
   const SellOp A{Sell{sliceptr, cdesc, cols, vals, ncols}};
   return dist_launch(mode, b, n, 0, ns, 0, A, xext, own_off, y, raux, part, ticket, out,
                      status, (cudaStream_t)stream);
+}
+
+// Block-local scope in the reference's summation order: y = A_ff x + hadd,
+// hadd = A_fh x_halo computed beforehand (spai_csr_spmv on the halo block).
+extern "C" int spai_dist_spmv_split_st(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
+                                       const int64_t* cdesc, const int32_t* cols,
+                                       const double* vals, const double* hadd,
+                                       const double* xext, int64_t own_off, double* y,
+                                       const double* raux, void* partials_ws, double* out,
+                                       const int* status, void* stream) {
+  const int64_t ns = (n + kSell - 1) / kSell;
+  if (ns == 0) {
+    if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
+    return SPAI_OK;
+  }
+  if (mode == 4) { set_error("dist_spmv_split: mode 4 has no operator"); return SPAI_E_ARG; }
+  static unsigned blocks = 0;
+  if (!blocks) blocks = sell_blocks((const void*)dist_spmv_kernel<1, SellOp>, 1 << 30);
+  const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (ns * 32 + 255) / 256));
+  unsigned int* ticket = (unsigned int*)partials_ws;
+  double* part = (double*)((char*)partials_ws + 256);
+  const SellOp A{Sell{sliceptr, cdesc, cols, vals, ncols}};
+  return dist_launch(mode, b, n, 0, ns, 0, A, xext, own_off, y, raux, part, ticket, out,
+                     status, (cudaStream_t)stream, hadd);
 }
 
 extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,

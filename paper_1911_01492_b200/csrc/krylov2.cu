@@ -41,7 +41,10 @@ __device__ __forceinline__ void vec_loop(int64_t n, const F& f) {
 __global__ void bicg_b1(int64_t n, KVecs v, const KScal* sc) {
   if (!krun(sc)) return;
   const double beta = (sc->rho / sc->rho_old) * (sc->alpha / sc->omega), om = sc->omega;
-  vec_loop(n, [&](int64_t i) { v.p[i] = v.r[i] + beta * (v.p[i] - om * v.v[i]); });
+  // explicitly rounded (no fma contraction): the oracle's numpy expression
+  vec_loop(n, [&](int64_t i) {
+    v.p[i] = __dadd_rn(v.r[i], __dmul_rn(beta, __dsub_rn(v.p[i], __dmul_rn(om, v.v[i]))));
+  });
 }
 
 // y = M x (or copy when no M)
@@ -87,7 +90,7 @@ bicg_b3(int64_t n, int64_t nslices, OPA A, KVecs v, KScal* sc) {
 __global__ void bicg_b4(int64_t n, KVecs v, const KScal* sc) {
   if (!krun(sc)) return;
   const double al = sc->alpha;
-  vec_loop(n, [&](int64_t i) { v.s[i] = v.r[i] - al * v.v[i]; });
+  vec_loop(n, [&](int64_t i) { v.s[i] = __dsub_rn(v.r[i], __dmul_rn(al, v.v[i])); });
 }
 
 // B6: t = A sh, [(t,s),(t,t)] -> omega
@@ -124,8 +127,8 @@ bicg_b7(int64_t n, KVecs v, KScal* sc) {
   double acc[2] = {0.0, 0.0};
   for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * kSpmvThreads) {
-    v.x[i] = v.x[i] + al * v.ph[i] + om * v.sh[i];
-    const double ri = v.s[i] - om * v.t[i];
+    v.x[i] = __dadd_rn(__dadd_rn(v.x[i], __dmul_rn(al, v.ph[i])), __dmul_rn(om, v.sh[i]));
+    const double ri = __dsub_rn(v.s[i], __dmul_rn(om, v.t[i]));
     v.r[i] = ri;
     acc[0] = fma(v.rh[i], ri, acc[0]);
     acc[1] = fma(ri, ri, acc[1]);
@@ -159,7 +162,7 @@ rich_r1(int64_t n, int64_t nslices, OPM M, KVecs v, const KScal* sc) {
     double z = 0.0;
     if (HAS_M) z = M.row(s, lane, [&](int32_t j) { return __ldg(v.r + j); });
     const int64_t i = s * kSell + lane;
-    if (i < n) v.x[i] = v.x[i] + om * (HAS_M ? z : v.r[i]);
+    if (i < n) v.x[i] = __dadd_rn(v.x[i], __dmul_rn(om, HAS_M ? z : v.r[i]));
   }
 }
 
@@ -384,6 +387,12 @@ extern "C" int spai_ksolver_history(spai_ksolver* s, double* host_out, int64_t c
 extern "C" int spai_ksolver_x(spai_ksolver* s, double** x) {
   SPAI_CUDA(cudaStreamSynchronize(s->stream));
   *x = s->v.x;
+  return SPAI_OK;
+}
+
+extern "C" int spai_ksolver_grid(spai_ksolver* s, int* blocks) {
+  if (!s || !blocks) { set_error("spai_ksolver_grid: bad arguments"); return SPAI_E_ARG; }
+  *blocks = (int)s->bs;
   return SPAI_OK;
 }
 

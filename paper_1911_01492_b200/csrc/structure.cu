@@ -202,6 +202,41 @@ __global__ void tile_max_kernel(int64_t ntiles, const int64_t* rowptr,
   if ((threadIdx.x & 31) == 0) atomicMax(maxnnz, m);
 }
 
+// S = 0.5 (M + M^T) on pattern(M) u pattern(M^T) with exact zeros dropped:
+// the dense symmetrisation of the CLI factory (cli.py:189-194,
+// from_dense(tol=0) at sparse.py:78-81) for a structurally nonsymmetric
+// pattern.  Row i of M is the CSR row (cols sorted), row i of M^T is CSC
+// column i of M (rows sorted); one thread merges the two sorted lists.  An
+// entry present on one side only is 0.5 * (a + 0.0), as in the dense sum.
+template <bool FILL>
+__global__ void sym_union_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                 const int32_t* __restrict__ colidx,
+                                 const double* __restrict__ m_csr,
+                                 const int64_t* __restrict__ cscptr,
+                                 const int32_t* __restrict__ cscrow,
+                                 const double* __restrict__ m_csc, int64_t* __restrict__ srowptr,
+                                 int32_t* __restrict__ scol, double* __restrict__ sval) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = rowptr[i], ae = rowptr[i + 1], b = cscptr[i], be = cscptr[i + 1];
+    int64_t out = FILL ? srowptr[i] : 0, cnt = 0;
+    while (a < ae || b < be) {
+      int32_t ca = a < ae ? colidx[a] : INT32_MAX;
+      int32_t cb = b < be ? cscrow[b] : INT32_MAX;
+      int32_t c = ca < cb ? ca : cb;
+      double va = 0.0, vb = 0.0;
+      if (ca == c) va = m_csr[a++];
+      if (cb == c) vb = m_csc[b++];
+      double v = 0.5 * (va + vb);
+      if (v != 0.0) {
+        if (FILL) { scol[out + cnt] = c; sval[out + cnt] = v; }
+        ++cnt;
+      }
+    }
+    if (!FILL) srowptr[i + 1] = cnt;
+  }
+}
+
 static inline unsigned grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   int64_t cap = (int64_t)num_sms() * 32;
@@ -323,6 +358,44 @@ extern "C" int spai_csr_transpose_symmetric(int64_t n, int64_t nnz, const int64_
   SPAI_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
   SPAI_CUDA(cudaStreamSynchronize(s));
   *is_sym = h ? 0 : 1;
+  return SPAI_OK;
+}
+
+extern "C" int spai_symmetrize_union_count(int64_t n, const int64_t* rowptr,
+                                           const int32_t* colidx, const double* m_csr,
+                                           const int64_t* cscptr, const int32_t* cscrow,
+                                           const double* m_csc, int64_t* srowptr,
+                                           int64_t* snnz, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n <= 0) { set_error("symmetrize_union: empty matrix"); return SPAI_E_ARG; }
+  SPAI_CUDA(cudaMemsetAsync(srowptr, 0, sizeof(int64_t), s));
+  sym_union_kernel<false><<<grid_for(n, 256), 256, 0, s>>>(n, rowptr, colidx, m_csr, cscptr,
+                                                             cscrow, m_csc, srowptr, nullptr,
+                                                             nullptr);
+  SPAI_LAUNCH_CHECK("sym_union_kernel<count>");
+  size_t tb = 0;
+  SPAI_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, srowptr + 1, srowptr + 1, n, s));
+  void* tmp = nullptr;
+  SPAI_CUDA(cudaMallocAsync(&tmp, tb, s));
+  SPAI_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, srowptr + 1, srowptr + 1, n, s));
+  SPAI_CUDA(cudaFreeAsync(tmp, s));
+  SPAI_CUDA(cudaMemcpyAsync(snnz, srowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaStreamSynchronize(s));
+  return SPAI_OK;
+}
+
+extern "C" int spai_symmetrize_union_fill(int64_t n, const int64_t* rowptr,
+                                          const int32_t* colidx, const double* m_csr,
+                                          const int64_t* cscptr, const int32_t* cscrow,
+                                          const double* m_csc, const int64_t* srowptr,
+                                          int32_t* scol, double* sval, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n <= 0) { set_error("symmetrize_union: empty matrix"); return SPAI_E_ARG; }
+  sym_union_kernel<true><<<grid_for(n, 256), 256, 0, s>>>(n, rowptr, colidx, m_csr, cscptr,
+                                                            cscrow, m_csc,
+                                                            const_cast<int64_t*>(srowptr), scol,
+                                                            sval);
+  SPAI_LAUNCH_CHECK("sym_union_kernel<fill>");
   return SPAI_OK;
 }
 

@@ -179,6 +179,26 @@ class SymExtOperator:
         self.n_own, self.r0, self.n_ext = int(n_own), int(r0), int(ext.nrows)
 
 
+class SplitOperator:
+    """Block-local rank operator in the reference's summation order
+    (RankSystem.apply_A, krylov.py:210-216): y = spmv(A_ff, x) + spmv(A_fh,
+    x_halo).  Both parts index the extended vector; the halo part is
+    multiplied first (CSR, into `hadd`), the owned part runs in the fused
+    SELL kernel, which adds hadd row by row before its epilogue."""
+
+    def __init__(self, ff, fh):
+        import torch
+        self.ff, self.fh = ff, fh
+        self.nrows, self.ncols = ff.nrows, ff.ncols
+        self.hadd = torch.zeros(ff.nrows, dtype=torch.float64, device=ff.vals.device)
+
+    def sell(self):
+        return self.ff.sell()
+
+    def sell_values(self):
+        return self.ff.sell_values()
+
+
 # ------------------------------------------------------------------ GPU backend
 class GpuBackend:
     """Per-rank compute through the C-ABI (dist_* kernels, SELL-32 operators)."""
@@ -219,7 +239,23 @@ class GpuBackend:
                    "spai_dist_scal_read")
         return st.value, it.value, n0.value, nr.value, aux.value
 
+    def _split(self, mode, M, xext, own_off, y, raux, ws, out, status):
+        fh = M.fh
+        _lib.check(self.lib.spai_csr_spmv(fh.nrows, fh.nnz, _p(fh.rowptr), _p(fh.colidx),
+                                          _p(fh.vals), _p(xext), _p(M.hadd), self._s()),
+                   "spai_csr_spmv")
+        sliceptr, cdesc, cols = M.sell()
+        _lib.check(self.lib.spai_dist_spmv_split_st(
+            mode, M.nrows, M.ncols, _p(sliceptr), _p(cdesc), _p(cols), _p(M.sell_values()),
+            _p(M.hadd), _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out), C.c_void_p(status),
+            self._s()), "spai_dist_spmv_split_st")
+
     def spmv(self, mode, M, xext, own_off, y, raux, ws, out, scal):
+        if isinstance(M, SplitOperator):
+            # DistScal's status word sits at the same offset the kernel reads
+            self._split(mode, M, xext, own_off, y, raux, ws, out,
+                        self.lib.spai_dist_status_ptr(_p(scal)))
+            return
         if isinstance(M, SymExtOperator):
             _lib.check(self.lib.spai_dist_spmv_sym(
                 mode, M.n_own, M.r0, M.n_ext, C.cast(M.garr, C.c_void_p), len(M.g), _p(M.U),
@@ -240,6 +276,9 @@ class GpuBackend:
 
     def spmv_st(self, mode, M, xext, own_off, y, raux, ws, out, status):
         """dist SpMV with an explicit device status word (any solver)."""
+        if isinstance(M, SplitOperator):
+            self._split(mode, M, xext, own_off, y, raux, ws, out, status)
+            return
         if isinstance(M, SymExtOperator):
             _lib.check(self.lib.spai_dist_spmv_sym_st(
                 mode, M.n_own, M.r0, M.n_ext, C.cast(M.garr, C.c_void_p), len(M.g), _p(M.U),
@@ -611,6 +650,9 @@ class RankSetup:
         """symmetric: solve with half-storage operators of the extended blocks
         when A and S are exactly symmetric (global scope); else SELL-32."""
         sysr = LocalRankSystem(self.n_own, self.hlo, self.hhi, self.A_loc, M, self.b)
+        if self.scope == "block_local" and (self.hlo or self.hhi):
+            # the reference's multi-rank semantics: A_FF x + A_FH x_halo
+            sysr.A_op = _split_operator(self.A_loc, self.hlo, self.hlo + self.n_own)
         if symmetric and M is not None and self.S_ext is not None:
             try:
                 sysr.A_op = SymExtOperator(self.A_ext, self.n_own, self.hlo)
@@ -618,6 +660,25 @@ class RankSetup:
             except ValueError:
                 sysr.A_op = sysr.M_op = None
         return sysr
+
+
+def _split_operator(A, c0, c1):
+    """SplitOperator of a rank matrix on the extended range: columns [c0, c1)
+    (owned, A_FF) and the rest (halo, A_FH), both keeping extended indexing."""
+    import torch
+    from .sparse import DeviceCsr
+    rows = torch.repeat_interleave(torch.arange(A.nrows, device=A.vals.device),
+                                   A.rowptr[1:] - A.rowptr[:-1])
+    own = (A.colidx >= c0) & (A.colidx < c1)
+
+    def part(mask):
+        cnt = torch.bincount(rows[mask], minlength=A.nrows)
+        rp = torch.zeros(A.nrows + 1, dtype=torch.int64, device=A.vals.device)
+        rp[1:] = torch.cumsum(cnt, 0)
+        return DeviceCsr(A.nrows, A.ncols, rp, A.colidx[mask].contiguous(),
+                         A.vals[mask].contiguous())
+
+    return SplitOperator(part(own), part(~own))
 
 
 def _principal(S, a, b, like):
@@ -777,10 +838,14 @@ class RankSystem:
             np.zeros(0, dtype=np.int64)
         cfh = np.asarray(fh.col_indices, dtype=np.int64) if fh.ncols else np.zeros(0, np.int64)
         cfh = np.where(cfh < hlo, cfh, cfh + n)
-        A_ext = CsrMatrix.from_coo(n, hlo + n + hhi, np.concatenate([rows_ff, rows_fh]),
-                                   np.concatenate([np.asarray(ff.col_indices) + hlo, cfh]),
-                                   np.concatenate([ff.values, fh.values if fh.ncols
-                                                   else np.zeros(0)]))
+        ne = hlo + n + hhi
+        A_ff = as_device(CsrMatrix(n, ne, np.asarray(ff.row_offsets),
+                                   np.asarray(ff.col_indices) + hlo, ff.values))
+        if len(cfh):
+            A_fh = as_device(CsrMatrix.from_coo(n, ne, rows_fh, cfh, fh.values))
+            A_op = SplitOperator(A_ff, A_fh)
+        else:
+            A_op = A_ff
         M_ext = None
         if self.M is not None:
             Mm = getattr(self.M, "M", None)
@@ -793,7 +858,7 @@ class RankSystem:
                                                  np.asarray(Mm.col_indices) + hlo, Mm.values))
         bd = b if isinstance(b, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(b, dtype=np.float64))
-        return LocalRankSystem(n, hlo, hhi, as_device(A_ext), M_ext, bd.cuda().double())
+        return LocalRankSystem(n, hlo, hhi, A_op, M_ext, bd.cuda().double())
 
 
 def fused_allreduce(comm, values, overlapped=False, rank=None):

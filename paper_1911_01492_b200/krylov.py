@@ -132,7 +132,9 @@ class LocalSystem:
 
     @property
     def device_A(self) -> DeviceCsr:
-        if self._dA is None:
+        # a host CsrMatrix keeps its own upload cache (re-uploaded when its
+        # arrays are replaced), so ask it every time
+        if self._dA is None or not isinstance(self.A, DeviceCsr):
             self._dA = as_device(self.A)
         return self._dA
 
@@ -691,6 +693,12 @@ class DeviceKrylov:
         _lib.check(self.lib.spai_ksolver_poll(self.h, C.byref(st), C.byref(it), C.byref(n0),
                                               C.byref(nr), C.byref(bk)), "spai_ksolver_poll")
         return st.value, it.value, n0.value, nr.value, bk.value
+
+    def grid(self) -> int:
+        """Blocks of the fused reduction kernels (fixes the summation order)."""
+        g = C.c_int(0)
+        _lib.check(self.lib.spai_ksolver_grid(self.h, C.byref(g)), "spai_ksolver_grid")
+        return g.value
 
     def history(self, count):
         out = np.zeros(max(count, 0))

@@ -59,7 +59,9 @@ class SparseMatrixPreconditioner(Preconditioner):
         self._dev = M if isinstance(M, DeviceCsr) else None
 
     def device_matrix(self) -> DeviceCsr:
-        if self._dev is None:
+        # a host CsrMatrix keeps its own upload cache (re-uploaded when its
+        # arrays are replaced), so ask it every time
+        if self._dev is None or not isinstance(self.M, DeviceCsr):
             self._dev = as_device(self.M)
         return self._dev
 
@@ -166,17 +168,19 @@ def spai1_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
 
 
 def spai1_symmetric_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
-    """0.5*(M + M^T) on pattern(A) (cli.py:189-194 semantics on the stored pattern).
+    """0.5*(M + M^T) (cli.py:189-194).
 
-    Needs a structurally symmetric A (all FEM matrices here are); the
-    reference additionally drops exact zeros (`from_dense(tol=0)`), which
-    `to_reference_symmetric` reproduces on the host copy.
+    Structurally symmetric A (every FEM matrix here): S stays on pattern(A)
+    (K4 gather); the reference additionally drops exact zeros
+    (`from_dense(tol=0)`), which `drop_exact_zeros` reproduces on the host
+    copy.  Structurally nonsymmetric A: S lives on pattern(M) u pattern(M^T)
+    with exact zeros dropped, exactly the reference's dense result
+    (`spai_symmetrize_union_*`).
     """
     torch = _require_cuda()
     A = as_device(A)
     if not A.structurally_symmetric():
-        raise DimensionMismatchError(
-            "symmetrised SPAI(1) needs a structurally symmetric pattern")
+        return _symmetrize_union(A, spai1_columns_device(A, stats))
     # the solve will want A's half storage anyway; building it first also
     # certifies A = A^T bit for bit, so the CSC values alias A's values
     A.ssell_values()
@@ -187,6 +191,33 @@ def spai1_symmetric_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
                                            stream_handle()), "spai_symmetrize")
     S = A.with_values(vals)
     S.symmetric_by_construction = True     # 0.5 (m_p + m_p^T): bit-symmetric
+    return S
+
+
+def _symmetrize_union(A: DeviceCsr, m_csc) -> DeviceCsr:
+    """S = 0.5 (M + M^T) on the union pattern, exact zeros dropped (K4u)."""
+    torch = _require_cuda()
+    lib = _lib.load()
+    cscptr, cscrow, csc2csr = A.csc()
+    dev = A.vals.device
+    m_csr = torch.empty_like(m_csc)
+    s = stream_handle()
+    _lib.check(lib.spai_csc_to_csr_values(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(m_csr), s),
+               "spai_csc_to_csr_values")
+    srowptr = torch.empty(A.nrows + 1, dtype=torch.int64, device=dev)
+    snnz = C.c_int64(0)
+    _lib.check(lib.spai_symmetrize_union_count(A.nrows, ptr(A.rowptr), ptr(A.colidx), ptr(m_csr),
+                                               ptr(cscptr), ptr(cscrow), ptr(m_csc),
+                                               ptr(srowptr), C.byref(snnz), s),
+               "spai_symmetrize_union_count")
+    scol = torch.empty(max(snnz.value, 1), dtype=torch.int32, device=dev)
+    sval = torch.empty(max(snnz.value, 1), dtype=torch.float64, device=dev)
+    _lib.check(lib.spai_symmetrize_union_fill(A.nrows, ptr(A.rowptr), ptr(A.colidx), ptr(m_csr),
+                                              ptr(cscptr), ptr(cscrow), ptr(m_csc),
+                                              ptr(srowptr), ptr(scol), ptr(sval), s),
+               "spai_symmetrize_union_fill")
+    S = DeviceCsr(A.nrows, A.ncols, srowptr, scol[: snnz.value], sval[: snnz.value])
+    S.symmetric_by_construction = True     # 0.5 (m_ij + m_ji) == 0.5 (m_ji + m_ij)
     return S
 
 
@@ -246,8 +277,7 @@ def spai1_symmetric_from_host(rowptr, colidx, vals, nchunks: int = 8,
         t.record_stream(copy)
     if not A.structurally_symmetric():
         comp.wait_event(events[-1])
-        raise DimensionMismatchError(
-            "symmetrised SPAI(1) needs a structurally symmetric pattern")
+        return A, spai1_symmetric_device(A, stats)
     g = A.ssell_offsets()
     bw = int(max(g)) if g else n                 # no bandwidth bound: wait for everything
     cscptr, cscrow, csc2csr = A.csc()
@@ -260,7 +290,11 @@ def spai1_symmetric_from_host(rowptr, colidx, vals, nchunks: int = 8,
                                        C.byref(hmax), C.byref(plans), s), "spai_assemble_begin")
     waited = -1
     for j in range(len(rows) - 1):
-        need = min(n, int(rows[j + 1]) + bw) - 1          # last row this block reads
+        # last row this block reads: the plan replay reads CSC lists of the
+        # stencil columns (rows <= c1 - 1 + bw), but the hash / merge / QR
+        # paths (plans off or declined, a column failing plan verification)
+        # read A[I_k, J_k] through CSR rows of I_k, up to c1 - 1 + 2 bw
+        need = min(n, int(rows[j + 1]) + 2 * bw) - 1
         k = int(np.searchsorted(rows, need, side="right")) - 1
         k = min(max(k, 0), len(events) - 1)
         if k > waited:
@@ -277,12 +311,14 @@ def spai1_symmetric_from_host(rowptr, colidx, vals, nchunks: int = 8,
                                ptr(m_csc), ptr(ws), wsb, hmax.value, plans.value, C.byref(bad),
                                C.byref(nfb), s)
     _lib.check(st, "spai_assemble_end")
-    if st != _lib.SPAI_OK:
-        _raise_assembly(st, bad.value)
     sym_values = A.ssell_values() is not None if g else A.csc_values() is A.vals
     if not sym_values:
-        # not bit-symmetric: the overlapped pass read CSR values as CSC values
+        # not bit-symmetric: the overlapped pass solved the problems of A^T
+        # (CSR values read as CSC values); its status is meaningless, so
+        # discard it and assemble again through the CSC gather
         m_csc = spai1_columns_device(A, stats)
+    elif st != _lib.SPAI_OK:
+        _raise_assembly(st, bad.value)
     elif stats is not None:
         stats.n_merge = nfb.value >> 32
         stats.n_fallback = nfb.value & 0xFFFFFFFF

@@ -174,9 +174,21 @@ class CsrMatrix:
 
     # ---- device side
     def device(self) -> "DeviceCsr":
-        """HBM copy of this matrix (cached; re-uploaded if the arrays were replaced)."""
-        key = (id(self.row_offsets), id(self.col_indices), id(self.values))
-        if self._dev is None or self._dev[0] != key:
+        """HBM copy of this matrix (cached; re-uploaded if the arrays were replaced).
+
+        The first upload swaps the three fields for read-only views, so an
+        in-place edit (`A.values[:] = ...`) raises instead of leaving a stale
+        device copy; assigning new arrays (`A.values = v`) re-uploads."""
+        for name in ("row_offsets", "col_indices", "values"):
+            arr = getattr(self, name)
+            if arr.flags.writeable:
+                view = arr.view()
+                view.setflags(write=False)
+                setattr(self, name, view)
+        # the key holds the array objects themselves (compared by identity), so
+        # a replaced array cannot be confused with a new one at a reused id()
+        key = (self.row_offsets, self.col_indices, self.values)
+        if self._dev is None or any(a is not b for a, b in zip(self._dev[0], key)):
             self._dev = (key, DeviceCsr.from_host(self))
         return self._dev[1]
 
@@ -210,10 +222,15 @@ class DeviceCsr:
         torch = _require_cuda()
         if A.nrows >= 2**31 - 1 or A.ncols >= 2**31 - 1:
             raise DimensionMismatchError("matrix dimension exceeds int32 indices")
+        import warnings
         dev = torch.device("cuda")
-        rowptr = torch.from_numpy(np.ascontiguousarray(A.row_offsets)).to(dev)
-        colidx = torch.from_numpy(A.col_indices.astype(np.int32)).to(dev)
-        vals = torch.from_numpy(np.ascontiguousarray(A.values)).to(dev)
+        with warnings.catch_warnings():
+            # the container's arrays are read-only views (CsrMatrix.device);
+            # they are only read here, by the copy to the device
+            warnings.simplefilter("ignore", UserWarning)
+            rowptr = torch.from_numpy(np.ascontiguousarray(A.row_offsets)).to(dev)
+            colidx = torch.from_numpy(A.col_indices.astype(np.int32)).to(dev)
+            vals = torch.from_numpy(np.ascontiguousarray(A.values)).to(dev)
         return cls(A.nrows, A.ncols, rowptr, colidx, vals)
 
     def to_host(self) -> CsrMatrix:

@@ -35,6 +35,44 @@ def _single_gpu(dims, tol=1e-8):
     return A, S, x, rec
 
 
+def _block_local_floor(world):
+    """Rounding sensitivity of the reference's block-local run (FD5 32x32,
+    strips, M = blockdiag of the ranks' symmetrised SPAI(1)): how far the
+    oracle's own history moves when only the summation order changes."""
+    import oracle
+    from oracle.krylov import rounding_sensitivity
+    A = oracle.fd5_poisson(32, 32)
+    D = A.to_dense()
+    n = A.nrows
+    cuts = np.linspace(0, 32, world + 1).astype(int) * 32
+
+    def csr(Dm):
+        r, c = np.nonzero(Dm)
+        offs = np.zeros(Dm.shape[0] + 1, dtype=np.int64)
+        np.cumsum(np.bincount(r, minlength=Dm.shape[0]), out=offs[1:])
+        return oracle.Csr(Dm.shape[0], Dm.shape[1], offs, c.astype(np.int64), Dm[r, c])
+
+    Mb = np.zeros((n, n))
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        Mb[a:b, a:b] = oracle.symmetrize_dense_reference(oracle.spai1(csr(D[a:b, a:b]))).to_dense()
+    return rounding_sensitivity(A, csr(Mb), oracle.make_rhs_ones(A))
+
+
+def _assert_block_local_history(h, ref, world):
+    """Block-local multi-rank (the reference's RankSystem semantics): the
+    operator is summed as A_FF x + A_FH x_halo like krylov.py:210-216
+    (SplitOperator).  This problem is far more rounding-sensitive than the
+    single-rank one: the oracle's own history moves ~1e-5 relative in the
+    tail when only the summation order of its dots or row sums changes
+    (single rank: ~1e-13), so the bar is 1e-8 on the head (residual above
+    1e-6 ||r0||) and, over the whole run, within 10x of that measured floor."""
+    rel = np.abs(h - ref) / ref
+    head = ref > 1e-6 * ref[0]
+    assert np.max(rel[head]) <= 1e-8, np.max(rel[head])
+    floor = _block_local_floor(world)
+    assert np.max(rel) <= max(1e-8, 10 * floor), (np.max(rel), floor)
+
+
 def test_one_rank_distributed_equals_single_gpu():
     dims = (20, 18, 16)
     _, S, x1, rec1 = _single_gpu(dims)
@@ -173,8 +211,7 @@ def test_reference_rank_system_api_matches_reference(golden):
     ref = golden["multirank/fd5_32x32/2/hist"]
     h = np.array(out[0][5])
     m = min(len(h), len(ref))
-    head = ref[:m] > 1e-6 * ref[0]
-    assert np.max((np.abs(h[:m] - ref[:m]) / ref[:m])[head]) <= 1e-8
+    _assert_block_local_history(h[:m], ref[:m], world=2)
     x = np.zeros(32 * 32)
     for _, r0, r1, xr, *_ in out:
         x[r0:r1] = xr
@@ -222,10 +259,4 @@ def test_two_ranks_block_local_matches_reference(golden):
     ref = golden["multirank/fd5_32x32/2/hist"]
     h = np.array(out[0][5])
     m = min(len(h), len(ref))
-    rel = np.abs(h[:m] - ref[:m]) / ref[:m]
-    # RankSystem.apply_A sums A_FF x + A_FH x_halo as two products; the GPU sums
-    # each extended row once, in column order.  That rounding difference is
-    # amplified by CG only in the last decades of the solve.
-    head = ref[:m] > 1e-6 * ref[0]
-    assert np.max(rel[head]) <= 1e-8
-    assert np.max(rel) <= 1e-3
+    _assert_block_local_history(h[:m], ref[:m], world=2)

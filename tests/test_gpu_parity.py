@@ -573,6 +573,63 @@ def test_bicgstab_matches_oracle(dims, conv):
     assert r0.iterations > rec.iterations
 
 
+@pytest.mark.parametrize("dims,conv,eps,precond", [
+    ((24, 20), (4.0, -2.0), None, "spai"), ((12, 11, 10), (1.0, 0.5, 0.25), None, "spai"),
+    ((160, 130), (4.0, -2.0), None, "spai"), ((34, 31, 29), (1.0, 0.5, 0.25), None, "spai"),
+    ((64, 64), None, (1.0, 1e-3), "spai"), ((40, 37), (2.0, 1.0), None, "none")])
+def test_bicgstab_whole_history_matches_device_order_oracle(dims, conv, eps, precond):
+    """K9 BiCGStab vs the oracle restated in the device's operation order
+    (oracle/devorder.c: SELL-32 fma chains, blocked dot tree, separately
+    rounded updates): the WHOLE residual history to 1e-8 (north star), the
+    same iteration count and termination status, x to 1e-10."""
+    from oracle import devorder
+    from paper_1911_01492_b200.krylov import DeviceKrylov
+    A = pb.q1_device(dims, conv=conv, eps=eps)
+    M = pb.spai1_device(A) if precond == "spai" else None
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    s = DeviceKrylov(1, A, M, 1e-10, 3000, symmetric=False)
+    assert s.operator_format == "sell"
+    st = s.run(b)
+    h = s.history(st[1])
+    x = s.x().cpu().numpy()
+    grid = s.grid()
+    s.close()
+    Ah = A.to_host()
+    Mh = M.to_host() if M is not None else None
+    xo, ho, sto, n0, _ = devorder.bicgstab_devorder(Ah, Mh, b.cpu().numpy(), 1e-10, 3000, grid)
+    assert st[0] == sto == 1
+    assert len(h) == len(ho)
+    assert st[2] == n0
+    rel = np.max(np.abs(h - ho) / ho)
+    assert rel <= HIST_TOL, rel
+    assert np.max(np.abs(x - xo)) <= 1e-10 * np.max(np.abs(xo))
+    # the semantic oracle (NumPy order) converges to the same solution in
+    # +-1 iterations of the same length scale
+    _, rr = oracle.bicgstab_right(_ocsr(Ah), _ocsr(Mh) if Mh is not None else None,
+                                  b.cpu().numpy(), tol=1e-10, maxit=3000)
+    assert abs(rr.iterations - len(h)) <= max(1, len(h) // 20)
+
+
+def test_richardson_matches_device_order_oracle():
+    """K9 Richardson vs oracle/devorder.c: histories and x bit-level."""
+    from oracle import devorder
+    from paper_1911_01492_b200.krylov import DeviceKrylov
+    A = pb.q1_device((96, 80), conv=(2.0, -1.0))
+    M = pb.spai1_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    s = DeviceKrylov(2, A, M, 1e-300, 300, 1.0, False, symmetric=False)
+    st = s.run(b)
+    h = s.history(st[1])
+    x = s.x().cpu().numpy()
+    grid = s.grid()
+    s.close()
+    xo, ho, sto, _ = devorder.richardson_devorder(A.to_host(), M.to_host(), b.cpu().numpy(),
+                                                  1.0, 300, grid)
+    assert st[0] == sto == 2 and len(h) == len(ho) == 300
+    assert np.max(np.abs(h - ho) / ho) <= 1e-12
+    assert np.max(np.abs(x - xo)) <= 1e-12 * np.max(np.abs(xo))
+
+
 def test_richardson_matches_oracle_fixed_sweeps():
     """configs[0]: 2D Q1 64x64, SPAI(1)-preconditioned Richardson, fixed sweeps."""
     A = pb.assemble_q1((64, 64))
@@ -656,8 +713,8 @@ def test_spai1_symmetric_from_host_matches_device_path(dims, conv, nchunks):
 
 def test_spai1_symmetric_from_host_irregular_and_errors():
     """No half-storage layout (> 16 distinct offsets): no bandwidth bound, the
-    columns wait for every value block; a non-symmetric pattern raises like
-    spai1_symmetric_device."""
+    columns wait for every value block; a non-symmetric pattern gets the
+    union-pattern S of the reference CLI factory."""
     rng = np.random.default_rng(8)
     n = 3000
     r = rng.integers(0, n, 12000)
@@ -679,8 +736,12 @@ def test_spai1_symmetric_from_host_irregular_and_errors():
     assert torch.equal(S.vals, ref.vals)
     B = pb.CsrMatrix.from_coo(3, 3, np.array([0, 0, 1, 2]), np.array([0, 1, 1, 2]),
                               np.array([2.0, 1.0, 2.0, 2.0]))
-    with pytest.raises(pb.DimensionMismatchError):
-        pb.spai1_symmetric_from_host(B.row_offsets, B.col_indices.astype(np.int32), B.values)
+    # structurally nonsymmetric: the union-pattern symmetrisation (cli.py:189-194)
+    _, SB = pb.spai1_symmetric_from_host(B.row_offsets, B.col_indices.astype(np.int32), B.values)
+    SBr = oracle.symmetrize_dense_reference(oracle.spai1(_ocsr(B)))
+    assert np.array_equal(SB.rowptr.cpu().numpy(), SBr.row_offsets)
+    assert np.array_equal(SB.colidx.cpu().numpy(), SBr.col_indices)
+    assert np.allclose(SB.vals.cpu().numpy(), SBr.values, rtol=1e-12, atol=0)
     # fewer rows than value blocks
     T = pb.CsrMatrix.from_dense(np.array([[4.0, -1.0, 0.0], [-1.0, 4.0, -1.0],
                                           [0.0, -1.0, 4.0]]))

@@ -197,3 +197,35 @@ def test_hierarchy_transfers_match_reference(golden, name):
         c = omg.restrict_full(h, x, l)
         assert np.array_equal(c, golden[f"{pre}/{l}/restrict"])
         assert np.array_equal(omg.prolongate_full(h, c, l), golden[f"{pre}/{l}/round_trip"])
+
+
+@pytest.mark.parametrize("dims,conv", [((24, 20), (4.0, -2.0)), ((12, 11, 10), (1.0, 0.5, 0.25)),
+                                       ((70, 65), None)])
+def test_device_order_oracle_restates_the_numpy_oracle(dims, conv):
+    """oracle/devorder.c (the device's summation order) is the same algorithm
+    as oracle/krylov.py: Richardson histories agree to rounding; BiCGStab
+    agrees to rounding on the first iterations, converges in the same number
+    of iterations (+-1) to the same solution, and reports the same norm0."""
+    from oracle import devorder
+    A = oracle.stencil_csr(dims, *oracle.q1_stencil(len(dims), conv=conv))
+    M = oracle.spai1(A)
+    b = oracle.make_rhs_ones(A)
+    for grid in (1, 3, 300):
+        x, h, st, n0, _ = devorder.bicgstab_devorder(A, M, b, 1e-10, 1000, grid)
+        xr, rr = oracle.bicgstab_right(A, M, b, tol=1e-10, maxit=1000)
+        hr = np.array(rr.residual_norms)
+        assert st == 1 and abs(len(h) - len(hr)) <= 1
+        assert abs(n0 - rr.initial_residual) <= 1e-14 * n0
+        assert np.max(np.abs(h[:3] - hr[:3]) / hr[:3]) <= 1e-12
+        assert np.max(np.abs(x - xr)) <= 1e-8
+        xq, hq, stq, _ = devorder.richardson_devorder(A, M, b, 1.0, 60, grid)
+        xqr, rq = oracle.richardson(A, M, b, omega=1.0, maxit=60)
+        assert stq == 2 and len(hq) == 60
+        # r = b - A x cancels: rounding of b - Ax is relative to ||b||
+        assert np.all(np.abs(hq - np.array(rq.residual_norms)) <= 1e-12 * hq + 1e-14 * hq[0])
+        assert np.max(np.abs(xq - xqr)) <= 1e-12 * np.max(np.abs(xqr))
+    # without a preconditioner and through a breakdown path (zero rhs)
+    _, h0, st0, _, _ = devorder.bicgstab_devorder(A, None, b, 1e-10, 5000, 2)
+    assert st0 == 1 and len(h0) > len(h)
+    _, hz, stz, n0z, _ = devorder.bicgstab_devorder(A, M, np.zeros(A.nrows), 1e-10, 10, 2)
+    assert stz == 1 and n0z == 0.0 and len(hz) == 0
