@@ -145,3 +145,72 @@ def make_rhs_ones(A: Csr):
     """`make_rhs(..., "ones")` = spmv(A, 1) (`grids.py:166-167`)."""
     from .krylov import spmv
     return spmv(A, np.ones(A.ncols))
+
+
+def q1_element_assembly(dims, kappa, h: float = 1.0) -> Csr:
+    """Q1 Galerkin matrix of -div(kappa grad u) with a piecewise-constant
+    coefficient per cell, assembled element by element (our definition; the
+    reference has no Q1 generator): interior nodes of a structured grid,
+    Dirichlet boundary eliminated, x fastest.  `kappa` has one entry per
+    cell, shape dims[::-1] + 1 (cells between the boundary nodes, z-major).
+    The element stiffness is the tensor product of the 1D element matrices
+    k = [[1,-1],[-1,1]] / h and m = [[1/3,1/6],[1/6,1/3]] h; with kappa == 1
+    the assembled interior stencil is `q1_stencil(dim)` (to rounding).
+    Every structural coupling is stored (exact zeros included)."""
+    dims = tuple(int(d) for d in dims)
+    dim = len(dims)
+    kappa = np.asarray(kappa, dtype=np.float64)
+    cells = tuple(d + 1 for d in dims)
+    assert kappa.shape == cells[::-1], (kappa.shape, cells[::-1])
+    k1 = np.array([[1.0, -1.0], [-1.0, 1.0]]) / h
+    m1 = np.array([[1.0 / 3.0, 1.0 / 6.0], [1.0 / 6.0, 1.0 / 3.0]]) * h
+    corners = [tuple((c >> a) & 1 for a in range(dim)) for c in range(2 ** dim)]
+    Ke = np.zeros((2 ** dim, 2 ** dim))
+    for i, ci in enumerate(corners):
+        for j, cj in enumerate(corners):
+            s = 0.0
+            for a in range(dim):
+                p = 1.0
+                for b in range(dim):
+                    p *= (k1 if b == a else m1)[ci[b], cj[b]]
+                s += p
+            Ke[i, j] = s
+    # cell coordinates (x first), flattened z-major like kappa
+    cc = np.indices(cells[::-1]).reshape(dim, -1)[::-1]
+    kap = kappa.reshape(-1)
+    strides = np.cumprod((1,) + dims[:-1])
+    rows_l, cols_l, vals_l = [], [], []
+    for i, ci in enumerate(corners):
+        # interior node index of corner ci of every cell (full coord - 1)
+        ok_i = np.ones(cc.shape[1], dtype=bool)
+        node_i = np.zeros(cc.shape[1], dtype=np.int64)
+        for a in range(dim):
+            q = cc[a] + ci[a] - 1
+            ok_i &= (q >= 0) & (q < dims[a])
+            node_i += q * strides[a]
+        for j, cj in enumerate(corners):
+            ok = ok_i.copy()
+            node_j = np.zeros(cc.shape[1], dtype=np.int64)
+            for a in range(dim):
+                q = cc[a] + cj[a] - 1
+                ok &= (q >= 0) & (q < dims[a])
+                node_j += q * strides[a]
+            rows_l.append(node_i[ok])
+            cols_l.append(node_j[ok])
+            vals_l.append(kap[ok] * Ke[i, j])
+    rows = np.concatenate(rows_l)
+    cols = np.concatenate(cols_l)
+    vals = np.concatenate(vals_l)
+    n = int(np.prod(dims))
+    key = rows * n + cols
+    order = np.argsort(key, kind="stable")
+    key, vals = key[order], vals[order]
+    first = np.ones(len(key), dtype=bool)
+    first[1:] = key[1:] != key[:-1]
+    starts = np.flatnonzero(first)
+    summed = np.add.reduceat(vals, starts)
+    ukey = key[starts]
+    r, c = ukey // n, ukey % n
+    offs = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=offs[1:])
+    return Csr(n, n, offs, c.astype(np.int64), summed)

@@ -229,3 +229,21 @@ def test_device_order_oracle_restates_the_numpy_oracle(dims, conv):
     assert st0 == 1 and len(h0) > len(h)
     _, hz, stz, n0z, _ = devorder.bicgstab_devorder(A, M, np.zeros(A.nrows), 1e-10, 10, 2)
     assert stz == 1 and n0z == 0.0 and len(hz) == 0
+
+
+@pytest.mark.parametrize("dims", [(7, 6), (6, 5, 4)])
+def test_element_assembly_with_unit_coefficient_is_the_q1_stencil(dims):
+    """The variable-coefficient generator (oracle.problems.q1_element_assembly)
+    with kappa == 1 reproduces the constant Q1 stencil bit for bit; a random
+    kappa keeps the pattern and symmetry."""
+    from oracle.problems import q1_element_assembly
+    cells = tuple(d + 1 for d in dims)[::-1]
+    A = q1_element_assembly(dims, np.ones(cells))
+    B = oracle.stencil_csr(dims, *oracle.q1_stencil(len(dims)))
+    assert np.array_equal(A.row_offsets, B.row_offsets)
+    assert np.array_equal(A.col_indices, B.col_indices)
+    assert np.array_equal(A.values, B.values)
+    K = q1_element_assembly(dims, np.random.default_rng(1).uniform(0.1, 10.0, cells))
+    assert np.array_equal(K.col_indices, B.col_indices)
+    D = K.to_dense()
+    assert np.array_equal(D, D.T) and np.all(np.linalg.eigvalsh(D) > 0)
