@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--variant", default="classic",
                     choices=["classic", "chronopoulos_gear", "pipelined"],
                     help="PCG variant (krylov.py:348-535); the headline is classic")
+    ap.add_argument("--solver", default="cg", choices=("cg", "bicgstab"),
+                    help="cg: configs[2] (3D Q1 Poisson, sym-SPAI(1)+CG, the headline); "
+                         "bicgstab: configs[4] (3D Q1 convection-diffusion, raw "
+                         "SPAI(1)+BiCGStab)")
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=20000)
     ap.add_argument("--no-e2e", action="store_true")
@@ -694,10 +698,180 @@ def _advanced(rec):
     return int(getattr(rec, "launched_iterations", rec.iterations))
 
 
+CD_CONV = (1.0, 0.5, 0.25)      # constant b = (1, 0.5, 0.25)
+
+
+def run_bicgstab(args):
+    """configs[4]: 3D convection-diffusion Q1 N^3, raw SPAI(1) + right-
+    preconditioned BiCGStab (K9 on one GPU; DistributedBiCGStab over a z-slab
+    row partition with NCCL halos and rank-tree reductions for N > 1).  One
+    step = SPAI(1) assembly (transpose, CSC values, assembly, CSR scatter)
+    + BiCGStab to tol on inputs in HBM."""
+    import torch
+    import torch.distributed as dist
+    import paper_1911_01492_b200 as pb
+    from paper_1911_01492_b200.sparse import DeviceCsr
+    from paper_1911_01492_b200.distributed import (DistributedBiCGStab, GpuBackend, RankSetup,
+                                                   SlabPartition, TorchComm)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+        dist.barrier()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    N = args.grid
+    dims = (N, N, N)
+    n = N ** 3
+    table, stored = pb.q1_stencil(3, conv=CD_CONV)
+    with torch.cuda.stream(stream):
+        if world == 1:
+            A = pb.q1_device(dims, conv=CD_CONV)
+            b = A.matvec(torch.ones(n, dtype=torch.float64, device=dev))
+            n_own = n
+        else:
+            part = SlabPartition(N, N * N, world)
+            rs = RankSetup(dims, table, stored, part, rank, "global", symmetric_spai=False)
+            comm, be = TorchComm(), GpuBackend(dev)
+            n_own = rs.n_own
+    stream.synchronize()
+
+    def step():
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        if world == 1:
+            A2 = DeviceCsr(n, n, A.rowptr, A.colidx, A.vals)       # no cached CSC
+            M = pb.spai1_device(A2)
+            e1.record(stream)
+            x, rec = pb.bicgstab(pb.LocalSystem(A2, pb.SparseMatrixPreconditioner(M)), b,
+                                 tol=args.tol, maxit=args.maxit)
+        else:
+            M = rs.preconditioner()
+            e1.record(stream)
+            x, rec = DistributedBiCGStab(rs.system(M, symmetric=False), comm, be, tol=args.tol,
+                                         maxit=args.maxit, chunk=32).solve()
+        e2.record(stream)
+        e2.synchronize()
+        step.x, step.M = x, M
+        return e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3, rec
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        barrier()
+        times = []
+        with Clocks(local) as clk:
+            ts, te = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ts.record(stream)
+            for _ in range(args.steps):
+                times.append(step())
+            te.record(stream)
+            te.synchronize()
+        barrier()
+    total_s = ts.elapsed_time(te) / 1e3
+    asm = max(t[0] for t in times)
+    if world > 1:
+        t = torch.tensor([total_s, asm], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s, asm = float(t[0]), float(t[1])
+    rec = times[-1][2]
+    its = rec.iterations
+    value = sum(n * t[2].iterations for t in times) / total_s
+    t_sol = statistics.mean(t[1] for t in times)
+    hbm, peak_kind = peaks()
+    # bytes per BiCGStab iteration on this rank (SELL operators, krylov2.cu /
+    # dbicg.cu op sequence): 2 x A + 2 x M streams of 8 B per stored value,
+    # plus the vectors (x gathers, writes, updates) = 200 B per row
+    with torch.cuda.stream(stream):
+        if world == 1:
+            nv = A.sell_stats()[0] + step.M.sell_stats()[0]
+        else:
+            sysr = rs.system(step.M, symmetric=False)
+            nv = sysr.A.sell_stats()[0] + sysr.M.sell_stats()[0]
+    b_it = 16 * nv + 200 * n_own
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        with torch.cuda.stream(stream):
+            h = [A.rowptr.cpu().pin_memory(), A.colidx.cpu().pin_memory(),
+                 A.vals.cpu().pin_memory(), b.cpu().pin_memory()]
+            h_x = torch.empty(n, dtype=torch.float64).pin_memory()
+            barrier()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, min(args.steps, 3))
+            work = 0
+            ea.record(stream)
+            for _ in range(reps):
+                d = [t.to(dev, non_blocking=True) for t in h]
+                Ad = DeviceCsr(n, n, d[0], d[1], d[2])
+                Md = pb.spai1_device(Ad)
+                xe, re_ = pb.bicgstab(pb.LocalSystem(Ad, pb.SparseMatrixPreconditioner(Md)), d[3],
+                                      tol=args.tol, maxit=args.maxit)
+                h_x.copy_(xe, non_blocking=True)
+                work += n * re_.iterations
+                del Ad, Md, d
+            eb.record(stream)
+            eb.synchronize()
+            e_t = ea.elapsed_time(eb) / 1e3
+            e2e = {"value": work / e_t, "unit": UNIT, "steps": reps,
+                   "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in h),
+                   "d2h_bytes_per_step": n * 8}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_s / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"configs[4]: 3D convection-diffusion Q1 {N}^3 ({n} DOF), "
+                                   f"b=(1,0.5,0.25), raw SPAI(1)+BiCGStab (right), b=A*1, "
+                                   f"x0=0, tol {args.tol}",
+                       "n_dof": n, "iterations": its,
+                       "parallelism": f"rows x{world} (z-slabs, {dist.get_backend()})"
+                                      if world > 1 else "single GPU",
+                       "spai_scope": "global",
+                       "l2": "inputs far larger than the 126 MB L2"},
+            "assembly": {"ms_max_rank": asm * 1e3, "cols_per_s": n / asm},
+            "solve": {"ms": t_sol * 1e3, "iterations": its, "dof_it_per_s": n * its / t_sol,
+                      "ms_per_iteration": t_sol / max(its, 1) * 1e3},
+            "roofline": {"bound": "hbm", "kernel": "BiCGStab iteration (rank 0)",
+                         "achieved": b_it * its / t_sol / 1e9, "peak": hbm,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": b_it * its / t_sol / 1e9 / hbm, "traffic": None,
+                         "algorithmic_bytes_per_iteration": b_it},
+            "clocks": clk.summary(),
+            # our kernels per step (ncu launch list, profiles/r02_launches_bicg64.txt):
+            # one GPU: transpose, CSC values, classes, signatures, plans, replay,
+            # CSC->CSR, SELL layout (analyze, 2 scans x 2, structure, 2 value
+            # fills), half-storage probe of A (3), start = 20, then 7 per
+            # launched iteration; N > 1: 10 per launched iteration (3 updates,
+            # 4 SpMV, 3 reduction steps) + the rank's assembly (~14)
+            "gpu_launches": sum((20 + 7 * t[2].launched_iterations) if world == 1 else
+                                (14 + 10 * t[2].launched_iterations) for t in times),
+            "e2e": e2e,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.solver == "bicgstab":
+        run_bicgstab(args)
     else:
         run_ours(args)
 

@@ -405,6 +405,33 @@ int spai_dist_spmv_split_st(int mode, int64_t n, int64_t ncols, const int64_t* s
                             const double* hadd, const double* xext, int64_t own_off,
                             double* y, const double* raux, void* partials_ws, double* out,
                             const int* status, void* stream);
+/* Blocks of the SELL dist SpMV for n owned rows (its reduction order).    */
+int spai_dist_grid(int64_t n);
+/* Row-partitioned right-preconditioned BiCGStab (configs[4]; the reference
+ * has none, SPEC.md:343 -- the K9 iteration on owned rows).  dist_spmv modes
+ * 7 (v = A ph, [(r^,v)], r^ = raux) and 8 (t = A sh, [(t,s),(t,t)], s = raux)
+ * produce the fused partials; start/update_xr produce [(b,b)] / [(r^,r),(r,r)]
+ * with the same grid; step(stage 0 start, 1 alpha, 2 omega, 3 final) sums
+ * the all-gathered partials in commsim's ascending-rank tree
+ * (commsim.py:336-347) and runs the scalar recurrence on the device.
+ * status: 0 running, 1 converged, 2 maxit, 3 breakdown (kind as K9), 4
+ * divergence.                                                              */
+size_t spai_dbicg_scal_bytes(void);
+int spai_dbicg_scal_init(void* scal, double tol, int64_t maxit, void* stream);
+void* spai_dbicg_status_ptr(void* scal);
+int spai_dbicg_read(const void* scal, int* status, int64_t* it, double* norm0, double* norm,
+                    int* kind, void* stream);
+int spai_dbicg_start(int64_t n, const double* b, double* x, double* r, double* rh, double* p,
+                     double* v, void* partials_ws, double* out, void* stream);
+int spai_dbicg_step(int stage, int nranks, const double* gathered, void* scal, double* hist,
+                    void* stream);
+int spai_dbicg_update_p(int64_t n, double* p, const double* r, const double* v,
+                        const void* scal, void* stream);
+int spai_dbicg_update_s(int64_t n, double* s, const double* r, const double* v,
+                        const void* scal, void* stream);
+int spai_dbicg_update_xr(int64_t n, double* x, double* r, const double* s, const double* t,
+                         const double* ph, const double* sh, const double* rh,
+                         const void* scal, void* partials_ws, double* out, void* stream);
 /* Row-partitioned Chronopoulos-Gear / pipelined CG (DistributedCGV): the
  * scalar state is a K10 VScal; variant 1 = chronopoulos_gear, 3 = pipelined */
 size_t spai_dcgv_scal_bytes(void);

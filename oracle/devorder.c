@@ -199,17 +199,45 @@ typedef struct {
   int G;
   double* acc;      /* [G * NT] per-thread accumulators of one product */
   double* part;     /* [G] */
+  /* row partition (multi-rank): rank k owns rows [split[k], split[k+1]) and
+   * reduces them with grid[k] blocks; ranks combine in commsim's tree */
+  int nranks;
+  const int64_t* split;
+  const int* grid;
 } Red;
 
 static void red_init(Red* R, int G) {
   R->G = G;
   R->acc = (double*)malloc(sizeof(double) * (size_t)G * NT);
   R->part = (double*)malloc(sizeof(double) * (size_t)G);
+  R->nranks = 0;
 }
 static void red_free(Red* R) { free(R->acc); free(R->part); }
 
-/* sum_i a[i] * b[i] in the device order (fma chains per thread) */
+static double dev_dot1(Red* R, int64_t n, const double* a, const double* b);
+
+/* sum_i a[i] * b[i] in the device order: per rank the blocked fma-chain sum,
+ * then the ascending-rank pairwise tree (commsim.py:336-347) */
 static double dev_dot(Red* R, int64_t n, const double* a, const double* b) {
+  if (R->nranks <= 0) return dev_dot1(R, n, a, b);
+  double buf[64];
+  int m = R->nranks;
+  for (int k = 0; k < m; ++k) {
+    Red Rk;
+    red_init(&Rk, R->grid[k]);
+    const int64_t lo = R->split[k], hi = R->split[k + 1];
+    buf[k] = hi > lo ? dev_dot1(&Rk, hi - lo, a + lo, b + lo) : 0.0;
+    red_free(&Rk);
+  }
+  while (m > 1) {
+    int o = 0;
+    for (int i = 0; i < m; i += 2) buf[o++] = (i + 1 < m) ? buf[i] + buf[i + 1] : buf[i];
+    m = o;
+  }
+  return buf[0];
+}
+
+static double dev_dot1(Red* R, int64_t n, const double* a, const double* b) {
   const int64_t nthreads = (int64_t)R->G * NT;
   memset(R->acc, 0, sizeof(double) * (size_t)nthreads);
   for (int64_t i = 0; i < n; ++i) {
@@ -231,7 +259,8 @@ static double dev_dot(Red* R, int64_t n, const double* a, const double* b) {
 int oracle_bicgstab_devorder(int64_t n, const int64_t* a_ptr, const int32_t* a_col,
                              const double* a_val, const int64_t* m_ptr, const int32_t* m_col,
                              const double* m_val, const double* b, double tol, int64_t maxit,
-                             int grid, double* x, double* hist, int64_t* iters, double* norm0_out,
+                             int grid, int nranks, const int64_t* split, const int* grids,
+                             double* x, double* hist, int64_t* iters, double* norm0_out,
                              int* kind_out) {
   Sell A, M;
   sell_build(&A, n, a_ptr, a_col, a_val);
@@ -239,6 +268,9 @@ int oracle_bicgstab_devorder(int64_t n, const int64_t* a_ptr, const int32_t* a_c
   if (hasM) sell_build(&M, n, m_ptr, m_col, m_val);
   Red R;
   red_init(&R, grid);
+  R.nranks = nranks;
+  R.split = split;
+  R.grid = grids;
   double *r = malloc(8 * n), *rh = malloc(8 * n), *p = calloc(n, 8), *v = calloc(n, 8),
          *s = malloc(8 * n), *t = malloc(8 * n), *ph = malloc(8 * n), *sh = malloc(8 * n);
   for (int64_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; rh[i] = b[i]; }

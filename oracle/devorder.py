@@ -39,8 +39,8 @@ def _load():
         vp, i64, dbl, i32 = C.c_void_p, C.c_int64, C.c_double, C.c_int
         _lib.oracle_bicgstab_devorder.restype = i32
         _lib.oracle_bicgstab_devorder.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp, dbl, i64, i32,
-                                                  vp, vp, C.POINTER(i64), C.POINTER(dbl),
-                                                  C.POINTER(i32)]
+                                                  i32, vp, vp, vp, vp, C.POINTER(i64),
+                                                  C.POINTER(dbl), C.POINTER(i32)]
         _lib.oracle_richardson_devorder.restype = i32
         _lib.oracle_richardson_devorder.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp, dbl, dbl, i32,
                                                     i64, i32, vp, vp, C.POINTER(i64),
@@ -57,8 +57,14 @@ def _arrays(A):
     return keep, tuple(k.ctypes.data for k in keep)
 
 
-def bicgstab_devorder(A, M, b, tol, maxit, grid):
-    """-> (x, history, status, norm0, breakdown kind); status as spai_ksolver_poll."""
+def bicgstab_devorder(A, M, b, tol, maxit, grid, ranks=None):
+    """-> (x, history, status, norm0, breakdown kind); status as spai_ksolver_poll.
+
+    ranks: None (one device, `grid` blocks) or [(row0, row1, grid_k), ...]
+    for the row-partitioned solver (DistributedBiCGStab): every dot is the
+    per-rank blocked sum, combined in commsim's ascending-rank tree.  The
+    SpMV rows are the single-device ones (the per-rank SELL slices are the
+    global slices when the rank boundaries are multiples of 32 rows)."""
     lib = _load()
     ka, pa = _arrays(A)
     km, pm = _arrays(M)
@@ -67,10 +73,17 @@ def bicgstab_devorder(A, M, b, tol, maxit, grid):
     x = np.zeros(n)
     hist = np.zeros(max(int(maxit), 1))
     its, n0, kind = C.c_int64(0), C.c_double(0), C.c_int(0)
+    if ranks:
+        split = np.array([r[0] for r in ranks] + [ranks[-1][1]], dtype=np.int64)
+        grids = np.array([r[2] for r in ranks], dtype=np.int32)
+        nr, sp, gp = len(ranks), split.ctypes.data, grids.ctypes.data
+    else:
+        split = grids = None
+        nr, sp, gp = 0, None, None
     st = lib.oracle_bicgstab_devorder(n, *pa, *pm, b.ctypes.data, float(tol), int(maxit),
-                                      int(grid), x.ctypes.data, hist.ctypes.data, C.byref(its),
-                                      C.byref(n0), C.byref(kind))
-    del ka, km
+                                      int(grid), nr, sp, gp, x.ctypes.data, hist.ctypes.data,
+                                      C.byref(its), C.byref(n0), C.byref(kind))
+    del ka, km, split, grids
     return x, hist[: its.value].copy(), st, n0.value, kind.value
 
 

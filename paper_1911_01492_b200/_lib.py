@@ -88,6 +88,18 @@ _SIGS = {
                                      _vp, _vp, _vp, _vp]),
     "spai_dist_spmv_split_st": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
                                        _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dist_grid": (_i32, [_i64]),
+    "spai_dbicg_scal_bytes": (_sz, []),
+    "spai_dbicg_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),
+    "spai_dbicg_status_ptr": (_vp, [_vp]),
+    "spai_dbicg_read": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),
+                               C.POINTER(_dbl), C.POINTER(_i32), _vp]),
+    "spai_dbicg_start": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dbicg_step": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp]),
+    "spai_dbicg_update_p": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dbicg_update_s": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "spai_dbicg_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp]),
     "spai_dcgv_scal_bytes": (_sz, []),
     "spai_dcgv_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),
     "spai_dcgv_status_ptr": (_vp, [_vp]),

@@ -34,7 +34,7 @@ dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
                  const double* __restrict__ raux, double* partials, unsigned int* ticket,
                  double* out, const int* status, const double* __restrict__ hadd) {
   if (MODE != 0 && *status != dRunning) return;
-  constexpr int K = (MODE == 1 || MODE >= 5) ? 3 : (MODE == 2 ? 1 : 2);
+  constexpr int K = (MODE == 1 || MODE == 5 || MODE == 6) ? 3 : ((MODE == 2 || MODE == 7) ? 1 : 2);
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
@@ -70,6 +70,11 @@ dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
         acc[0] = fma(xi, ri, acc[0]);
         acc[1] = fma(xi, v, acc[1]);
         acc[2] = fma(ri, ri, acc[2]);
+      } else if (MODE == 7) {            // BiCGStab v = A ph, [(r^, v)] (r^ = raux)
+        acc[0] = fma(raux[i], v, acc[0]);
+      } else if (MODE == 8) {            // BiCGStab t = A sh, [(t, s), (t, t)] (s = raux)
+        acc[0] = fma(v, raux[i], acc[0]);
+        acc[1] = fma(v, v, acc[1]);
       } else if (MODE >= 3) {
         acc[0] = fma(v, xi, acc[0]);
         acc[1] = fma(xi, xi, acc[1]);
@@ -181,6 +186,8 @@ static int dist_launch(int mode, unsigned b, int64_t n, int64_t s0, int64_t s1, 
     case 4: dist_spmv_kernel<4, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
     case 5: dist_spmv_kernel<5, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
     case 6: dist_spmv_kernel<6, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 7: dist_spmv_kernel<7, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 8: dist_spmv_kernel<8, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
     default: set_error("bad dist_spmv mode %d", mode); return SPAI_E_ARG;
   }
   SPAI_LAUNCH_CHECK("dist_spmv_kernel");
@@ -222,6 +229,15 @@ extern "C" void* spai_dist_status_ptr(void* scal) { return &((DistScal*)scal)->s
 
 extern "C" size_t spai_dist_partials_bytes(void) {
   return 256 + (size_t)num_sms() * 32 * 3 * sizeof(double);
+}
+
+// Blocks of the SELL dist SpMV for n owned rows (fixes its dot order; the
+// BiCGStab update kernel launches the same grid so all its reductions match).
+extern "C" int spai_dist_grid(int64_t n) {
+  const int64_t ns = (n + kSell - 1) / kSell;
+  static unsigned blocks = 0;
+  if (!blocks) blocks = sell_blocks((const void*)dist_spmv_kernel<1, SellOp>, 1 << 30);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (ns * 32 + 255) / 256));
 }
 
 extern "C" int spai_dist_spmv_st(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,

@@ -304,6 +304,45 @@ class GpuBackend:
         _lib.check(self.lib.spai_dist_reduce_step(nranks, _p(gathered), K, stage, _p(scal),
                                                   _p(hist), self._s()), "spai_dist_reduce_step")
 
+    # -- row-partitioned BiCGStab (csrc/dbicg.cu)
+    def dbicg_scal(self, tol, maxit):
+        t = self.torch.empty(self.lib.spai_dbicg_scal_bytes(), dtype=self.torch.uint8,
+                             device=self.dev)
+        _lib.check(self.lib.spai_dbicg_scal_init(_p(t), float(tol), int(maxit), self._s()),
+                   "spai_dbicg_scal_init")
+        return t
+
+    def dbicg_status(self, scal):
+        return self.lib.spai_dbicg_status_ptr(_p(scal))
+
+    def dbicg_read(self, scal):
+        st, it, n0, nr, kind = C.c_int(0), C.c_int64(0), C.c_double(0), C.c_double(0), C.c_int(0)
+        _lib.check(self.lib.spai_dbicg_read(_p(scal), C.byref(st), C.byref(it), C.byref(n0),
+                                            C.byref(nr), C.byref(kind), self._s()),
+                   "spai_dbicg_read")
+        return st.value, it.value, n0.value, nr.value, kind.value
+
+    def dbicg_start(self, b, x, r, rh, p, v, ws, out):
+        _lib.check(self.lib.spai_dbicg_start(x.numel(), _p(b), _p(x), _p(r), _p(rh), _p(p), _p(v),
+                                             _p(ws), _p(out), self._s()), "spai_dbicg_start")
+
+    def dbicg_step(self, stage, nranks, gathered, scal, hist):
+        _lib.check(self.lib.spai_dbicg_step(stage, nranks, _p(gathered), _p(scal), _p(hist),
+                                            self._s()), "spai_dbicg_step")
+
+    def dbicg_update_p(self, p, r, v, scal):
+        _lib.check(self.lib.spai_dbicg_update_p(p.numel(), _p(p), _p(r), _p(v), _p(scal),
+                                                self._s()), "spai_dbicg_update_p")
+
+    def dbicg_update_s(self, s, r, v, scal):
+        _lib.check(self.lib.spai_dbicg_update_s(s.numel(), _p(s), _p(r), _p(v), _p(scal),
+                                                self._s()), "spai_dbicg_update_s")
+
+    def dbicg_update_xr(self, x, r, s, t, ph, sh, rh, scal, ws, out):
+        _lib.check(self.lib.spai_dbicg_update_xr(x.numel(), _p(x), _p(r), _p(s), _p(t), _p(ph),
+                                                 _p(sh), _p(rh), _p(scal), _p(ws), _p(out),
+                                                 self._s()), "spai_dbicg_update_xr")
+
 
 def _p(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
@@ -556,6 +595,113 @@ class DistributedCGV:
         return self._own("x"), rec
 
 
+class DistributedBiCGStab:
+    """Row-partitioned right-preconditioned BiCGStab (configs[4]): the K9
+    iteration (krylov2.cu; oracle/krylov.py bicgstab_right -- the reference
+    has no BiCGStab) on each rank's owned rows, with a halo of
+    p, ph, s and sh before every SpMV (commsim.py:588-596) and three fused
+    reductions per iteration, each an all-gather of per-rank partials summed
+    on the device in the ascending-rank tree (commsim.py:336-347).  M is the
+    raw (nonsymmetric) SPAI(1) on the rank's rows, or None."""
+
+    def __init__(self, system: LocalRankSystem, comm, backend, tol=1e-8, maxit=1000,
+                 chunk=16):
+        self.sys, self.comm, self.be = system, comm, backend
+        self.tol, self.maxit, self.chunk = tol, int(maxit), int(chunk)
+        be = backend
+        n, ne = system.n_own, system.n_ext
+        self.ext = {k: be.zeros(ne) for k in ("p", "ph", "s", "sh")}
+        self.own_v = {k: be.zeros(n) for k in ("x", "r", "rh", "v", "t")}
+        self.out = be.zeros(3)
+        self.gathered = be.zeros(3 * comm.size)
+        self.hist = be.zeros(self.maxit)
+        self.ws = be.partials()
+        self.scal = be.dbicg_scal(tol, self.maxit)
+        self.status = be.dbicg_status(self.scal)
+        self.launched = 0
+
+    def _own(self, name):
+        if name in self.own_v:
+            return self.own_v[name]
+        return self.ext[name][self.sys.hlo:self.sys.hlo + self.sys.n_own]
+
+    def _halo(self, name):
+        s = self.sys
+        self.comm.halo(self.ext[name], s.hlo, s.n_own, s.hlo, s.hhi)
+
+    def _precond(self, src, dst):
+        """dst(owned) = M src (src's halo exchanged first)."""
+        s = self.sys
+        M = s.M_op or s.M
+        if M is None:
+            self._own(dst).copy_(self._own(src))
+            return
+        self._halo(src)
+        self.be.spmv_st(0, M, self.ext[src], s.hlo, self._own(dst), None, self.ws, self.out,
+                        self.status)
+
+    def _reduce(self, K, stage):
+        c = self.comm
+        c.allgather(self.out[:K], self.gathered[:K * c.size])
+        self.be.dbicg_step(stage, c.size, self.gathered, self.scal, self.hist)
+
+    def start(self):
+        o = self._own
+        self.be.dbicg_start(self.sys.b, o("x"), o("r"), o("rh"), o("p"), o("v"), self.ws,
+                            self.out)
+        self._reduce(1, 0)
+
+    def iteration(self):
+        s, be, o = self.sys, self.be, self._own
+        A = s.A_op or s.A
+        be.dbicg_update_p(o("p"), o("r"), o("v"), self.scal)
+        self._precond("p", "ph")
+        self._halo("ph")
+        be.spmv_st(7, A, self.ext["ph"], s.hlo, o("v"), o("rh"), self.ws, self.out, self.status)
+        self._reduce(1, 1)
+        be.dbicg_update_s(o("s"), o("r"), o("v"), self.scal)
+        self._precond("s", "sh")
+        self._halo("sh")
+        be.spmv_st(8, A, self.ext["sh"], s.hlo, o("t"), o("s"), self.ws, self.out, self.status)
+        self._reduce(2, 2)
+        be.dbicg_update_xr(o("x"), o("r"), o("s"), o("t"), o("ph"), o("sh"), o("rh"),
+                           self.scal, self.ws, self.out)
+        self._reduce(2, 3)
+        self.launched += 1
+
+    def run(self):
+        self.start()
+        st = self.be.dbicg_read(self.scal)
+        done = 0
+        while st[0] == 0 and done < self.maxit:
+            for _ in range(min(self.chunk, self.maxit - done)):
+                self.iteration()
+                done += 1
+            st = self.be.dbicg_read(self.scal)
+        return st
+
+    def solve(self):
+        """(x_owned, ConvergenceRecord) with K9 / bicgstab_right semantics."""
+        from .krylov import _BREAKDOWN_MSG
+        status, it, norm0, norm, kind = self.run()
+        if status == 3:
+            raise BreakdownError(_BREAKDOWN_MSG.get(kind, "breakdown"))
+        if status == 4:
+            raise DivergenceError("non-finite value in solver recurrence")
+        rec = ConvergenceRecord(variant="bicgstab")
+        rec.initial_residual = norm0
+        rec.iterations = it
+        h = self.hist[:it].cpu().numpy() if it > 0 else np.zeros(0)
+        rec.residual_norms = [float(v) for v in h]
+        rec.reductions_cum = [1 + 3 * (i + 1) for i in range(it)]
+        rec.overlapped_cum = [0] * it
+        rec.total_reductions = 1 + 3 * it
+        rec.converged = status == 1
+        rec.final_residual = norm if it > 0 else norm0
+        rec.launched_iterations = self.launched
+        return self._own("x"), rec
+
+
 # ------------------------------------------------------------------ local operators
 def _rebase(dcsr, row0, row1, col0, ncols_ext):
     """Rows [row0,row1) of a DeviceCsr with columns shifted by -col0 (device ops)."""
@@ -571,19 +717,22 @@ def _rebase(dcsr, row0, row1, col0, ncols_ext):
 
 
 def q1_rank_system(dims, part: SlabPartition, rank: int, spai_scope="global", eps=None,
-                   conv=None, h=1.0, precondition=True):
+                   conv=None, h=1.0, precondition=True, symmetric_spai=True):
     """Rank-local operators of the Q1 matrix on `dims` (x fastest, slabs along the
-    last axis), generated directly on this GPU.  b = A 1 restricted to the rank."""
+    last axis), generated directly on this GPU.  b = A 1 restricted to the rank.
+    symmetric_spai=False keeps the raw SPAI(1) M (non-CG solvers)."""
     from .grids import q1_stencil
     table, stored = q1_stencil(len(dims), eps, conv, h)
-    return stencil_rank_system(dims, table, stored, part, rank, spai_scope, precondition)
+    return stencil_rank_system(dims, table, stored, part, rank, spai_scope, precondition,
+                               symmetric_spai)
 
 
 def stencil_rank_system(dims, table, stored, part: SlabPartition, rank: int,
-                        spai_scope="global", precondition=True):
+                        spai_scope="global", precondition=True, symmetric_spai=True):
     """Rank-local operators of a 3^d box-stencil matrix (see grids.stencil_device)."""
-    rs = RankSetup(dims, table, stored, part, rank, spai_scope)
-    return rs.system(rs.preconditioner() if precondition else None)
+    rs = RankSetup(dims, table, stored, part, rank, spai_scope, symmetric_spai)
+    return rs.system(rs.preconditioner() if precondition else None,
+                     symmetric=symmetric_spai)
 
 
 class RankSetup:
@@ -593,9 +742,10 @@ class RankSetup:
     runs transpose + assembly + symmetrisation on the device."""
 
     def __init__(self, dims, table, stored, part: SlabPartition, rank: int,
-                 spai_scope="global"):
+                 spai_scope="global", symmetric_spai=True):
         import torch
         from .grids import stencil_device
+        self.symmetric_spai = bool(symmetric_spai)
         self.dims = tuple(int(d) for d in dims)
         self.table, self.stored, self.part, self.rank = table, stored, part, rank
         self.scope = spai_scope
@@ -631,6 +781,18 @@ class RankSetup:
         from .precond import spai1_symmetric_device
         from .sparse import DeviceCsr
         plane = self.plane
+        if self.scope == "global" and not self.symmetric_spai:
+            # raw M (BiCGStab / Richardson): the owned rows of M
+            # need the columns of the slab +- 1 plane, assembled exactly on
+            # the 3-ghost-plane copy (a column's problem reaches 2 planes)
+            A3 = self.A_spai
+            A3 = DeviceCsr(A3.nrows, A3.ncols, A3.rowptr, A3.colidx, A3.vals)
+            M3 = _raw_range(A3, (self.e0 - self.g0) * plane, (self.e1 - self.g0) * plane,
+                            self.g0 * plane)
+            M = _rebase(M3, (self.z0 - self.g0) * plane, (self.z1 - self.g0) * plane,
+                        (self.e0 - self.g0) * plane, self.n_ext)
+            M._pat = self.A_loc._pat
+            return M
         if self.scope == "global":
             A3 = self.A_spai
             A3 = DeviceCsr(A3.nrows, A3.ncols, A3.rowptr, A3.colidx, A3.vals)   # fresh CSC
@@ -642,6 +804,10 @@ class RankSetup:
                                     self.A_ext)
             return M
         Aff = self.A_spai
+        if not self.symmetric_spai:
+            from .precond import spai1_device
+            Mff = spai1_device(DeviceCsr(Aff.nrows, Aff.ncols, Aff.rowptr, Aff.colidx, Aff.vals))
+            return _rebase(Mff, 0, Mff.nrows, -self.hlo, self.n_ext)
         Sff = spai1_symmetric_device(DeviceCsr(Aff.nrows, Aff.ncols, Aff.rowptr, Aff.colidx,
                                                Aff.vals))
         return _rebase(Sff, 0, Sff.nrows, -self.hlo, self.n_ext)
@@ -693,6 +859,41 @@ def _principal(S, a, b, like):
     if sub_cols.numel() != like.nnz or not torch.equal(sub_cols, like.colidx):
         return None
     return like.with_values(S.vals[lo:hi][keep].contiguous())
+
+
+def _assemble_range(A, c0, c1, col_base=0):
+    """M's columns [c0, c1) of pattern(A) in CSC order (others 0); a rank
+    deficient column raises with its global index (col_base + local)."""
+    import torch
+    from .sparse import ptr, stream_handle
+    from .precond import _raise_assembly
+    lib = _lib.load()
+    cscptr, cscrow, csc2csr = A.csc()
+    cscval = A.csc_values()
+    m_csc = torch.zeros(A.nnz, dtype=torch.float64, device=A.vals.device)
+    wsb = lib.spai_assemble_workspace_bytes(A.nrows)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=A.vals.device)
+    bad, nfb = C.c_int64(-1), C.c_int64(0)
+    st = lib.spai_assemble_range(A.nrows, A.nnz, ptr(A.rowptr), ptr(A.colidx), ptr(A.vals),
+                                 ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(cscval), c0, c1,
+                                 ptr(m_csc), ptr(ws), wsb, C.byref(bad), C.byref(nfb),
+                                 stream_handle())
+    _lib.check(st, "spai_assemble_range")
+    if st != _lib.SPAI_OK:
+        _raise_assembly(st, col_base + bad.value)
+    return m_csc, csc2csr
+
+
+def _raw_range(A, c0, c1, col_base=0):
+    """SPAI(1) M (not symmetrised) on pattern(A), CSR values, columns [c0, c1)
+    assembled (rows whose couplings stay inside the range are exact)."""
+    import torch
+    from .sparse import ptr, stream_handle
+    m_csc, csc2csr = _assemble_range(A, c0, c1, col_base)
+    vals = torch.empty_like(m_csc)
+    _lib.check(_lib.load().spai_csc_to_csr_values(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals),
+                                                  stream_handle()), "spai_csc_to_csr_values")
+    return A.with_values(vals)
 
 
 def _symmetric_range(A, c0, c1):

@@ -170,3 +170,131 @@ def fd5_rank_system(nx, ny, part, rank, block_local=True):
     M_loc = HostCsr(Sff.nrows, Sff.ncols, Sff.row_offsets, Sff.col_indices, Sff.values)
     M_loc.apply = lambda xe, M=M_loc: oracle.spmv(M.c, xe[hlo:hlo + Sff.nrows])
     return LocalRankSystem(r1 - r0, hlo, hhi, A_loc, M_loc, torch.from_numpy(b.copy()))
+
+
+class NumpyBiCGBackend(NumpyBackend):
+    """CPU double of the row-partitioned BiCGStab kernels (csrc/dbicg.cu and
+    dist_spmv modes 0 / 7 / 8): the K9 iteration in NumPy on each rank."""
+
+    def dbicg_scal(self, tol, maxit):
+        return {"rho": 0.0, "rho_old": 1.0, "alpha": 1.0, "omega": 1.0, "norm0": float("nan"),
+                "norm": float("inf"), "tol": tol, "it": 0, "maxit": maxit, "status": 0,
+                "kind": 0}
+
+    def dbicg_status(self, sc):
+        return sc
+
+    def dbicg_read(self, sc):
+        return sc["status"], sc["it"], sc["norm0"], sc["norm"], sc["kind"]
+
+    def spmv_st(self, mode, M, xext, own_off, y, raux, ws, out, sc):
+        if mode != 0 and sc["status"] != 0:
+            return
+        xe = xext.numpy()
+        v = M.apply(xe)
+        y.copy_(torch.from_numpy(v))
+        if mode == 7:
+            out[0] = float(np.dot(raux.numpy(), v))
+        elif mode == 8:
+            s = raux.numpy()
+            out[:2] = torch.tensor([float(np.dot(v, s)), float(np.dot(v, v))],
+                                   dtype=torch.float64)
+
+    def dbicg_start(self, b, x, r, rh, p, v, ws, out):
+        x.zero_()
+        r.copy_(b)
+        rh.copy_(b)
+        p.zero_()
+        v.zero_()
+        out[0] = float(np.dot(b.numpy(), b.numpy()))
+
+    def dbicg_step(self, stage, nranks, gathered, sc, hist):
+        g = gathered.numpy()
+        K = 1 if stage < 2 else 2
+        tot = oracle.tree_sum([np.array(g[r * K:(r + 1) * K]) for r in range(nranks)])
+        if stage == 0:
+            rr0 = float(tot[0])
+            sc.update(norm0=math.sqrt(rr0), rho=rr0, rho_old=1.0, alpha=1.0, omega=1.0, it=0)
+            sc["norm"] = sc["norm0"]
+            if sc["norm0"] == 0.0:
+                sc["status"] = 1
+            elif not math.isfinite(rr0):
+                sc["status"] = 4
+            return
+        if sc["status"] != 0:
+            return
+        if stage == 1:
+            rv = float(tot[0])
+            if not math.isfinite(rv):
+                sc["status"] = 4
+            elif rv == 0.0:
+                sc["status"], sc["kind"] = 3, 2
+            else:
+                sc["alpha"] = sc["rho"] / rv
+        elif stage == 2:
+            ts, tt = float(tot[0]), float(tot[1])
+            if not (math.isfinite(ts) and math.isfinite(tt)):
+                sc["status"] = 4
+            elif tt == 0.0:
+                sc["status"], sc["kind"] = 3, 3
+            else:
+                sc["omega"] = ts / tt
+        else:
+            rho, rr = float(tot[0]), float(tot[1])
+            if not (math.isfinite(rho) and math.isfinite(rr)):
+                sc["status"] = 4
+                return
+            sc["rho_old"], sc["rho"] = sc["rho"], rho
+            norm = math.sqrt(rr)
+            sc["it"] += 1
+            hist[sc["it"] - 1] = norm
+            sc["norm"] = norm
+            if sc["omega"] == 0.0 and norm > sc["tol"] * sc["norm0"]:
+                sc["status"], sc["kind"] = 3, 4
+            elif norm <= sc["tol"] * sc["norm0"]:
+                sc["status"] = 1
+            elif sc["it"] >= sc["maxit"]:
+                sc["status"] = 2
+            elif rho == 0.0:
+                sc["status"], sc["kind"] = 3, 1
+
+    def dbicg_update_p(self, p, r, v, sc):
+        if sc["status"] != 0:
+            return
+        beta = (sc["rho"] / sc["rho_old"]) * (sc["alpha"] / sc["omega"])
+        p.copy_(r + beta * (p - sc["omega"] * v))
+
+    def dbicg_update_s(self, s, r, v, sc):
+        if sc["status"] != 0:
+            return
+        s.copy_(r - sc["alpha"] * v)
+
+    def dbicg_update_xr(self, x, r, s, t, ph, sh, rh, sc, ws, out):
+        if sc["status"] != 0:
+            return
+        x.copy_(x + sc["alpha"] * ph + sc["omega"] * sh)
+        r.copy_(s - sc["omega"] * t)
+        rn = r.numpy()
+        out[:2] = torch.tensor([float(np.dot(rh.numpy(), rn)), float(np.dot(rn, rn))],
+                               dtype=torch.float64)
+
+
+def cd_rank_system(dims, conv, part, rank):
+    """Rank operators of the 2D convection-diffusion Q1 matrix for a
+    row-partitioned BiCGStab: A's owned rows in extended columns and the raw
+    global SPAI(1) M's owned rows (columns of the slab +- 1 plane)."""
+    from paper_1911_01492_b200.distributed import LocalRankSystem
+    A = oracle.stencil_csr(dims, *oracle.q1_stencil(len(dims), conv=conv))
+    M = oracle.spai1(A)
+    r0, r1 = part.rows(rank)
+    hlo, hhi = part.halo(rank)
+    e0 = r0 - hlo
+    ne = hlo + (r1 - r0) + hhi
+
+    def rows(C):
+        lo, hi = C.row_offsets[r0], C.row_offsets[r1]
+        return HostCsr(r1 - r0, ne, C.row_offsets[r0:r1 + 1] - lo, C.col_indices[lo:hi] - e0,
+                       C.values[lo:hi])
+
+    b = oracle.make_rhs_ones(A)[r0:r1]
+    return LocalRankSystem(r1 - r0, hlo, hhi, rows(A), rows(M), torch.from_numpy(b.copy())), A, M

@@ -157,6 +157,19 @@ def _worker(rank, world, port, case, q):
             q.put((rank, r0, r1, x.cpu().numpy(), rec.iterations, list(rec.residual_norms),
                    rec.reductions_cum, rec.overlapped_cum, rec.total_reductions))
             return
+        if case == "bicg_cd":
+            from paper_1911_01492_b200.distributed import DistributedBiCGStab
+            dims, conv = BICG_DIMS, BICG_CONV
+            part = SlabPartition(dims[-1], dims[0] * dims[1], world)
+            sysr = q1_rank_system(dims, part, rank, "global", conv=conv, symmetric_spai=False)
+            x, rec = DistributedBiCGStab(sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                                         maxit=1000).solve()
+            r0, r1 = part.rows(rank)
+            from paper_1911_01492_b200 import _lib
+            q.put((rank, r0, r1, x.cpu().numpy(), rec.iterations, list(rec.residual_norms),
+                   rec.total_reductions, sysr.M.vals.cpu().numpy(), sysr.M.colidx.cpu().numpy(),
+                   sysr.hlo, int(_lib.load().spai_dist_grid(r1 - r0))))
+            return
         if case == "q1_global":
             dims = (20, 18, 16)
             part = SlabPartition(dims[-1], dims[0] * dims[1], world)
@@ -171,6 +184,41 @@ def _worker(rank, world, port, case, q):
         q.put((rank, r0, r1, x.cpu().numpy(), rec.iterations, list(rec.residual_norms)))
     finally:
         dist.destroy_process_group()
+
+
+BICG_DIMS, BICG_CONV = (32, 30, 24), (1.0, 0.5, 0.25)
+
+
+def test_row_partitioned_bicgstab_matches_device_order_oracle():
+    """configs[4] (3D convection-diffusion, raw SPAI(1) + BiCGStab, row
+    partition): each rank's rows of M equal the single-GPU M bit for bit
+    (global scope on the 3-ghost-plane slab, no symmetrisation), and the
+    1- and 2-rank DistributedBiCGStab histories match the oracle restated
+    in the device order with per-rank dots and commsim's rank tree
+    (oracle/devorder.c) over the whole run, <= 1e-8."""
+    from oracle import devorder
+    A = pb.q1_device(BICG_DIMS, conv=BICG_CONV)
+    M = pb.spai1_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    Ah, Mh, bh = A.to_host(), M.to_host(), b.cpu().numpy()
+    for world in (1, 2):
+        out = _run(world, "bicg_cd")
+        its = {o[4] for o in out}
+        assert len(its) == 1
+        ranks = []
+        x = np.zeros(A.nrows)
+        for rank, r0, r1, xr, it, hist, red, mv, mc, hlo, grid in out:
+            lo, hi = Mh.row_offsets[r0], Mh.row_offsets[r1]
+            assert np.array_equal(mv, Mh.values[lo:hi])
+            assert np.array_equal(mc.astype(np.int64), Mh.col_indices[lo:hi] - (r0 - hlo))
+            ranks.append((r0, r1, grid))
+            x[r0:r1] = xr
+            assert red == 1 + 3 * it
+        xo, ho, st, _, _ = devorder.bicgstab_devorder(Ah, Mh, bh, 1e-10, 1000, 0, ranks=ranks)
+        h = np.array(out[0][5])
+        assert st == 1 and len(h) == len(ho), (world, len(h), len(ho))
+        assert np.max(np.abs(h - ho) / ho) <= 1e-8
+        assert np.max(np.abs(x - xo)) <= 1e-10 * np.max(np.abs(xo))
 
 
 def _run(world, case):
