@@ -44,6 +44,9 @@ enum {
 
 const char* spai_last_error(void);
 int spai_version(void);
+/* Reads and clears the CUDA runtime's last non-sticky error (returns it);
+ * used after an aborted CUDA-graph capture before falling back to eager.  */
+int spai_clear_cuda_error(void);
 
 /* ------------------------------------------------------------------ K0
  * Structured-grid stencil generator (no reference counterpart for Q1; the
@@ -387,15 +390,20 @@ int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext, const int
                        void* stream);
 /* same two entries with an explicit device status word (any solver's), and
  * modes 5 ([(r,u),(w,u),(r,r)] with u = x, w = y, r = raux: Chronopoulos-
- * Gear) and 6 ([(p,r),(p,q),(r,r)] with p = x, q = y: pipelined setup)     */
+ * Gear) and 6 ([(p,r),(p,q),(r,r)] with p = x, q = y: pipelined setup).
+ * Halo overlap: phase 0 = one pass; phase 1 = the rows of slices with
+ * bflag[s] == 0 (no halo coupling; may run while the halo is in flight,
+ * no epilogue); phase 2 = the remaining slices + the epilogue over all rows
+ * (bit-identical to phase 0).  bflag[nslices of the operator] from setup. */
 int spai_dist_spmv_st(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
                       const int64_t* cdesc, const int32_t* cols, const double* vals,
                       const double* xext, int64_t own_off, double* y, const double* raux,
-                      void* partials_ws, double* out, const int* status, void* stream);
+                      void* partials_ws, double* out, const int* status,
+                      const uint8_t* bflag, int phase, void* stream);
 int spai_dist_spmv_sym_st(int mode, int64_t n, int64_t r0, int64_t n_ext, const int32_t* g,
                           int w, const double* U, const double* xext, int64_t own_off,
                           double* y, const double* raux, void* partials_ws, double* out,
-                          const int* status, void* stream);
+                          const int* status, const uint8_t* bflag, int phase, void* stream);
 /* Block-local scope (the reference's RankSystem.apply_A, krylov.py:210-216):
  * y = spmv(A_ff, x) + hadd with hadd = spmv(A_fh, x_halo) precomputed by the
  * caller (spai_csr_spmv on the halo block), so each row is summed in the
@@ -404,7 +412,8 @@ int spai_dist_spmv_split_st(int mode, int64_t n, int64_t ncols, const int64_t* s
                             const int64_t* cdesc, const int32_t* cols, const double* vals,
                             const double* hadd, const double* xext, int64_t own_off,
                             double* y, const double* raux, void* partials_ws, double* out,
-                            const int* status, void* stream);
+                            const int* status, const uint8_t* bflag, int phase,
+                            void* stream);
 /* Blocks of the SELL dist SpMV for n owned rows (its reduction order).    */
 int spai_dist_grid(int64_t n);
 /* Row-partitioned right-preconditioned BiCGStab (configs[4]; the reference

@@ -39,6 +39,7 @@ _sz = C.c_size_t
 _SIGS = {
     "spai_last_error": (C.c_char_p, []),
     "spai_version": (_i32, []),
+    "spai_clear_cuda_error": (_i32, []),
     "spai_stencil_nnz": (_i32, [_i32, _vp, _vp, C.POINTER(_i64)]),
     "spai_stencil_csr": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_transpose_workspace_bytes": (_sz, [_i64, _i64, _i64]),
@@ -83,11 +84,11 @@ _SIGS = {
     "spai_dist_spmv_sym": (_i32, [_i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i64, _vp, _vp,
                                   _vp, _vp, _vp, _vp]),
     "spai_dist_spmv_st": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp,
-                                 _vp, _vp, _vp]),
+                                 _vp, _vp, _vp, _i32, _vp]),
     "spai_dist_spmv_sym_st": (_i32, [_i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _i64, _vp, _vp,
-                                     _vp, _vp, _vp, _vp]),
+                                     _vp, _vp, _vp, _vp, _i32, _vp]),
     "spai_dist_spmv_split_st": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
-                                       _vp, _vp, _vp, _vp, _vp, _vp]),
+                                       _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "spai_dist_grid": (_i32, [_i64]),
     "spai_dbicg_scal_bytes": (_sz, []),
     "spai_dbicg_scal_init": (_i32, [_vp, _dbl, _i64, _vp]),

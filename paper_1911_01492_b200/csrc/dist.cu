@@ -27,12 +27,20 @@ struct DistScal {
 // The operator's rows are slices [s0, s1); row 32 s + lane is owned row
 // i = 32 s + lane - r0 (SELL: the owned rows themselves, r0 = 0; half
 // storage: the extended principal submatrix, r0 = halo below).
+//
+// Halo overlap (phase != 0, bflag[s - s0] = 1 for slices with a row that
+// couples into the halo): phase 1 computes the interior slices' rows only
+// (no halo values needed, so it runs while the halo is in flight); phase 2
+// computes the boundary slices and reads the interior rows back, and does
+// the epilogue over all rows in the same thread / slice order as phase 0 --
+// the result is bit-identical to the single pass.
 template <int MODE, class OP>
 __global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
 dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
                  const double* __restrict__ xext, int64_t own_off, double* __restrict__ y,
                  const double* __restrict__ raux, double* partials, unsigned int* ticket,
-                 double* out, const int* status, const double* __restrict__ hadd) {
+                 double* out, const int* status, const double* __restrict__ hadd,
+                 const uint8_t* __restrict__ bflag, int phase) {
   if (MODE != 0 && *status != dRunning) return;
   constexpr int K = (MODE == 1 || MODE == 5 || MODE == 6) ? 3 : ((MODE == 2 || MODE == 7) ? 1 : 2);
   const int lane = threadIdx.x & 31;
@@ -43,16 +51,25 @@ dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
   for (int64_t s = s0 + w0; s < s1; s += nw) {
+    const bool bnd = phase != 0 && bflag[s - s0];
+    if (phase == 1 && bnd) continue;                 // warp-uniform
+    const bool fresh = phase != 2 || bnd;            // compute (else read back) this slice
     double v = 0.0;
-    if (MODE != 4) v = A.row(s, lane, [&](int32_t j) { return __ldg(xext + j); });
+    if (MODE != 4 && fresh) v = A.row(s, lane, [&](int32_t j) { return __ldg(xext + j); });
     const int64_t i = s * kSell + lane - r0;
     if (i >= 0 && i < n) {
+      if (!fresh) {
+        v = y[i];
+      } else {
+        if (MODE == 4) v = xo[i];
+        // block-local reference order: spmv(A_ff, x) + spmv(A_fh, x_halo),
+        // the second product precomputed into hadd (krylov.py:210-216); an
+        // interior row has no halo coupling (hadd = 0)
+        if (hadd && phase != 1) v = v + hadd[i];
+        y[i] = v;
+      }
+      if (phase == 1) continue;
       const double xi = xo[i];
-      if (MODE == 4) v = xi;
-      // block-local reference order: spmv(A_ff, x) + spmv(A_fh, x_halo),
-      // the second product precomputed into hadd (krylov.py:210-216)
-      if (hadd) v = v + hadd[i];
-      y[i] = v;
       if (MODE == 1) {
         const double ri = raux[i];
         acc[0] = fma(xi, v, acc[0]);
@@ -81,7 +98,7 @@ dist_spmv_kernel(int64_t n, int64_t s0, int64_t s1, int64_t r0, OP A,
       }
     }
   }
-  if (MODE == 0) return;
+  if (MODE == 0 || phase == 1) return;
   grid_finalize<K>(acc, partials, ticket, [&](double (&tot)[K]) {
 #pragma unroll
     for (int k = 0; k < K; ++k) out[k] = tot[k];
@@ -177,17 +194,18 @@ template <class OP>
 static int dist_launch(int mode, unsigned b, int64_t n, int64_t s0, int64_t s1, int64_t r0,
                        const OP& A, const double* xext, int64_t own_off, double* y,
                        const double* raux, double* part, unsigned int* ticket, double* out,
-                       const int* sc, cudaStream_t s, const double* hadd = nullptr) {
+                       const int* sc, cudaStream_t s, const double* hadd = nullptr,
+                       const uint8_t* bflag = nullptr, int phase = 0) {
   switch (mode) {
-    case 0: dist_spmv_kernel<0, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 1: dist_spmv_kernel<1, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 2: dist_spmv_kernel<2, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 3: dist_spmv_kernel<3, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 4: dist_spmv_kernel<4, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 5: dist_spmv_kernel<5, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 6: dist_spmv_kernel<6, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 7: dist_spmv_kernel<7, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
-    case 8: dist_spmv_kernel<8, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd); break;
+    case 0: dist_spmv_kernel<0, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 1: dist_spmv_kernel<1, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 2: dist_spmv_kernel<2, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 3: dist_spmv_kernel<3, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 4: dist_spmv_kernel<4, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 5: dist_spmv_kernel<5, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 6: dist_spmv_kernel<6, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 7: dist_spmv_kernel<7, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
+    case 8: dist_spmv_kernel<8, OP><<<b, kSpmvThreads, 0, s>>>(n, s0, s1, r0, A, xext, own_off, y, raux, part, ticket, out, sc, hadd, bflag, phase); break;
     default: set_error("bad dist_spmv mode %d", mode); return SPAI_E_ARG;
   }
   SPAI_LAUNCH_CHECK("dist_spmv_kernel");
@@ -244,7 +262,8 @@ extern "C" int spai_dist_spmv_st(int mode, int64_t n, int64_t ncols, const int64
                                  const int64_t* cdesc, const int32_t* cols,
                                  const double* vals, const double* xext, int64_t own_off,
                                  double* y, const double* raux, void* partials_ws, double* out,
-                                 const int* status, void* stream) {
+                                 const int* status, const uint8_t* bflag, int phase,
+                                 void* stream) {
   const int64_t ns = (n + kSell - 1) / kSell;
   if (ns == 0) {
     if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
@@ -257,7 +276,7 @@ extern "C" int spai_dist_spmv_st(int mode, int64_t n, int64_t ncols, const int64
   double* part = (double*)((char*)partials_ws + 256);
   const SellOp A{Sell{sliceptr, cdesc, cols, vals, ncols}};
   return dist_launch(mode, b, n, 0, ns, 0, A, xext, own_off, y, raux, part, ticket, out,
-                     status, (cudaStream_t)stream);
+                     status, (cudaStream_t)stream, nullptr, bflag, phase);
 }
 
 // Block-local scope in the reference's summation order: y = A_ff x + hadd,
@@ -267,7 +286,8 @@ extern "C" int spai_dist_spmv_split_st(int mode, int64_t n, int64_t ncols, const
                                        const double* vals, const double* hadd,
                                        const double* xext, int64_t own_off, double* y,
                                        const double* raux, void* partials_ws, double* out,
-                                       const int* status, void* stream) {
+                                       const int* status, const uint8_t* bflag, int phase,
+                                       void* stream) {
   const int64_t ns = (n + kSell - 1) / kSell;
   if (ns == 0) {
     if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
@@ -281,7 +301,7 @@ extern "C" int spai_dist_spmv_split_st(int mode, int64_t n, int64_t ncols, const
   double* part = (double*)((char*)partials_ws + 256);
   const SellOp A{Sell{sliceptr, cdesc, cols, vals, ncols}};
   return dist_launch(mode, b, n, 0, ns, 0, A, xext, own_off, y, raux, part, ticket, out,
-                     status, (cudaStream_t)stream, hadd);
+                     status, (cudaStream_t)stream, hadd, bflag, phase);
 }
 
 extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t* sliceptr,
@@ -290,7 +310,8 @@ extern "C" int spai_dist_spmv(int mode, int64_t n, int64_t ncols, const int64_t*
                               const double* raux, void* partials_ws, double* out,
                               const void* scal, void* stream) {
   return spai_dist_spmv_st(mode, n, ncols, sliceptr, cdesc, cols, vals, xext, own_off, y, raux,
-                           partials_ws, out, &((const DistScal*)scal)->status, stream);
+                           partials_ws, out, &((const DistScal*)scal)->status, nullptr, 0,
+                           stream);
 }
 
 // Same on the half-storage extended principal submatrix (n_ext rows; the
@@ -299,7 +320,8 @@ extern "C" int spai_dist_spmv_sym_st(int mode, int64_t n, int64_t r0, int64_t n_
                                      const int32_t* g, int w, const double* U,
                                      const double* xext, int64_t own_off, double* y,
                                      const double* raux, void* partials_ws, double* out,
-                                     const int* status, void* stream) {
+                                     const int* status, const uint8_t* bflag, int phase,
+                                     void* stream) {
   if (n == 0) {
     if (mode != 0) SPAI_CUDA(cudaMemsetAsync(out, 0, 3 * sizeof(double), (cudaStream_t)stream));
     return SPAI_OK;
@@ -315,7 +337,7 @@ extern "C" int spai_dist_spmv_sym_st(int mode, int64_t n, int64_t r0, int64_t n_
     const unsigned b = std::max(1u, std::min(ssell_blocks((const void*)dist_spmv_kernel<1, SymOp<WM>>, s1 - s0),
                                              (unsigned)num_sms() * 32));
     st = dist_launch(mode, b, n, s0, s1, r0, op, xext, own_off, y, raux, part, ticket, out,
-                     status, (cudaStream_t)stream);
+                     status, (cudaStream_t)stream, nullptr, bflag, phase);
   });
   return st;
 }
@@ -326,7 +348,7 @@ extern "C" int spai_dist_spmv_sym(int mode, int64_t n, int64_t r0, int64_t n_ext
                                   void* partials_ws, double* out, const void* scal,
                                   void* stream) {
   return spai_dist_spmv_sym_st(mode, n, r0, n_ext, g, w, U, xext, own_off, y, raux, partials_ws,
-                               out, &((const DistScal*)scal)->status, stream);
+                               out, &((const DistScal*)scal)->status, nullptr, 0, stream);
 }
 
 extern "C" int spai_dist_update_p(int64_t n, double* p, const double* z, const void* scal,

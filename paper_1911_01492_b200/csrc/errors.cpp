@@ -34,3 +34,6 @@ int* small_scratch() {
 
 extern "C" const char* spai_last_error(void) { return spai::g_err; }
 extern "C" int spai_version(void) { return 1; }
+// Clear the CUDA runtime's last (non-sticky) error, e.g. after an aborted
+// stream capture, so the next launch check does not report it again.
+extern "C" int spai_clear_cuda_error(void) { return (int)cudaGetLastError(); }

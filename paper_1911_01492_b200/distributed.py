@@ -110,6 +110,37 @@ class TorchComm:
         self.reductions += 1
         return self.dist.all_gather_into_tensor(gathered, out, group=self.group, async_op=True)
 
+    @property
+    def capturable(self) -> bool:
+        """Whether an iteration's communication can live inside a CUDA graph
+        (NCCL P2P and collectives are stream operations; gloo stages through
+        the host)."""
+        return self.size == 1 or not self.stage
+
+    def halo_start(self, xext, own_off: int, n_own: int, hlo: int, hhi: int):
+        """Start the plane exchange of `halo`; returns an object whose wait()
+        makes the current stream wait for the received planes (NCCL: the
+        transfer runs on the communicator's stream, overlapping whatever is
+        enqueued before the wait)."""
+        if self.size == 1 or self.stage:
+            self.halo(xext, own_off, n_own, hlo, hhi)
+            return _Done()
+        return _Works(self._halo_ops(xext, own_off, n_own, hlo, hhi))
+
+    def _halo_ops(self, xext, own_off, n_own, hlo, hhi):
+        d = self.dist
+        ops = []
+        r = self.rank
+        if hlo:
+            ops.append(d.P2POp(d.irecv, xext[:hlo], r - 1, self.group))
+            ops.append(d.P2POp(d.isend, xext[own_off:own_off + hlo], r - 1, self.group))
+        if hhi:
+            ops.append(d.P2POp(d.irecv, xext[own_off + n_own:own_off + n_own + hhi], r + 1,
+                               self.group))
+            ops.append(d.P2POp(d.isend, xext[own_off + n_own - hhi:own_off + n_own], r + 1,
+                               self.group))
+        return d.batch_isend_irecv(ops) if ops else []
+
     def halo(self, xext, own_off: int, n_own: int, hlo: int, hhi: int):
         """Fill xext[:hlo] from rank-1's last rows, xext[own_off+n_own:] from rank+1."""
         if self.size == 1:
@@ -141,6 +172,85 @@ class TorchComm:
 class _Done:
     def wait(self):
         return True
+
+
+class _Works:
+    def __init__(self, works):
+        self.works = works
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        return True
+
+
+class _RankLoop:
+    """What the row-partitioned solvers share: the operator application
+    with the halo overlapped (interior slices while the planes are in
+    flight, then the boundary slices and the fused epilogue -- bit-identical
+    to the single pass), and CUDA-graph replay of `chunk` steady-state
+    iterations when the communicator is capturable (one graph launch per
+    chunk; eager otherwise, e.g. gloo)."""
+
+    overlap = True
+    use_graphs = True
+
+    def _init_loop(self):
+        self._flags = {}
+        self.graph = None
+        self.graph_error = None
+        self._warm = False
+
+    def _bflag(self, op):
+        if not self.overlap or self.comm.size == 1 or op is None:
+            return None
+        key = id(op)
+        if key not in self._flags:
+            fn = getattr(self.be, "boundary_flags", None)
+            self._flags[key] = (op, fn(op, self.sys.hlo, self.sys.n_own) if fn else None)
+        return self._flags[key][1]
+
+    def _apply_halo(self, call, op, xext):
+        """call(bflag, phase) launches the SpMV of `op` on xext."""
+        s, c = self.sys, self.comm
+        bflag = self._bflag(op)
+        if bflag is None:
+            c.halo(xext, s.hlo, s.n_own, s.hlo, s.hhi)
+            call(None, 0)
+            return
+        h = c.halo_start(xext, s.hlo, s.n_own, s.hlo, s.hhi)
+        call(bflag, 1)
+        h.wait()
+        call(bflag, 2)
+
+    def _advance(self, k):
+        """k steady-state iterations (graph replay when k == chunk)."""
+        import torch
+        if (self.use_graphs and k == self.chunk and self.graph_error is None and self._warm
+                and getattr(self.comm, "capturable", False) and hasattr(self.be, "lib")):
+            if self.graph is None:
+                try:
+                    torch.cuda.current_stream().synchronize()
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                        for _ in range(k):
+                            self._body()
+                    self.graph = g
+                except Exception as e:            # capture unsupported: stay eager
+                    self.graph_error = f"{type(e).__name__}: {e}"[:200]
+                    self.graph = None
+                    torch.cuda.synchronize()
+                    self.be.lib.spai_clear_cuda_error()
+            if self.graph is not None:
+                self.graph.replay()
+                self.launched += k
+                return
+        # eager (the first chunk always: it builds the operators' lazy
+        # layouts, which synchronise with the host and cannot be captured)
+        for _ in range(k):
+            self._body()
+            self.launched += 1
+        self._warm = True
 
 
 # ------------------------------------------------------------------ local system
@@ -199,6 +309,37 @@ class SplitOperator:
         return self.ff.sell_values()
 
 
+def boundary_flags(M, hlo: int, n_own: int):
+    """uint8 flag per slice of a rank operator (device): 1 when one of the
+    slice's owned rows has a coupling outside the owned column range
+    [hlo, hlo + n_own) of the extended vector, i.e. needs halo values."""
+    import torch
+    if isinstance(M, SymExtOperator):
+        # rows r0 .. r0 + n of the extended block, couplings i +- g_k
+        gmax = int(max(M.g))
+        s0, s1 = M.r0 // 32, (M.r0 + M.n_own + 31) // 32
+        rows = torch.arange(s0 * 32, s1 * 32, device=M.U.device)
+        own = (rows >= M.r0) & (rows < M.r0 + M.n_own)
+        touch = own & ((rows - gmax < M.r0) | (rows + gmax >= M.r0 + M.n_own))
+        return touch.view(-1, 32).any(dim=1).to(torch.uint8).contiguous()
+    if isinstance(M, SplitOperator):
+        A = M.fh                       # rows with halo entries
+        row_touch = (A.rowptr[1:] - A.rowptr[:-1]) > 0
+    else:
+        A = M
+        cols = A.colidx
+        out_col = ((cols < hlo) | (cols >= hlo + n_own)).to(torch.int32)
+        rows = torch.repeat_interleave(torch.arange(A.nrows, device=cols.device),
+                                       A.rowptr[1:] - A.rowptr[:-1])
+        cnt = torch.zeros(A.nrows, dtype=torch.int32, device=cols.device)
+        cnt.index_add_(0, rows, out_col)
+        row_touch = cnt > 0
+    ns = (A.nrows + 31) // 32
+    pad = torch.zeros(ns * 32, dtype=torch.bool, device=row_touch.device)
+    pad[:A.nrows] = row_touch
+    return pad.view(ns, 32).any(dim=1).to(torch.uint8).contiguous()
+
+
 # ------------------------------------------------------------------ GPU backend
 class GpuBackend:
     """Per-rank compute through the C-ABI (dist_* kernels, SELL-32 operators)."""
@@ -239,58 +380,53 @@ class GpuBackend:
                    "spai_dist_scal_read")
         return st.value, it.value, n0.value, nr.value, aux.value
 
-    def _split(self, mode, M, xext, own_off, y, raux, ws, out, status):
-        fh = M.fh
-        _lib.check(self.lib.spai_csr_spmv(fh.nrows, fh.nnz, _p(fh.rowptr), _p(fh.colidx),
-                                          _p(fh.vals), _p(xext), _p(M.hadd), self._s()),
-                   "spai_csr_spmv")
+    def _split(self, mode, M, xext, own_off, y, raux, ws, out, status, bflag=None, phase=0):
+        if phase != 1:          # the halo part needs the halo: not in the overlapped pass
+            fh = M.fh
+            _lib.check(self.lib.spai_csr_spmv(fh.nrows, fh.nnz, _p(fh.rowptr), _p(fh.colidx),
+                                              _p(fh.vals), _p(xext), _p(M.hadd), self._s()),
+                       "spai_csr_spmv")
         sliceptr, cdesc, cols = M.sell()
         _lib.check(self.lib.spai_dist_spmv_split_st(
             mode, M.nrows, M.ncols, _p(sliceptr), _p(cdesc), _p(cols), _p(M.sell_values()),
             _p(M.hadd), _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out), C.c_void_p(status),
-            self._s()), "spai_dist_spmv_split_st")
+            _p(bflag), phase, self._s()), "spai_dist_spmv_split_st")
 
-    def spmv(self, mode, M, xext, own_off, y, raux, ws, out, scal):
-        if isinstance(M, SplitOperator):
-            # DistScal's status word sits at the same offset the kernel reads
-            self._split(mode, M, xext, own_off, y, raux, ws, out,
-                        self.lib.spai_dist_status_ptr(_p(scal)))
-            return
-        if isinstance(M, SymExtOperator):
-            _lib.check(self.lib.spai_dist_spmv_sym(
-                mode, M.n_own, M.r0, M.n_ext, C.cast(M.garr, C.c_void_p), len(M.g), _p(M.U),
-                _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out), _p(scal), self._s()),
-                "spai_dist_spmv_sym")
-            return
-        if M is None:       # identity preconditioner (mode 4)
-            _lib.check(self.lib.spai_dist_spmv(4, y.numel(), xext.numel(), None, None, None, None,
-                                               _p(xext), own_off, _p(y), None, _p(ws), _p(out),
-                                               _p(scal), self._s()), "spai_dist_spmv")
-            return
-        sliceptr, cdesc, cols = M.sell()
-        vals = M.sell_values()
-        _lib.check(self.lib.spai_dist_spmv(mode, M.nrows, M.ncols, _p(sliceptr), _p(cdesc),
-                                           _p(cols), _p(vals), _p(xext), own_off, _p(y),
-                                           _p(raux), _p(ws), _p(out), _p(scal), self._s()),
-                   "spai_dist_spmv")
+    def spmv(self, mode, M, xext, own_off, y, raux, ws, out, scal, bflag=None, phase=0):
+        """dist SpMV on a classic-PCG scal block (DistScal)."""
+        self.spmv_st(mode, M, xext, own_off, y, raux, ws, out,
+                     self.lib.spai_dist_status_ptr(_p(scal)), bflag, phase)
 
-    def spmv_st(self, mode, M, xext, own_off, y, raux, ws, out, status):
-        """dist SpMV with an explicit device status word (any solver)."""
+    def spmv_st(self, mode, M, xext, own_off, y, raux, ws, out, status, bflag=None, phase=0):
+        """dist SpMV with an explicit device status word (any solver);
+        phase 1 / 2 split it around the halo (see spai_dist_spmv_st)."""
+        st = C.c_void_p(status)
         if isinstance(M, SplitOperator):
-            self._split(mode, M, xext, own_off, y, raux, ws, out, status)
+            self._split(mode, M, xext, own_off, y, raux, ws, out, status, bflag, phase)
             return
         if isinstance(M, SymExtOperator):
             _lib.check(self.lib.spai_dist_spmv_sym_st(
                 mode, M.n_own, M.r0, M.n_ext, C.cast(M.garr, C.c_void_p), len(M.g), _p(M.U),
-                _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out), C.c_void_p(status),
+                _p(xext), own_off, _p(y), _p(raux), _p(ws), _p(out), st, _p(bflag), phase,
                 self._s()), "spai_dist_spmv_sym_st")
+            return
+        if M is None:       # identity preconditioner (mode 4)
+            _lib.check(self.lib.spai_dist_spmv_st(4, y.numel(), xext.numel(), None, None, None,
+                                                  None, _p(xext), own_off, _p(y), None, _p(ws),
+                                                  _p(out), st, None, 0, self._s()),
+                       "spai_dist_spmv_st")
             return
         sliceptr, cdesc, cols = M.sell()
         vals = M.sell_values()
         _lib.check(self.lib.spai_dist_spmv_st(mode, M.nrows, M.ncols, _p(sliceptr), _p(cdesc),
                                               _p(cols), _p(vals), _p(xext), own_off, _p(y),
-                                              _p(raux), _p(ws), _p(out), C.c_void_p(status),
+                                              _p(raux), _p(ws), _p(out), st, _p(bflag), phase,
                                               self._s()), "spai_dist_spmv_st")
+
+    def boundary_flags(self, M, hlo, n_own):
+        """Per-slice flags of the operator: 1 if a row of the slice couples
+        into the halo (computed in the pass after the halo arrived)."""
+        return boundary_flags(M, hlo, n_own)
 
     def update_p(self, p_own, z, scal):
         _lib.check(self.lib.spai_dist_update_p(z.numel(), _p(p_own), _p(z), _p(scal), self._s()),
@@ -349,7 +485,7 @@ def _p(t):
 
 
 # ------------------------------------------------------------------ solver
-class DistributedPCG:
+class DistributedPCG(_RankLoop):
     """Classic PCG on a row partition; device-resident, host polls every `chunk`."""
 
     def __init__(self, system: LocalRankSystem, comm, backend, tol=1e-8, maxit=1000,
@@ -369,9 +505,16 @@ class DistributedPCG:
         self.ws = be.partials()
         self.scal = be.scal(tol, maxit)
         self.launched = 0
+        self._init_loop()
 
     def _own(self, v):
         return v[self.sys.hlo:self.sys.hlo + self.sys.n_own]
+
+    def _spmv(self, mode, op, xext, y, raux):
+        s, be = self.sys, self.be
+        self._apply_halo(lambda bf, ph: be.spmv(mode, op, xext, s.hlo, y, raux, self.ws,
+                                                self.out, self.scal, bflag=bf, phase=ph),
+                         op, xext)
 
     def start(self):
         s, be, c = self.sys, self.be, self.comm
@@ -389,32 +532,30 @@ class DistributedPCG:
         p_own, r_own = self._own(self.pext), self._own(self.rext)
         if not first:
             be.update_p(p_own, self.z, self.scal)
-        c.halo(self.pext, s.hlo, s.n_own, s.hlo, s.hhi)
         K1 = 3 if first else 1
-        be.spmv(1 if first else 2, s.A_op or s.A, self.pext, s.hlo, self.q, r_own, self.ws,
-                self.out, self.scal)
+        self._spmv(1 if first else 2, s.A_op or s.A, self.pext, self.q, r_own)
         c.allgather(self.out[:K1], self.gathered[:K1 * c.size])
         be.reduce_step(c.size, self.gathered, K1, 1, self.scal, self.hist)
         be.update_xr(self.x, r_own, p_own, self.q, self.scal)
-        c.halo(self.rext, s.hlo, s.n_own, s.hlo, s.hhi)
-        be.spmv(3, s.M_op or s.M, self.rext, s.hlo, self.z, None, self.ws, self.out, self.scal)
+        self._spmv(3, s.M_op or s.M, self.rext, self.z, None)
         c.allgather(self.out[:2], self.gathered[:2 * c.size])
         be.reduce_step(c.size, self.gathered, 2, 2, self.scal, self.hist)
-        self.launched += 1
+
+    def _body(self):
+        self.iteration(first=False)
 
     def run(self):
         self.start()
-        done = 0
+        self.iteration(first=True)
+        self.launched += 1
+        done = 1
         while True:
-            n = min(self.chunk, self.maxit - done) if done < self.maxit else 1
-            for _ in range(n):
-                self.iteration(first=(done == 0))
-                done += 1
             st = self.be.read(self.scal)
-            if st[0] != 0:
+            if st[0] != 0 or done >= self.maxit:
                 return st
-            if done >= self.maxit:
-                return st
+            k = min(self.chunk, self.maxit - done)
+            self._advance(k)
+            done += k
 
     def solve(self):
         """Returns (x_owned, ConvergenceRecord) with _solve_classic semantics."""
@@ -442,7 +583,7 @@ class DistributedPCG:
         return self.x, rec
 
 
-class DistributedCGV:
+class DistributedCGV(_RankLoop):
     """Row-partitioned Chronopoulos-Gear or pipelined CG (krylov.py:348-399,
     461-535) with the reference's record semantics.  Each reduction is the
     per-rank partials -> all-gather -> on-device ascending-rank tree sum and
@@ -475,6 +616,7 @@ class DistributedCGV:
                    "spai_dcgv_scal_init")
         self.status = be.lib.spai_dcgv_status_ptr(_p(self.scal))
         self.launched = 0
+        self._init_loop()
 
     def _own(self, name):
         t = self.v[name]
@@ -487,13 +629,16 @@ class DistributedCGV:
         self.comm.halo(self.v[name], s.hlo, s.n_own, s.hlo, s.hhi)
 
     def _apply(self, op, src, dst, mode=0, raux=None):
-        """dst(owned) = op src_ext (after the halo of src); op None = identity."""
+        """dst(owned) = op src_ext (halo of src exchanged, overlapped with the
+        interior rows); op None = identity."""
         s = self.sys
         if op is None:
             self._own(dst).copy_(self._own(src))
             return
-        self.be.spmv_st(mode, op, self.v[src], s.hlo, self._own(dst), raux, self.ws, self.out,
-                        self.status)
+        xe = self.v[src]
+        self._apply_halo(lambda bf, ph: self.be.spmv_st(mode, op, xe, s.hlo, self._own(dst), raux,
+                                                        self.ws, self.out, self.status,
+                                                        bflag=bf, phase=ph), op, xe)
 
     def _head(self, count_issue, count_body):
         _lib.check(self.be.lib.spai_dcgv_head(self.code, self.comm.size, _p(self.gathered),
@@ -505,22 +650,16 @@ class DistributedCGV:
         A, M = s.A_op or s.A, s.M_op or s.M
         self._own("r").copy_(s.b)
         if self.variant == "chronopoulos_gear":
-            self._halo("r")
             self._apply(M, "r", "u")
-            self._halo("u")
             self._apply(A, "u", "w", 5, self._own("r"))
             self.comm.allgather(self.out, self.gathered)
             self._head(0, 0)
         else:
-            self._halo("r")
             self._apply(M, "r", "p")
-            self._halo("p")
             self._apply(A, "p", "q", 6, self._own("r"))
             self.comm.allgather(self.out, self.gathered)
             self._head(1, 0)
-            self._halo("q")
             self._apply(M, "q", "s")
-            self._halo("s")
             self._apply(A, "s", "t")
             self._own("z").copy_(self._own("p"))
             self._own("w").copy_(self._own("q"))
@@ -533,9 +672,7 @@ class DistributedCGV:
             _lib.check(be.lib.spai_dcgv_cg_update(s.n_own, _p(o("x")), _p(o("r")), _p(o("p")),
                                                   _p(o("q")), _p(o("u")), _p(o("w")),
                                                   _p(self.scal), be._s()), "spai_dcgv_cg_update")
-            self._halo("r")
             self._apply(M, "r", "u")
-            self._halo("u")
             self._apply(A, "u", "w", 5, o("r"))
             self.comm.allgather(self.out, self.gathered)
             self._head(0, 1)
@@ -545,13 +682,13 @@ class DistributedCGV:
                 _p(o("s")), _p(o("t")), _p(o("u")), _p(o("v")), _p(self.ws), _p(self.out),
                 _p(self.scal), be._s()), "spai_dcgv_pipe_update")
             pending = self.comm.allgather_async(self.out, self.gathered)
-            self._halo("w")
             self._apply(M, "w", "v")
-            self._halo("v")
             self._apply(A, "v", "u")
             pending.wait()
             self._head(1, 1)
-        self.launched += 1
+
+    def _body(self):
+        self.iteration()
 
     def read(self):
         state = np.zeros(7, dtype=np.int64)
@@ -569,8 +706,7 @@ class DistributedCGV:
         self.start()
         st = self.read()
         while st["status"] == 0:
-            for _ in range(self.chunk):
-                self.iteration()
+            self._advance(self.chunk)
             st = self.read()
         if st["status"] == 3:
             raise BreakdownError(_CGV_BREAKDOWN[self.variant].format(st["aux"]))
@@ -595,7 +731,7 @@ class DistributedCGV:
         return self._own("x"), rec
 
 
-class DistributedBiCGStab:
+class DistributedBiCGStab(_RankLoop):
     """Row-partitioned right-preconditioned BiCGStab (configs[4]): the K9
     iteration (krylov2.cu; oracle/krylov.py bicgstab_right -- the reference
     has no BiCGStab) on each rank's owned rows, with a halo of
@@ -619,6 +755,7 @@ class DistributedBiCGStab:
         self.scal = be.dbicg_scal(tol, self.maxit)
         self.status = be.dbicg_status(self.scal)
         self.launched = 0
+        self._init_loop()
 
     def _own(self, name):
         if name in self.own_v:
@@ -629,16 +766,22 @@ class DistributedBiCGStab:
         s = self.sys
         self.comm.halo(self.ext[name], s.hlo, s.n_own, s.hlo, s.hhi)
 
+    def _op(self, mode, op, src, dst, raux=None):
+        """dst(owned) = op src_ext, src's halo overlapped with the interior."""
+        s = self.sys
+        xe = self.ext[src]
+        self._apply_halo(lambda bf, ph: self.be.spmv_st(mode, op, xe, s.hlo, self._own(dst), raux,
+                                                        self.ws, self.out, self.status,
+                                                        bflag=bf, phase=ph), op, xe)
+
     def _precond(self, src, dst):
-        """dst(owned) = M src (src's halo exchanged first)."""
+        """dst(owned) = M src."""
         s = self.sys
         M = s.M_op or s.M
         if M is None:
             self._own(dst).copy_(self._own(src))
             return
-        self._halo(src)
-        self.be.spmv_st(0, M, self.ext[src], s.hlo, self._own(dst), None, self.ws, self.out,
-                        self.status)
+        self._op(0, M, src, dst)
 
     def _reduce(self, K, stage):
         c = self.comm
@@ -656,27 +799,27 @@ class DistributedBiCGStab:
         A = s.A_op or s.A
         be.dbicg_update_p(o("p"), o("r"), o("v"), self.scal)
         self._precond("p", "ph")
-        self._halo("ph")
-        be.spmv_st(7, A, self.ext["ph"], s.hlo, o("v"), o("rh"), self.ws, self.out, self.status)
+        self._op(7, A, "ph", "v", o("rh"))
         self._reduce(1, 1)
         be.dbicg_update_s(o("s"), o("r"), o("v"), self.scal)
         self._precond("s", "sh")
-        self._halo("sh")
-        be.spmv_st(8, A, self.ext["sh"], s.hlo, o("t"), o("s"), self.ws, self.out, self.status)
+        self._op(8, A, "sh", "t", o("s"))
         self._reduce(2, 2)
         be.dbicg_update_xr(o("x"), o("r"), o("s"), o("t"), o("ph"), o("sh"), o("rh"),
                            self.scal, self.ws, self.out)
         self._reduce(2, 3)
-        self.launched += 1
+
+    def _body(self):
+        self.iteration()
 
     def run(self):
         self.start()
         st = self.be.dbicg_read(self.scal)
         done = 0
         while st[0] == 0 and done < self.maxit:
-            for _ in range(min(self.chunk, self.maxit - done)):
-                self.iteration()
-                done += 1
+            k = min(self.chunk, self.maxit - done)
+            self._advance(k)
+            done += k
             st = self.be.dbicg_read(self.scal)
         return st
 

@@ -73,7 +73,7 @@ class NumpyBackend:
     def read(self, sc):
         return sc["status"], sc["it"], sc["norm0"], sc["norm"], sc["aux"]
 
-    def spmv(self, mode, M, xext, own_off, y, raux, ws, out, sc):
+    def spmv(self, mode, M, xext, own_off, y, raux, ws, out, sc, bflag=None, phase=0):
         if mode != 0 and sc["status"] != 0:
             return
         xe = xext.numpy()
@@ -187,7 +187,7 @@ class NumpyBiCGBackend(NumpyBackend):
     def dbicg_read(self, sc):
         return sc["status"], sc["it"], sc["norm0"], sc["norm"], sc["kind"]
 
-    def spmv_st(self, mode, M, xext, own_off, y, raux, ws, out, sc):
+    def spmv_st(self, mode, M, xext, own_off, y, raux, ws, out, sc, bflag=None, phase=0):
         if mode != 0 and sc["status"] != 0:
             return
         xe = xext.numpy()

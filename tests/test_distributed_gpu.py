@@ -157,6 +157,31 @@ def _worker(rank, world, port, case, q):
             q.put((rank, r0, r1, x.cpu().numpy(), rec.iterations, list(rec.residual_norms),
                    rec.reductions_cum, rec.overlapped_cum, rec.total_reductions))
             return
+        if case.startswith("overlap_"):
+            # the same solves with and without the halo-overlapped SpMV
+            from paper_1911_01492_b200.distributed import DistributedBiCGStab, _RankLoop
+            dims = (20, 18, 16)
+            part = SlabPartition(dims[-1], dims[0] * dims[1], world)
+            res = []
+            for ov in (False, True):
+                _RankLoop.overlap = ov
+                if case == "overlap_cg":
+                    sysr = q1_rank_system(dims, part, rank, "global")
+                    _, rec = DistributedPCG(sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                                            maxit=2000).solve()
+                elif case == "overlap_bl":
+                    sysr = q1_rank_system(dims, part, rank, "block_local", symmetric_spai=True)
+                    _, rec = DistributedPCG(sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                                            maxit=2000).solve()
+                else:
+                    sysr = q1_rank_system(dims, part, rank, "global", conv=BICG_CONV,
+                                          symmetric_spai=False)
+                    _, rec = DistributedBiCGStab(sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                                                 maxit=2000).solve()
+                res.append(list(rec.residual_norms))
+            _RankLoop.overlap = True
+            q.put((rank, res[0], res[1]))
+            return
         if case == "bicg_cd":
             from paper_1911_01492_b200.distributed import DistributedBiCGStab
             dims, conv = BICG_DIMS, BICG_CONV
@@ -219,6 +244,47 @@ def test_row_partitioned_bicgstab_matches_device_order_oracle():
         assert st == 1 and len(h) == len(ho), (world, len(h), len(ho))
         assert np.max(np.abs(h - ho) / ho) <= 1e-8
         assert np.max(np.abs(x - xo)) <= 1e-10 * np.max(np.abs(xo))
+
+
+@pytest.mark.parametrize("case", ["overlap_cg", "overlap_bl", "overlap_bicg"])
+def test_halo_overlapped_spmv_is_bit_identical(case):
+    """Two ranks: the SpMV split around the halo (interior slices, wait,
+    boundary slices + epilogue) gives bit-identical histories to the single
+    pass -- half-storage (global CG), split block-local and SELL (BiCGStab)
+    operators."""
+    out = _run(2, case)
+    for rank, plain, overlapped in out:
+        assert plain == overlapped and len(plain) > 5
+
+
+def test_rank_loop_graph_replay_matches_eager():
+    """One rank (capturable communicator): the steady-state iterations run
+    as one CUDA graph per chunk, with the same history and x as eager."""
+    from paper_1911_01492_b200.distributed import DistributedBiCGStab
+    dims = (20, 18, 16)
+    part = SlabPartition(dims[-1], dims[0] * dims[1], 1)
+    for make in ("cg", "bicg", "cgv"):
+        outs = []
+        for graphs in (False, True):
+            if make == "bicg":
+                sysr = q1_rank_system(dims, part, 0, "global", conv=BICG_CONV,
+                                      symmetric_spai=False)
+                solver = DistributedBiCGStab(sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                                             maxit=2000, chunk=8)
+            elif make == "cg":
+                sysr = q1_rank_system(dims, part, 0, "global")
+                solver = DistributedPCG(sysr, TorchComm(), GpuBackend(), tol=1e-10, maxit=2000,
+                                        chunk=8)
+            else:
+                sysr = q1_rank_system(dims, part, 0, "global")
+                solver = DistributedCGV("pipelined", sysr, TorchComm(), GpuBackend(), tol=1e-10,
+                                        maxit=2000, chunk=8)
+            solver.use_graphs = graphs
+            x, rec = solver.solve()
+            assert (solver.graph is not None) == graphs, solver.graph_error
+            outs.append((list(rec.residual_norms), x.cpu().numpy(), rec.iterations))
+        assert outs[0][0] == outs[1][0] and outs[0][2] == outs[1][2]
+        assert np.array_equal(outs[0][1], outs[1][1])
 
 
 def _run(world, case):
