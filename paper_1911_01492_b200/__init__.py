@@ -18,7 +18,8 @@ from .sparse import (CsrMatrix, DeviceCsr, as_device, read_matrix_market, read_v
 from .grids import (Anisotropy, Partition, StructuredGrid, assemble_poisson, assemble_q1,
                     extract_local_system, fd5_stencil, make_rhs, partition_1d_strips,
                     q1_device, q1_stencil, stencil_device)
-from .distributed import RankSystem, fused_allreduce, halo_exchange
+from .distributed import (RankSystem, fused_allreduce, halo_exchange, gather_ghost_rows,
+                          global_spai1_rank_preconditioner)
 from .precond import (IdentityPreconditioner, JacobiPreconditioner,
                       Preconditioner, SparseMatrixPreconditioner, SpaiStats,
                       drop_exact_zeros, jacobi, make_spai1_factory,

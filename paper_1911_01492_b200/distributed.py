@@ -1146,6 +1146,14 @@ class RankSystem:
     def apply_M(self, x):
         if self.M is None:
             return np.array(x, dtype=np.float64, copy=True)
+        if isinstance(self.M, RankGlobalPreconditioner):
+            from .sparse import spmv
+            x = np.asarray(x, dtype=np.float64)
+            x_halo = self._exchange(x) if self.comm.size > 1 else np.zeros(0)
+            y = spmv(self.M.M_ff, x)
+            if self.M.M_fh.ncols:
+                y = y + spmv(self.M.M_fh, x_halo)
+            return y
         return self.M.apply(x)
 
     def fused_dots(self, pairs, overlapped=False):
@@ -1191,7 +1199,19 @@ class RankSystem:
         else:
             A_op = A_ff
         M_ext = None
-        if self.M is not None:
+        if isinstance(self.M, RankGlobalPreconditioner):
+            mf, mh = self.M.M_ff, self.M.M_fh
+            rm = [np.repeat(np.arange(n), np.diff(mf.row_offsets))]
+            cm = [np.asarray(mf.col_indices, dtype=np.int64) + hlo]
+            vm = [mf.values]
+            if mh.ncols and mh.nnz:
+                rm.append(np.repeat(np.arange(n), np.diff(mh.row_offsets)))
+                ch = np.asarray(mh.col_indices, dtype=np.int64)
+                cm.append(np.where(ch < hlo, ch, ch + n))
+                vm.append(mh.values)
+            M_ext = as_device(CsrMatrix.from_coo(n, ne, np.concatenate(rm), np.concatenate(cm),
+                                                 np.concatenate(vm)))
+        elif self.M is not None:
             Mm = getattr(self.M, "M", None)
             if Mm is None:
                 raise NotImplementedError("device multi-rank solve needs a sparse-matrix "
@@ -1203,6 +1223,172 @@ class RankSystem:
         bd = b if isinstance(b, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(b, dtype=np.float64))
         return LocalRankSystem(n, hlo, hhi, A_op, M_ext, bd.cuda().double())
+
+
+# ------------------------------------------------------------------ global SPAI(1) for rank matrices
+def _rank_rows(A_ff, A_fh, part, rank):
+    """This rank's rows of the global matrix: (global row ids, rowptr, global
+    columns sorted per row, values) from the extract_local_system pair."""
+    owned = np.asarray(part.owned[rank], dtype=np.int64)
+    halo = np.asarray(part.halo[rank], dtype=np.int64)
+    n = len(owned)
+    rows = [np.repeat(np.arange(n), np.diff(np.asarray(A_ff.row_offsets)))]
+    cols = [owned[np.asarray(A_ff.col_indices, dtype=np.int64)]]
+    vals = [np.asarray(A_ff.values, dtype=np.float64)]
+    if A_fh.ncols and A_fh.nnz:
+        rows.append(np.repeat(np.arange(n), np.diff(np.asarray(A_fh.row_offsets))))
+        cols.append(halo[np.asarray(A_fh.col_indices, dtype=np.int64)])
+        vals.append(np.asarray(A_fh.values, dtype=np.float64))
+    r, c, v = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    order = np.lexsort((c, r))
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=rp[1:])
+    return owned, rp, c[order], v[order]
+
+
+def _select_rows(gids, rp, cols, vals, want):
+    """Rows `want` (global ids, all present in sorted `gids`) as a row set."""
+    pos = np.searchsorted(gids, want)
+    lens = rp[pos + 1] - rp[pos]
+    idx = np.repeat(rp[pos] - np.cumsum(lens) + lens, lens) + np.arange(int(lens.sum()))
+    out_rp = np.zeros(len(want) + 1, dtype=np.int64)
+    np.cumsum(lens, out=out_rp[1:])
+    return np.asarray(want, dtype=np.int64), out_rp, cols[idx], vals[idx]
+
+
+def gather_ghost_rows(A_ff, A_fh, part, rank, comm=None, depth: int = 3):
+    """One-time exchange of A's rows for global SPAI(1) on a row partition
+    (SURVEY 8(e)): every rank collects the rows within graph distance
+    `depth` of its owned rows (3 = what the owned rows of M need: their
+    columns j are 1 away, and j's problem A[I_j, J_j] reaches 2 further),
+    asking the owners round by round.  Returns the local matrix on the
+    sorted row set L: (L, rowptr, local column indices, values), columns
+    restricted to L.  Needs a structurally symmetric pattern (the rows
+    referencing a column are then that column's own neighbours)."""
+    comm = comm if comm is not None else TorchComm()
+    mine = _rank_rows(A_ff, A_fh, part, rank)
+    starts = np.array([np.asarray(o)[0] if len(o) else np.iinfo(np.int64).max
+                       for o in part.owned], dtype=np.int64)
+    gids, rp, cols, vals = mine
+    known_g = [gids]
+    parts = [mine]
+    frontier_src = mine
+    for _ in range(depth):
+        allknown = np.unique(np.concatenate(known_g))
+        want = np.setdiff1d(np.unique(frontier_src[2]), allknown)
+        owner = np.searchsorted(starts, want, side="right") - 1
+        req = {int(r): want[owner == r] for r in np.unique(owner)}
+        if comm.size == 1:
+            if len(want):
+                raise InvalidPartitionError("columns outside the matrix on a single rank")
+            break
+        reqs = [None] * comm.size
+        comm.dist.all_gather_object(reqs, req, group=comm.group)
+        answer = {q: _select_rows(gids, rp, cols, vals, r[rank])
+                  for q, r in enumerate(reqs) if rank in r and len(r[rank])}
+        answers = [None] * comm.size
+        comm.dist.all_gather_object(answers, answer, group=comm.group)
+        got = [a[rank] for a in answers if rank in a]
+        if not got:
+            frontier_src = (np.zeros(0, np.int64),) * 4
+            continue
+        g = np.concatenate([x[0] for x in got])
+        rps = [x[1] for x in got]
+        c = np.concatenate([x[2] for x in got])
+        v = np.concatenate([x[3] for x in got])
+        lens = np.concatenate([np.diff(x) for x in rps])
+        rpn = np.zeros(len(g) + 1, dtype=np.int64)
+        np.cumsum(lens, out=rpn[1:])
+        frontier_src = (g, rpn, c, v)
+        parts.append(frontier_src)
+        known_g.append(g)
+    # merge the row sets, sort by global row id, restrict columns to L
+    allg = np.concatenate([p[0] for p in parts])
+    order = np.argsort(allg, kind="stable")
+    L = allg[order]
+    lens_all = np.concatenate([np.diff(p[1]) for p in parts])
+    offs_all = np.concatenate([[0], np.cumsum(lens_all)])
+    c_all = np.concatenate([p[2] for p in parts])
+    v_all = np.concatenate([p[3] for p in parts])
+    lens = lens_all[order]
+    idx = np.repeat(offs_all[:-1][order] - np.cumsum(lens) + lens, lens) + \
+        np.arange(int(lens.sum()))
+    c, v = c_all[idx], v_all[idx]
+    r = np.repeat(np.arange(len(L)), lens)
+    pos = np.searchsorted(L, c)
+    pos_c = np.minimum(pos, len(L) - 1)
+    keep = L[pos_c] == c
+    rpl = np.zeros(len(L) + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r[keep], minlength=len(L)), out=rpl[1:])
+    return L, rpl, pos_c[keep].astype(np.int64), v[keep]
+
+
+class RankGlobalPreconditioner:
+    """Owned rows of a rank-count-independent SPAI(1) (raw M or the CLI
+    symmetrisation S) in the reference's rank layout: M_ff (owned columns)
+    and M_fh (halo columns ordered like part.halo[rank]).  RankSystem
+    applies it with the halo exchange, like A."""
+
+    def __init__(self, M_ff, M_fh):
+        self.M_ff, self.M_fh = M_ff, M_fh
+
+
+def global_spai1_rank_preconditioner(A_ff, A_fh, part, rank, comm=None, symmetric=True):
+    """SPAI(1) of the GLOBAL matrix restricted to this rank's rows, from the
+    rank's own rows plus a one-time ghost-row exchange (gather_ghost_rows):
+    the result equals the single-rank spai1 (+ CLI symmetrisation) rows, so
+    iteration counts do not depend on the rank count -- the spai_scope
+    "global" of SURVEY 8(e) for user matrices (the reference's multi-rank
+    CLI uses the block-local spai1(A_FF), cli.py:239-240)."""
+    import torch
+    from .sparse import CsrMatrix, DeviceCsr, ptr, stream_handle
+    comm = comm if comm is not None else TorchComm()
+    L, rpl, cl, vl = gather_ghost_rows(A_ff, A_fh, part, rank, comm)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nL = len(L)
+    A = DeviceCsr(nL, nL, torch.from_numpy(rpl).to(dev),
+                  torch.from_numpy(cl.astype(np.int32)).to(dev), torch.from_numpy(vl).to(dev))
+    if not A.structurally_symmetric():
+        raise InvalidPartitionError("global SPAI(1) on a rank partition needs a structurally "
+                                    "symmetric pattern")
+    owned = np.asarray(part.owned[rank], dtype=np.int64)
+    halo = np.asarray(part.halo[rank], dtype=np.int64)
+    need = np.searchsorted(L, np.union1d(owned, halo))
+    cuts = np.flatnonzero(np.diff(need) != 1) + 1
+    cscptr, cscrow, csc2csr = A.csc()
+    cscval = A.csc_values()
+    m_csc = torch.zeros(A.nnz, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    wsb = lib.spai_assemble_workspace_bytes(nL)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    from .precond import _raise_assembly
+    for run in np.split(need, cuts):
+        bad, nfb = C.c_int64(-1), C.c_int64(0)
+        st = lib.spai_assemble_range(nL, A.nnz, ptr(A.rowptr), ptr(A.colidx), ptr(A.vals),
+                                     ptr(cscptr), ptr(cscrow), ptr(csc2csr), ptr(cscval),
+                                     int(run[0]), int(run[-1]) + 1, ptr(m_csc), ptr(ws), wsb,
+                                     C.byref(bad), C.byref(nfb), stream_handle())
+        _lib.check(st, "spai_assemble_range")
+        if st != _lib.SPAI_OK:
+            _raise_assembly(st, int(L[bad.value]))
+    out = torch.empty_like(m_csc)
+    fn = lib.spai_symmetrize if symmetric else lib.spai_csc_to_csr_values
+    _lib.check(fn(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(out), stream_handle()), "symmetrize")
+    vals = out.cpu().numpy()
+    # owned rows, columns to the (owned | halo) layout of extract_local_system
+    po = np.searchsorted(L, owned)
+    lens = rpl[po + 1] - rpl[po]
+    idx = np.repeat(rpl[po] - np.cumsum(lens) + lens, lens) + np.arange(int(lens.sum()))
+    r = np.repeat(np.arange(len(owned)), lens)
+    g = L[cl[idx]]
+    v = vals[idx]
+    is_own = np.isin(g, owned)
+    n = len(owned)
+    M_ff = CsrMatrix.from_coo(n, n, r[is_own], np.searchsorted(owned, g[is_own]), v[is_own])
+    hpos = {int(h): k for k, h in enumerate(halo)}
+    hcols = np.array([hpos[int(x)] for x in g[~is_own]], dtype=np.int64)
+    M_fh = CsrMatrix.from_coo(n, len(halo), r[~is_own], hcols, v[~is_own])
+    return RankGlobalPreconditioner(M_ff, M_fh)
 
 
 def fused_allreduce(comm, values, overlapped=False, rank=None):

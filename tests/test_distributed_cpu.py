@@ -199,3 +199,59 @@ def test_row_partitioned_bicgstab_matches_oracle(world):
     for _, r0, r1, xs, *_ in out:
         x[r0:r1] = xs
     assert np.max(np.abs(x - 1.0)) <= 1e-7
+
+
+def _ghost_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, REPO)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1911_01492_b200 as pb
+        from paper_1911_01492_b200.grids import Partition  # noqa: F401
+        import oracle
+        Ao = oracle.stencil_csr((12, 15), *oracle.q1_stencil(2))
+        A = pb.CsrMatrix(Ao.nrows, Ao.ncols, Ao.row_offsets, Ao.col_indices, Ao.values)
+        part = pb.partition_1d_strips(pb.StructuredGrid(12, 15), world)
+        A_ff, A_fh = pb.extract_local_system(A, part, rank)
+        L, rp, cl, vl = pb.gather_ghost_rows(A_ff, A_fh, part, rank, TorchComm())
+        q.put((rank, L, rp, cl, vl))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_ghost_row_exchange_collects_distance_three_rows(world):
+    """The one-time A-row exchange for global SPAI(1) on user matrices: each
+    rank ends with exactly the rows within graph distance 3 of its owned
+    rows (fetched from their owners, also across more than one neighbour
+    when strips are thin), as the principal submatrix of A on that set."""
+    import sys
+    sys.path.insert(0, REPO)
+    import oracle
+    import paper_1911_01492_b200 as pb
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ghost_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=300) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    Ao = oracle.stencil_csr((12, 15), *oracle.q1_stencil(2))
+    D = Ao.to_dense()
+    adj = D != 0
+    part = pb.partition_1d_strips(pb.StructuredGrid(12, 15), world)
+    for rank, L, rp, cl, vl in out:
+        reach = np.zeros(Ao.nrows, dtype=bool)
+        reach[part.owned[rank]] = True
+        for _ in range(3):
+            reach = reach | adj[reach].any(axis=0)
+        assert np.array_equal(L, np.flatnonzero(reach))
+        sub = D[np.ix_(L, L)]
+        got = np.zeros_like(sub)
+        got[np.repeat(np.arange(len(L)), np.diff(rp)), cl] = vl
+        assert np.array_equal(got, sub)

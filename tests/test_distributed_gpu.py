@@ -157,6 +157,24 @@ def _worker(rank, world, port, case, q):
             q.put((rank, r0, r1, x.cpu().numpy(), rec.iterations, list(rec.residual_norms),
                    rec.reductions_cum, rec.overlapped_cum, rec.total_reductions))
             return
+        if case in ("rank_global", "rank_global_raw"):
+            # user matrix on the reference's strip partition + global SPAI(1)
+            import oracle
+            Ao = oracle.stencil_csr((40, 36), *oracle.q1_stencil(2, eps=(1.0, 0.2)))
+            A = pb.CsrMatrix(Ao.nrows, Ao.ncols, Ao.row_offsets, Ao.col_indices, Ao.values)
+            part = pb.partition_1d_strips(pb.StructuredGrid(40, 36), world)
+            A_ff, A_fh = pb.extract_local_system(A, part, rank)
+            P = pb.global_spai1_rank_preconditioner(A_ff, A_fh, part, rank, TorchComm(),
+                                                    symmetric=(case == "rank_global"))
+            rs = pb.RankSystem(A_ff, A_fh, part, rank, M=P)
+            own = part.owned[rank]
+            b = pb.spmv(A, np.ones(A.nrows))
+            v = np.linspace(-1.0, 2.0, A.nrows)
+            zM = rs.apply_M(v[own])
+            x, rec = pb.solve(rs, b[own], pb.SolverConfig(tol=1e-10, maxit=2000))
+            q.put((rank, int(own[0]), int(own[-1]) + 1, x, rec.iterations,
+                   list(rec.residual_norms), zM, None))
+            return
         if case.startswith("overlap_"):
             # the same solves with and without the halo-overlapped SpMV
             from paper_1911_01492_b200.distributed import DistributedBiCGStab, _RankLoop
@@ -244,6 +262,33 @@ def test_row_partitioned_bicgstab_matches_device_order_oracle():
         assert st == 1 and len(h) == len(ho), (world, len(h), len(ho))
         assert np.max(np.abs(h - ho) / ho) <= 1e-8
         assert np.max(np.abs(x - xo)) <= 1e-10 * np.max(np.abs(xo))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_global_spai_for_user_matrices_on_rank_partition(world):
+    """spai_scope "global" through the reference multi-rank API on a user
+    matrix (no generator): after the one-time ghost-row exchange every
+    rank's rows of S equal the single-rank CLI S, so M r through the rank
+    protocol (with its halo) equals the global product, and the solve has
+    the single-rank iteration count and history."""
+    import oracle
+    Ao = oracle.stencil_csr((40, 36), *oracle.q1_stencil(2, eps=(1.0, 0.2)))
+    A = pb.CsrMatrix(Ao.nrows, Ao.ncols, Ao.row_offsets, Ao.col_indices, Ao.values)
+    S = pb.make_spai1_factory()(A).device_matrix()
+    b = pb.spmv(A, np.ones(A.nrows))
+    v = np.linspace(-1.0, 2.0, A.nrows)
+    zg = S.matvec(torch.from_numpy(v).cuda()).cpu().numpy()
+    x1, rec1 = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                        pb.SolverConfig(tol=1e-10, maxit=2000))
+    out = _run(world, "rank_global")
+    x = np.zeros(A.nrows)
+    for rank, r0, r1, xr, it, hist, zM, _ in out:
+        assert np.max(np.abs(zM - zg[r0:r1])) <= 1e-14 * np.max(np.abs(zg))
+        assert it == rec1.iterations
+        h1 = np.array(rec1.residual_norms)
+        assert np.max(np.abs(np.array(hist) - h1) / h1) <= 1e-8
+        x[r0:r1] = xr
+    assert np.max(np.abs(x - x1)) <= 1e-9
 
 
 @pytest.mark.parametrize("case", ["overlap_cg", "overlap_bl", "overlap_bicg"])
