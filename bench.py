@@ -327,7 +327,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         A = pb.q1_device(dims)
         n, nnz = A.nrows, A.nnz
-        b = A.matvec(torch.ones(n, dtype=torch.float64, device=dev))
+        b = A.matvec_csr(torch.ones(n, dtype=torch.float64, device=dev))
     stream.synchronize()
     cfg = pb.SolverConfig(tol=args.tol, maxit=args.maxit, variant=args.variant)
     launches = {"n": 0}
@@ -420,7 +420,7 @@ def run_ours(args):
                 "lsu_pipe_busy_pct_ncu": 91}
     solve_gbs = b_it * its / t_sol / 1e9
 
-    # ---- SpMV alone (K5 plain and TMA-staged) with CUDA events
+    # ---- SpMV alone (K5 formats) with CUDA events
     spmv = {}
     with torch.cuda.stream(stream):
         xx = torch.rand(n, dtype=torch.float64, device=dev)
@@ -431,9 +431,10 @@ def run_ours(args):
         if A.ssell_values() is not None:
             ssell_bytes = 8 * 32 * ((n + 31) // 32) * len(A.ssell_offsets()) + 16 * n
             kernels.insert(0, ("ssell", lambda: A.matvec_ssell(xx, out=yy), ssell_bytes))
+        # the public spmv()/apply() path dispatches to the half storage when
+        # built, else SELL-32 (DeviceCsr.matvec)
         for name, fn, sp_bytes in kernels + [
-                                   ("csr", lambda: A.matvec(xx, out=yy), csr_bytes),
-                                   ("csr_tma", lambda: A.matvec_tma(xx, out=yy), csr_bytes)]:
+                                   ("csr", lambda: A.matvec_csr(xx, out=yy), csr_bytes)]:
             for _ in range(3):
                 fn()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -734,7 +735,7 @@ def run_bicgstab(args):
     with torch.cuda.stream(stream):
         if world == 1:
             A = pb.q1_device(dims, conv=CD_CONV)
-            b = A.matvec(torch.ones(n, dtype=torch.float64, device=dev))
+            b = A.matvec_csr(torch.ones(n, dtype=torch.float64, device=dev))
             n_own = n
         else:
             part = SlabPartition(N, N * N, world)

@@ -174,19 +174,6 @@ int spai_symmetrize_union_fill(int64_t n, const int64_t* rowptr, const int32_t* 
 int spai_csr_spmv(int64_t n, int64_t nnz, const int64_t* rowptr,
                   const int32_t* colidx, const double* vals, const double* x,
                   double* y, void* stream);
-/* Row tiling for the TMA-staged SpMV (computed once per pattern).
- * ntiles_out is synchronous; tile_rows has ntiles+1 entries.               */
-int spai_tile_count(int64_t n, int64_t nnz, int64_t* ntiles_out);
-int spai_tile_rows(int64_t n, const int64_t* rowptr, int64_t ntiles,
-                   int64_t* tile_rows, int32_t* max_tile_nnz, void* stream);
-/* TMA-staged SpMV: each CTA streams the colidx/vals segment of its row tiles
- * into a shared-memory ring with cp.async.bulk (16-byte granules, so
- * colidx/vals must be 16-byte aligned and readable up to the next 16 bytes
- * past nnz -- true for every cudaMalloc/torch allocation).                */
-int spai_csr_spmv_tma(int64_t n, const int64_t* rowptr, const int32_t* colidx,
-                      const double* vals, const int64_t* tile_rows,
-                      int64_t ntiles, int32_t max_tile_nnz, const double* x,
-                      double* y, void* stream);
 
 /* ------------------------------------------------------------------ K6/K7
  * Deterministic fused dot products (LocalSystem.fused_dots,
@@ -224,12 +211,6 @@ int spai_sell_fill_vals(int64_t n, const int64_t* rowptr, const int32_t* colidx,
 int spai_sell_spmv(int64_t n, int64_t ncols, const int64_t* sliceptr,
                    const int64_t* cdesc, const int32_t* cols, const double* vals,
                    const double* x, double* y, void* stream);
-/* TMA-staged SELL-32 SpMV: one persistent CTA of 8 warps per SM, each warp
- * streams its slices with cp.async.bulk into a 2-stage shared-memory ring.
- * wmax = widest slice (in slots); needs 8*2*wmax*384 B <= 200 KB.          */
-int spai_sell_spmv_tma(int64_t n, int64_t ncols, const int64_t* sliceptr,
-                       const int64_t* cdesc, const int32_t* cols, const double* vals,
-                       int wmax, const double* x, double* y, void* stream);
 
 /* ------------------------------------------------------------------ K5c
  * Symmetric half-storage SELL-32 (the apply_A / apply_M of a numerically
@@ -253,11 +234,6 @@ int spai_ssell_fill(int64_t n, const int64_t* rowptr, const int32_t* colidx,
                     int* is_symmetric, void* stream);
 int spai_ssell_spmv(int64_t n, const int32_t* g, int w, const double* U,
                     const double* x, double* y, void* stream);
-/* Same product; each warp streams its next slices' upper values into a
- * shared-memory ring with cp.async.bulk (TMA) while it gathers.  w must be
- * 3, 5 or 14 (other widths use spai_ssell_spmv).                          */
-int spai_ssell_spmv_tma(int64_t n, const int32_t* g, int w, const double* U,
-                          const double* x, double* y, void* stream);
 
 /* ------------------------------------------------------------------ K8
  * Device-resident classic PCG (replaces _solve_classic, krylov.py:301-345)
@@ -277,12 +253,6 @@ int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* sliceptr,
 int spai_pcg_create_sym(spai_pcg** out, int64_t n, const int32_t* g, int w,
                         const double* A_U, const double* M_U, double tol,
                         int64_t maxit, void* ws, size_t ws_bytes, void* stream);
-/* 0 (default): 4 kernels per iteration (vector updates in their own
- * kernels, one gather per stored entry); 1: 2 kernels (vector updates
- * recomputed inside the SpMV gathers).  Same arithmetic, same results.    */
-int spai_pcg_set_fused(spai_pcg* s, int fused);
-/* 1 (default when the widest slice fits): U1/U2 stream SELL slices with TMA. */
-int spai_pcg_set_tma(spai_pcg* s, int tma);
 /* Start from x0 (device, may be NULL -> zero); b device, copied.          */
 int spai_pcg_start(spai_pcg* s, const double* b, const double* x0);
 /* Enqueue up to `iters` more iterations (no host sync; CUDA graphs of 16). */

@@ -119,9 +119,6 @@ _SIGS = {
     "spai_symmetrize_union_fill": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                           _vp]),
     "spai_csr_spmv": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "spai_tile_count": (_i32, [_i64, _i64, C.POINTER(_i64)]),
-    "spai_tile_rows": (_i32, [_i64, _vp, _i64, _vp, _vp, _vp]),
-    "spai_csr_spmv_tma": (_i32, [_i64, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp]),
     "spai_dots_workspace_bytes": (_sz, [_i64]),
     "spai_fused_dots": (_i32, [_i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "spai_axpby": (_i32, [_i64, _dbl, _vp, _dbl, _vp, _vp]),
@@ -132,12 +129,10 @@ _SIGS = {
     "spai_sell_fill_cols": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_sell_fill_vals": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_sell_spmv": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "spai_sell_spmv_tma": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "spai_ssell_offsets": (_i32, [_i64, _vp, _vp, _vp, C.POINTER(_i32), _vp]),
     "spai_ssell_vals_count": (_sz, [_i64, _i32]),
     "spai_ssell_fill": (_i32, [_i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, C.POINTER(_i32), _vp]),
     "spai_ssell_spmv": (_i32, [_i64, _vp, _i32, _vp, _vp, _vp, _vp]),
-    "spai_ssell_spmv_tma": (_i32, [_i64, _vp, _i32, _vp, _vp, _vp, _vp]),
     "spai_pcg_create_sym": (_i32, [C.POINTER(_vp), _i64, _vp, _i32, _vp, _vp, _dbl, _i64, _vp,
                                    _sz, _vp]),
     "spai_cgv_workspace_bytes": (_sz, [_i64, _i64]),
@@ -152,8 +147,6 @@ _SIGS = {
     "spai_pcg_workspace_bytes": (_sz, [_i64, _i64]),
     "spai_pcg_create": (_i32, [C.POINTER(_vp), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                _dbl, _i64, _vp, _sz, _vp]),
-    "spai_pcg_set_fused": (_i32, [_vp, _i32]),
-    "spai_pcg_set_tma": (_i32, [_vp, _i32]),
     "spai_pcg_start": (_i32, [_vp, _vp, _vp]),
     "spai_pcg_advance": (_i32, [_vp, _i64]),
     "spai_pcg_poll": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_dbl),

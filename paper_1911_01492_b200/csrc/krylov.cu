@@ -1,15 +1,13 @@
 // K8: device-resident classic PCG (replaces _solve_classic, krylov.py:301-345).
 //
-// One iteration = two fused SELL-32 kernels, no host synchronisation:
-//   K1  p' = z + beta p (gathered on the fly), q = A p', [(p',q)]     (+ [(p,r),(r,r)] at it 1)
-//   K2  x += lambda p, r' = r - lambda q, z = M r' (gathered on the fly), [(z,r'),(r',r')]
-// The gathered operands are recomputed with the same fma the owning row uses,
-// so they are bit-identical to the stored vectors.  The last block of each
-// kernel reduces the partial dots in a fixed order (deterministic) and runs
-// the scalar recurrence (lambda, beta, breakdown / divergence / convergence
-// tests) on the device; a status word turns later launches into no-ops, so a
-// CUDA graph of 16 iterations is replayed blindly and the host only polls
-// between graphs.
+// One iteration = four kernels, no host synchronisation (V1 / U1 / V2 / U2
+// below).  The reducing kernels' last block sums the partial dots in a fixed
+// order (deterministic) and runs the scalar recurrence (lambda, beta,
+// breakdown / divergence / convergence tests) on the device; a status word
+// turns later launches into no-ops, so a CUDA graph of 16 iterations is
+// replayed blindly and the host only polls between graphs.  (A 2-kernel form
+// that recomputes p' and r' inside the SpMV gathers, and TMA-staged slices,
+// both measured slower on B200 and were removed -- DESIGN.md.)
 #include "ops.cuh"
 
 namespace spai {
@@ -35,120 +33,7 @@ struct PcgVecs {
   double* partials;
 };
 
-template <bool FIRST>
-__device__ __forceinline__ void k1_body(int64_t n, int64_t nslices, const Sell& A,
-                                        const PcgVecs& v, const PcgScal* sc, double (&acc)[3]) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
-  const int pc = sc->pcur;
-  const double* __restrict__ pold = pc ? v.p1 : v.p0;
-  double* __restrict__ pnew = pc ? v.p0 : v.p1;
-  const double* __restrict__ z = v.z;
-  const double* __restrict__ r = sc->rcur ? v.r1 : v.r0;
-  const double beta = sc->beta;
-  for (int64_t s = w0; s < nslices; s += nw) {
-    double q;
-    if (FIRST) q = sell_row(A, s, lane, [&](int32_t j) { return __ldg(pold + j); });
-    else q = sell_row(A, s, lane, [&](int32_t j) { return fma(beta, __ldg(pold + j), __ldg(z + j)); });
-    const int64_t i = s * kSell + lane;
-    if (i < n) {
-      v.q[i] = q;
-      double pi;
-      if (FIRST) {
-        pi = pold[i];
-        const double ri = r[i];
-        acc[1] = fma(pi, ri, acc[1]);
-        acc[2] = fma(ri, ri, acc[2]);
-      } else {
-        pi = fma(beta, pold[i], z[i]);
-        pnew[i] = pi;
-      }
-      acc[0] = fma(pi, q, acc[0]);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kSpmvThreads)
-pcg_k1(int64_t n, int64_t nslices, Sell A, PcgVecs v, PcgScal* sc) {
-  if (sc->status != kRunning) return;
-  const bool first = sc->it == 0;
-  double acc[3] = {0.0, 0.0, 0.0};
-  if (first) k1_body<true>(n, nslices, A, v, sc, acc);
-  else k1_body<false>(n, nslices, A, v, sc, acc);
-  grid_finalize<3>(acc, v.partials, &sc->ticket1, [&](double (&tot)[3]) {
-    double rho;
-    const double delta = tot[0];
-    if (first) {
-      rho = tot[1];
-      sc->rho = rho;
-      sc->norm0 = sqrt(tot[2]);
-      sc->it = 1;
-      if (sc->norm0 == 0.0) { sc->norm = 0.0; sc->status = kConverged; return; }
-    } else {
-      rho = sc->rho;
-      sc->it += 1;
-      sc->pcur ^= 1;
-    }
-    if (!isfinite(delta) || !isfinite(rho)) { sc->status = kDivergence; return; }
-    if (delta <= 0.0) {
-      if (rho == 0.0) {
-        if (first) sc->norm = sc->norm0;
-        sc->status = kConverged;
-      } else {
-        sc->aux = delta;
-        sc->status = kBreakdown;
-      }
-      return;
-    }
-    sc->lambda = rho / delta;
-  });
-}
-
-template <bool HAS_M>
-__global__ void __launch_bounds__(kSpmvThreads)
-pcg_k2(int64_t n, int64_t nslices, Sell M, PcgVecs v, PcgScal* sc) {
-  if (sc->status != kRunning) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
-  const double lambda = sc->lambda;
-  const int rc = sc->rcur;
-  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
-  const double* __restrict__ rold = rc ? v.r1 : v.r0;
-  double* __restrict__ rnew = rc ? v.r0 : v.r1;
-  const double* __restrict__ q = v.q;
-  double acc[2] = {0.0, 0.0};
-  for (int64_t s = w0; s < nslices; s += nw) {
-    double zi = 0.0;
-    if (HAS_M)
-      zi = sell_row(M, s, lane, [&](int32_t j) { return fma(-lambda, __ldg(q + j), __ldg(rold + j)); });
-    const int64_t i = s * kSell + lane;
-    if (i < n) {
-      const double rn = fma(-lambda, q[i], rold[i]);
-      rnew[i] = rn;
-      v.x[i] = fma(lambda, p[i], v.x[i]);
-      if (!HAS_M) zi = rn;
-      v.z[i] = zi;
-      acc[0] = fma(zi, rn, acc[0]);
-      acc[1] = fma(rn, rn, acc[1]);
-    }
-  }
-  grid_finalize<2>(acc, v.partials, &sc->ticket2, [&](double (&tot)[2]) {
-    const double rho_new = tot[0], rr = tot[1];
-    sc->rcur ^= 1;
-    if (!isfinite(rho_new) || !isfinite(rr)) { sc->status = kDivergence; return; }
-    const double norm = sqrt(rr);
-    v.hist[sc->it - 1] = norm;
-    sc->norm = norm;
-    sc->beta = rho_new / sc->rho;
-    sc->rho = rho_new;
-    if (norm <= sc->tol * sc->norm0) sc->status = kConverged;
-    else if (sc->it >= sc->maxit) sc->status = kMaxit;
-  });
-}
-
-// ---- unfused variant: vector updates in their own kernels, one gather per nnz
+// ---- vector updates in their own kernels, one gather per stored value
 // V1: p' = z + beta p (it >= 2)          U1: q = A p', [(p',q)] (+ [(p,r),(r,r)] at it 1)
 // V2: x += lambda p, r' = r - lambda q    U2: z = M r', [(z,r'),(r',r')]
 __global__ void __launch_bounds__(kSpmvThreads)
@@ -267,93 +152,6 @@ pcg_u2(int64_t n, int64_t nslices, OP M, PcgVecs v, PcgScal* sc) {
   });
 }
 
-// ---- TMA-staged versions of U1 / U2 (persistent: one CTA of 8 warps per SM)
-__global__ void __launch_bounds__(kTmaWarps * 32)
-pcg_u1_tma(int64_t n, int64_t nslices, Sell A, int wmax, PcgVecs v, PcgScal* sc) {
-  if (sc->status != kRunning) return;
-  extern __shared__ __align__(128) unsigned char tsm[];
-  const bool first = sc->it == 0;
-  const int lane = threadIdx.x & 31;
-  const int pc = first ? sc->pcur : (sc->pcur ^ 1);
-  const double* __restrict__ p = pc ? v.p1 : v.p0;
-  const double* __restrict__ r = sc->rcur ? v.r1 : v.r0;
-  double acc[3] = {0.0, 0.0, 0.0};
-  sell_tma_loop(nslices, A, wmax, tsm + (threadIdx.x >> 5) * SellTmaSmem::warp_bytes(wmax),
-                [&](int32_t j) { return __ldg(p + j); },
-                [&](int64_t s, double q) {
-                  const int64_t i = s * kSell + lane;
-                  if (i < n) {
-                    v.q[i] = q;
-                    const double pi = p[i];
-                    acc[0] = fma(pi, q, acc[0]);
-                    if (first) {
-                      const double ri = r[i];
-                      acc[1] = fma(pi, ri, acc[1]);
-                      acc[2] = fma(ri, ri, acc[2]);
-                    }
-                  }
-                });
-  grid_finalize<3>(acc, v.partials, &sc->ticket1, [&](double (&tot)[3]) {
-    double rho;
-    const double delta = tot[0];
-    if (first) {
-      rho = tot[1];
-      sc->rho = rho;
-      sc->norm0 = sqrt(tot[2]);
-      sc->it = 1;
-      if (sc->norm0 == 0.0) { sc->norm = 0.0; sc->status = kConverged; return; }
-    } else {
-      rho = sc->rho;
-      sc->it += 1;
-      sc->pcur ^= 1;
-    }
-    if (!isfinite(delta) || !isfinite(rho)) { sc->status = kDivergence; return; }
-    if (delta <= 0.0) {
-      if (rho == 0.0) {
-        if (first) sc->norm = sc->norm0;
-        sc->status = kConverged;
-      } else {
-        sc->aux = delta;
-        sc->status = kBreakdown;
-      }
-      return;
-    }
-    sc->lambda = rho / delta;
-  });
-}
-
-__global__ void __launch_bounds__(kTmaWarps * 32)
-pcg_u2_tma(int64_t n, int64_t nslices, Sell M, int wmax, PcgVecs v, PcgScal* sc) {
-  if (sc->status != kRunning) return;
-  extern __shared__ __align__(128) unsigned char tsm[];
-  const int lane = threadIdx.x & 31;
-  const double* __restrict__ rnew = sc->rcur ? v.r0 : v.r1;
-  double acc[2] = {0.0, 0.0};
-  sell_tma_loop(nslices, M, wmax, tsm + (threadIdx.x >> 5) * SellTmaSmem::warp_bytes(wmax),
-                [&](int32_t j) { return __ldg(rnew + j); },
-                [&](int64_t s, double zi) {
-                  const int64_t i = s * kSell + lane;
-                  if (i < n) {
-                    const double rn = rnew[i];
-                    v.z[i] = zi;
-                    acc[0] = fma(zi, rn, acc[0]);
-                    acc[1] = fma(rn, rn, acc[1]);
-                  }
-                });
-  grid_finalize<2>(acc, v.partials, &sc->ticket2, [&](double (&tot)[2]) {
-    const double rho_new = tot[0], rr = tot[1];
-    sc->rcur ^= 1;
-    if (!isfinite(rho_new) || !isfinite(rr)) { sc->status = kDivergence; return; }
-    const double norm = sqrt(rr);
-    v.hist[sc->it - 1] = norm;
-    sc->norm = norm;
-    sc->beta = rho_new / sc->rho;
-    sc->rho = rho_new;
-    if (norm <= sc->tol * sc->norm0) sc->status = kConverged;
-    else if (sc->it >= sc->maxit) sc->status = kMaxit;
-  });
-}
-
 // ---- external preconditioner (multigrid V-cycle, K11): r lives in r0 (no
 // double buffering), z = V(r) is written by the V-cycle kernels between V2ext
 // and Zext, p alternates as usual.
@@ -391,15 +189,6 @@ pcg_z_ext(int64_t n, PcgVecs v, PcgScal* sc) {
     if (norm <= sc->tol * sc->norm0) sc->status = kConverged;
     else if (sc->it >= sc->maxit) sc->status = kMaxit;
   });
-}
-
-__global__ void width_max_kernel(int64_t nslices, const int64_t* sliceptr, int* out) {
-  int m = 0;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices;
-       s += (int64_t)gridDim.x * blockDim.x)
-    m = max(m, (int)((sliceptr[s + 1] - sliceptr[s]) >> 5));
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 // start: r = b - A x0 (or b), p = M r (or r)
@@ -458,10 +247,6 @@ struct spai_pcg {
   PcgScal* sc = nullptr;
   PcgScal* host_init = nullptr;
   unsigned blocks1 = 1, blocks2 = 1, vblocks = 1;
-  bool fused = false;   // measured on B200: 4 single-gather kernels beat 2 double-gather ones
-  bool tma = false;     // TMA-staged SELL slices (set when the stage fits in smem)
-  int wmaxA = 0, wmaxM = 0;
-  size_t smemA = 0, smemM = 0;
   bool sym = false;     // symmetric half-storage operators (ssell.cuh) for A and M
   SymSell As{}, Ms{};
   unsigned sblocks = 1;
@@ -514,30 +299,12 @@ static int launch_iteration(spai_pcg* s) {
     SPAI_LAUNCH_CHECK("pcg symmetric iteration");
     return SPAI_OK;
   }
-  if (!s->fused && s->tma) {
-    const unsigned g = (unsigned)num_sms();
-    pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
-    pcg_u1_tma<<<g, kTmaWarps * 32, s->smemA, s->stream>>>(s->n, s->nslices, s->A, s->wmaxA, s->v, s->sc);
-    pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
-    if (s->hasM) pcg_u2_tma<<<g, kTmaWarps * 32, s->smemM, s->stream>>>(s->n, s->nslices, s->M, s->wmaxM, s->v, s->sc);
-    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
-    SPAI_LAUNCH_CHECK("pcg unfused TMA iteration");
-    return SPAI_OK;
-  }
-  if (!s->fused) {
-    pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
-    pcg_u1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->A}, s->v, s->sc);
-    pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
-    if (s->hasM) pcg_u2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
-    else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
-    SPAI_LAUNCH_CHECK("pcg unfused iteration");
-    return SPAI_OK;
-  }
-  pcg_k1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->A, s->v, s->sc);
-  SPAI_LAUNCH_CHECK("pcg_k1");
-  if (s->hasM) pcg_k2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
-  else pcg_k2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, s->M, s->v, s->sc);
-  SPAI_LAUNCH_CHECK("pcg_k2");
+  pcg_v1<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  pcg_u1<<<s->blocks1, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->A}, s->v, s->sc);
+  pcg_v2<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  if (s->hasM) pcg_u2<true><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
+  else pcg_u2<false><<<s->blocks2, kSpmvThreads, 0, s->stream>>>(s->n, s->nslices, SellOp{s->M}, s->v, s->sc);
+  SPAI_LAUNCH_CHECK("pcg iteration");
   return SPAI_OK;
 }
 
@@ -578,9 +345,9 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
   }
   static unsigned b1 = 0, b2t = 0, b2f = 0;
   if (!b1) {
-    b1 = sell_blocks((const void*)pcg_k1, 1 << 30);
-    b2t = sell_blocks((const void*)pcg_k2<true>, 1 << 30);
-    b2f = sell_blocks((const void*)pcg_k2<false>, 1 << 30);
+    b1 = sell_blocks((const void*)pcg_u1<SellOp>, 1 << 30);
+    b2t = sell_blocks((const void*)pcg_u2<true, SellOp>, 1 << 30);
+    b2f = sell_blocks((const void*)pcg_u2<false, SellOp>, 1 << 30);
   }
   const int64_t need64 = (s->nslices * 32 + kSpmvThreads - 1) / kSpmvThreads;
   const unsigned need = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need64, 1 << 30));
@@ -588,32 +355,6 @@ extern "C" int spai_pcg_create(spai_pcg** out, int64_t n, const int64_t* slicept
   s->blocks2 = std::min(s->hasM ? b2t : b2f, need);
   s->vblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kSpmvThreads - 1) / kSpmvThreads,
                                                                 (int64_t)num_sms() * 8));
-  {
-    const char* e = getenv("SPAI_PCG_FUSED");
-    if (e && *e) s->fused = *e != '0';
-  }
-  {  // TMA staging: needs the widest slice of A (and M) to fit a 2-stage ring per warp
-    int* d = small_scratch();
-    if (!d) { delete s; set_error("scratch allocation failed"); return SPAI_E_CUDA; }
-    SPAI_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(int), s->stream));
-    const unsigned wb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((s->nslices + 255) / 256, num_sms() * 8));
-    width_max_kernel<<<wb, 256, 0, s->stream>>>(s->nslices, s->A.sliceptr, d);
-    if (s->hasM) width_max_kernel<<<wb, 256, 0, s->stream>>>(s->nslices, s->M.sliceptr, d + 1);
-    int h[2] = {0, 0};
-    SPAI_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
-    SPAI_CUDA(cudaStreamSynchronize(s->stream));
-    s->wmaxA = std::max(h[0], 1);
-    s->wmaxM = std::max(h[1], 1);
-    s->smemA = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(s->wmaxA);
-    s->smemM = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(s->wmaxM);
-    const char* e = getenv("SPAI_PCG_TMA");
-    const bool want = e && *e == '1';   // measured slower than the LDG SELL path
-    s->tma = want && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024 && s->nslices >= 148 * 8;
-    if (s->tma) {
-      SPAI_CUDA(cudaFuncSetAttribute(pcg_u1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemA));
-      SPAI_CUDA(cudaFuncSetAttribute(pcg_u2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemM));
-    }
-  }
   if (std::max(s->blocks1, s->blocks2) > (unsigned)num_sms() * 32) {
     set_error("grid larger than the partials buffer");
     delete s;
@@ -665,24 +406,6 @@ extern "C" int spai_pcg_set_preconditioner_mg(spai_pcg* s, const spai_mg* mg) {
   if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
   s->mg = mg;
   s->hasM = false;
-  s->fused = false;
-  s->tma = false;
-  return SPAI_OK;
-}
-
-extern "C" int spai_pcg_set_fused(spai_pcg* s, int fused) {
-  if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
-  s->fused = fused != 0 && !s->sym && !s->mg;
-  return SPAI_OK;
-}
-
-extern "C" int spai_pcg_set_tma(spai_pcg* s, int tma) {
-  if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
-  s->tma = tma != 0 && !s->sym && !s->mg && s->smemA <= 200 * 1024 && s->smemM <= 200 * 1024;
-  if (s->tma) {
-    SPAI_CUDA(cudaFuncSetAttribute(pcg_u1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemA));
-    SPAI_CUDA(cudaFuncSetAttribute(pcg_u2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smemM));
-  }
   return SPAI_OK;
 }
 

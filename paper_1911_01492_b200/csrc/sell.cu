@@ -151,18 +151,6 @@ sell_spmv_kernel(int64_t n, int64_t nslices, Sell A, const double* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(kTmaWarps * 32)
-sell_spmv_tma_kernel(int64_t n, int64_t nslices, Sell A, int wmax, const double* __restrict__ x,
-                     double* __restrict__ y) {
-  extern __shared__ __align__(128) unsigned char tsm[];
-  const int lane = threadIdx.x & 31;
-  sell_tma_loop(nslices, A, wmax, tsm + (threadIdx.x >> 5) * SellTmaSmem::warp_bytes(wmax),
-                [&](int32_t j) { return __ldg(x + j); },
-                [&](int64_t s, double acc) {
-                  const int64_t r = s * kSell + lane;
-                  if (r < n) y[r] = acc;
-                });
-}
 
 unsigned sell_blocks(const void* kern, int64_t nslices) {
   int per_sm = 0;
@@ -256,19 +244,6 @@ extern "C" int spai_sell_fill_vals(int64_t n, const int64_t* rowptr, const int32
   return SPAI_OK;
 }
 
-extern "C" int spai_sell_spmv_tma(int64_t n, int64_t ncols, const int64_t* sliceptr,
-                                  const int64_t* cdesc, const int32_t* cols, const double* vals,
-                                  int wmax, const double* x, double* y, void* stream) {
-  const int64_t ns = spai_sell_nslices(n);
-  if (ns == 0) return SPAI_OK;
-  const size_t smem = (size_t)kTmaWarps * SellTmaSmem::warp_bytes(wmax);
-  if (smem > 200 * 1024) { set_error("slice width %d too large for the TMA ring", wmax); return SPAI_E_UNSUPPORTED; }
-  SPAI_CUDA(cudaFuncSetAttribute(sell_spmv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  sell_spmv_tma_kernel<<<num_sms(), kTmaWarps * 32, smem, (cudaStream_t)stream>>>(
-      n, ns, Sell{sliceptr, cdesc, cols, vals, ncols}, wmax, x, y);
-  SPAI_LAUNCH_CHECK("sell_spmv_tma_kernel");
-  return SPAI_OK;
-}
 
 extern "C" int spai_sell_spmv(int64_t n, int64_t ncols, const int64_t* sliceptr,
                               const int64_t* cdesc, const int32_t* cols, const double* vals,

@@ -129,118 +129,3 @@ extern "C" int spai_axpby(int64_t n, double a, const double* x, double b, double
   SPAI_LAUNCH_CHECK("axpby_kernel");
   return SPAI_OK;
 }
-
-// ---------------------------------------------------------------- TMA SpMV
-namespace spai {
-
-constexpr int kTmaStages = 4;
-
-template <int L>
-__global__ void __launch_bounds__(kSpmvThreads)
-spmv_tma_kernel(Csr A, const int64_t* __restrict__ tile_rows, int64_t ntiles, int sv_cap,
-                int sc_cap, const double* __restrict__ x, double* __restrict__ y) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kTmaStages;
-  double* sv = reinterpret_cast<double*>(smem + 128);
-  int32_t* sc = reinterpret_cast<int32_t*>(sv + (size_t)kTmaStages * sv_cap);
-  constexpr int kWarps = kSpmvThreads / 32;
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const int64_t cnt = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto issue = [&](int64_t i) {
-    const int s = (int)(i % kTmaStages);
-    const int64_t t = blockIdx.x + i * gridDim.x;
-    const int64_t e0 = A.rowptr[tile_rows[t]], e1 = A.rowptr[tile_rows[t + 1]];
-    const int64_t a0 = e0 & ~1LL, a1 = (e1 + 1) & ~1LL;
-    const int64_t c0 = e0 & ~3LL, c1 = (e1 + 3) & ~3LL;
-    const uint32_t bv = (uint32_t)((a1 - a0) * 8), bc = (uint32_t)((c1 - c0) * 4);
-    mbar_arrive_expect_tx(&full[s], bv + bc);
-    if (bv) bulk_g2s(sv + (size_t)s * sv_cap, A.vals + a0, bv, &full[s]);
-    if (bc) bulk_g2s(sc + (size_t)s * sc_cap, A.colidx + c0, bc, &full[s]);
-  };
-  if (threadIdx.x == 0)
-    for (int64_t i = 0; i < cnt && i < kTmaStages; ++i) issue(i);
-  const int sub = threadIdx.x & (L - 1);
-  const int grp = threadIdx.x / L;
-  constexpr int kGroups = kSpmvThreads / L;
-  for (int64_t i = 0; i < cnt; ++i) {
-    const int s = (int)(i % kTmaStages);
-    const uint32_t phase = (uint32_t)((i / kTmaStages) & 1);
-    const int64_t t = blockIdx.x + i * gridDim.x;
-    const int64_t r0 = tile_rows[t], r1 = tile_rows[t + 1];
-    const int64_t e0 = A.rowptr[r0];
-    const int64_t a0 = e0 & ~1LL, c0 = e0 & ~3LL;
-    const double* __restrict__ tv = sv + (size_t)s * sv_cap - a0;
-    const int32_t* __restrict__ tc = sc + (size_t)s * sc_cap - c0;
-    mbar_wait(&full[s], phase);
-    const int wg0 = grp - ((threadIdx.x & 31) / L);   // first group of this warp
-    for (int64_t rw = r0 + wg0; rw < r1; rw += kGroups) {   // warp-uniform trip count
-      const int64_t r = rw + (grp - wg0);
-      const bool valid = r < r1;
-      const int64_t lo = valid ? A.rowptr[r] : 0, hi = valid ? A.rowptr[r + 1] : 0;
-      double acc = 0.0, acc2 = 0.0;
-      int64_t e = lo + sub;
-      for (; e + L < hi; e += 2 * L) {
-        acc = fma(tv[e], __ldg(x + tc[e]), acc);
-        acc2 = fma(tv[e + L], __ldg(x + tc[e + L]), acc2);
-      }
-      if (e < hi) acc = fma(tv[e], __ldg(x + tc[e]), acc);
-      acc = group_sum<L>(acc + acc2);
-      if (valid && sub == 0) y[r] = acc;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (threadIdx.x == 0 && i + kTmaStages < cnt) {
-      mbar_wait(&empty[s], phase);
-      issue(i + kTmaStages);
-    }
-  }
-}
-
-template <int L>
-static int launch_tma(int64_t n, Csr A, const int64_t* tile_rows, int64_t ntiles, int maxnnz,
-                      const double* x, double* y, cudaStream_t s) {
-  const int sv_cap = ((maxnnz + 2 + 1) / 2) * 2 + 2;
-  const int sc_cap = ((maxnnz + 4 + 3) / 4) * 4 + 4;
-  const size_t smem = 128 + (size_t)kTmaStages * (sv_cap * 8 + sc_cap * 4);
-  if (smem > 220 * 1024) { set_error("tile too large for shared memory (%d nnz)", maxnnz); return SPAI_E_UNSUPPORTED; }
-  auto kern = spmv_tma_kernel<L>;
-  SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  SPAI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpmvThreads, smem));
-  if (per_sm < 1) per_sm = 1;
-  int64_t blocks = std::min<int64_t>(ntiles, (int64_t)num_sms() * per_sm);
-  if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, kSpmvThreads, smem, s>>>(A, tile_rows, ntiles, sv_cap, sc_cap, x, y);
-  SPAI_LAUNCH_CHECK("spmv_tma_kernel");
-  (void)n;
-  return SPAI_OK;
-}
-
-}  // namespace spai
-
-extern "C" int spai_csr_spmv_tma(int64_t n, const int64_t* rowptr, const int32_t* colidx,
-                                 const double* vals, const int64_t* tile_rows, int64_t ntiles,
-                                 int32_t max_tile_nnz, const double* x, double* y,
-                                 void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  if (n == 0) return SPAI_OK;
-  if (((uintptr_t)vals & 15) || ((uintptr_t)colidx & 15)) {
-    set_error("spai_csr_spmv_tma needs 16-byte aligned colidx/vals");
-    return SPAI_E_ARG;
-  }
-  Csr A{rowptr, colidx, vals};
-  const int64_t nnz_est = (int64_t)ntiles * 2048;
-  switch (lanes_for(n, nnz_est < n ? n : nnz_est)) {
-    case 2: return launch_tma<2>(n, A, tile_rows, ntiles, max_tile_nnz, x, y, s);
-    case 4: return launch_tma<4>(n, A, tile_rows, ntiles, max_tile_nnz, x, y, s);
-    case 8: return launch_tma<8>(n, A, tile_rows, ntiles, max_tile_nnz, x, y, s);
-    case 16: return launch_tma<16>(n, A, tile_rows, ntiles, max_tile_nnz, x, y, s);
-    default: return launch_tma<32>(n, A, tile_rows, ntiles, max_tile_nnz, x, y, s);
-  }
-}

@@ -106,19 +106,6 @@ ssell_spmv_kernel(int64_t n, int64_t nslices, SymSell A, const double* __restric
   }
 }
 
-template <int W>
-__global__ void __launch_bounds__(kSymTmaWarps * 32, 3)
-ssell_spmv_tma_kernel(int64_t n, int64_t nslices, SymSell A, const double* __restrict__ x,
-                      double* __restrict__ y) {
-  extern __shared__ __align__(128) unsigned char ssm[];
-  const int lane = threadIdx.x & 31;
-  ssell_tma_loop<W>(nslices, A, ssm, [&](int32_t j) { return __ldg(x + j); },
-                    [&](int64_t s, double v) {
-                      const int64_t i = s * kSell + lane;
-                      if (i < n) y[i] = v;
-                    });
-}
-
 // Grid of the symmetric kernels: at most one resident wave (a second wave
 // would process its slices after the first one finished, far outside the L2
 // reuse window of the lower-triangle reads), and fewer resident warps than
@@ -236,31 +223,3 @@ extern "C" int spai_ssell_spmv(int64_t n, const int32_t* g, int w, const double*
   return SPAI_OK;
 }
 
-// grid of a TMA-staged symmetric kernel: resident blocks only (<= bps per SM)
-unsigned ssell_tma_blocks(const void* kern, size_t smem, int64_t nslices) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSymTmaWarps * 32, smem);
-  per_sm = std::max(1, per_sm);
-  int64_t b = (nslices + kSymTmaWarps - 1) / kSymTmaWarps;
-  const int64_t cap = (int64_t)num_sms() * per_sm;
-  if (b > cap) b = cap;
-  if (b < 1) b = 1;
-  return (unsigned)b;
-}
-
-extern "C" int spai_ssell_spmv_tma(int64_t n, const int32_t* g, int w, const double* U,
-                                   const double* x, double* y, void* stream) {
-  SymSell A;
-  if (!make_symsell(g, w, U, n, &A)) { set_error("ssell: bad offset table"); return SPAI_E_ARG; }
-  const int64_t ns = (n + kSell - 1) / kSell;
-  if (ns == 0) return SPAI_OK;
-  if (w != 14 && w != 5 && w != 3) return spai_ssell_spmv(n, g, w, U, x, y, stream);
-  const size_t smem = (size_t)kSymTmaWarps * ssell_tma_warp_bytes(w);
-  SPAI_SSELL_DISPATCH(w, if constexpr (WM > 0) {
-    SPAI_CUDA(cudaFuncSetAttribute(ssell_spmv_tma_kernel<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const unsigned b = ssell_tma_blocks((const void*)ssell_spmv_tma_kernel<WM>, smem, ns);
-    ssell_spmv_tma_kernel<WM><<<b, kSymTmaWarps * 32, smem, (cudaStream_t)stream>>>(n, ns, A, x, y);
-  });
-  SPAI_LAUNCH_CHECK("ssell_spmv_tma_kernel");
-  return SPAI_OK;
-}

@@ -147,64 +147,6 @@ __device__ __forceinline__ double ssell_row(const SymSell& A, int64_t s, int lan
   return ssell_row_generic(A, up, row0, lane, xf);
 }
 
-// ---- TMA-staged variant: lane 0 of every warp streams its next slices' upper
-// values (one contiguous 32 w x 8 B block per slice) into a 2-stage
-// shared-memory ring with cp.async.bulk, so the HBM latency of the values is
-// hidden without registers; the warp only waits on the L2-resident gathers.
-constexpr int kSymTmaStages = 2;
-constexpr int kSymTmaWarps = 8;
-
-__host__ __device__ __forceinline__ size_t ssell_tma_warp_bytes(int w) {
-  return 64 + (size_t)kSymTmaStages * w * kSell * sizeof(double);
-}
-
-template <int W, class XF, class EPI>
-__device__ __forceinline__ void ssell_tma_loop(int64_t nslices, const SymSell& A, unsigned char* smem,
-                                               const XF& xf, const EPI& epi) {
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  unsigned char* wbase = smem + warp * ssell_tma_warp_bytes(W);
-  uint64_t* full = reinterpret_cast<uint64_t*>(wbase);
-  double* stage0 = reinterpret_cast<double*>(wbase + 64);
-  constexpr uint32_t kBytes = W * kSell * sizeof(double);
-  constexpr int64_t kSw = (int64_t)W * kSell;
-  if (lane == 0) {
-#pragma unroll
-    for (int st = 0; st < kSymTmaStages; ++st) mbar_init(&full[st], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  auto issue = [&](int64_t s, int st) {
-    mbar_arrive_expect_tx(&full[st], kBytes);
-    bulk_g2s(stage0 + st * kSw, A.vals + s * kSw, kBytes, &full[st]);
-  };
-  if (lane == 0) {
-#pragma unroll
-    for (int st = 0; st < kSymTmaStages; ++st)
-      if (gw + st * nw < nslices) issue(gw + st * nw, st);
-  }
-  int t = 0;
-  for (int64_t s = gw; s < nslices; s += nw, ++t) {
-    const int st = t % kSymTmaStages;
-    const int64_t row0 = s * kSell;
-    const double* __restrict__ ug = A.vals + s * kSw + lane;
-    mbar_wait(&full[st], (uint32_t)((t / kSymTmaStages) & 1));
-    double v;
-    if (row0 - A.gmax >= 0 && row0 + (kSell - 1) + A.gmax < A.n)
-      v = ssell_row_fixed<W, true>(A, stage0 + st * kSw + lane, (int32_t)(row0 + lane), lane, xf, ug);
-    else
-      v = ssell_row_generic(A, ug, row0, lane, xf);
-    __syncwarp();                               // stage consumed by every lane
-    if (lane == 0 && s + kSymTmaStages * nw < nslices) {
-      fence_proxy_async();
-      issue(s + kSymTmaStages * nw, st);
-    }
-    epi(s, v);
-  }
-}
-
 // dispatch on the exact width (3: FD5, 5: 2D Q1, 14: 3D Q1; 0: generic)
 #define SPAI_SSELL_DISPATCH(w, ...)                          \
   do {                                                       \

@@ -1,5 +1,5 @@
 // K0 stencil generator, K1 CSR->CSC transpose structure, symmetry check, and
-// the nnz-balanced row tiling used by the TMA-staged SpMV.
+// the union-pattern symmetrisation of a structurally nonsymmetric M.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -172,35 +172,6 @@ __global__ void sym_transpose_kernel(int64_t n, const int64_t* __restrict__ rowp
   if (__any_sync(0xffffffffu, miss) && lane == 0) atomicOr(bad, 1);
 }
 
-// ---- nnz-balanced tiling: tile t starts at the first row with rowptr >= t*B
-constexpr int64_t kTileNnz = 2048;
-
-__global__ void tile_rows_kernel(int64_t n, const int64_t* rowptr, int64_t ntiles,
-                                 int64_t* tile_rows) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    if (t == ntiles) { tile_rows[t] = n; continue; }
-    const int64_t target = t * kTileNnz;
-    int64_t lo = 0, hi = n;        // lower_bound over rowptr[0..n]
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (rowptr[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    tile_rows[t] = lo;
-  }
-}
-
-__global__ void tile_max_kernel(int64_t ntiles, const int64_t* rowptr,
-                                const int64_t* tile_rows, int32_t* maxnnz) {
-  int32_t m = 0;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t v = rowptr[tile_rows[t + 1]] - rowptr[tile_rows[t]];
-    m = max(m, (int32_t)min(v, (int64_t)INT32_MAX));
-  }
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(maxnnz, m);
-}
 
 // S = 0.5 (M + M^T) on pattern(M) u pattern(M^T) with exact zeros dropped:
 // the dense symmetrisation of the CLI factory (cli.py:189-194,
@@ -399,20 +370,3 @@ extern "C" int spai_symmetrize_union_fill(int64_t n, const int64_t* rowptr,
   return SPAI_OK;
 }
 
-extern "C" int spai_tile_count(int64_t n, int64_t nnz, int64_t* ntiles_out) {
-  (void)n;
-  *ntiles_out = nnz > 0 ? (nnz + kTileNnz - 1) / kTileNnz : 1;
-  return SPAI_OK;
-}
-
-extern "C" int spai_tile_rows(int64_t n, const int64_t* rowptr, int64_t ntiles,
-                              int64_t* tile_rows, int32_t* max_tile_nnz, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  tile_rows_kernel<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(n, rowptr, ntiles, tile_rows);
-  SPAI_LAUNCH_CHECK("tile_rows_kernel");
-  SPAI_CUDA(cudaMemsetAsync(max_tile_nnz, 0, sizeof(int32_t), s));
-  tile_max_kernel<<<grid_for(ntiles, 256), 256, 0, s>>>(ntiles, rowptr, tile_rows,
-                                                         max_tile_nnz);
-  SPAI_LAUNCH_CHECK("tile_max_kernel");
-  return SPAI_OK;
-}

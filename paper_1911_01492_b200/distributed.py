@@ -907,7 +907,7 @@ class RankSetup:
         self.S_ext = None
         self.A_loc = _rebase(A1, (z0 - self.e0) * plane, (z1 - self.e0) * plane, 0, self.n_ext)
         ones = torch.ones(A1.nrows, dtype=torch.float64, device=A1.vals.device)
-        self.b = A1.matvec(ones)[(z0 - self.e0) * plane:(z1 - self.e0) * plane].clone()
+        self.b = A1.matvec_csr(ones)[(z0 - self.e0) * plane:(z1 - self.e0) * plane].clone()
         self.g0, self.g1 = max(z0 - 3, 0), min(z1 + 3, nz)
         if spai_scope == "global":
             self.A_spai = gen(self.g1 - self.g0)

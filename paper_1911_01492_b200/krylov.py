@@ -282,12 +282,6 @@ class DevicePCG:
             _lib.check(self.lib.spai_pcg_set_preconditioner_mg(self.h, mg.h),
                        "spai_pcg_set_preconditioner_mg")
 
-    def set_tma(self, tma: bool):
-        _lib.check(self.lib.spai_pcg_set_tma(self.h, 1 if tma else 0), "spai_pcg_set_tma")
-
-    def set_fused(self, fused: bool):
-        _lib.check(self.lib.spai_pcg_set_fused(self.h, 1 if fused else 0), "spai_pcg_set_fused")
-
     def start(self, b, x0=None):
         _lib.check(self.lib.spai_pcg_start(self.h, ptr(b), ptr(x0) if x0 is not None
                                            else C.c_void_p(0)), "spai_pcg_start")

@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib
 from .errors import DimensionMismatchError
 from .precond import Preconditioner, spai1_symmetric_device
-from .sparse import CsrMatrix, DeviceCsr, _require_cuda, as_device, ptr, spmv, stream_handle
+from .sparse import CsrMatrix, DeviceCsr, _require_cuda, as_device, ptr, stream_handle
 
 
 # ---------------------------------------------------------------- reference API
@@ -92,17 +92,29 @@ def build_hierarchy(grid, levels: int) -> Hierarchy:
     return Hierarchy(out)
 
 
+def _csr_product(M, x):
+    """M x on the GPU with the row-sequential CSR kernel (one-off transfer
+    products: no layout worth building; same rounding as the reference's
+    short-row sums)."""
+    torch = _require_cuda()
+    on_dev = isinstance(x, torch.Tensor) and x.is_cuda
+    xd = x.to(torch.float64) if on_dev else torch.from_numpy(
+        np.ascontiguousarray(x, dtype=np.float64)).cuda()
+    y = as_device(M).matvec_csr(xd)
+    return y if on_dev else y.cpu().numpy()
+
+
 def restrict_full(hier: Hierarchy, x, level: int):
     """precond.py:384-388 (products on the GPU)."""
     for _, R, _ in hier.levels[1:level + 1]:
-        x = spmv(R, x)
+        x = _csr_product(R, x)
     return x
 
 
 def prolongate_full(hier: Hierarchy, xc, level: int):
     """precond.py:391-395 (products on the GPU)."""
     for _, _, P in reversed(hier.levels[1:level + 1]):
-        xc = spmv(P, xc)
+        xc = _csr_product(P, xc)
     return xc
 
 

@@ -194,10 +194,10 @@ class CsrMatrix:
 
 
 class _PatternCache:
-    __slots__ = ("csc", "sym", "tiles", "sell", "sell_wmax", "ssell")
+    __slots__ = ("csc", "sym", "sell", "sell_wmax", "ssell")
 
     def __init__(self):
-        self.csc = self.sym = self.tiles = self.sell = self.sell_wmax = self.ssell = None
+        self.csc = self.sym = self.sell = self.sell_wmax = self.ssell = None
 
 
 class DeviceCsr:
@@ -387,25 +387,6 @@ class DeviceCsr:
                 if sliceptr.numel() > 1 else 1
         return self._pat.sell_wmax
 
-    def matvec_sell_tma(self, x, out=None):
-        """y = A x with the TMA-staged SELL-32 kernel."""
-        torch = _require_cuda()
-        if x.numel() != self.ncols:
-            raise DimensionMismatchError(
-                f"spmv: {self.ncols} columns vs vector of {x.numel()}")
-        if out is None:
-            out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
-        sliceptr, cdesc, cols = self.sell()
-        vals = self.sell_values()
-        st = _lib.check(_lib.load().spai_sell_spmv_tma(self.nrows, self.ncols, ptr(sliceptr),
-                                                       ptr(cdesc), ptr(cols),
-                                                       ptr(vals), self.sell_width(),
-                                                       ptr(x.contiguous()), ptr(out),
-                                                       stream_handle()), "spai_sell_spmv_tma")
-        if st != _lib.SPAI_OK:
-            raise _lib.NativeLibraryError(_lib.last_error())
-        return out
-
     # K5c: symmetric half-storage SELL-32 (numerically symmetric operators)
     allow_symmetric_sell = True
 
@@ -448,9 +429,8 @@ class DeviceCsr:
                 self._ssell_vals = U if ok.value else False
         return self._ssell_vals if self._ssell_vals is not False else None
 
-    def matvec_ssell(self, x, out=None, tma=False):
-        """y = A x with the symmetric half-storage kernel (K5c); tma selects the
-        TMA-staged variant."""
+    def matvec_ssell(self, x, out=None):
+        """y = A x with the symmetric half-storage kernel (K5c)."""
         torch = _require_cuda()
         if x.numel() != self.ncols:
             raise DimensionMismatchError(
@@ -462,41 +442,21 @@ class DeviceCsr:
             out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
         g = self.ssell_offsets()
         garr = (C.c_int32 * len(g))(*g)
-        fn = _lib.load().spai_ssell_spmv_tma if tma else _lib.load().spai_ssell_spmv
-        _lib.check(fn(self.nrows, C.cast(garr, C.c_void_p), len(g), ptr(U), ptr(x.contiguous()),
+        _lib.check(_lib.load().spai_ssell_spmv(self.nrows, C.cast(garr, C.c_void_p), len(g), ptr(U), ptr(x.contiguous()),
                       ptr(out), stream_handle()), "spai_ssell_spmv")
         return out
 
-    def tiles(self):
-        """nnz-balanced row tiles of the TMA-staged SpMV (cached per pattern)."""
-        if self._pat.tiles is None:
-            torch = _require_cuda()
-            lib = _lib.load()
-            nt = C.c_int64(0)
-            lib.spai_tile_count(self.nrows, self.nnz, C.byref(nt))
-            tile_rows = torch.empty(nt.value + 1, dtype=torch.int64, device=self.vals.device)
-            mx = torch.zeros(1, dtype=torch.int32, device=self.vals.device)
-            _lib.check(lib.spai_tile_rows(self.nrows, ptr(self.rowptr), nt.value, ptr(tile_rows),
-                                          ptr(mx), stream_handle()), "spai_tile_rows")
-            self._pat.tiles = (tile_rows, nt.value, int(mx.item()))
-        return self._pat.tiles
-
-    def matvec_tma(self, x, out=None):
-        """y = A x with the TMA (cp.async.bulk) staged kernel."""
-        torch = _require_cuda()
-        if x.numel() != self.ncols:
-            raise DimensionMismatchError(
-                f"spmv: {self.ncols} columns vs vector of {x.numel()}")
-        if out is None:
-            out = torch.empty(self.nrows, dtype=torch.float64, device=x.device)
-        tile_rows, nt, mx = self.tiles()
-        _lib.check(_lib.load().spai_csr_spmv_tma(
-            self.nrows, ptr(self.rowptr), ptr(self.colidx), ptr(self.vals), ptr(tile_rows), nt,
-            mx, ptr(x.contiguous()), ptr(out), stream_handle()), "spai_csr_spmv_tma")
-        return out
-
     def matvec(self, x, out=None):
-        """y = A x on device tensors (K5)."""
+        """y = A x on device tensors through the fastest layout: the symmetric
+        half storage when it has been built (a bit-symmetric operator of the
+        solve), else SELL-32 (built on first use and cached per pattern;
+        8 B per stored value for stencil rows instead of CSR's 12 B)."""
+        if isinstance(self._ssell_vals, _torch().Tensor):
+            return self.matvec_ssell(x, out)
+        return self.matvec_sell(x, out)
+
+    def matvec_csr(self, x, out=None):
+        """y = A x with the CSR kernel (K5, no layout to build: one-off products)."""
         torch = _require_cuda()
         if x.numel() != self.ncols:
             raise DimensionMismatchError(

@@ -297,9 +297,8 @@ def test_spmv_matches_oracle():
         assert np.max(np.abs(y - yr)) <= tol
         dA = A.device()
         xd = torch.from_numpy(x).cuda()
-        outs = [dA.matvec_sell(xd), dA.matvec_tma(xd)]
-        if dA.sell_width() <= 64:          # TMA ring needs the widest slice to fit in smem
-            outs.append(dA.matvec_sell_tma(xd))
+        # the public product (SELL-32 built on first use), SELL, CSR
+        outs = [dA.matvec(xd), dA.matvec_sell(xd), dA.matvec_csr(xd)]
         for y2 in outs:
             assert np.max(np.abs(y2.cpu().numpy() - yr)) <= tol
     with pytest.raises(pb.DimensionMismatchError):
@@ -359,9 +358,11 @@ def test_symmetric_half_storage_spmv(make, w):
     assert U.numel() == 32 * ((A.nrows + 31) // 32) * w
     x = rng.standard_normal(A.ncols)
     yr = oracle.spmv(_ocsr(A), x)
-    for tma in (False, True):
-        y = dA.matvec_ssell(torch.from_numpy(x).cuda(), tma=tma).cpu().numpy()
-        assert np.max(np.abs(y - yr)) <= 1e-13 * max(np.max(np.abs(yr)), 1.0)
+    y = dA.matvec_ssell(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.max(np.abs(y - yr)) <= 1e-13 * max(np.max(np.abs(yr)), 1.0)
+    # with the half storage built, the public product uses it
+    yp = dA.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(yp, y)
     # the SPAI(1) preconditioner is symmetric bit for bit, shares the table
     if A.nrows > 1:
         S = pb.spai1_symmetric_device(dA)
@@ -522,25 +523,23 @@ def test_large_3d_spai_cg_properties():
     assert h[-1] <= 1e-8 * rec.initial_residual
 
 
-def test_pcg_tma_and_ldg_paths_agree_with_oracle():
-    """At a size where U1/U2 take the TMA-staged SELL path (>= 1184 slices)."""
+def test_pcg_sell_and_half_storage_paths_agree_with_oracle():
+    """40^3 (2000 slices): the SELL-32 and symmetric half-storage PCG against
+    each other and the oracle."""
     from paper_1911_01492_b200.krylov import DevicePCG
     A = pb.q1_device((40, 40, 40))
     S = pb.spai1_symmetric_device(A)
     b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
     hists = {}
-    for tma, fused, sym in ((True, False, False), (False, False, False), (False, True, False),
-                            (False, False, None)):
+    for sym in (False, None):
         s = DevicePCG(A, S, 1e-8, 500, symmetric=sym)
         assert s.symmetric == (sym is None)
-        s.set_fused(fused)
-        s.set_tma(tma)
         s.start(b)
         st = s.run()
         assert st[0] == 1
-        hists[(tma, fused, sym)] = s.history(st[1])
+        hists[sym] = s.history(st[1])
         s.close()
-    ref = hists[(True, False, False)]
+    ref = hists[False]
     for k, h in hists.items():
         assert len(h) == len(ref)
         assert np.max(np.abs(h - ref) / ref) <= 1e-10, k
