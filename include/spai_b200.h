@@ -129,9 +129,16 @@ int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr,
  * end finishes the leftover columns (QR / merge fallbacks) and reports the
  * first error as spai_assemble does.  spai_assemble_range = begin + one
  * columns call + end.                                                     */
-int spai_assemble_begin(int64_t n, const int64_t* cscptr, const int32_t* cscrow, int64_t c0,
+int spai_assemble_begin(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                        const int64_t* cscptr, const int32_t* cscrow, int64_t c0,
                         int64_t c1, void* ws, size_t ws_bytes, int* hmax, int* plans,
                         void* stream);
+/* *plans: 0 no plans (hash / merge paths), 1 plan replay (product program
+ * per column), 2 the B path (bgram.cuh: B = A^T A formed once per row, each
+ * column's G gathered from it, Crout Cholesky) -- chosen when the CSC
+ * structure is the CSR structure (rowptr == cscptr, colidx == cscrow: a
+ * structurally symmetric pattern) and the plans' J offsets fit 64 slots. */
+int spai_set_assembly_bpath(int enable);
 int spai_assemble_columns(int64_t n, const double* vals, const int64_t* cscptr,
                           const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
                           int64_t c0, int64_t c1, double* m_csc, void* ws, size_t ws_bytes,

@@ -23,7 +23,7 @@ from .distributed import (RankSystem, fused_allreduce, halo_exchange, gather_gho
 from .precond import (IdentityPreconditioner, JacobiPreconditioner,
                       Preconditioner, SparseMatrixPreconditioner, SpaiStats,
                       drop_exact_zeros, jacobi, make_spai1_factory,
-                      pattern_sets, set_assembly_plans, spai1, spai1_device,
+                      pattern_sets, set_assembly_bpath, set_assembly_plans, spai1, spai1_device,
                       spai1_symmetric_device, spai1_symmetric_from_host)
 from .block import (GRAM_MODES, GramMatrix, MultiVector, axpy, block_solve, copy, dot_block,
                     norm2, scale, spmm_multi)

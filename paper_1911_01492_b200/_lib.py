@@ -55,7 +55,8 @@ _SIGS = {
     "spai_set_assembly_plans": (_i32, [_i32]),
     "spai_assemble_range": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp,
                                    _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
-    "spai_assemble_begin": (_i32, [_i64, _vp, _vp, _i64, _i64, _vp, _sz, C.POINTER(_i32),
+    "spai_set_assembly_bpath": (_i32, [_i32]),
+    "spai_assemble_begin": (_i32, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _sz, C.POINTER(_i32),
                                    C.POINTER(_i32), _vp]),
     "spai_assemble_columns": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _sz,
                                      _i32, _i32, _vp]),

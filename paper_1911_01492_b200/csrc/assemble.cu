@@ -1336,12 +1336,23 @@ __global__ void symmetrize_kernel(int64_t nnz, const int64_t* __restrict__ csc2c
     s_csr[p] = 0.5 * (m_csc[csc2csr[p]] + m_csc[p]);
 }
 
+}  // namespace spai
+
+#include "bgram.cuh"
+
+namespace spai {
+
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
   return 1024 + 5 * align256((size_t)n * sizeof(int32_t)) +
          align256((size_t)kPlanTable * 16) + align256((size_t)kClassTable * 12) +
-         align256((size_t)kMaxPlans * kPlanWords * sizeof(uint32_t));
+         align256((size_t)kMaxPlans * kPlanWords * sizeof(uint32_t)) +
+         // B path: header + offsets, offset -> slot map, per-plan gather tables,
+         // per-plan B programs, generic-row list
+         512 + align256((size_t)n + 1) + align256((size_t)kMaxPlans * kBTab * sizeof(int32_t)) +
+         align256((size_t)kMaxPlans * kBProgWords * sizeof(uint32_t)) +
+         align256((size_t)n * sizeof(int32_t));
 }
 
 // Assembly in three phases, so a caller can overlap the value upload with the
@@ -1352,6 +1363,7 @@ extern "C" size_t spai_assemble_workspace_bytes(int64_t n) {
 struct AsmCtx {
   AsmWs ws;
   PlanWs pw;
+  BPathWs bw;
   int* maxlen;
   int* ndirect;
   int32_t* direct;
@@ -1386,11 +1398,44 @@ static AsmCtx carve_ws(void* wsp, int64_t n) {
   c.pw.slot_plan = (int32_t*)(p + (size_t)kPlanTable * 12);
   p += align256((size_t)kPlanTable * 16);
   c.pw.plans = (uint32_t*)p;
+  p += align256((size_t)kMaxPlans * kPlanWords * sizeof(uint32_t));
+  c.bw.hdr = (int32_t*)p;
+  c.bw.dplus = (int32_t*)(p + 256);
+  p += 512;
+  c.bw.dslot = (uint8_t*)p;
+  p += align256((size_t)n + 1);
+  c.bw.btab = (int32_t*)p;
+  p += align256((size_t)kMaxPlans * kBTab * sizeof(int32_t));
+  c.bw.bprog = (uint32_t*)p;
+  p += align256((size_t)kMaxPlans * kBProgWords * sizeof(uint32_t));
+  c.bw.brow_list = (int32_t*)p;
+  c.bw.nbrow = (int*)(c.bw.hdr + 8);
   return c;
 }
 
 // phase 1 with plans: classes of all columns, signatures of [c0, c1), plan
 // build.  Returns true when the plans are usable for the range.
+// B path (bgram.cuh) after the plans are built: the offsets D, the offset ->
+// slot map and the per-plan gather tables.  Returns 2 (B path), or 1 (plan
+// replay) when D has more than kBW offsets.
+static int setup_bpath(int64_t n, const int64_t* cscptr, const int32_t* cscrow, int64_t sig0,
+                       int64_t sig1, PlanWs pw, BPathWs bw, cudaStream_t s) {
+  bpath_offsets_kernel<<<1, 1024, 0, s>>>(pw, bw);
+  int32_t hdr[4] = {-1, 0, 0, 0};
+  if (cudaMemcpyAsync(hdr, bw.hdr, sizeof(hdr), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return 1;
+  if (hdr[0] <= 0 || hdr[1] >= n) return 1;
+  cudaMemsetAsync(bw.dslot, 0xFF, (size_t)hdr[1] + 1, s);
+  bpath_slots_kernel<<<1, kBW, 0, s>>>(bw);
+  bpath_tables_kernel<<<kMaxPlans, kBTab, 0, s>>>(pw, bw);
+  bpath_prog_kernel<<<kPlanTable, 32, 0, s>>>(cscptr, cscrow, pw, bw);
+  const int32_t sig[2] = {(int32_t)sig0, (int32_t)sig1};
+  cudaMemcpyAsync(bw.hdr + 4, sig, sizeof(sig), cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  return cudaGetLastError() == cudaSuccess ? 2 : 1;
+}
+
 static bool build_plans(int64_t c0, int64_t c1, const int64_t* cscptr, const int32_t* cscrow,
                         PlanWs pw, cudaStream_t s, int* st) {
   *st = SPAI_OK;
@@ -1427,11 +1472,102 @@ static bool build_plans(int64_t c0, int64_t c1, const int64_t* cscptr, const int
   return true;
 }
 
+// B path for columns [c0, c1): chunks of kBChunk columns, each with its
+// window of B rows [c0 + min jrel, c1 - 1 + max jrel] in a stream-ordered
+// temporary (K_B), then the per-column solves (K_G).
+constexpr int64_t kBChunk = (int64_t)1 << 23;
+constexpr int kBRowWarps = 8, kBSolveWarps = 8, kBPlanWarps = 8;
+
+template <int NJ, int CAPL>
+static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
+                         const int64_t* cscptr, const int32_t* cscrow, const int64_t* csc2csr,
+                         const double* cscval, double* m_csc, const AsmCtx& c, cudaStream_t s) {
+  int32_t hdr[6];
+  SPAI_CUDA(cudaMemcpyAsync(hdr, c.bw.hdr, sizeof(hdr), cudaMemcpyDeviceToHost, s));
+  SPAI_CUDA(cudaStreamSynchronize(s));
+  const int64_t jmin = hdr[2], jmax = hdr[3];
+  const int64_t chunk = std::min<int64_t>(kBChunk, c1 - c0);
+  const int64_t wmax_rows = chunk + (jmax - jmin) + 1;
+  static bool pool_set = false;
+  if (!pool_set) {      // keep freed window memory in the pool (no re-map per call)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set = true;
+  }
+  double* Bw = nullptr;
+  SPAI_CUDA(cudaMallocAsync(&Bw, (size_t)wmax_rows * kBW * sizeof(double), s));
+  static int rows_per_sm = 0, solve_per_sm = 0;
+  if (!rows_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rows_per_sm, bgram_list_kernel<kBRowWarps>,
+                                                  kBRowWarps * 32, 0);
+    rows_per_sm = std::max(rows_per_sm, 1);
+  }
+  const size_t psm = (size_t)kBPlanWarps * ((size_t)(CAPL + 1) * 8 + kBW * 8 + 32 * 8);
+  static int plan_per_sm = 0, plan_capl = -1;
+  if (plan_capl != CAPL) {
+    SPAI_CUDA(cudaFuncSetAttribute(bgram_plan_kernel<CAPL, kBPlanWarps>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&plan_per_sm, bgram_plan_kernel<CAPL, kBPlanWarps>,
+                                                  kBPlanWarps * 32, psm);
+    plan_per_sm = std::max(plan_per_sm, 1);
+    plan_capl = CAPL;
+  }
+  const size_t ssm = (size_t)kBSolveWarps * kLsDoubles(NJ) * sizeof(double);
+  static int solve_nj = -1;
+  if (solve_nj != NJ) {
+    SPAI_CUDA(cudaFuncSetAttribute(bsolve_kernel<NJ, kBSolveWarps>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&solve_per_sm, bsolve_kernel<NJ, kBSolveWarps>,
+                                                  kBSolveWarps * 32, ssm);
+    solve_per_sm = std::max(solve_per_sm, 1);
+    solve_nj = NJ;
+  }
+  int st = SPAI_OK;
+  for (int64_t a = c0; a < c1 && st == SPAI_OK; a += chunk) {
+    const int64_t b = std::min(c1, a + chunk);
+    const int64_t w0 = std::max<int64_t>(0, a + jmin), w1 = std::min<int64_t>(n, b - 1 + jmax + 1);
+    const int64_t reach = std::max<int64_t>(-jmin, jmax);
+    const Traversal trows = make_traversal(w0, w1, reach), tcols = make_traversal(a, b, reach);
+    // B rows: plan rows through their B programs (gathers pipelined), the
+    // rest (no usable plan) through the generic row walk
+    SPAI_CUDA(cudaMemsetAsync(c.bw.nbrow, 0, sizeof(int), s));
+    const int64_t gp = std::min<int64_t>((w1 - w0 + kBPlanWarps - 1) / kBPlanWarps,
+                                         (int64_t)num_sms() * plan_per_sm);
+    bgram_plan_kernel<CAPL, kBPlanWarps><<<(unsigned)std::max<int64_t>(gp, 1), kBPlanWarps * 32,
+                                           psm, s>>>(trows, w0, hdr[4], hdr[5], cscptr, cscrow,
+                                                     vals, c.pw, c.bw, Bw);
+    const cudaError_t e0 = cudaGetLastError();
+    if (e0 != cudaSuccess) { st = cuda_fail(e0, "bgram_plan_kernel"); break; }
+    bgram_list_kernel<kBRowWarps><<<(unsigned)num_sms() * rows_per_sm, kBRowWarps * 32, 0, s>>>(
+        w0, c.bw.brow_list, c.bw.nbrow, cscptr, cscrow, vals, cscval, csc2csr, c.bw.dslot,
+        hdr[1], Bw);
+    const cudaError_t e1 = cudaGetLastError();
+    if (e1 != cudaSuccess) { st = cuda_fail(e1, "bgram_list_kernel"); break; }
+    const int64_t gs = std::min<int64_t>((b - a + kBSolveWarps - 1) / kBSolveWarps,
+                                         (int64_t)num_sms() * solve_per_sm);
+    bsolve_kernel<NJ, kBSolveWarps><<<(unsigned)std::max<int64_t>(gs, 1), kBSolveWarps * 32, ssm, s>>>(
+        tcols, w0, cscptr, cscrow, vals, Bw, m_csc, c.ws, c.pw, c.bw, c.direct, c.ndirect);
+    const cudaError_t e2 = cudaGetLastError();
+    if (e2 != cudaSuccess) { st = cuda_fail(e2, "bsolve_kernel"); break; }
+  }
+  const cudaError_t ef = cudaFreeAsync(Bw, s);
+  if (st == SPAI_OK && ef != cudaSuccess) st = cuda_fail(ef, "cudaFreeAsync");
+  return st;
+}
+
 template <int NJ, int CAPL, int MW, int WARPS>
 static int columns_impl(int64_t c0, int64_t c1, const double* vals, const int64_t* cscptr,
                         const int32_t* cscrow, const int64_t* csc2csr, const double* cscval,
-                        double* m_csc, const AsmCtx& c, bool plans, cudaStream_t s) {
+                        double* m_csc, const AsmCtx& c, int plans, cudaStream_t s) {
   if (c1 <= c0) return SPAI_OK;
+  if constexpr (NJ <= kBMaxNJ) {
+    if (plans == 2) return bpath_columns<NJ, CAPL>(c.pw.ntot, c0, c1, vals, cscptr, cscrow,
+                                                   csc2csr, cscval, m_csc, c, s);
+  }
   if (!plans)
     return launch_hash<NJ, CAPL, MW, WARPS>(c1, vals, cscptr, cscrow, csc2csr, m_csc, c.ws,
                                             nullptr, nullptr, c1 - c0, c0, s);
@@ -1481,7 +1617,15 @@ extern "C" int spai_set_assembly_plans(int enable) {
   return SPAI_OK;
 }
 
-extern "C" int spai_assemble_begin(int64_t n, const int64_t* cscptr, const int32_t* cscrow,
+static int g_use_bpath = -1;
+
+extern "C" int spai_set_assembly_bpath(int enable) {
+  g_use_bpath = enable ? 1 : 0;
+  return SPAI_OK;
+}
+
+extern "C" int spai_assemble_begin(int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                                   const int64_t* cscptr, const int32_t* cscrow,
                                    int64_t c0, int64_t c1, void* wsp, size_t ws_bytes,
                                    int* hmax_out, int* plans_out, void* stream) {
   if (!hmax_out || !plans_out || c0 < 0 || c1 > n || c0 > c1) { set_error("spai_assemble_begin: bad arguments"); return SPAI_E_ARG; }
@@ -1505,9 +1649,20 @@ extern "C" int spai_assemble_begin(int64_t n, const int64_t* cscptr, const int32
   SPAI_CUDA(cudaStreamSynchronize(s));
   *hmax_out = hmax;
   if (g_use_plans == 1 && c1 > c0) {
+    if (g_use_bpath < 0) {
+      const char* e = getenv("SPAI_NO_BPATH");
+      g_use_bpath = (e && *e && *e != '0') ? 0 : 1;
+    }
+    // B path: the CSC structure must BE the CSR structure (structurally
+    // symmetric pattern, aliased arrays: spai_csr_transpose_symmetric); its
+    // B rows reach beyond [c0, c1), so every column gets a signature
+    const bool bpath = g_use_bpath == 1 && rowptr == cscptr && colidx == cscrow && hmax <= kBMaxNJ;
+    const int64_t s0 = bpath ? 0 : c0, s1 = bpath ? n : c1;
     int st = SPAI_OK;
-    *plans_out = build_plans(c0, c1, cscptr, cscrow, c.pw, s, &st) ? 1 : 0;
+    *plans_out = build_plans(s0, s1, cscptr, cscrow, c.pw, s, &st) ? 1 : 0;
     if (st) return st;
+    if (*plans_out == 1 && bpath)
+      *plans_out = setup_bpath(n, cscptr, cscrow, s0, s1, c.pw, c.bw, s);
   }
   return SPAI_OK;
 }
@@ -1521,7 +1676,7 @@ extern "C" int spai_assemble_columns(int64_t n, const double* vals, const int64_
   if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
   const AsmCtx c = carve_ws(wsp, n);
   cudaStream_t s = (cudaStream_t)stream;
-#define SPAI_COLS(A, B, C_, D) columns_impl<A, B, C_, D>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, c, plans != 0, s)
+#define SPAI_COLS(A, B, C_, D) columns_impl<A, B, C_, D>(c0, c1, vals, cscptr, cscrow, csc2csr, cscval, m_csc, c, plans, s)
   return SPAI_ASM_DISPATCH(hmax, SPAI_COLS);
 #undef SPAI_COLS
 }
@@ -1584,14 +1739,15 @@ extern "C" int spai_assemble_range(int64_t n, int64_t nnz, const int64_t* rowptr
                                    int64_t c0, int64_t c1, double* m_csc, void* wsp,
                                    size_t ws_bytes, int64_t* bad_col, int64_t* n_fallback,
                                    void* stream) {
-  (void)rowptr; (void)colidx; (void)nnz;
+  (void)nnz;
   if (c0 < 0 || c1 > n || c0 > c1) { set_error("bad column range [%lld, %lld)", (long long)c0, (long long)c1); return SPAI_E_ARG; }
   if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
   if (bad_col) *bad_col = -1;
   if (n_fallback) *n_fallback = 0;
   if (c1 == c0) return SPAI_OK;
   int hmax = 0, plans = 0;
-  int st = spai_assemble_begin(n, cscptr, cscrow, c0, c1, wsp, ws_bytes, &hmax, &plans, stream);
+  int st = spai_assemble_begin(n, rowptr, colidx, cscptr, cscrow, c0, c1, wsp, ws_bytes, &hmax,
+                               &plans, stream);
   if (st) return st;
   st = spai_assemble_columns(n, vals, cscptr, cscrow, csc2csr, cscval, c0, c1, m_csc, wsp,
                              ws_bytes, hmax, plans, stream);

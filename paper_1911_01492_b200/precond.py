@@ -121,6 +121,13 @@ def set_assembly_plans(enable: bool) -> None:
     _lib.load().spai_set_assembly_plans(1 if enable else 0)
 
 
+def set_assembly_bpath(enable: bool) -> None:
+    """Enable/disable the B = A^T A path of the plan columns (K3b, default on
+    for structurally symmetric patterns); off = the per-column product-program
+    replay.  Same pattern, results agree to rounding."""
+    _lib.load().spai_set_assembly_bpath(1 if enable else 0)
+
+
 class SpaiStats:
     """Columns that left the hash/bitmask fast path: n_merge (pattern too large,
     sorted-merge kernel) and n_fallback (Householder-QR kernel)."""
@@ -286,8 +293,9 @@ def spai1_symmetric_from_host(rowptr, colidx, vals, nchunks: int = 8,
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     hmax, plans = C.c_int(0), C.c_int(0)
     s = stream_handle()
-    _lib.check(lib.spai_assemble_begin(n, ptr(cscptr), ptr(cscrow), 0, n, ptr(ws), wsb,
-                                       C.byref(hmax), C.byref(plans), s), "spai_assemble_begin")
+    _lib.check(lib.spai_assemble_begin(n, ptr(d_rowptr), ptr(d_colidx), ptr(cscptr), ptr(cscrow),
+                                       0, n, ptr(ws), wsb, C.byref(hmax), C.byref(plans), s),
+               "spai_assemble_begin")
     waited = -1
     for j in range(len(rows) - 1):
         # last row this block reads: the plan replay reads CSC lists of the

@@ -183,10 +183,18 @@ def test_variable_coefficient_q1_through_plan_replay(dims):
     wsb = lib.spai_assemble_workspace_bytes(A.nrows)
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     hmax, plans = C.c_int(0), C.c_int(0)
-    assert lib.spai_assemble_begin(A.nrows, ptr(cscptr), ptr(cscrow), 0, A.nrows, ptr(ws), wsb,
-                                   C.byref(hmax), C.byref(plans), stream_handle()) == 0
-    assert plans.value == 1
+    assert lib.spai_assemble_begin(A.nrows, ptr(A.rowptr), ptr(A.colidx), ptr(cscptr),
+                                   ptr(cscrow), 0, A.nrows, ptr(ws), wsb, C.byref(hmax),
+                                   C.byref(plans), stream_handle()) == 0
+    assert plans.value == 2                               # the B = A^T A path
     m_plan = pb.precond.spai1_columns_device(A).clone()
+    # the per-column product-program replay agrees with the B path
+    pb.precond.set_assembly_bpath(False)
+    try:
+        m_replay = pb.precond.spai1_columns_device(
+            pb.sparse.DeviceCsr(A.nrows, A.ncols, A.rowptr, A.colidx, A.vals))
+    finally:
+        pb.precond.set_assembly_bpath(True)
     pb.set_assembly_plans(False)
     try:
         m_direct = pb.precond.spai1_columns_device(
@@ -195,6 +203,7 @@ def test_variable_coefficient_q1_through_plan_replay(dims):
         pb.set_assembly_plans(True)
     scale = float(m_direct.abs().max())
     assert float((m_plan - m_direct).abs().max()) <= 1e-12 * scale
+    assert float((m_replay - m_direct).abs().max()) <= 1e-12 * scale
     rng2 = np.random.default_rng(7)
     cols = np.concatenate([rng2.integers(0, A.nrows, 3000), _plan_class_columns(dims)])
     _check_columns(A, m_plan, cols)
