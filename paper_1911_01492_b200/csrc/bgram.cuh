@@ -158,13 +158,15 @@ struct Traversal {
   int64_t a, b, S, L, Z;     // Z = planes of stride S in [a, b)
   __device__ __forceinline__ int64_t count() const { return S ? Z * S : b - a; }
   // k for visit index t, or -1 when t maps outside the range
+  // (32-bit division: the visit count of a range is < 2^31, int32 indices)
   __device__ __forceinline__ int64_t at(int64_t t) const {
     if (!S) return a + t;
-    const int64_t zb = t / L, off = t - zb * L;
-    const int64_t z = zb % Z, bb = zb / Z;
-    const int64_t inplane = bb * L + off;
+    const uint32_t tt = (uint32_t)t, LL = (uint32_t)L, ZZ = (uint32_t)Z;
+    const uint32_t zb = tt / LL, off = tt - zb * LL;
+    const uint32_t bb = zb / ZZ, z = zb - bb * ZZ;
+    const int64_t inplane = (int64_t)bb * L + off;
     if (inplane >= S) return -1;
-    const int64_t k = a + z * S + inplane;
+    const int64_t k = a + (int64_t)z * S + inplane;
     return k < b ? k : -1;
   }
 };
@@ -172,9 +174,11 @@ struct Traversal {
 __host__ inline Traversal make_traversal(int64_t a, int64_t b, int64_t reach) {
   Traversal t{a, b, 0, 1, 1};
   // block only when three planes of B rows (8 * kBW bytes each) exceed L2
-  if (reach * 3 * kBW * 8 > ((int64_t)48 << 20) && b - a > 4 * reach) {
+  static int64_t tile = -1;
+  if (tile < 0) { const char* e = getenv("SPAI_BTILE"); tile = e ? atoll(e) : 8192; }
+  if (tile > 0 && reach * 3 * kBW * 8 > ((int64_t)48 << 20) && b - a > 4 * reach) {
     t.S = reach;
-    const int64_t nb = (reach + 8191) / 8192;
+    const int64_t nb = (reach + tile - 1) / tile;
     t.L = (reach + nb - 1) / nb;
     t.Z = (b - a + reach - 1) / reach;
   }
@@ -231,7 +235,7 @@ bpath_prog_kernel(const int64_t* __restrict__ cscptr, const int32_t* __restrict_
   int t0 = 0;
   const int nrounds = (ns + 31) / 32;
   for (int r = 0; r < nrounds; ++r) {
-    const int len = (cnt[order[32 * r]] + 1) & ~1;
+    const int len = (cnt[order[32 * r]] + 3) & ~3;      // whole pairs of pairs
     if (t0 + len > kBSteps) return;
     B[kBP_rlen + r] = (uint32_t)len;
     for (int l = 0; l < 32; ++l) {
@@ -449,12 +453,21 @@ bgram_plan_kernel(Traversal tv, int64_t w0, int64_t sig0, int64_t sig1,
         const int len = (int)B[kBP_rlen + r];
         if (len == 0) break;
         double sacc = 0.0;
-        for (int t = 0; t < len; t += 2) {
-          const uint2 oo = ops[((t0 + t) >> 1) * 32];
-          sacc = fma(*reinterpret_cast<const double*>(lv + (oo.x >> 16)),
-                     *reinterpret_cast<const double*>(lv + (oo.x & 0xFFFFu)), sacc);
-          sacc = fma(*reinterpret_cast<const double*>(lv + (oo.y >> 16)),
-                     *reinterpret_cast<const double*>(lv + (oo.y & 0xFFFFu)), sacc);
+        for (int t = 0; t < len; t += 4) {            // one fma chain: the generic walk's order
+          const uint2 o0 = ops[((t0 + t) >> 1) * 32];
+          const uint2 o1 = ops[((t0 + t) >> 1) * 32 + 32];
+          const double a0 = *reinterpret_cast<const double*>(lv + (o0.x >> 16));
+          const double b0 = *reinterpret_cast<const double*>(lv + (o0.x & 0xFFFFu));
+          const double a1 = *reinterpret_cast<const double*>(lv + (o0.y >> 16));
+          const double b1 = *reinterpret_cast<const double*>(lv + (o0.y & 0xFFFFu));
+          const double a2 = *reinterpret_cast<const double*>(lv + (o1.x >> 16));
+          const double b2 = *reinterpret_cast<const double*>(lv + (o1.x & 0xFFFFu));
+          const double a3 = *reinterpret_cast<const double*>(lv + (o1.y >> 16));
+          const double b3 = *reinterpret_cast<const double*>(lv + (o1.y & 0xFFFFu));
+          sacc = fma(a0, b0, sacc);
+          sacc = fma(a1, b1, sacc);
+          sacc = fma(a2, b2, sacc);
+          sacc = fma(a3, b3, sacc);
         }
         const uint16_t dst = rdst[r * 32];
         if (dst != 0xFFFFu) bacc[dst] = sacc;
@@ -552,22 +565,23 @@ bsolve_kernel(Traversal tv, int64_t w0, const int64_t* __restrict__ cscptr,
         // G(r, c+1) - sum_{j < c} L(r, j) L(c+1, j): aligned 16-byte
         // broadcasts of row c + 1, two chains
         const double* rn = Ls + (c + 1) * LS;
-        double s0 = g[c + 1], s1 = 0.0;
+        double s0 = g[c + 1], s1 = 0.0, s2 = 0.0, s3 = 0.0;
         const int j0 = (((c + 1) * LS) & 1);         // 1 when row c+1 starts 8 bytes off 16
         if (j0 == 1 && c > 0) s1 = fma(-g[0], rn[0], s1);
 #pragma unroll
         for (int j = j0; j + 1 < c; j += 2) {
           const double2 v = *reinterpret_cast<const double2*>(rn + j);
-          if (((j - j0) >> 1) & 1) {
-            s1 = fma(-g[j], v.x, s1);
-            s1 = fma(-g[j + 1], v.y, s1);
+          const int q = ((j - j0) >> 1) & 1;
+          if (q) {
+            s2 = fma(-g[j], v.x, s2);
+            s3 = fma(-g[j + 1], v.y, s3);
           } else {
             s0 = fma(-g[j], v.x, s0);
-            s0 = fma(-g[j + 1], v.y, s0);
+            s1 = fma(-g[j + 1], v.y, s1);
           }
         }
         if (c > j0 && ((c - j0) & 1)) s0 = fma(-g[c - 1], rn[c - 1], s0);
-        pn = s0 + s1;
+        pn = (s0 + s1) + (s2 + s3);
       }
       const double d = __shfl_sync(0xffffffffu, sacc, c);
       const double l = sacc * rsqrt(d);
