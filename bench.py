@@ -341,12 +341,13 @@ def run_ours(args):
         x, rec = pb.solve(pb.LocalSystem(A2, pb.SparseMatrixPreconditioner(S)), bdev, cfg)
         e2.record(stream)
         e2.synchronize()
-        # per step (ncu launch list, profiles/r01_launches_400_final.txt):
-        # structure check, sym transpose, half-storage offsets + fill + verify
-        # of A, longest column, classes, signatures, plan build, replay,
-        # symmetrise, fill of S, PCG start (2) = 14 kernels, then 4 per
-        # launched PCG iteration
-        launches["n"] += 14 + 4 * _advanced(rec)
+        # per step (ncu launch list, profiles/r02_launches_400.txt): sym
+        # transpose, structure check, half-storage offsets + fill + verify of
+        # A, longest column, classes, signatures, plan build, B-path setup (4),
+        # symmetrise, fill of S, PCG start (2) = 17 kernels; per chunk of
+        # 2^23 columns the B rows (plan + generic list) and the solves (3);
+        # then 4 per launched PCG iteration
+        launches["n"] += 17 + 3 * ((n + (1 << 23) - 1) >> 23) + 4 * _advanced(rec)
         return e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3, rec, x
 
     def barrier():
@@ -399,25 +400,26 @@ def run_ours(args):
         nvals = A.sell_stats()[0]
     b_it = 16 * nvals + 104 * n
     b_it_csr = 24 * nnz + 104 * n
-    # assembly vs the FP64 CUDA-core peak: per interior 3D Q1
-    # column the normal equations execute 2 x 3794 (G = A^T A restricted) +
-    # 27^3 / 3 (Cholesky) + 2 x 27^2 (two solves) = 15,607 flop; the
-    # reference's Householder QR would need 2 n^2 (m - n/3) + n^2 = 169,857
+    # assembly vs the FP64 CUDA-core peak.  The B path (K3b)
+    # executes per interior 3D Q1 column: its B row (378 products = 756
+    # flop), the Cholesky of G = B[J, J] (27^3 / 3 = 6,561), forward and
+    # backward solves (2 x 351 x 2 = 1,404) = 8,721 flop; the reference's
+    # Householder QR would need 2 n^2 (m - n/3) + n^2 = 169,857
     fp64 = fp64_peak_tflops(stream)
-    exec_tf = n * 15607 / t_asm / 1e12
-    asm_roof = {"bound": "fp64 on paper; the shared-memory data pipe in practice",
+    exec_tf = n * 8721 / t_asm / 1e12
+    asm_roof = {"bound": "fp64 on paper; issue / dependency latency in practice",
                 "unit": "TFLOP/s",
                 "achieved_executed": exec_tf, "peak_measured_dfma": fp64,
                 "frac": exec_tf / fp64,
                 "householder_equivalent": n * 169857 / t_asm / 1e12,
-                "flop_per_column": {"executed_normal_equations": 15607,
+                "flop_per_column": {"executed_b_path": 8721,
                                     "householder_qr_reference": 169857},
-                # ncu of the replay kernel (profiles/r01_replay_lines_200.txt):
-                # ~1,550 shared-memory wavefronts per column, LSU pipe ~91 % busy;
-                # floor of the design ~1,070 (operands 474 + broadcast of L 364
-                # + gather 80 + Gram / factor stores ~150)
-                "shared_wavefronts_per_column": {"measured_ncu": 1554, "design_floor": 1070},
-                "lsu_pipe_busy_pct_ncu": 91}
+                # ncu (profiles/r02_ncu_bpath_400.txt): per chunk of 8.4 M
+                # columns B rows 17 ms + solves 28 ms; solves ~1,700
+                # warp-instructions per column at ~1.7 IPC / SM (16 warps,
+                # 128 registers), stalls mostly fixed-latency FP64 / shuffle
+                # chains of the factorisation
+                "warp_instructions_per_column_ncu": {"b_rows": 1055, "solve": 1710}}
     solve_gbs = b_it * its / t_sol / 1e9
 
     # ---- SpMV alone (K5 formats) with CUDA events
