@@ -1015,6 +1015,8 @@ __device__ __forceinline__ void product_program(const uint32_t* __restrict__ P, 
 #pragma unroll
     for (int i = 0; i < kOpAhead; ++i) {
       const uint2 oo = ring[i];
+      SPAI_DCHECK((oo.x & 0xFFFFu) < (kPlanCap + 1) * 8u && (oo.x >> 16) < (kPlanCap + 1) * 8u &&
+                  (oo.y & 0xFFFFu) < (kPlanCap + 1) * 8u && (oo.y >> 16) < (kPlanCap + 1) * 8u);
       a[i][0] = *reinterpret_cast<const double*>(lv + (oo.x & 0xFFFFu));
       a[i][1] = *reinterpret_cast<const double*>(lv + (oo.x >> 16));
       a[i][2] = *reinterpret_cast<const double*>(lv + (oo.y & 0xFFFFu));
@@ -1027,6 +1029,7 @@ __device__ __forceinline__ void product_program(const uint32_t* __restrict__ P, 
       s0 = fma(a[i][0], a[i][1], s0);
       s1 = fma(a[i][2], a[i][3], s1);
       if (p + 1 == rend) {
+        SPAI_DCHECK(dcur == 0xFFFFu || dcur < tri(kPlanNJ));
         if (dcur != 0xFFFFu) G[dcur] = s0 + s1;
         s0 = 0.0;
         s1 = 0.0;
@@ -1550,7 +1553,7 @@ static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
     const int64_t gs = std::min<int64_t>((b - a + kBSolveWarps - 1) / kBSolveWarps,
                                          (int64_t)num_sms() * solve_per_sm);
     bsolve_kernel<NJ, kBSolveWarps><<<(unsigned)std::max<int64_t>(gs, 1), kBSolveWarps * 32, ssm, s>>>(
-        tcols, w0, cscptr, cscrow, vals, Bw, m_csc, c.ws, c.pw, c.bw, c.direct, c.ndirect);
+        tcols, w0, w1, cscptr, cscrow, vals, Bw, m_csc, c.ws, c.pw, c.bw, c.direct, c.ndirect);
     const cudaError_t e2 = cudaGetLastError();
     if (e2 != cudaSuccess) { st = cuda_fail(e2, "bsolve_kernel"); break; }
   }
@@ -1628,6 +1631,7 @@ extern "C" int spai_assemble_begin(int64_t n, const int64_t* rowptr, const int32
                                    const int64_t* cscptr, const int32_t* cscrow,
                                    int64_t c0, int64_t c1, void* wsp, size_t ws_bytes,
                                    int* hmax_out, int* plans_out, void* stream) {
+  SPAI_NVTX("spai_assemble_begin");
   if (!hmax_out || !plans_out || c0 < 0 || c1 > n || c0 > c1) { set_error("spai_assemble_begin: bad arguments"); return SPAI_E_ARG; }
   if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
@@ -1672,6 +1676,7 @@ extern "C" int spai_assemble_columns(int64_t n, const double* vals, const int64_
                                      const double* cscval, int64_t c0, int64_t c1,
                                      double* m_csc, void* wsp, size_t ws_bytes, int hmax,
                                      int plans, void* stream) {
+  SPAI_NVTX("spai_assemble_columns");
   if (c0 < 0 || c1 > n || c0 > c1) { set_error("bad column range [%lld, %lld)", (long long)c0, (long long)c1); return SPAI_E_ARG; }
   if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
   const AsmCtx c = carve_ws(wsp, n);
@@ -1685,6 +1690,7 @@ extern "C" int spai_assemble_end(int64_t n, const double* vals, const int64_t* c
                                  const int32_t* cscrow, const int64_t* csc2csr, double* m_csc,
                                  void* wsp, size_t ws_bytes, int hmax, int plans,
                                  int64_t* bad_col, int64_t* n_fallback, void* stream) {
+  SPAI_NVTX("spai_assemble_end");
   if (ws_bytes < spai_assemble_workspace_bytes(n)) { set_error("assemble workspace too small"); return SPAI_E_ARG; }
   if (bad_col) *bad_col = -1;
   if (n_fallback) *n_fallback = 0;
@@ -1795,6 +1801,7 @@ extern "C" int spai_csc_to_csr_values(int64_t nnz, const int64_t* csc2csr, const
 
 extern "C" int spai_symmetrize(int64_t nnz, const int64_t* csc2csr, const double* m_csc,
                                double* s_csr, void* stream) {
+  SPAI_NVTX("spai_symmetrize");
   if (nnz == 0) return SPAI_OK;
   int64_t blocks = std::min<int64_t>((nnz + 255) / 256, (int64_t)num_sms() * 16);
   symmetrize_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(nnz, csc2csr, m_csc, s_csr);

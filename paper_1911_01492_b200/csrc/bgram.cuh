@@ -296,6 +296,7 @@ __device__ __forceinline__ void brow_accumulate(int64_t c, const int64_t* __rest
         const int64_t d = (int64_t)cj - c;
         if (d >= 0 && d <= dmax) {
           const int s = dslot[d];
+          SPAI_DCHECK(s == 0xFF || s < kBW);
           if (s != 0xFF) acc[s] = fma(wv, vj, acc[s]);   // A(i, c) A(i, c + d)
         }
       }
@@ -412,6 +413,7 @@ bgram_plan_kernel(Traversal tv, int64_t w0, int64_t sig0, int64_t sig1,
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int e = b0 + 32 * u + lane;
+        SPAI_DCHECK(e >= total || (((ids >> (8 * u)) & 255u) < (unsigned)nj && e < CAPL));
         if (e < total) cp_async_8(lval + e, vals + lsrc[(ids >> (8 * u)) & 255u] + e);
       }
     }
@@ -456,6 +458,11 @@ bgram_plan_kernel(Traversal tv, int64_t w0, int64_t sig0, int64_t sig1,
         for (int t = 0; t < len; t += 4) {            // one fma chain: the generic walk's order
           const uint2 o0 = ops[((t0 + t) >> 1) * 32];
           const uint2 o1 = ops[((t0 + t) >> 1) * 32 + 32];
+          SPAI_DCHECK(t0 + t + 4 <= kBSteps &&
+                      max(max(o0.x & 0xFFFFu, o0.y & 0xFFFFu), max(o1.x & 0xFFFFu, o1.y & 0xFFFFu)) <=
+                          (uint32_t)CAPL * 8u &&
+                      max(max(o0.x >> 16, o0.y >> 16), max(o1.x >> 16, o1.y >> 16)) <=
+                          (uint32_t)CAPL * 8u);
           const double a0 = *reinterpret_cast<const double*>(lv + (o0.x >> 16));
           const double b0 = *reinterpret_cast<const double*>(lv + (o0.x & 0xFFFFu));
           const double a1 = *reinterpret_cast<const double*>(lv + (o0.y >> 16));
@@ -470,6 +477,7 @@ bgram_plan_kernel(Traversal tv, int64_t w0, int64_t sig0, int64_t sig1,
           sacc = fma(a3, b3, sacc);
         }
         const uint16_t dst = rdst[r * 32];
+        SPAI_DCHECK(dst == 0xFFFFu || dst < kBW);
         if (dst != 0xFFFFu) bacc[dst] = sacc;
         t0 += len;
       }
@@ -501,7 +509,7 @@ bgram_plan_kernel(Traversal tv, int64_t w0, int64_t sig0, int64_t sig1,
 // (K_G) plan columns [c0, c1): G from B, Crout Cholesky, solves -> m_csc
 template <int NJ, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 2)
-bsolve_kernel(Traversal tv, int64_t w0, const int64_t* __restrict__ cscptr,
+bsolve_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__ cscptr,
               const int32_t* __restrict__ cscrow, const double* __restrict__ vals,
               const double* __restrict__ Bw, double* __restrict__ m_csc, AsmWs ws, PlanWs pw,
               BPathWs bw, int32_t* __restrict__ direct, int* __restrict__ ndirect) {
@@ -540,7 +548,11 @@ bsolve_kernel(Traversal tv, int64_t w0, const int64_t* __restrict__ cscptr,
     const double* src = lane == kRhsLane ? vals + jlo : Bw + (k - w0) * kBW;
     double g[NJ];
 #pragma unroll
-    for (int c = 0; c < NJ; ++c) g[c] = src[T[c * 32]];
+    for (int c = 0; c < NJ; ++c) {
+      SPAI_DCHECK(lane == kRhsLane || ((k - w0) * kBW + T[c * 32] >= 0 &&
+                                       (k - w0) * kBW + T[c * 32] < (w1 - w0) * kBW));
+      g[c] = src[T[c * 32]];
+    }
     if (__any_sync(0xffffffffu, nj != NJ)) {       // boundary plan: identity padding rows
 #pragma unroll
       for (int c = 0; c < NJ; ++c) {

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/spai_b200.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (no link; inert without a tool)
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "libspaib200 is written for sm_100a (B200) only"
@@ -31,6 +32,25 @@ int cuda_fail(cudaError_t e, const char* where);
   } while (0)
 
 constexpr int kNumSMs = 148;
+
+// NVTX range over a C-ABI entry point (nsys / ncu --nvtx timelines of the
+// assembly phases, solver chunks and halos); free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define SPAI_NVTX(name) ::spai::NvtxRange spai_nvtx_range_(name)
+
+// Device-side invariant checks of the shared-memory / index arithmetic,
+// compiled in by the checked build (SPAI_BUILD_DEFINES=SPAI_CHECK=1,
+// scripts/checked_tests.sh): a violated bound traps the kernel instead of
+// reading or writing out of range.  compute-sanitizer is not available on
+// this GPU pool; these checks stand in for its memcheck on our own indices.
+#if defined(SPAI_CHECK) && SPAI_CHECK
+#define SPAI_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define SPAI_DCHECK(cond) do { } while (0)
+#endif
 
 // A small persistent device buffer (256 ints per device) for the status flags
 // that synchronous entry points read back; avoids per-call allocations (and

@@ -423,6 +423,7 @@ static void launch_sym_start(spai_pcg* s, bool x0) {
 }
 
 extern "C" int spai_pcg_start(spai_pcg* s, const double* b, const double* x0) {
+  SPAI_NVTX("spai_pcg_start");
   const size_t vb = (size_t)s->n * sizeof(double);
   PcgScal* h = s->host_init;   // lives as long as the solver: safe for the async copy
   *h = PcgScal{};
@@ -461,6 +462,7 @@ extern "C" int spai_pcg_start(spai_pcg* s, const double* b, const double* x0) {
 }
 
 extern "C" int spai_pcg_advance(spai_pcg* s, int64_t iters) {
+  SPAI_NVTX("spai_pcg_advance");
   constexpr int64_t kChunk = 16;
   while (iters >= kChunk) {
     if (!s->graph) {

@@ -341,6 +341,7 @@ extern "C" int spai_ksolver_start(spai_ksolver* s, const double* b) {
 }
 
 extern "C" int spai_ksolver_advance(spai_ksolver* s, int64_t iters) {
+  SPAI_NVTX("spai_ksolver_advance");
   constexpr int64_t kChunk = 16;
   while (iters >= kChunk) {
     if (!s->graph) {

@@ -521,6 +521,7 @@ extern "C" int spai_cgv_start(spai_cgv* s, const double* b, const double* x0) {
 }
 
 extern "C" int spai_cgv_advance(spai_cgv* s, int64_t iters) {
+  SPAI_NVTX("spai_cgv_advance");
   constexpr int64_t kChunk = 16;
   while (iters >= kChunk) {
     if (!s->graph) {

@@ -274,6 +274,7 @@ extern "C" int spai_csr_transpose(int64_t nrows, int64_t ncols, int64_t nnz,
                                   const int64_t* rowptr, const int32_t* colidx,
                                   int64_t* cscptr, int32_t* cscrow, int64_t* csc2csr,
                                   void* ws, size_t ws_bytes, void* stream) {
+  SPAI_NVTX("spai_csr_transpose");
   cudaStream_t s = (cudaStream_t)stream;
   if (ws_bytes < spai_transpose_workspace_bytes(nrows, ncols, nnz)) {
     set_error("transpose workspace too small");
@@ -316,6 +317,7 @@ extern "C" int spai_structure_is_symmetric(int64_t n, int64_t nnz, const int64_t
 extern "C" int spai_csr_transpose_symmetric(int64_t n, int64_t nnz, const int64_t* rowptr,
                                             const int32_t* colidx, int64_t* csc2csr,
                                             int* is_sym, void* stream) {
+  SPAI_NVTX("spai_csr_transpose_symmetric");
   cudaStream_t s = (cudaStream_t)stream;
   (void)nnz;
   int* d = small_scratch();

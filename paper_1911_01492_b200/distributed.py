@@ -74,6 +74,19 @@ class SlabPartition:
 
 
 # ------------------------------------------------------------------ comm
+def _nvtx(name):
+    """NVTX range for the host-side communication steps (inert without a
+    profiler; a no-op context on machines without CUDA)."""
+    import contextlib
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.nvtx.range(name)
+    except Exception:                              # pragma: no cover
+        pass
+    return contextlib.nullcontext()
+
+
 class TorchComm:
     """torch.distributed plumbing: all-gather of partial sums, plane halos."""
 
@@ -90,6 +103,10 @@ class TorchComm:
 
     def allgather(self, out, gathered):
         """gathered[r*K:(r+1)*K] = out of rank r (K = out.numel())."""
+        with _nvtx("allgather_partials"):
+            self._allgather(out, gathered)
+
+    def _allgather(self, out, gathered):
         self.reductions += 1
         if self.size == 1:
             gathered.copy_(out)
@@ -125,7 +142,8 @@ class TorchComm:
         if self.size == 1 or self.stage:
             self.halo(xext, own_off, n_own, hlo, hhi)
             return _Done()
-        return _Works(self._halo_ops(xext, own_off, n_own, hlo, hhi))
+        with _nvtx("halo_start"):
+            return _Works(self._halo_ops(xext, own_off, n_own, hlo, hhi))
 
     def _halo_ops(self, xext, own_off, n_own, hlo, hhi):
         d = self.dist
