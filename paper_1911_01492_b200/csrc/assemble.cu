@@ -1621,9 +1621,12 @@ extern "C" int spai_set_assembly_plans(int enable) {
 }
 
 static int g_use_bpath = -1;
+static bool g_use_bpath_forced = false;
 
+// 0 off, 1 on (large 3D problems), 2 on for every eligible size (tests)
 extern "C" int spai_set_assembly_bpath(int enable) {
   g_use_bpath = enable ? 1 : 0;
+  g_use_bpath_forced = enable == 2;
   return SPAI_OK;
 }
 
@@ -1660,7 +1663,11 @@ extern "C" int spai_assemble_begin(int64_t n, const int64_t* rowptr, const int32
     // B path: the CSC structure must BE the CSR structure (structurally
     // symmetric pattern, aliased arrays: spai_csr_transpose_symmetric); its
     // B rows reach beyond [c0, c1), so every column gets a signature
-    const bool bpath = g_use_bpath == 1 && rowptr == cscptr && colidx == cscrow && hmax <= kBMaxNJ;
+    // (3D stencils: |J| = 17..28; the 2D problems' 9 x 9 normal equations are
+    // cheaper per column through the replay's exact 9-row template than
+    // through a 64-slot B row, and below ~2^17 columns the setup dominates)
+    const bool bpath = g_use_bpath == 1 && rowptr == cscptr && colidx == cscrow &&
+                       hmax > 16 && hmax <= kBMaxNJ && (g_use_bpath_forced || n >= (1 << 17));
     const int64_t s0 = bpath ? 0 : c0, s1 = bpath ? n : c1;
     int st = SPAI_OK;
     *plans_out = build_plans(s0, s1, cscptr, cscrow, c.pw, s, &st) ? 1 : 0;

@@ -121,11 +121,12 @@ def set_assembly_plans(enable: bool) -> None:
     _lib.load().spai_set_assembly_plans(1 if enable else 0)
 
 
-def set_assembly_bpath(enable: bool) -> None:
-    """Enable/disable the B = A^T A path of the plan columns (K3b, default on
-    for structurally symmetric patterns); off = the per-column product-program
-    replay.  Same pattern, results agree to rounding."""
-    _lib.load().spai_set_assembly_bpath(1 if enable else 0)
+def set_assembly_bpath(enable) -> None:
+    """The B = A^T A path of the plan columns (K3b): True (default) for
+    structurally symmetric 3D patterns (|J| 17..28) of at least 2^17 columns,
+    "always" for every eligible size, False = the per-column replay.  Same
+    pattern, results agree to rounding."""
+    _lib.load().spai_set_assembly_bpath(2 if enable == "always" else (1 if enable else 0))
 
 
 class SpaiStats:

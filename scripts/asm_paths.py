@@ -34,13 +34,13 @@ def main():
     res = {"N": N, "conv": conv}
     outs = {}
     for name, bpath in (("bpath", True), ("replay", False)):
-        pb.set_assembly_bpath(bpath)
+        pb.set_assembly_bpath("always" if bpath else False)
         fresh = lambda: pb.precond.spai1_columns_device(A)
         ms, m = timed(fresh)
         res[name + "_ms"] = ms
         outs[name] = m.clone()
         del m
-    pb.set_assembly_bpath(True)
+    pb.set_assembly_bpath("always")
     d = (outs["bpath"] - outs["replay"]).abs().max().item()
     res["max_abs_diff"] = d
     res["max_abs"] = outs["replay"].abs().max().item()

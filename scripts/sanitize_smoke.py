@@ -19,9 +19,9 @@ def main():
     # assembly paths
     A3 = pb.q1_device((12, 11, 10), conv=(1.0, 0.5, 0.25))
     for bpath in (True, False):
-        pb.set_assembly_bpath(bpath)
+        pb.set_assembly_bpath("always" if bpath else False)
         pb.spai1_device(pb.sparse.DeviceCsr(A3.nrows, A3.ncols, A3.rowptr, A3.colidx, A3.vals))
-    pb.set_assembly_bpath(True)
+    pb.set_assembly_bpath("always")
     pb.set_assembly_plans(False)
     pb.spai1_device(pb.sparse.DeviceCsr(A3.nrows, A3.ncols, A3.rowptr, A3.colidx, A3.vals))
     pb.set_assembly_plans(True)

@@ -20,3 +20,18 @@ def golden():
 
 def golden_names(g, prefix):
     return sorted({k.split("/")[1] for k in g.files if k.startswith(prefix + "/")})
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _bpath_everywhere():
+    """GPU sessions run the B = A^T A assembly path (K3b) at every eligible
+    size (the product default starts at 2^17 columns), so the small 3D
+    parity cases cover it; tests of the replay switch it off explicitly."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            import paper_1911_01492_b200 as pb
+            pb.set_assembly_bpath("always")
+    except Exception:        # no library / no device: nothing to configure
+        pass
+    yield

@@ -122,6 +122,7 @@ def _worker(rank, world, port, case, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
+    pb.set_assembly_bpath("always")         # as the parent session (conftest)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1911_01492_b200.grids import fd5_stencil

@@ -186,7 +186,8 @@ def test_variable_coefficient_q1_through_plan_replay(dims):
     assert lib.spai_assemble_begin(A.nrows, ptr(A.rowptr), ptr(A.colidx), ptr(cscptr),
                                    ptr(cscrow), 0, A.nrows, ptr(ws), wsb, C.byref(hmax),
                                    C.byref(plans), stream_handle()) == 0
-    assert plans.value == 2                               # the B = A^T A path
+    # 3D: the B = A^T A path; 2D (|J| = 9): the replay's exact 9-row template
+    assert plans.value == (2 if len(dims) == 3 else 1)
     m_plan = pb.precond.spai1_columns_device(A).clone()
     # the per-column product-program replay agrees with the B path
     pb.precond.set_assembly_bpath(False)
@@ -194,7 +195,7 @@ def test_variable_coefficient_q1_through_plan_replay(dims):
         m_replay = pb.precond.spai1_columns_device(
             pb.sparse.DeviceCsr(A.nrows, A.ncols, A.rowptr, A.colidx, A.vals))
     finally:
-        pb.precond.set_assembly_bpath(True)
+        pb.precond.set_assembly_bpath("always")
     pb.set_assembly_plans(False)
     try:
         m_direct = pb.precond.spai1_columns_device(
