@@ -60,7 +60,7 @@ def parse():
     return ap.parse_args()
 
 
-PROFILE_FULL = {"sell": "r01_ncu_full_400_final.json", "ssell": "r01_ncu_full_400_ssell.json"}
+PROFILE_FULL = {"sell": "r01_ncu_full_400_final.json", "ssell": "r02_ncu_full_pcg_400.json"}
 
 
 def profiled_traffic(fmt):
