@@ -1421,6 +1421,11 @@ static AsmCtx carve_ws(void* wsp, int64_t n) {
 // B path (bgram.cuh) after the plans are built: the offsets D, the offset ->
 // slot map and the per-plan gather tables.  Returns 2 (B path), or 1 (plan
 // replay) when D has more than kBW offsets.
+// host copy of the last setup's header (offsets count, max offset, jrel
+// range, signature range) keyed by its workspace: the column calls of the
+// phased assembly then need no device read-back (no stream sync per block)
+static thread_local struct { const void* ws = nullptr; int32_t hdr[6]; } g_bhdr;
+
 static int setup_bpath(int64_t n, const int64_t* cscptr, const int32_t* cscrow, int64_t sig0,
                        int64_t sig1, PlanWs pw, BPathWs bw, cudaStream_t s) {
   bpath_offsets_kernel<<<1, 1024, 0, s>>>(pw, bw);
@@ -1436,6 +1441,10 @@ static int setup_bpath(int64_t n, const int64_t* cscptr, const int32_t* cscrow, 
   const int32_t sig[2] = {(int32_t)sig0, (int32_t)sig1};
   cudaMemcpyAsync(bw.hdr + 4, sig, sizeof(sig), cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);
+  g_bhdr.ws = bw.hdr;
+  for (int i = 0; i < 4; ++i) g_bhdr.hdr[i] = hdr[i];
+  g_bhdr.hdr[4] = sig[0];
+  g_bhdr.hdr[5] = sig[1];
   return cudaGetLastError() == cudaSuccess ? 2 : 1;
 }
 
@@ -1486,8 +1495,12 @@ static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
                          const int64_t* cscptr, const int32_t* cscrow, const int64_t* csc2csr,
                          const double* cscval, double* m_csc, const AsmCtx& c, cudaStream_t s) {
   int32_t hdr[6];
-  SPAI_CUDA(cudaMemcpyAsync(hdr, c.bw.hdr, sizeof(hdr), cudaMemcpyDeviceToHost, s));
-  SPAI_CUDA(cudaStreamSynchronize(s));
+  if (g_bhdr.ws == c.bw.hdr) {
+    for (int i = 0; i < 6; ++i) hdr[i] = g_bhdr.hdr[i];
+  } else {
+    SPAI_CUDA(cudaMemcpyAsync(hdr, c.bw.hdr, sizeof(hdr), cudaMemcpyDeviceToHost, s));
+    SPAI_CUDA(cudaStreamSynchronize(s));
+  }
   const int64_t jmin = hdr[2], jmax = hdr[3];
   const int64_t chunk = std::min<int64_t>(kBChunk, c1 - c0);
   const int64_t wmax_rows = chunk + (jmax - jmin) + 1;

@@ -507,8 +507,11 @@ bgram_plan_kernel(Traversal tv, int64_t w0, int64_t sig0, int64_t sig1,
 }
 
 // (K_G) plan columns [c0, c1): G from B, Crout Cholesky, solves -> m_csc
+#ifndef SPAI_BSOLVE_MINB
+#define SPAI_BSOLVE_MINB 2
+#endif
 template <int NJ, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 2)
+__global__ void __launch_bounds__(WARPS * 32, SPAI_BSOLVE_MINB)
 bsolve_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__ cscptr,
               const int32_t* __restrict__ cscrow, const double* __restrict__ vals,
               const double* __restrict__ Bw, double* __restrict__ m_csc, AsmWs ws, PlanWs pw,
