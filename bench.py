@@ -862,10 +862,11 @@ def run_bicgstab(args):
             # one GPU: transpose, CSC values, classes, signatures, plans, replay,
             # CSC->CSR, SELL layout (analyze, 2 scans x 2, structure, 2 value
             # fills), half-storage probe of A (3), start = 20, then 7 per
-            # launched iteration; N > 1: 10 per launched iteration (3 updates,
-            # 4 SpMV, 3 reduction steps) + the rank's assembly (~14)
+            # launched iteration; N > 1: 14 per launched iteration (3 updates,
+            # 4 SpMVs split around their halos = 8, 3 reduction steps) + the
+            # rank's assembly (~14)
             "gpu_launches": sum((20 + 7 * t[2].launched_iterations) if world == 1 else
-                                (14 + 10 * t[2].launched_iterations) for t in times),
+                                (14 + 14 * t[2].launched_iterations) for t in times),
             "e2e": e2e,
             "cpu_baseline": None,
         }
