@@ -217,3 +217,82 @@ def _transpose(A: Csr) -> Csr:
 def pcg_vcycle(A, levels, coarse_inv, b, tol=1e-8, maxit=500, nu_pre=2, nu_post=2, omega=1.0):
     return pcg_classic(A, lambda r: vcycle(levels, coarse_inv, r, nu_pre, nu_post, omega),
                        b, tol=tol, maxit=maxit)
+
+
+# ---------------------------------------------------------------- sparse forms (large grids)
+# The same definitions with scipy.sparse arithmetic, for the 4096^2 parity
+# test of config C4 (the dense Galerkin above holds ~10^4 unknowns at most).
+# Only the summation order differs from the dense forms.
+def _scipy():
+    import scipy.sparse as sp
+    return sp
+
+
+def to_scipy(A: Csr):
+    sp = _scipy()
+    return sp.csr_matrix((A.values, A.col_indices, A.row_offsets), shape=(A.nrows, A.ncols))
+
+
+def prolongation_sparse(dims):
+    """`prolongation` (x innermost) as a scipy CSR matrix."""
+    sp = _scipy()
+    P = None
+    for n in dims:
+        p = to_scipy(coarsen_1d(n)[1])
+        P = p if P is None else sp.kron(p, P, format="csr")
+    return P.tocsr()
+
+
+def box_values(Ac, dims_c):
+    """Values of the scipy matrix Ac on the coarse 3^d box pattern (explicit
+    zeros where Ac stores nothing); asserts Ac has no entry outside it."""
+    off, cols = box_pattern(dims_c)
+    n = len(off) - 1
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(off))
+    want = rows * n + cols
+    Ac = Ac.tocoo()
+    have = Ac.row.astype(np.int64) * n + Ac.col.astype(np.int64)
+    o = np.argsort(have)
+    have, hv = have[o], Ac.data[o]
+    pos = np.searchsorted(want, have)
+    assert np.all(pos < len(want)) and np.array_equal(want[pos], have), \
+        "Galerkin product has couplings outside the 3^d box"
+    vals = np.zeros(len(want))
+    np.add.at(vals, pos, hv)
+    return Csr(n, n, off, cols, vals)
+
+
+def galerkin_sparse(A: Csr, dims_f, dims_c) -> Csr:
+    """`galerkin` with sparse products: P^T (A P), symmetrised when A = A^T."""
+    As = to_scipy(A)
+    P = prolongation_sparse(dims_f)
+    Ac = (P.T.tocsr() @ (As @ P)).tocsr()
+    if (As != As.T).nnz == 0:
+        Ac = (0.5 * (Ac + Ac.T)).tocsr()
+    return box_values(Ac, dims_c)
+
+
+def sparse_levels(levels):
+    """[(dims, A_l, M_l)] (oracle Csr) -> scipy form with each level's P, P^T."""
+    out = []
+    for l, (dl, A, M) in enumerate(levels):
+        P = prolongation_sparse(dl) if l < len(levels) - 1 else None
+        out.append((dl, to_scipy(A), to_scipy(M) if M is not None else None, P,
+                    P.T.tocsr() if P is not None else None))
+    return out
+
+
+def vcycle_sparse(slevels, coarse_inv, b, nu_pre=2, nu_post=2, omega=1.0, l=0):
+    """`vcycle` on `sparse_levels` output (same operation sequence)."""
+    _, A, M, P, Pt = slevels[l]
+    if l == len(slevels) - 1:
+        return coarse_inv @ b
+    x = omega * (M @ b)
+    for _ in range(nu_pre - 1):
+        x = x + omega * (M @ (b - A @ x))
+    r = b - A @ x
+    ec = vcycle_sparse(slevels, coarse_inv, Pt @ r, nu_pre, nu_post, omega, l + 1)
+    x = x + P @ ec
+    for _ in range(nu_post):
+        x = x + omega * (M @ (b - A @ x))
+    return x

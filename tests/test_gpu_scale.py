@@ -208,3 +208,109 @@ def test_variable_coefficient_q1_through_plan_replay(dims):
     rng2 = np.random.default_rng(7)
     cols = np.concatenate([rng2.integers(0, A.nrows, 3000), _plan_class_columns(dims)])
     _check_columns(A, m_plan, cols)
+
+
+def _host(A):
+    Ah = A.to_host()
+    return oracle.Csr(Ah.nrows, Ah.ncols, np.asarray(Ah.row_offsets), np.asarray(Ah.col_indices),
+                      np.asarray(Ah.values))
+
+
+def test_c2_bicgstab_4096sq_first_100_iterations_match_device_order_oracle():
+    """configs[1] scale: 2D Q1 4096^2 (16.8 M DOF), raw SPAI(1) + K9
+    BiCGStab.  SPAI columns sampled against the reference QR solve; the first
+    100 iterations of the device solver (A and M in SELL-32, the format
+    oracle/devorder.c restates) against the device-order oracle on the
+    downloaded A and M: residual histories <= 1e-8, x <= 1e-10.  (The bench
+    runs A on half storage; its products are the same sums in another order.)"""
+    from oracle import devorder
+    from paper_1911_01492_b200.krylov import DeviceKrylov
+    N = 4096
+    A = pb.q1_device((N, N))
+    m_csc = pb.precond.spai1_columns_device(A)
+    n = A.nrows
+    rng = np.random.default_rng(4096)
+    cols = np.concatenate([rng.integers(0, n, 5000), _plan_class_columns((N, N)),
+                           np.arange(64), np.arange(n - 64, n)])
+    worst = _check_columns(A, m_csc, cols)
+    M = pb.spai1_device(A)
+    b = A.matvec(torch.ones(n, dtype=torch.float64, device="cuda"))
+    its = 100
+    s = DeviceKrylov(1, A, M, 1e-300, its, symmetric=False)
+    assert s.operator_format == "sell"
+    st = s.run(b)
+    h = s.history(st[1])
+    x = s.x().cpu().numpy()
+    grid = s.grid()
+    s.close()
+    xo, ho, sto, n0, _ = devorder.bicgstab_devorder(_host(A), _host(M), b.cpu().numpy(), 1e-300,
+                                                    its, grid)
+    assert len(h) == len(ho) == its and st[0] == sto
+    assert st[2] == n0
+    rel = np.max(np.abs(h - ho) / ho)
+    print(f"C2 4096^2: SPAI worst {worst:.2e} on {len(np.unique(cols))} columns, "
+          f"history rel {rel:.2e}")
+    assert rel <= HIST_TOL, rel
+    assert np.max(np.abs(x - xo)) <= 1e-10 * np.max(np.abs(xo))
+
+
+def test_c4_multigrid_4096sq_matches_sparse_oracle():
+    """configs[3] scale: 2D anisotropic Q1 4096^2 (eps_y = 1e-3), 8-level
+    V-cycle.  Every level is checked against the oracle on its own input:
+    Galerkin P^T A_l P (scipy products, oracle/multigrid.py) <= 1e-12, the
+    raw SPAI(1) on sampled columns vs the reference QR solve <= 1e-10 and the
+    smoother M_l = 0.5 (M + M^T) of it; then one V-cycle and the first 10
+    MG-PCG iterations against the oracle V-cycle on the downloaded levels
+    (<= 1e-9 / histories <= 1e-8)."""
+    from oracle import multigrid as omg
+    N = 4096
+    dims = (N, N)
+    A = pb.q1_device(dims, eps=(1.0, 1e-3))
+    P = pb.MultigridPreconditioner(A, dims, nu_pre=2, nu_post=2)
+    assert P.nlevels == 8 and tuple(P.dims[-1]) == (32, 32)
+    rng = np.random.default_rng(44)
+    levels = []
+    for l in range(P.nlevels):
+        Al = P.A[l]
+        host = _host(Al)
+        if l > 0:
+            ref = omg.galerkin_sparse(levels[-1][1], P.dims[l - 1], P.dims[l])
+            assert np.array_equal(host.row_offsets, ref.row_offsets)
+            assert np.array_equal(host.col_indices, ref.col_indices)
+            err = np.max(np.abs(host.values - ref.values)) / np.max(np.abs(ref.values))
+            assert err <= 1e-12, (l, err)
+        Ml = None
+        if l < P.nlevels - 1:
+            n = Al.nrows
+            m_csc = pb.precond.spai1_columns_device(Al)
+            cols = np.concatenate([rng.integers(0, n, 2000), _plan_class_columns(P.dims[l])])
+            _check_columns(Al, m_csc, cols)
+            # S = 0.5 (M + M^T): CSR position p = (i, j) holds 0.5 (m_j[i] + m_i[j])
+            m = m_csc.cpu().numpy()
+            rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(host.row_offsets))
+            key = rows * n + host.col_indices
+            tp = np.searchsorted(key, host.col_indices * n + rows)
+            Ml = _host(P.M[l])
+            assert np.array_equal(Ml.col_indices, host.col_indices)
+            assert np.array_equal(Ml.values, 0.5 * (m + m[tp])), l
+        levels.append((tuple(P.dims[l]), host, Ml))
+    cinv = P.coarse_inv.cpu().numpy()
+    slev = omg.sparse_levels(levels)
+    r = rng.standard_normal(A.nrows)
+    z = P.apply(r)
+    zr = omg.vcycle_sparse(slev, cinv, r)
+    assert np.max(np.abs(z - zr)) <= 1e-9 * np.max(np.abs(zr))
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    its = 10
+    x, rec = pb.solve(pb.LocalSystem(A, P), b, pb.SolverConfig(tol=1e-300, maxit=its))
+    assert rec.iterations == its and not rec.converged
+    As = slev[0][1]
+    xr, rr = oracle.pcg_classic(levels[0][1], lambda v: omg.vcycle_sparse(slev, cinv, v),
+                                b.cpu().numpy(), tol=1e-300, maxit=its,
+                                matvec=lambda _A, v: As @ v)
+    h, hr = np.array(rec.residual_norms), np.array(rr.residual_norms)
+    assert len(h) == len(hr) == its
+    rel = np.max(np.abs(h - hr) / hr)
+    print(f"C4 4096^2: V-cycle ok, MG-PCG history rel {rel:.2e}")
+    assert rel <= HIST_TOL, rel
+    assert np.max(np.abs(x.cpu().numpy() - xr)) <= 1e-9 * np.max(np.abs(xr))

@@ -247,3 +247,23 @@ def test_element_assembly_with_unit_coefficient_is_the_q1_stencil(dims):
     assert np.array_equal(K.col_indices, B.col_indices)
     D = K.to_dense()
     assert np.array_equal(D, D.T) and np.all(np.linalg.eigvalsh(D) > 0)
+
+
+@pytest.mark.parametrize("dims,eps,nlev", [((17, 13), (1.0, 1e-3), 3), ((7, 6, 5), None, 2)])
+def test_sparse_multigrid_forms_match_dense(dims, eps, nlev):
+    """The scipy forms used by the 4096^2 C4 parity test restate the dense
+    definitions: Galerkin operators and one V-cycle agree to rounding."""
+    from oracle import multigrid as omg
+    A = oracle.stencil_csr(dims, *oracle.q1_stencil(len(dims), eps=eps))
+    levels, cinv = omg.build_levels(A, dims, nlev)
+    for l in range(1, nlev):
+        dl, dc = levels[l - 1][0], levels[l][0]
+        ref = levels[l][1]
+        got = omg.galerkin_sparse(levels[l - 1][1], dl, dc)
+        assert np.array_equal(got.row_offsets, ref.row_offsets)
+        assert np.array_equal(got.col_indices, ref.col_indices)
+        assert np.max(np.abs(got.values - ref.values)) <= 1e-13 * np.max(np.abs(ref.values))
+    r = np.random.default_rng(3).standard_normal(A.nrows)
+    z = omg.vcycle_sparse(omg.sparse_levels(levels), cinv, r)
+    zr = omg.vcycle(levels, cinv, r)
+    assert np.max(np.abs(z - zr)) <= 1e-12 * np.max(np.abs(zr))
