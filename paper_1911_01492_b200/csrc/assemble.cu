@@ -1488,7 +1488,7 @@ static bool build_plans(int64_t c0, int64_t c1, const int64_t* cscptr, const int
 // window of B rows [c0 + min jrel, c1 - 1 + max jrel] in a stream-ordered
 // temporary (K_B), then the per-column solves (K_G).
 constexpr int64_t kBChunk = (int64_t)1 << 23;
-constexpr int kBRowWarps = 8, kBSolveWarps = 8, kBPlanWarps = 8;
+constexpr int kBRowWarps = 8, kBSolveWarps = 8, kBSolve2Warps = 4, kBPlanWarps = 8;
 
 template <int NJ, int CAPL>
 static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
@@ -1532,13 +1532,20 @@ static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
     plan_per_sm = std::max(plan_per_sm, 1);
     plan_capl = CAPL;
   }
-  const size_t ssm = (size_t)kBSolveWarps * kLsDoubles(NJ) * sizeof(double);
+  // solve kernel: two columns per warp (bsolve2_kernel) unless SPAI_BSOLVE=1
+  static int solve_var = -1;
+  if (solve_var < 0) { const char* e = getenv("SPAI_BSOLVE"); solve_var = e ? atoi(e) : 2; }
+  const bool two = NJ > 16 && solve_var != 1;    // rows l, l + 16 per lane need |J| > 16
+  const int swarps = two ? kBSolve2Warps : kBSolveWarps;
+  const size_t ssm = (size_t)swarps * (two ? 2 : 1) * kLsDoubles(NJ) * sizeof(double);
   static int solve_nj = -1;
   if (solve_nj != NJ) {
-    SPAI_CUDA(cudaFuncSetAttribute(bsolve_kernel<NJ, kBSolveWarps>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&solve_per_sm, bsolve_kernel<NJ, kBSolveWarps>,
-                                                  kBSolveWarps * 32, ssm);
+    const void* kern = (const void*)bsolve_kernel<NJ, kBSolveWarps>;
+    if constexpr (NJ > 16) {
+      if (two) kern = (const void*)bsolve2_kernel<NJ, kBSolve2Warps>;
+    }
+    SPAI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&solve_per_sm, kern, swarps * 32, ssm);
     solve_per_sm = std::max(solve_per_sm, 1);
     solve_nj = NJ;
   }
@@ -1563,10 +1570,17 @@ static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
         hdr[1], Bw);
     const cudaError_t e1 = cudaGetLastError();
     if (e1 != cudaSuccess) { st = cuda_fail(e1, "bgram_list_kernel"); break; }
-    const int64_t gs = std::min<int64_t>((b - a + kBSolveWarps - 1) / kBSolveWarps,
-                                         (int64_t)num_sms() * solve_per_sm);
-    bsolve_kernel<NJ, kBSolveWarps><<<(unsigned)std::max<int64_t>(gs, 1), kBSolveWarps * 32, ssm, s>>>(
-        tcols, w0, w1, cscptr, cscrow, vals, Bw, m_csc, c.ws, c.pw, c.bw, c.direct, c.ndirect);
+    const int64_t per_block = (int64_t)swarps * (two ? 2 : 1);
+    const unsigned gs = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((b - a + per_block - 1) / per_block, (int64_t)num_sms() * solve_per_sm));
+    if constexpr (NJ > 16) {
+      if (two)
+        bsolve2_kernel<NJ, kBSolve2Warps><<<gs, kBSolve2Warps * 32, ssm, s>>>(
+            tcols, w0, w1, cscptr, cscrow, vals, Bw, m_csc, c.ws, c.pw, c.bw, c.direct, c.ndirect);
+    }
+    if (!two)
+      bsolve_kernel<NJ, kBSolveWarps><<<gs, kBSolveWarps * 32, ssm, s>>>(
+          tcols, w0, w1, cscptr, cscrow, vals, Bw, m_csc, c.ws, c.pw, c.bw, c.direct, c.ndirect);
     const cudaError_t e2 = cudaGetLastError();
     if (e2 != cudaSuccess) { st = cuda_fail(e2, "bsolve_kernel"); break; }
   }

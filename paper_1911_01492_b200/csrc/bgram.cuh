@@ -639,4 +639,200 @@ bsolve_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__ 
   }
 }
 
+// (K_G, two columns per warp) the LSU data pipe bounds bsolve_kernel (87 %
+// of its wavefront peak at 400^3: ~635 shared + ~195 global wavefronts per
+// column, the fp64 pipe 33 % busy).  Here half-warp h = lane / 16 solves
+// column t = 2 w + h and lane l of a half owns rows l and l + 16 of
+// [G; rhs^T] (the right-hand side is row 31 = lane 15's second row), so
+// every shared-memory broadcast, shuffle and store instruction serves two
+// columns, and the first rows (l < 16) drop out of the factorisation after
+// step 15 (236 instead of 351 FMA instructions per column).  Same algorithm
+// as bsolve_kernel: Crout with look-ahead, forward solve as the rhs row,
+// zero-upper backward solve, the replay's pivot / rank tests per half.
+#ifndef SPAI_BSOLVE2_MINB
+#define SPAI_BSOLVE2_MINB 3
+#endif
+template <int NJ, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, SPAI_BSOLVE2_MINB)
+bsolve2_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__ cscptr,
+               const int32_t* __restrict__ cscrow, const double* __restrict__ vals,
+               const double* __restrict__ Bw, double* __restrict__ m_csc, AsmWs ws, PlanWs pw,
+               BPathWs bw, int32_t* __restrict__ direct, int* __restrict__ ndirect) {
+  static_assert(NJ > 16 && NJ <= kBMaxNJ, "rows l and l + 16 per lane, rhs as row 31");
+  constexpr int LS = kLStrideOf(NJ);
+  constexpr unsigned kFull = 0xffffffffu;
+  extern __shared__ __align__(16) double bs_smem[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = lane & 15;
+  const unsigned hmask = (lane & 16) ? 0xFFFF0000u : 0x0000FFFFu;
+  double* Ls = bs_smem + (size_t)(2 * w + (lane >> 4)) * kLsDoubles(NJ);
+  for (int i = l; i < kLsDoubles(NJ); i += 16) Ls[i] = 0.0;   // upper parts stay 0
+  __syncwarp();
+  const int r1 = l, r2 = l + 16;
+  double* row1 = Ls + r1 * LS;
+  double* row2 = Ls + r2 * LS;
+  double* dgl = Ls + 32 * LS;                        // L(c, c)
+  const bool keep2 = r2 < NJ || r2 == kRhsLane;
+  const int64_t nw = (int64_t)gridDim.x * WARPS * 2;
+  const int64_t nt = tv.count();
+  for (int64_t base = blockIdx.x * (int64_t)WARPS * 2; base < nt; base += nw) {
+    const int64_t t = base + 2 * w + (lane >> 4);
+    const int64_t kq = t < nt ? tv.at(t) : -1;
+    bool act = kq >= 0;                              // this half owns a column
+    if (__all_sync(kFull, !act)) continue;
+    // an idle half repeats its partner's column (results dropped): every
+    // load below runs on both halves, no half-divergent branch before the
+    // warp collectives (an idle half that skipped them sent its partner to
+    // the QR fallback in a measured build)
+    const int64_t kp = __shfl_xor_sync(kFull, kq, 16);
+    const int64_t k = act ? kq : kp;
+    const int slot = pw.plan_slot[k];
+    const int pi = slot >= 0 ? pw.slot_plan[slot] : -1;
+    const uint32_t* P = pi >= 0 ? pw.plans + (size_t)pi * kPlanWords : nullptr;
+    const int64_t jlo = cscptr[k];
+    int nj = (int)(cscptr[k + 1] - jlo);
+    bool bad = !(P != nullptr && P[kPH_nsteps] != 0xFFFFFFFFu && nj <= NJ && (int)P[kPH_nj] == nj);
+    if (!bad) {
+      if (r1 < nj) bad = (uint32_t)(cscrow[jlo + r1] - (int32_t)k) != P[kPO_jrel + r1];
+      if (r2 < nj) bad = bad || (uint32_t)(cscrow[jlo + r2] - (int32_t)k) != P[kPO_jrel + r2];
+    }
+    const bool hbad = (__ballot_sync(kFull, bad) & hmask) != 0;   // half-uniform
+    if (hbad && act && l == 0) direct[atomicAdd(ndirect, 1)] = (int32_t)k;
+    if (__all_sync(kFull, hbad || !act)) continue;
+    act = act && !hbad;
+    const bool ok_tab = !hbad;                       // this half's plan table is usable
+    if (hbad) nj = 0;                                // identity problem, dropped
+    // rows r1, r2 of G from B (the rhs row from A's row k); idle halves read
+    // offset 0 and are replaced by the identity below
+    const int32_t* T = bw.btab + (size_t)(ok_tab ? pi : 0) * kBTab;
+    const double* bsrc = Bw + (k - w0) * kBW;
+    const double* src2 = r2 == kRhsLane ? vals + jlo : bsrc;
+    double g1[16], g2[NJ];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const int32_t o = ok_tab ? T[c * 32 + r1] : 0;
+      SPAI_DCHECK((k - w0) * kBW + o >= 0 && (k - w0) * kBW + o < (w1 - w0) * kBW);
+      g1[c] = bsrc[o];
+    }
+#pragma unroll
+    for (int c = 0; c < NJ; ++c) {
+      const int32_t o = ok_tab ? T[c * 32 + r2] : 0;
+      SPAI_DCHECK(r2 == kRhsLane ||
+                  ((k - w0) * kBW + o >= 0 && (k - w0) * kBW + o < (w1 - w0) * kBW));
+      g2[c] = src2[o];
+    }
+    if (__any_sync(kFull, nj != NJ)) {               // boundary plan / bad half: identity rows
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (r1 >= nj) g1[c] = c == r1 ? 1.0 : 0.0;
+#pragma unroll
+      for (int c = 0; c < NJ; ++c) {
+        if (r2 >= nj && r2 < NJ) g2[c] = c == r2 ? 1.0 : 0.0;
+        if (r2 == kRhsLane && c >= nj) g2[c] = 0.0;
+      }
+    }
+    double p1 = g1[0], p2 = g2[0];
+#pragma unroll
+    for (int c = 0; c < NJ; ++c) {
+      double s1 = p1, s2 = p2;
+      if (c > 0) {
+        const double lc = Ls[c * LS + c - 1];
+        if (c < 16) s1 = fma(-g1[c - 1], lc, p1);
+        s2 = fma(-g2[c - 1], lc, p2);
+      }
+      // look-ahead: step c + 1's sums over j < c (row c + 1 final since step c - 1)
+      double n1 = 0.0, n2 = 0.0;
+      if (c + 1 < NJ) {
+        const double* rn = Ls + (c + 1) * LS;
+        const bool two = c + 1 < 16;                 // row l still factoring
+        const int j0 = ((c + 1) * LS) & 1;
+        double a0 = two ? g1[c + 1] : 0.0, a1 = 0.0;
+        double b0 = g2[c + 1], b1 = 0.0, b2 = 0.0, b3 = 0.0;
+        if (j0 == 1 && c > 0) {
+          const double v = rn[0];
+          if (two) a1 = fma(-g1[0], v, a1);
+          b1 = fma(-g2[0], v, b1);
+        }
+#pragma unroll
+        for (int j = j0; j + 1 < c; j += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(rn + j);
+          if (two) {
+            a0 = fma(-g1[j], v.x, a0);
+            a1 = fma(-g1[j + 1], v.y, a1);
+            b0 = fma(-g2[j], v.x, b0);
+            b1 = fma(-g2[j + 1], v.y, b1);
+          } else if (((j - j0) >> 1) & 1) {
+            b2 = fma(-g2[j], v.x, b2);
+            b3 = fma(-g2[j + 1], v.y, b3);
+          } else {
+            b0 = fma(-g2[j], v.x, b0);
+            b1 = fma(-g2[j + 1], v.y, b1);
+          }
+        }
+        if (c > j0 && ((c - j0) & 1)) {
+          const double v = rn[c - 1];
+          if (two) a0 = fma(-g1[c - 1], v, a0);
+          b0 = fma(-g2[c - 1], v, b0);
+        }
+        n1 = a0 + a1;
+        n2 = (b0 + b1) + (b2 + b3);
+      }
+      const double d = __shfl_sync(kFull, c < 16 ? s1 : s2, (c & 15) | (lane & 16));
+      const double rs = rsqrt(d);
+      const double l2 = s2 * rs;
+      g2[c] = l2;
+      if (r2 > c && keep2) row2[c] = l2;             // strict lower part only
+      if (c < 16) {
+        const double l1 = s1 * rs;
+        g1[c] = l1;
+        if (r1 > c) row1[c] = l1;
+        if (r1 == c) dgl[c] = l1;
+      } else if (r2 == c) {
+        dgl[c] = l2;
+      }
+      p1 = n1;
+      p2 = n2;
+      __syncwarp();
+    }
+    // pivot tests per half (the replay's): L_rr^2 > 1e-4 G_rr, rank guard
+    const bool real1 = r1 < nj, real2 = r2 < nj;
+    const int me1 = real1 ? r1 : 0, me2 = real2 ? r2 : 0;
+    const double lrr1 = dgl[me1], lrr2 = dgl[me2];
+    const double gd1 = bsrc[ok_tab ? T[me1 * 32 + me1] : 0];
+    const double gd2 = bsrc[ok_tab ? T[me2 * 32 + me2] : 0];
+    const double d1 = lrr1 * lrr1, d2 = lrr2 * lrr2;
+    const bool badp = (real1 && !(d1 > kFlagPivot * gd1)) || (real2 && !(d2 > kFlagPivot * gd2));
+    double dmin = fmin(real1 ? d1 : 1e300, real2 ? d2 : 1e300);
+    double dmx = fmax(real1 ? d1 : 0.0, real2 ? d2 : 0.0);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      dmin = fmin(dmin, __shfl_xor_sync(kFull, dmin, o));
+      dmx = fmax(dmx, __shfl_xor_sync(kFull, dmx, o));
+    }
+    const bool hbadp = (__ballot_sync(kFull, badp) & hmask) != 0;   // all lanes vote
+    const bool qr = act && (hbadp || !(sqrt(dmin) > kRankGuard * fmax(sqrt(dmx), 1.0)));
+    if (qr && l == 0) to_qr(ws, k);
+    // backward: L^T m = y, y = row 31 of L; zero upper parts, so each lane
+    // ends with m_r1, m_r2 (rows >= 17 only see columns c > 16)
+    const double inv1 = 1.0 / lrr1, inv2 = 1.0 / lrr2;
+    double y1 = Ls[kRhsLane * LS + me1] * inv1;
+    double y2 = Ls[kRhsLane * LS + me2] * inv2;
+#pragma unroll
+    for (int c = NJ - 1; c >= 0; --c) {
+      const double mc = __shfl_sync(kFull, c < 16 ? y1 : y2, (c & 15) | (lane & 16));
+      const double lc1 = Ls[c * LS + me1] * inv1;
+      if (c > 16) {
+        const double lc2 = Ls[c * LS + me2] * inv2;
+        y2 = fma(-lc2, mc, y2);
+      }
+      y1 = fma(-lc1, mc, y1);
+    }
+    if (act && !qr) {
+      if (real1) m_csc[jlo + r1] = y1;
+      if (real2) m_csc[jlo + r2] = y2;
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace spai
