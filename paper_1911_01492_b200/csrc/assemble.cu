@@ -644,6 +644,7 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t last_h = 0;                         // the warp's last signature and its slot
   int last_slot = -1;
+  int last_nj = -1, last_rel = 0, last_cls = 0;   // ... and its (J - k, class) lanes
   for (int64_t k = c0 + w0; k < n; k += nw) {
     const int64_t jlo = cscptr[k];
     const int nj = (int)(cscptr[k + 1] - jlo);
@@ -652,8 +653,15 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
     if (lane < nj) {
       c = cscrow[jlo + lane];
       cls = pw.col_class[c];
-      len = (int)(cscptr[c + 1] - cscptr[c]);
     }
+    // most columns repeat the warp's last signature exactly: no lengths,
+    // hash or table probe
+    if (nj == last_nj && last_slot >= 0 &&
+        __all_sync(0xffffffffu, lane >= nj || (c - (int32_t)k == last_rel && cls == last_cls))) {
+      if (lane == 0) pw.plan_slot[k] = last_slot;
+      continue;
+    }
+    if (lane < nj) len = (int)(cscptr[c + 1] - cscptr[c]);
     int total = len;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
@@ -687,6 +695,9 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
     }
     last_slot = __shfl_sync(0xffffffffu, last_slot, 0);
     last_h = last_slot >= 0 ? h : 0;
+    last_nj = nj;
+    last_rel = c - (int32_t)k;
+    last_cls = cls;
   }
 }
 
@@ -1537,7 +1548,8 @@ static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
   if (solve_var < 0) { const char* e = getenv("SPAI_BSOLVE"); solve_var = e ? atoi(e) : 2; }
   const bool two = NJ > 16 && solve_var != 1;    // rows l, l + 16 per lane need |J| > 16
   const int swarps = two ? kBSolve2Warps : kBSolveWarps;
-  const size_t ssm = (size_t)swarps * (two ? 2 : 1) * kLsDoubles(NJ) * sizeof(double);
+  const size_t ssm = two ? (size_t)swarps * 2 * kLs2Doubles(NJ) * sizeof(double)
+                        : (size_t)swarps * kLsDoubles(NJ) * sizeof(double);
   static int solve_nj = -1;
   if (solve_nj != NJ) {
     const void* kern = (const void*)bsolve_kernel<NJ, kBSolveWarps>;

@@ -652,6 +652,9 @@ bsolve_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__ 
 #ifndef SPAI_BSOLVE2_MINB
 #define SPAI_BSOLVE2_MINB 3
 #endif
+// per half: rows 0..NJ-1 of L, the right-hand side row stored as row NJ
+// (lane rows NJ..30 are padding and never stored), then the diagonal
+__host__ __device__ constexpr int kLs2Doubles(int nj) { return ((nj + 1) * kLStrideOf(nj) + 32 + 1) & ~1; }
 template <int NJ, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, SPAI_BSOLVE2_MINB)
 bsolve2_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__ cscptr,
@@ -665,13 +668,13 @@ bsolve2_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int l = lane & 15;
   const unsigned hmask = (lane & 16) ? 0xFFFF0000u : 0x0000FFFFu;
-  double* Ls = bs_smem + (size_t)(2 * w + (lane >> 4)) * kLsDoubles(NJ);
-  for (int i = l; i < kLsDoubles(NJ); i += 16) Ls[i] = 0.0;   // upper parts stay 0
+  double* Ls = bs_smem + (size_t)(2 * w + (lane >> 4)) * kLs2Doubles(NJ);
+  for (int i = l; i < kLs2Doubles(NJ); i += 16) Ls[i] = 0.0;   // upper parts stay 0
   __syncwarp();
   const int r1 = l, r2 = l + 16;
   double* row1 = Ls + r1 * LS;
-  double* row2 = Ls + r2 * LS;
-  double* dgl = Ls + 32 * LS;                        // L(c, c)
+  double* row2 = Ls + (r2 == kRhsLane ? NJ : r2) * LS;   // used only when r2 < NJ or rhs
+  double* dgl = Ls + (NJ + 1) * LS;                  // L(c, c)
   const bool keep2 = r2 < NJ || r2 == kRhsLane;
   const int64_t nw = (int64_t)gridDim.x * WARPS * 2;
   const int64_t nt = tv.count();
@@ -812,11 +815,11 @@ bsolve2_kernel(Traversal tv, int64_t w0, int64_t w1, const int64_t* __restrict__
     const bool hbadp = (__ballot_sync(kFull, badp) & hmask) != 0;   // all lanes vote
     const bool qr = act && (hbadp || !(sqrt(dmin) > kRankGuard * fmax(sqrt(dmx), 1.0)));
     if (qr && l == 0) to_qr(ws, k);
-    // backward: L^T m = y, y = row 31 of L; zero upper parts, so each lane
+    // backward: L^T m = y, y = the stored rhs row of L; zero upper parts, so each lane
     // ends with m_r1, m_r2 (rows >= 17 only see columns c > 16)
     const double inv1 = 1.0 / lrr1, inv2 = 1.0 / lrr2;
-    double y1 = Ls[kRhsLane * LS + me1] * inv1;
-    double y2 = Ls[kRhsLane * LS + me2] * inv2;
+    double y1 = Ls[NJ * LS + me1] * inv1;
+    double y2 = Ls[NJ * LS + me2] * inv2;
 #pragma unroll
     for (int c = NJ - 1; c >= 0; --c) {
       const double mc = __shfl_sync(kFull, c < 16 ? y1 : y2, (c & 15) | (lane & 16));

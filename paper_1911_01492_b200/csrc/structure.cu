@@ -161,6 +161,14 @@ __global__ void sym_transpose_kernel(int64_t n, const int64_t* __restrict__ rowp
       const int32_t i = colidx[q];
       int64_t a = rowptr[i], b = rowptr[i + 1];
       const int64_t end = b;
+      // first probe at the mirrored index (exact for point-symmetric row
+      // patterns, i.e. every interior stencil row): one dependent load
+      // instead of a 5-step search
+      const int64_t guess = a + (b - a - 1) - (q - lo);
+      if (guess >= a && guess < b && colidx[guess] == (int32_t)c) {
+        csc2csr[q] = guess;
+        continue;
+      }
       while (a < b) {
         const int64_t mid = (a + b) >> 1;
         if (colidx[mid] < (int32_t)c) a = mid + 1; else b = mid;
