@@ -155,6 +155,10 @@ int spai_set_assembly_plans(int enable);
  * CSC-ordered M values -> CSR values of M (from_coo, precond.py:199). */
 int spai_csc_to_csr_values(int64_t nnz, const int64_t* csc2csr,
                            const double* m_csc, double* m_csr, void* stream);
+/* dst[p] = src[perm[p]].  With perm = csc2csr of a structurally symmetric
+ * pattern (an involution) this is spai_csc_to_csr_values as a gather.      */
+int spai_gather_values(int64_t nnz, const int64_t* perm, const double* src,
+                       double* dst, void* stream);
 /* 0.5*(M + M^T) kept on pattern(A) (replaces cli.py:189-194 dense
  * symmetrisation; requires a structurally symmetric pattern, see
  * spai_structure_is_symmetric).  s_csr may alias nothing.                 */

@@ -114,6 +114,7 @@ _SIGS = {
     "spai_dist_update_xr": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "spai_dist_reduce_step": (_i32, [_i32, _vp, _i32, _i32, _vp, _vp, _vp]),
     "spai_csc_to_csr_values": (_i32, [_i64, _vp, _vp, _vp, _vp]),
+    "spai_gather_values": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_symmetrize": (_i32, [_i64, _vp, _vp, _vp, _vp]),
     "spai_symmetrize_union_count": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                            C.POINTER(_i64), _vp]),

@@ -1048,13 +1048,9 @@ def _assemble_range(A, c0, c1, col_base=0):
 def _raw_range(A, c0, c1, col_base=0):
     """SPAI(1) M (not symmetrised) on pattern(A), CSR values, columns [c0, c1)
     assembled (rows whose couplings stay inside the range are exact)."""
-    import torch
-    from .sparse import ptr, stream_handle
-    m_csc, csc2csr = _assemble_range(A, c0, c1, col_base)
-    vals = torch.empty_like(m_csc)
-    _lib.check(_lib.load().spai_csc_to_csr_values(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals),
-                                                  stream_handle()), "spai_csc_to_csr_values")
-    return A.with_values(vals)
+    from .precond import csc_to_csr_values
+    m_csc, _ = _assemble_range(A, c0, c1, col_base)
+    return A.with_values(csc_to_csr_values(A, m_csc))
 
 
 def _symmetric_range(A, c0, c1):

@@ -168,11 +168,21 @@ def spai1_device(A, stats: SpaiStats | None = None) -> DeviceCsr:
     torch = _require_cuda()
     A = as_device(A)
     m_csc = spai1_columns_device(A, stats)
+    return A.with_values(csc_to_csr_values(A, m_csc))
+
+
+def csc_to_csr_values(A: DeviceCsr, m_csc):
+    """M's CSC-ordered values in CSR order (precond.py:199's from_coo): a
+    gather through the involution csc2csr when pattern(A) is symmetric, the
+    scatter otherwise."""
+    torch = _require_cuda()
+    lib = _lib.load()
     _, _, csc2csr = A.csc()
     vals = torch.empty_like(m_csc)
-    _lib.check(_lib.load().spai_csc_to_csr_values(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals),
-                                                  stream_handle()), "spai_csc_to_csr_values")
-    return A.with_values(vals)
+    fn = lib.spai_gather_values if A.structurally_symmetric() else lib.spai_csc_to_csr_values
+    _lib.check(fn(A.nnz, ptr(csc2csr), ptr(m_csc), ptr(vals), stream_handle()),
+               "csc_to_csr_values")
+    return vals
 
 
 def spai1_symmetric_device(A, stats: SpaiStats | None = None) -> DeviceCsr:

@@ -786,3 +786,23 @@ def test_phased_assembly_any_column_blocks():
     assert lib.spai_assemble_columns(n, ptr(A.vals), ptr(cscptr), ptr(cscrow), ptr(csc2csr),
                                      ptr(A.csc_values()), 5, 2, ptr(m), ptr(ws), wsb,
                                      hmax.value, plans.value, s) == _lib.SPAI_E_ARG
+
+
+def test_csc_to_csr_gather_equals_scatter():
+    """Structurally symmetric pattern: the CSR-order values of M through the
+    gather (csc2csr is an involution) equal the scatter form bit for bit."""
+    from paper_1911_01492_b200 import _lib
+    from paper_1911_01492_b200.sparse import ptr, stream_handle
+    A = pb.q1_device((37, 23, 19), conv=(1.0, -0.5, 0.25))
+    assert A.structurally_symmetric()
+    m = torch.randn(A.nnz, dtype=torch.float64, device="cuda")
+    _, _, perm = A.csc()
+    a, b = torch.empty_like(m), torch.empty_like(m)
+    lib = _lib.load()
+    assert lib.spai_csc_to_csr_values(A.nnz, ptr(perm), ptr(m), ptr(a), stream_handle()) == 0
+    assert lib.spai_gather_values(A.nnz, ptr(perm), ptr(m), ptr(b), stream_handle()) == 0
+    assert torch.equal(a, b)
+    assert lib.spai_gather_values(A.nnz, ptr(perm), ptr(m), ptr(m), stream_handle()) == \
+        _lib.SPAI_E_ARG                                   # in place is rejected
+    M = pb.spai1_device(A)
+    assert torch.equal(M.vals, pb.precond.csc_to_csr_values(A, pb.precond.spai1_columns_device(A)))
