@@ -346,8 +346,9 @@ def run_ours(args):
         # A, longest column, classes, signatures, plan build, B-path setup (4),
         # symmetrise, fill of S, PCG start (2) = 17 kernels; per chunk of
         # 2^23 columns the B rows (plan + generic list) and the solves (3);
-        # then 4 per launched PCG iteration
-        launches["n"] += 17 + 3 * ((n + (1 << 23) - 1) >> 23) + 4 * _advanced(rec)
+        # then 4 per launched PCG iteration and the x fix-up pair per advance
+        launches["n"] += (17 + 3 * ((n + (1 << 23) - 1) >> 23) + 4 * _advanced(rec) +
+                          2 * getattr(rec, "advance_calls", 0))
         return e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3, rec, x
 
     def barrier():
@@ -389,8 +390,9 @@ def run_ours(args):
     # compulsory bytes of one PCG iteration in the solve format (krylov.py:315-339
     # op sequence): A.p and M.r stream 8 B per stored SELL value (the relative
     # SELL slices carry no per-entry column index), x gather + y write per SpMV,
-    # and the vector updates -> 2 * 8 * nvals + 104 * n.  The CSR/int32 figure of
-    # SURVEY.md 8(d) (24 * nnz + 104 * n) is reported alongside.
+    # and the vector updates (12 vector streams of 8 B per row since the x
+    # update moved into V1, krylov.cu) -> 2 * 8 * nvals + 96 * n.  The CSR/int32
+    # figure of SURVEY.md 8(d) (24 * nnz + 104 * n) is reported alongside.
     fmt = getattr(rec, "operator_format", "sell")
     if fmt == "ssell":
         # symmetric half storage (K5c): each operator streams its upper-triangle
@@ -398,7 +400,7 @@ def run_ours(args):
         nvals = 32 * ((n + 31) // 32) * len(A.ssell_offsets())
     else:
         nvals = A.sell_stats()[0]
-    b_it = 16 * nvals + 104 * n
+    b_it = 16 * nvals + 96 * n
     b_it_csr = 24 * nnz + 104 * n
     # assembly vs the FP64 CUDA-core peak.  The B path (K3b)
     # executes per interior 3D Q1 column: its B row (378 products = 756

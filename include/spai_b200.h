@@ -266,7 +266,8 @@ int spai_pcg_create_sym(spai_pcg** out, int64_t n, const int32_t* g, int w,
                         int64_t maxit, void* ws, size_t ws_bytes, void* stream);
 /* Start from x0 (device, may be NULL -> zero); b device, copied.          */
 int spai_pcg_start(spai_pcg* s, const double* b, const double* x0);
-/* Enqueue up to `iters` more iterations (no host sync; CUDA graphs of 16). */
+/* Enqueue up to `iters` more iterations (no host sync; CUDA graphs of 16),
+ * then x's lagged update if the solver has stopped (2 small kernels).     */
 int spai_pcg_advance(spai_pcg* s, int64_t iters);
 /* Synchronous: status 0 running, 1 converged, 2 maxit, 3 breakdown,
  * 4 divergence; iterations done; norm0; last norm; breakdown value.       */
@@ -274,8 +275,13 @@ int spai_pcg_poll(spai_pcg* s, int* status, int64_t* iterations, double* norm0,
                   double* norm, double* aux);
 /* Synchronous copy of the residual history [0, count) to host.            */
 int spai_pcg_history(spai_pcg* s, double* host_out, int64_t count);
-/* Device pointers of the state vectors (x, r, p, z).                      */
+/* Device pointers of the state vectors (x, r, p, z).  While the solver is
+ * running x lags by one update (lambda p of the last iteration); it is
+ * complete once spai_pcg_poll reports a stop after spai_pcg_advance.      */
 int spai_pcg_vectors(spai_pcg* s, double** x, double** r, double** p, double** z);
+/* Synchronous: the current iterate x (lagged update applied) into `out`
+ * (device, n doubles) -- for reads while the solver runs.                */
+int spai_pcg_x(spai_pcg* s, double* out);
 int spai_pcg_destroy(spai_pcg* s);
 
 /* ------------------------------------------------------------------ K10

@@ -156,6 +156,7 @@ _SIGS = {
     "spai_pcg_history": (_i32, [_vp, _vp, _i64]),
     "spai_pcg_vectors": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                                 C.POINTER(_vp)]),
+    "spai_pcg_x": (_i32, [_vp, _vp]),
     "spai_pcg_destroy": (_i32, [_vp]),
     "spai_mg_create": (_i32, [C.POINTER(_vp), _i32, _i32, _vp, _i32, _i32, _dbl]),
     "spai_mg_set_level": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),

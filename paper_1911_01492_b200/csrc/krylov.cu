@@ -17,7 +17,8 @@ enum { kRunning = 0, kConverged = 1, kMaxit = 2, kBreakdown = 3, kDivergence = 4
 struct PcgScal {
   double rho, lambda, beta, norm0, norm, tol, aux;
   long long it, maxit;
-  int status, pcur, rcur, pad;
+  int status, pcur, rcur;
+  int xlag;            // x still owes lambda p of the last V2 (applied by the next V1 / XFIX)
   unsigned int ticket1, ticket2;
 };
 
@@ -34,17 +35,52 @@ struct PcgVecs {
 };
 
 // ---- vector updates in their own kernels, one gather per stored value
-// V1: p' = z + beta p (it >= 2)          U1: q = A p', [(p',q)] (+ [(p,r),(r,r)] at it 1)
-// V2: x += lambda p, r' = r - lambda q    U2: z = M r', [(z,r'),(r',r')]
+// V1: x += lambda p, p' = z + beta p (it >= 2)
+//                                         U1: q = A p', [(p',q)] (+ [(p,r),(r,r)] at it 1)
+// V2: r' = r - lambda q                   U2: z = M r', [(z,r'),(r',r')]
+// The x update of iteration k (x += lambda_k p_k, krylov.py:328) runs in
+// V1 of iteration k + 1, which reads p_k anyway (8 B per row less than
+// updating x in V2); after the last iteration XFIX applies it (same fma,
+// same bits).  While the solver runs, x lags by that one update (xlag).
 __global__ void __launch_bounds__(kSpmvThreads)
 pcg_v1(int64_t n, PcgVecs v, const PcgScal* sc) {
   if (sc->status != kRunning || sc->it == 0) return;
-  const double beta = sc->beta;
+  const double beta = sc->beta, lambda = sc->lambda;
+  const bool lag = sc->xlag != 0;
   const double* __restrict__ pold = sc->pcur ? v.p1 : v.p0;
   double* __restrict__ pnew = sc->pcur ? v.p0 : v.p1;
   for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kSpmvThreads) {
+    const double po = pold[i];
+    if (lag) v.x[i] = fma(lambda, po, v.x[i]);
+    pnew[i] = fma(beta, po, v.z[i]);
+  }
+}
+
+// after the loop stops: the x update V1 would have made
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_xfix(int64_t n, PcgVecs v, const PcgScal* sc) {
+  if (sc->status == kRunning || !sc->xlag) return;
+  const double lambda = sc->lambda;
+  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
+  for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * kSpmvThreads)
-    pnew[i] = fma(beta, pold[i], v.z[i]);
+    v.x[i] = fma(lambda, p[i], v.x[i]);
+}
+
+__global__ void pcg_xfix_done(PcgScal* sc) {
+  if (sc->status != kRunning) sc->xlag = 0;
+}
+
+// x with the lagged update applied, into `out` (mid-run reads: callbacks)
+__global__ void __launch_bounds__(kSpmvThreads)
+pcg_xcopy(int64_t n, PcgVecs v, const PcgScal* sc, double* __restrict__ out) {
+  const bool lag = sc->xlag != 0;
+  const double lambda = sc->lambda;
+  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
+  for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kSpmvThreads)
+    out[i] = lag ? fma(lambda, p[i], v.x[i]) : v.x[i];
 }
 
 template <class OP>
@@ -52,6 +88,9 @@ __global__ void __launch_bounds__(kSpmvThreads, OP::kMinBlocks)
 pcg_u1(int64_t n, int64_t nslices, OP A, PcgVecs v, PcgScal* sc) {
   if (sc->status != kRunning) return;
   const bool first = sc->it == 0;
+  // V1 has applied the lagged x update (every V1 block read xlag before this
+  // kernel started); V2 sets it again
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->xlag = 0;
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSpmvThreads) >> 5;
@@ -104,17 +143,15 @@ pcg_u1(int64_t n, int64_t nslices, OP A, PcgVecs v, PcgScal* sc) {
 }
 
 __global__ void __launch_bounds__(kSpmvThreads)
-pcg_v2(int64_t n, PcgVecs v, const PcgScal* sc) {
+pcg_v2(int64_t n, PcgVecs v, PcgScal* sc) {
   if (sc->status != kRunning) return;
   const double lambda = sc->lambda;
-  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
   const double* __restrict__ rold = sc->rcur ? v.r1 : v.r0;
   double* __restrict__ rnew = sc->rcur ? v.r0 : v.r1;
   for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * kSpmvThreads) {
+       i += (int64_t)gridDim.x * kSpmvThreads)
     rnew[i] = fma(-lambda, v.q[i], rold[i]);
-    v.x[i] = fma(lambda, p[i], v.x[i]);
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->xlag = 1;   // read by the next V1 / XFIX
 }
 
 template <bool HAS_M, class OP>
@@ -156,15 +193,13 @@ pcg_u2(int64_t n, int64_t nslices, OP M, PcgVecs v, PcgScal* sc) {
 // double buffering), z = V(r) is written by the V-cycle kernels between V2ext
 // and Zext, p alternates as usual.
 __global__ void __launch_bounds__(kSpmvThreads)
-pcg_v2_ext(int64_t n, PcgVecs v, const PcgScal* sc) {
+pcg_v2_ext(int64_t n, PcgVecs v, PcgScal* sc) {
   if (sc->status != kRunning) return;
   const double lambda = sc->lambda;
-  const double* __restrict__ p = sc->pcur ? v.p1 : v.p0;
   for (int64_t i = blockIdx.x * (int64_t)kSpmvThreads + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * kSpmvThreads) {
+       i += (int64_t)gridDim.x * kSpmvThreads)
     v.r0[i] = fma(-lambda, v.q[i], v.r0[i]);
-    v.x[i] = fma(lambda, p[i], v.x[i]);
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->xlag = 1;
 }
 
 // [(z,r),(r,r)] -> beta, norm, status (pcg_u2's finalize without the r swap)
@@ -483,6 +518,10 @@ extern "C" int spai_pcg_advance(spai_pcg* s, int64_t iters) {
     int st = launch_iteration(s);
     if (st) return st;
   }
+  // a stopped solver gets x's lagged update (no-ops while running)
+  pcg_xfix<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc);
+  pcg_xfix_done<<<1, 1, 0, s->stream>>>(s->sc);
+  SPAI_LAUNCH_CHECK("pcg_xfix");
   return SPAI_OK;
 }
 
@@ -516,6 +555,14 @@ extern "C" int spai_pcg_vectors(spai_pcg* s, double** x, double** r, double** p,
   if (r) *r = h.rcur ? s->v.r1 : s->v.r0;
   if (p) *p = h.pcur ? s->v.p1 : s->v.p0;
   if (z) *z = s->v.z;
+  return SPAI_OK;
+}
+
+extern "C" int spai_pcg_x(spai_pcg* s, double* out) {
+  if (!s || !out) { set_error("spai_pcg_x: bad arguments"); return SPAI_E_ARG; }
+  pcg_xcopy<<<s->vblocks, kSpmvThreads, 0, s->stream>>>(s->n, s->v, s->sc, out);
+  SPAI_LAUNCH_CHECK("pcg_xcopy");
+  SPAI_CUDA(cudaStreamSynchronize(s->stream));
   return SPAI_OK;
 }
 

@@ -228,6 +228,7 @@ class DevicePCG:
         self.n = A.nrows
         self.maxit = int(maxit)
         self.launched = 0
+        self.advance_calls = 0
         share_pattern(A, M)
         # symmetric operators on one pattern: half-storage SELL (K5c)
         g = A.ssell_offsets() if symmetric is not False else None
@@ -272,6 +273,7 @@ class DevicePCG:
         _lib.check(st, "spai_pcg_create")
         self.h = h
         self.launched = 0
+        self.advance_calls = 0
         self._attach_mg(mg)
 
     def _attach_mg(self, mg):
@@ -288,6 +290,7 @@ class DevicePCG:
 
     def advance(self, iters: int):
         self.launched += int(iters)
+        self.advance_calls += 1          # + the x fix-up pair (krylov.cu pcg_xfix)
         _lib.check(self.lib.spai_pcg_advance(self.h, int(iters)), "spai_pcg_advance")
 
     def poll(self):
@@ -311,6 +314,13 @@ class DevicePCG:
         _lib.check(self.lib.spai_pcg_vectors(self.h, *[C.byref(p) for p in ps]),
                    "spai_pcg_vectors")
         return [_wrap_device(p.value, self.n) for p in ps]
+
+    def x_current(self):
+        """The iterate x now (the device x lags by one update while running)."""
+        torch = _torch()
+        out = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        _lib.check(self.lib.spai_pcg_x(self.h, ptr(out)), "spai_pcg_x")
+        return out
 
     def run(self, chunk: int = 64):
         """Advance until the device status leaves 'running'; returns poll()."""
@@ -370,6 +380,7 @@ class DeviceCGV:
         self.n = A.nrows
         self.maxit = int(maxit)
         self.launched = 0
+        self.advance_calls = 0
         share_pattern(A, M)
         z = C.c_void_p(0)
         g = A.ssell_offsets() if symmetric is not False else None
@@ -583,7 +594,8 @@ def solve(system, b, cfg: SolverConfig, x0=None, callback=None):
                     rec.residual_norms = [float(v) for v in hist]
                     rec.reductions_cum = [2 * (i + 1) for i in range(it)]
                     rec.overlapped_cum = [0] * it
-                    xs, rs, ps, zs = solver.vectors()
+                    _, rs, ps, zs = solver.vectors()
+                    xs = solver.x_current()
                     st = KrylovState("classic", x=xs.cpu().numpy(), r=rs.cpu().numpy(),
                                      p=ps.cpu().numpy(), q=zs.cpu().numpy())
                     it_seen = it
@@ -620,6 +632,7 @@ def _finish(solver, rec, cfg, status, it, norm0, norm, aux, on_device):
     rec.total_reductions = 2 * noted + (1 if early else 0)
     rec.total_overlapped = 0
     rec.launched_iterations = solver.launched
+    rec.advance_calls = getattr(solver, "advance_calls", 0)
     rec.operator_format = "ssell" if getattr(solver, "symmetric", False) else "sell"
     x = solver.vectors()[0].clone()
     return (x if on_device else x.cpu().numpy()), rec

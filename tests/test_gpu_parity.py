@@ -505,6 +505,30 @@ def test_callback_sees_every_iteration():
     assert [s[0] for s in seen] == list(range(1, rec.iterations + 1))
 
 
+def test_callback_x_is_the_iterate_and_final_x_complete():
+    """The device applies x += lambda p one kernel late (krylov.cu V1 / XFIX):
+    the x a callback sees after iteration k equals the x a solve stopped at
+    maxit = k returns, bit for bit, and both equal the oracle's iterate."""
+    A = pb.q1_device((20, 18, 16))
+    S = pb.spai1_symmetric_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    xs = {}
+    pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+             pb.SolverConfig(tol=1e-300, maxit=12),
+             callback=lambda it, st, r: xs.__setitem__(it, st.x.copy()))
+    assert sorted(xs) == list(range(1, 13))
+    Ah, Sh = A.to_host(), S.to_host()
+    oA = oracle.Csr(Ah.nrows, Ah.ncols, Ah.row_offsets, Ah.col_indices, Ah.values)
+    oS = oracle.Csr(Sh.nrows, Sh.ncols, Sh.row_offsets, Sh.col_indices, Sh.values)
+    for k in (1, 2, 7, 12):
+        x, rec = pb.solve(pb.LocalSystem(A, pb.SparseMatrixPreconditioner(S)), b,
+                          pb.SolverConfig(tol=1e-300, maxit=k))
+        assert rec.iterations == k
+        assert np.array_equal(x.cpu().numpy(), xs[k]), k
+        xr, _ = oracle.pcg_classic(oA, oS, b.cpu().numpy(), tol=1e-300, maxit=k)
+        assert np.max(np.abs(xs[k] - xr)) <= 1e-12 * np.max(np.abs(xr)), k
+
+
 def test_large_3d_spai_cg_properties():
     """Size-independent properties at a size the oracle cannot check per column."""
     A = pb.q1_device((96, 96, 96))
