@@ -60,7 +60,7 @@ def parse():
     return ap.parse_args()
 
 
-PROFILE_FULL = {"sell": "r01_ncu_full_400_final.json", "ssell": "r02_ncu_full_pcg_400.json"}
+PROFILE_FULL = {"sell": "r01_ncu_full_400_final.json", "ssell": "r02_ncu_full_pcg_400_xlag.json"}
 
 
 def profiled_traffic(fmt):
@@ -409,19 +409,19 @@ def run_ours(args):
     # Householder QR would need 2 n^2 (m - n/3) + n^2 = 169,857
     fp64 = fp64_peak_tflops(stream)
     exec_tf = n * 8721 / t_asm / 1e12
-    asm_roof = {"bound": "fp64 on paper; issue / dependency latency in practice",
+    asm_roof = {"bound": "fp64 on paper; the LSU data pipe in practice",
                 "unit": "TFLOP/s",
                 "achieved_executed": exec_tf, "peak_measured_dfma": fp64,
                 "frac": exec_tf / fp64,
                 "householder_equivalent": n * 169857 / t_asm / 1e12,
                 "flop_per_column": {"executed_b_path": 8721,
                                     "householder_qr_reference": 169857},
-                # ncu (profiles/r02_ncu_bpath_400.txt): per chunk of 8.4 M
-                # columns B rows 17 ms + solves 28 ms; solves ~1,700
-                # warp-instructions per column at ~1.7 IPC / SM (16 warps,
-                # 128 registers), stalls mostly fixed-latency FP64 / shuffle
-                # chains of the factorisation
-                "warp_instructions_per_column_ncu": {"b_rows": 1055, "solve": 1710}}
+                # ncu (profiles/r02_ncu_full_bpath2_400.json): per chunk of
+                # 8.4 M columns B rows 17.7 ms + solves 20.1 ms (two columns
+                # per warp); both LSU-bound (data-pipe wavefronts 82 % / 79 %
+                # of peak), FP64 pipe 3 % / 30 %
+                "bound_in_practice": "LSU data pipe (shared + L1 wavefronts)",
+                "warp_instructions_per_column_ncu": {"b_rows": 1055, "solve": 1131}}
     solve_gbs = b_it * its / t_sol / 1e9
 
     # ---- SpMV alone (K5 formats) with CUDA events
