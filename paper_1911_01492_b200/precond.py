@@ -239,7 +239,7 @@ def _symmetrize_union(A: DeviceCsr, m_csc) -> DeviceCsr:
     return S
 
 
-def spai1_symmetric_from_host(rowptr, colidx, vals, nchunks: int = 8,
+def spai1_symmetric_from_host(rowptr, colidx, vals, nchunks: int = 16,
                               stats: SpaiStats | None = None):
     """Upload a host CSR matrix and build 0.5*(M + M^T) with the value upload
     overlapped with the assembly; returns (A on the device, S).
