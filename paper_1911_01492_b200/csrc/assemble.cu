@@ -1528,7 +1528,10 @@ static bool build_plans(int64_t c0, int64_t c1, const int64_t* cscptr, const int
 // window of B rows [c0 + min jrel, c1 - 1 + max jrel] in a stream-ordered
 // temporary (K_B), then the per-column solves (K_G).
 constexpr int64_t kBChunk = (int64_t)1 << 23;
-constexpr int kBRowWarps = 8, kBSolveWarps = 8, kBSolve2Warps = 4, kBPlanWarps = 8;
+#ifndef SPAI_BPLAN_WARPS
+#define SPAI_BPLAN_WARPS 8
+#endif
+constexpr int kBRowWarps = 8, kBSolveWarps = 8, kBSolve2Warps = 4, kBPlanWarps = SPAI_BPLAN_WARPS;
 
 template <int NJ, int CAPL>
 static int bpath_columns(int64_t n, int64_t c0, int64_t c1, const double* vals,
