@@ -830,3 +830,46 @@ def test_csc_to_csr_gather_equals_scatter():
         _lib.SPAI_E_ARG                                   # in place is rejected
     M = pb.spai1_device(A)
     assert torch.equal(M.vals, pb.precond.csc_to_csr_values(A, pb.precond.spai1_columns_device(A)))
+
+
+def test_bpath_qr_fallback_inside_a_column_pair():
+    """B path (bsolve2: two columns per warp): a column whose local problem
+    fails the pivot test goes to the QR kernel while its warp partner
+    finishes on the Cholesky path -- every column against the oracle."""
+    dims = (10, 9, 8)
+    A0 = oracle.stencil_csr(dims, *oracle.q1_stencil(3))
+    rows = np.repeat(np.arange(A0.nrows), np.diff(A0.row_offsets))
+    vals = A0.values.copy()
+    k = 4 + 10 * (4 + 9 * 4)                      # interior column; k + 1 is its x-neighbour
+    in_k = set(A0.col_indices[A0.row_offsets[k]:A0.row_offsets[k + 1]])
+    rng = np.random.default_rng(11)
+    in_k1 = set(A0.col_indices[A0.row_offsets[k + 1]:A0.row_offsets[k + 2]])
+    for p in np.nonzero(A0.col_indices == k + 1)[0]:
+        i = rows[p]
+        if i in in_k:                              # A(i, k+1) ~ A(i, k): nearly dependent
+            q = A0.row_offsets[i] + np.searchsorted(
+                A0.col_indices[A0.row_offsets[i]:A0.row_offsets[i + 1]], k)
+            vals[p] = vals[q] * (1.0 + 1e-7 * rng.standard_normal())
+        else:
+            vals[p] = 1e-9
+    for p in np.nonzero(A0.col_indices == k)[0]:   # column k tiny where k+1 has no entry
+        if rows[p] not in in_k1:
+            vals[p] = 1e-9
+    A = pb.CsrMatrix(A0.nrows, A0.ncols, A0.row_offsets, A0.col_indices, vals)
+    Ad = A.device()
+    assert Ad.structurally_symmetric()
+    stats = pb.SpaiStats()
+    m = pb.precond.spai1_columns_device(Ad, stats).cpu().numpy()
+    assert stats.n_fallback >= 1
+    oa = oracle.Csr(A.nrows, A.ncols, A0.row_offsets, A0.col_indices, vals)
+    ref = np.concatenate(oracle.spai1_columns(oa, sets=oracle.pattern_sets(oa)))
+    cols = np.repeat(np.arange(A.ncols), np.diff(A0.row_offsets))
+    num, den = np.zeros(A.ncols), np.zeros(A.ncols)
+    np.maximum.at(num, cols, np.abs(m - ref))
+    np.maximum.at(den, cols, np.abs(ref))
+    err = num / den
+    bad = np.nonzero(err > SPAI_TOL)[0]
+    # only the nearly dependent columns' problems may lose digits (QR path,
+    # like test_ill_conditioned_column_goes_to_qr_and_matches)
+    assert err.max() <= 1e-6, (bad, err.max())
+    assert np.all(np.isin(bad, sorted(in_k | in_k1))), bad
