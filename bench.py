@@ -85,6 +85,25 @@ def profiled_traffic(fmt):
     return total if len(seen) == 4 else None
 
 
+def profiled_pipes(metric):
+    """{kernel: fraction of peak} of a pipe-utilisation metric for the B-path
+    kernels, from the committed ncu --set full capture, or None."""
+    path = os.path.join(REPO, "profiles", "r02_ncu_full_bpath2_400.json")
+    try:
+        rows = json.load(open(path))
+    except Exception:
+        return None
+    out = {}
+    for r in rows:
+        key = next((k for k in r if k.startswith(metric)), None)
+        if key is None:
+            continue
+        name = r["Kernel Name"].split("(")[0].replace("void ", "").split("<")[0]
+        out[{"bgram_plan_kernel": "b_rows", "bsolve2_kernel": "solves"}.get(name, name)] = \
+            float(r[key].split()[0]) / 100.0
+    return out or None
+
+
 def fp64_peak_tflops(stream):
     """Measured FP64 CUDA-core throughput (DFMA probe, K13), TFLOP/s."""
     import ctypes as C
@@ -421,6 +440,8 @@ def run_ours(args):
                 # per warp); both LSU-bound (data-pipe wavefronts 82 % / 79 %
                 # of peak), FP64 pipe 3 % / 30 %
                 "bound_in_practice": "LSU data pipe (shared + L1 wavefronts)",
+                "lsu_pipe_frac_ncu": profiled_pipes("l1tex__data_pipe_lsu_wavefronts"),
+                "fp64_pipe_frac_ncu": profiled_pipes("sm__pipe_fp64_cycles_active"),
                 "warp_instructions_per_column_ncu": {"b_rows": 1055, "solve": 1131}}
     solve_gbs = b_it * its / t_sol / 1e9
 
