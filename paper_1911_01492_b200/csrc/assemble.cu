@@ -582,7 +582,6 @@ class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __res
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   // the warp's last class (its exact pattern in registers): most columns
   // repeat it, and then need no table probe and no representative compare
-  uint64_t last_h = 0;
   int last_slot = -1, last_len = -1;
   int32_t last_rel = 0;
   for (int64_t c = w0; c < n; c += nw) {
@@ -630,9 +629,8 @@ class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __res
       slot = (slot + 1) & (kClassTable - 1);
     }
     if (lane == 0) pw.col_class[c] = result;
-    if (result >= 0) { last_h = h; last_slot = result; last_len = len; last_rel = rel; }
+    if (result >= 0) { last_slot = result; last_len = len; last_rel = rel; }
   }
-  (void)last_h;
 }
 
 // (A) signature of every column: (nj, J_a - k, class(J_a)) -> plan-table slot
