@@ -318,29 +318,6 @@ __device__ __forceinline__ void brow_accumulate(int64_t c, const int64_t* __rest
 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
-bgram_rows_kernel(Traversal tv, int64_t w0, const int64_t* __restrict__ rowptr,
-                  const int32_t* __restrict__ colidx, const double* __restrict__ vals,
-                  const double* __restrict__ cscval, const int64_t* __restrict__ csc2csr,
-                  const uint8_t* __restrict__ dslot, int dmax, double* __restrict__ Bw) {
-  __shared__ double acc_all[WARPS][kBW];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* acc = acc_all[w];
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
-  const int64_t nt = tv.count();
-  for (int64_t base = blockIdx.x * (int64_t)WARPS; base < nt; base += nw) {
-    const int64_t t = base + w;
-    const int64_t c = t < nt ? tv.at(t) : -1;
-    if (__any_sync(0xffffffffu, c < 0)) continue;
-    brow_accumulate(c, rowptr, colidx, vals, cscval, csc2csr, dslot, dmax, acc, lane);
-    double* out = Bw + (c - w0) * kBW;
-    out[lane] = acc[lane];
-    out[lane + 32] = acc[lane + 32];
-    __syncwarp();
-  }
-}
-
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
 bgram_list_kernel(int64_t w0, const int32_t* __restrict__ list, const int* __restrict__ nlist,
                   const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
                   const double* __restrict__ vals, const double* __restrict__ cscval,
@@ -368,7 +345,7 @@ bgram_list_kernel(int64_t w0, const int32_t* __restrict__ list, const int* __res
 // the next row while this row's B program runs (as the replay pipelines its
 // gather), then 64 slot values out.  Rows without a usable plan / B program
 // go to bw.brow_list for bgram_list_kernel.  Same per-slot summation order
-// as bgram_rows_kernel (rows of column c ascending, one fma chain).
+// as bgram_list_kernel (rows of column c ascending, one fma chain).
 template <int CAPL, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 bgram_plan_kernel(Traversal tv, int64_t w0, int64_t sig0, int64_t sig1,
