@@ -314,3 +314,38 @@ def test_c4_multigrid_4096sq_matches_sparse_oracle():
     print(f"C4 4096^2: V-cycle ok, MG-PCG history rel {rel:.2e}")
     assert rel <= HIST_TOL, rel
     assert np.max(np.abs(x.cpu().numpy() - xr)) <= 1e-9 * np.max(np.abs(xr))
+
+
+def test_c5_bicgstab_200cubed_first_30_iterations_match_device_order_oracle():
+    """configs[4] at one GPU's share of the 8-GPU run: 3D Q1 convection-
+    diffusion 200^3 (8 M DOF, b = (1, 0.5, 0.25)), raw SPAI(1) through the B
+    path (sampled columns, every plan class, vs the reference QR solve) and
+    the first 30 K9 BiCGStab iterations vs the device-order oracle on the
+    downloaded A and M (SELL-32 for both): histories <= 1e-8, x <= 1e-10."""
+    from oracle import devorder
+    from paper_1911_01492_b200.krylov import DeviceKrylov
+    N = 200
+    A = pb.q1_device((N, N, N), conv=(1.0, 0.5, 0.25))
+    m_csc = pb.precond.spai1_columns_device(A)
+    n = A.nrows
+    rng = np.random.default_rng(200)
+    cols = np.concatenate([rng.integers(0, n, 4000), _plan_class_columns((N, N, N)),
+                           np.arange(32), np.arange(n - 32, n)])
+    worst = _check_columns(A, m_csc, cols)            # structurally symmetric: rows = columns
+    M = pb.spai1_device(A)
+    b = A.matvec(torch.ones(n, dtype=torch.float64, device="cuda"))
+    its = 30
+    s = DeviceKrylov(1, A, M, 1e-300, its, symmetric=False)
+    assert s.operator_format == "sell"
+    st = s.run(b)
+    h = s.history(st[1])
+    x = s.x().cpu().numpy()
+    grid = s.grid()
+    s.close()
+    xo, ho, sto, n0, _ = devorder.bicgstab_devorder(_host(A), _host(M), b.cpu().numpy(), 1e-300,
+                                                    its, grid)
+    assert len(h) == len(ho) == its and st[0] == sto and st[2] == n0
+    rel = np.max(np.abs(h - ho) / ho)
+    print(f"C5 200^3: SPAI worst {worst:.2e}, history rel {rel:.2e}")
+    assert rel <= HIST_TOL, rel
+    assert np.max(np.abs(x - xo)) <= 1e-10 * np.max(np.abs(xo))
