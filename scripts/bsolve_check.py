@@ -1,7 +1,9 @@
-"""Compare the B-path solve kernels (SPAI_BSOLVE=1 one column per warp, =2
-two columns per warp) on one matrix: run as two processes, diff the m_csc.
+"""Compare two settings of an assembly environment knob on one matrix (by
+default the B-path solve kernels, SPAI_BSOLVE=1 one column per warp vs =2
+two columns per warp): run as two processes, diff the m_csc.
 
-  python scripts/bsolve_check.py DIMS...   (e.g. 30 26 22)
+  python scripts/bsolve_check.py DIMS...              (e.g. 30 26 22)
+  AB_ENV=SPAI_BPIPE AB_VALUES=0,1 python scripts/bsolve_check.py 400 400 400
 """
 import os
 import subprocess
@@ -26,7 +28,8 @@ def run(dims, out):
     m = pb.precond.spai1_columns_device(A, st)
     torch.cuda.synchronize()
     np.save(out, m.cpu().numpy())
-    print(f"BSOLVE={os.environ.get('SPAI_BSOLVE')} n={A.nrows} fallback={st.n_fallback} "
+    knob = os.environ.get("AB_ENV", "SPAI_BSOLVE")
+    print(f"{knob}={os.environ.get(knob)} n={A.nrows} fallback={st.n_fallback} "
           f"merge={st.n_merge} t={time.time() - t:.3f}s nan={int(torch.isnan(m).sum())}")
 
 
@@ -36,9 +39,10 @@ if __name__ == "__main__":
         sys.exit(0)
     dims = sys.argv[1:]
     outs = []
-    for v in ("1", "2"):
+    knob = os.environ.get("AB_ENV", "SPAI_BSOLVE")
+    for v in os.environ.get("AB_VALUES", "1,2").split(","):
         out = f"/tmp/bsolve_{v}.npy"
-        env = dict(os.environ, SPAI_BSOLVE=v)
+        env = dict(os.environ, **{knob: v})
         subprocess.run([sys.executable, __file__, "--child", out, *dims], env=env, check=True,
                        timeout=600)
         outs.append(np.load(out))
