@@ -41,7 +41,7 @@ if __name__ == "__main__":
     outs = []
     knob = os.environ.get("AB_ENV", "SPAI_BSOLVE")
     for v in os.environ.get("AB_VALUES", "1,2").split(","):
-        out = f"/tmp/bsolve_{v}.npy"
+        out = f"/tmp/bsolve_{abs(hash(v))}.npy"
         env = dict(os.environ, **{knob: v})
         subprocess.run([sys.executable, __file__, "--child", out, *dims], env=env, check=True,
                        timeout=600)
