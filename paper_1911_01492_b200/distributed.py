@@ -32,7 +32,6 @@ gloo.
 from __future__ import annotations
 
 import ctypes as C
-import math
 from dataclasses import dataclass
 
 import numpy as np

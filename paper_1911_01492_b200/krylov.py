@@ -11,7 +11,6 @@ iteration count and the termination rule are the reference's.
 from __future__ import annotations
 
 import ctypes as C
-import math
 from dataclasses import dataclass, field
 
 import numpy as np

@@ -2,13 +2,11 @@
 plan replay (K3), and their agreement.  Usage: python scripts/asm_paths.py [N]"""
 import json
 import sys
-import time
 
 import torch
 
 sys.path.insert(0, ".")
 import paper_1911_01492_b200 as pb  # noqa: E402
-from paper_1911_01492_b200.sparse import DeviceCsr  # noqa: E402
 
 
 def timed(fn, reps=3):

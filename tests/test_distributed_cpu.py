@@ -209,7 +209,6 @@ def _ghost_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_1911_01492_b200 as pb
-        from paper_1911_01492_b200.grids import Partition  # noqa: F401
         import oracle
         Ao = oracle.stencil_csr((12, 15), *oracle.q1_stencil(2))
         A = pb.CsrMatrix(Ao.nrows, Ao.ncols, Ao.row_offsets, Ao.col_indices, Ao.values)
