@@ -590,7 +590,30 @@ def cpu_baseline(args, dev, stream, n_work, its_work):
                      "DOF*it/s at the large size); not measured end to end"}
     except Exception as e:          # pragma: no cover - keep the bench line
         res["phases"]["solve_large_error"] = str(e)[:200]
+    # the reference spai1 alone at the largest sizes its
+    # O(n^2) densify allows (3D Q1 32^3: an 8.6 GB dense copy; 2D Q1 128^2)
+    try:
+        res["phases"]["spai1_large"] = time_reference_spai1([(32, 32, 32), (128, 128)])
+    except Exception as e:          # pragma: no cover - keep the bench line
+        res["phases"]["spai1_large_error"] = str(e)[:200]
     return res
+
+
+def time_reference_spai1(shapes):
+    """Unmodified `ftkrylov.spai1` (precond.py:175-199), one run per shape,
+    cols/s on one host core (OpenBLAS 1 thread)."""
+    import oracle
+    fk, _ = load_reference()
+    out = {}
+    with _blas_threads(1):
+        for dims in shapes:
+            c = oracle.stencil_csr(dims, *oracle.q1_stencil(len(dims)))
+            A = fk.CsrMatrix(c.nrows, c.ncols, c.row_offsets, c.col_indices, c.values)
+            t0 = time.perf_counter()
+            fk.spai1(A)
+            t = time.perf_counter() - t0
+            out["x".join(map(str, dims))] = {"cols_per_s": c.nrows / t, "s": t}
+    return out
 
 
 def run_distributed(args, world, rank, local):
