@@ -148,6 +148,27 @@ __global__ void sym_check_kernel(int64_t n, int64_t nnz, const int64_t* rowptr,
 // CSC slot q (an entry (c, i) of row c) maps to the CSR position of (i, c):
 // csc2csr[q] = rowptr[i] + lower_bound(row i, c).  Gather form: coalesced
 // writes, one short binary search per entry, no atomics, no sort.
+#ifndef SPAI_SYMT_ROWS
+#define SPAI_SYMT_ROWS 4
+#endif
+constexpr int kSymTransposeRows = SPAI_SYMT_ROWS;
+
+// one lane per entry of R rows per warp, the R dependent-load chains
+// (row extent -> column -> that row's extent -> probe) interleaved
+__device__ __forceinline__ bool sym_transpose_search(const int64_t* __restrict__ rowptr,
+                                                     const int32_t* __restrict__ colidx,
+                                                     int64_t c, int64_t a, int64_t b,
+                                                     int64_t* out) {
+  const int64_t end = b;
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if (colidx[mid] < (int32_t)c) a = mid + 1; else b = mid;
+  }
+  if (a < end && colidx[a] == (int32_t)c) { *out = a; return true; }
+  return false;
+}
+
+template <int R>
 __global__ void sym_transpose_kernel(int64_t n, const int64_t* __restrict__ rowptr,
                                      const int32_t* __restrict__ colidx,
                                      int64_t* __restrict__ csc2csr, int* bad) {
@@ -155,26 +176,42 @@ __global__ void sym_transpose_kernel(int64_t n, const int64_t* __restrict__ rowp
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int miss = 0;
-  for (int64_t c = w0; c < n; c += nw) {
-    const int64_t lo = rowptr[c], hi = rowptr[c + 1];
-    for (int64_t q = lo + lane; q < hi; q += 32) {
-      const int32_t i = colidx[q];
-      int64_t a = rowptr[i], b = rowptr[i + 1];
-      const int64_t end = b;
+  for (int64_t c0 = w0 * R; c0 < n; c0 += nw * R) {
+    int64_t lo[R], hi[R], q[R], a[R], b[R], g[R];
+    int32_t ci[R], gc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t c = c0 + r < n ? c0 + r : n - 1;
+      lo[r] = rowptr[c];
+      hi[r] = c0 + r < n ? rowptr[c + 1] : lo[r];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      q[r] = lo[r] + lane;
+      ci[r] = q[r] < hi[r] ? colidx[q[r]] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      a[r] = q[r] < hi[r] ? rowptr[ci[r]] : 0;
+      b[r] = q[r] < hi[r] ? rowptr[ci[r] + 1] : 0;
       // first probe at the mirrored index (exact for point-symmetric row
-      // patterns, i.e. every interior stencil row): one dependent load
-      // instead of a 5-step search
-      const int64_t guess = a + (b - a - 1) - (q - lo);
-      if (guess >= a && guess < b && colidx[guess] == (int32_t)c) {
-        csc2csr[q] = guess;
-        continue;
+      // patterns, i.e. every interior stencil row)
+      g[r] = a[r] + (b[r] - a[r] - 1) - lane;
+      gc[r] = (q[r] < hi[r] && g[r] >= a[r] && g[r] < b[r]) ? colidx[g[r]] : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t c = c0 + r;
+      if (q[r] < hi[r]) {
+        if (gc[r] == (int32_t)c) csc2csr[q[r]] = g[r];
+        else if (!sym_transpose_search(rowptr, colidx, c, a[r], b[r], csc2csr + q[r])) miss = 1;
       }
-      while (a < b) {
-        const int64_t mid = (a + b) >> 1;
-        if (colidx[mid] < (int32_t)c) a = mid + 1; else b = mid;
+      // rows longer than a warp: the rest serially
+      for (int64_t qq = lo[r] + 32 + lane; qq < hi[r]; qq += 32) {
+        const int32_t i = colidx[qq];
+        if (!sym_transpose_search(rowptr, colidx, c, rowptr[i], rowptr[i + 1], csc2csr + qq))
+          miss = 1;
       }
-      if (a < end && colidx[a] == (int32_t)c) csc2csr[q] = a;
-      else miss = 1;
     }
   }
   if (__any_sync(0xffffffffu, miss) && lane == 0) atomicOr(bad, 1);
@@ -332,7 +369,8 @@ extern "C" int spai_csr_transpose_symmetric(int64_t n, int64_t nnz, const int64_
   if (!d) { set_error("scratch allocation failed"); return SPAI_E_CUDA; }
   SPAI_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
   if (n > 0) {
-    sym_transpose_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, rowptr, colidx, csc2csr, d);
+    sym_transpose_kernel<kSymTransposeRows><<<grid_for((n + kSymTransposeRows - 1) / kSymTransposeRows * 32, 256), 256, 0, s>>>(
+        n, rowptr, colidx, csc2csr, d);
     SPAI_LAUNCH_CHECK("sym_transpose_kernel");
   }
   int h = 0;
