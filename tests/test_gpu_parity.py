@@ -873,3 +873,38 @@ def test_bpath_qr_fallback_inside_a_column_pair():
     # like test_ill_conditioned_column_goes_to_qr_and_matches)
     assert err.max() <= 1e-6, (bad, err.max())
     assert np.all(np.isin(bad, sorted(in_k | in_k1))), bad
+
+
+def test_bpath_rank_deficient_column_raises_the_reference_error():
+    """A 3D Q1 matrix (B path) whose columns k and k+1 are identical on
+    their common rows and zero elsewhere: the local problems that contain
+    both are rank-deficient.  The device raises the reference's
+    FactorBreakdownError for the same (first) column as the oracle's
+    restatement of precond.py:192-194."""
+    dims = (10, 9, 8)
+    A0 = oracle.stencil_csr(dims, *oracle.q1_stencil(3))
+    rows = np.repeat(np.arange(A0.nrows), np.diff(A0.row_offsets))
+    vals = A0.values.copy()
+    k = 4 + 10 * (4 + 9 * 4)
+    in_k = set(A0.col_indices[A0.row_offsets[k]:A0.row_offsets[k + 1]])
+    in_k1 = set(A0.col_indices[A0.row_offsets[k + 1]:A0.row_offsets[k + 2]])
+    for p in np.nonzero(A0.col_indices == k + 1)[0]:
+        i = rows[p]
+        if i in in_k:
+            q = A0.row_offsets[i] + np.searchsorted(
+                A0.col_indices[A0.row_offsets[i]:A0.row_offsets[i + 1]], k)
+            vals[p] = vals[q]
+        else:
+            vals[p] = 0.0
+    for p in np.nonzero(A0.col_indices == k)[0]:
+        if rows[p] not in in_k1:
+            vals[p] = 0.0
+    oa = oracle.Csr(A0.nrows, A0.ncols, A0.row_offsets, A0.col_indices, vals)
+    from oracle.spai import RankDeficient
+    with pytest.raises(RankDeficient) as ref:
+        oracle.spai1(oa)
+    A = pb.CsrMatrix(A0.nrows, A0.ncols, A0.row_offsets, A0.col_indices, vals)
+    assert A.device().structurally_symmetric()
+    with pytest.raises(pb.FactorBreakdownError) as got:
+        pb.spai1(A)
+    assert str(got.value) == str(ref.value)
