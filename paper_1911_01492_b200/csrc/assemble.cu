@@ -643,29 +643,23 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
   uint64_t last_h = 0;                         // the warp's last signature and its slot
   int last_slot = -1;
   int last_nj = -1, last_rel = 0, last_cls = 0;   // ... and its (J - k, class) lanes
-  for (int64_t k = c0 + w0; k < n; k += nw) {
-    const int64_t jlo = cscptr[k];
-    const int nj = (int)(cscptr[k + 1] - jlo);
-    if (nj == 0 || nj > kPlanNJ) { if (lane == 0) pw.plan_slot[k] = -1; continue; }
-    int c = 0, cls = 0, len = 0;
-    if (lane < nj) {
-      c = cscrow[jlo + lane];
-      cls = pw.col_class[c];
-    }
+  // one column's signature from its loaded (J, class) lanes
+  auto process = [&](int64_t k, int nj, int c, int cls) {
+    if (nj == 0 || nj > kPlanNJ) { if (lane == 0) pw.plan_slot[k] = -1; return; }
     // most columns repeat the warp's last signature exactly: no lengths,
     // hash or table probe
     if (nj == last_nj && last_slot >= 0 &&
         __all_sync(0xffffffffu, lane >= nj || (c - (int32_t)k == last_rel && cls == last_cls))) {
       if (lane == 0) pw.plan_slot[k] = last_slot;
-      continue;
+      return;
     }
-    if (lane < nj) len = (int)(cscptr[c + 1] - cscptr[c]);
+    const int len = lane < nj ? (int)(cscptr[c + 1] - cscptr[c]) : 0;
     int total = len;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
     if (__any_sync(0xffffffffu, lane < nj && cls < 0) || total > kPadIdx) {
       if (lane == 0) pw.plan_slot[k] = -1;
-      continue;
+      return;
     }
     uint64_t h = lane < nj ? mix64(((uint64_t)(lane + 1) << 48) ^ ((uint64_t)(uint32_t)cls << 32) ^
                                    (uint32_t)(c - (int32_t)k))
@@ -676,7 +670,7 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
     if (h == 0) h = 1;
     if (h == last_h) {                         // the warp's last signature: same slot
       if (lane == 0) pw.plan_slot[k] = last_slot;
-      continue;
+      return;
     }
     if (lane == 0) {
       int slot = (int)(h & (kPlanTable - 1));
@@ -696,6 +690,26 @@ plan_sig_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __
     last_nj = nj;
     last_rel = c - (int32_t)k;
     last_cls = cls;
+  };
+  // two consecutive columns per pass: their dependent load chains (extent ->
+  // J -> classes) are in flight together
+  for (int64_t k0 = c0 + 2 * w0; k0 < n; k0 += 2 * nw) {
+    int64_t jlo[2];
+    int nj[2], c[2] = {0, 0}, cls[2] = {0, 0};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const bool ok = k0 + r < n;
+      jlo[r] = ok ? cscptr[k0 + r] : 0;
+      nj[r] = ok ? (int)(cscptr[k0 + r + 1] - jlo[r]) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (lane < nj[r] && nj[r] <= kPlanNJ) c[r] = cscrow[jlo[r] + lane];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (lane < nj[r] && nj[r] <= kPlanNJ) cls[r] = pw.col_class[c[r]];
+    process(k0, nj[0], c[0], cls[0]);
+    if (k0 + 1 < n) process(k0 + 1, nj[1], c[1], cls[1]);
   }
 }
 
