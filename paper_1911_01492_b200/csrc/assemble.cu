@@ -584,14 +584,11 @@ class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __res
   // repeat it, and then need no table probe and no representative compare
   int last_slot = -1, last_len = -1;
   int32_t last_rel = 0;
-  for (int64_t c = w0; c < n; c += nw) {
-    const int64_t lo = cscptr[c];
-    const int len = (int)(cscptr[c + 1] - lo);
-    if (len > 32 || len == 0) { if (lane == 0) pw.col_class[c] = -1; continue; }
-    const int32_t rel = lane < len ? cscrow[lo + lane] - (int32_t)c : 0;
+  auto process = [&](int64_t c, int len, int32_t rel) {
+    if (len > 32 || len == 0) { if (lane == 0) pw.col_class[c] = -1; return; }
     if (len == last_len && __all_sync(0xffffffffu, lane >= len || rel == last_rel)) {
       if (lane == 0) pw.col_class[c] = last_slot;
-      continue;
+      return;
     }
     uint64_t h = lane < len ? mix64(((uint64_t)(lane + 1) << 32) ^ (uint32_t)rel) : 0;
 #pragma unroll
@@ -630,6 +627,23 @@ class_kernel(int64_t n, const int64_t* __restrict__ cscptr, const int32_t* __res
     }
     if (lane == 0) pw.col_class[c] = result;
     if (result >= 0) { last_slot = result; last_len = len; last_rel = rel; }
+  };
+  // two consecutive columns per pass: their load chains in flight together
+  for (int64_t c0 = 2 * w0; c0 < n; c0 += 2 * nw) {
+    int len[2];
+    int32_t rel[2] = {0, 0};
+    int64_t lo[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const bool ok = c0 + r < n;
+      lo[r] = ok ? cscptr[c0 + r] : 0;
+      len[r] = ok ? (int)(cscptr[c0 + r + 1] - lo[r]) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (lane < len[r] && len[r] <= 32) rel[r] = cscrow[lo[r] + lane] - (int32_t)(c0 + r);
+    process(c0, len[0], rel[0]);
+    if (c0 + 1 < n) process(c0 + 1, len[1], rel[1]);
   }
 }
 
