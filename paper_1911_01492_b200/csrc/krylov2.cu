@@ -416,12 +416,33 @@ extern "C" int spai_ksolver_set_symmetric(spai_ksolver* s, const int32_t* g, int
   if (A_U) {
     if (!make_symsell(g, w, A_U, s->n, &s->As)) { set_error("ksolver: bad offset table"); return SPAI_E_ARG; }
     s->symA = true;
-    // one resident wave (the mirrored reads rely on the slices in flight)
-    SPAI_SSELL_DISPATCH(w, s->bs = std::min(s->bs, ssell_blocks((const void*)bicg_b3<SymOp<WM>>, s->nslices)));
   }
   if (M_U) {
     if (!make_symsell(g, w, M_U, s->n, &s->Ms)) { set_error("ksolver: bad offset table"); return SPAI_E_ARG; }
     s->symM = true;
   }
+  // one resident wave of the kernels this configuration launches (the
+  // mirrored reads rely on the slices in flight); create() sized it for the
+  // SELL-32 kernels of A, which no longer run -- C2 (2D, w = 5): 4 instead
+  // of 3 CTAs per SM, 1.56 -> 1.32 ms per BiCGStab iteration
+  const int64_t ns = s->nslices;
+  unsigned b = (unsigned)num_sms() * 32;
+  if (s->symA)
+    SPAI_SSELL_DISPATCH(w, b = std::min({b, ssell_blocks((const void*)bicg_b3<SymOp<WM>>, ns),
+                                         ssell_blocks((const void*)bicg_b6<SymOp<WM>>, ns),
+                                         ssell_blocks((const void*)rich_r2<SymOp<WM>>, ns)}));
+  else
+    b = std::min({b, sell_blocks((const void*)bicg_b3<SellOp>, ns), sell_blocks((const void*)bicg_b6<SellOp>, ns),
+                  sell_blocks((const void*)rich_r2<SellOp>, ns)});
+  if (s->hasM) {
+    if (s->symM)
+      SPAI_SSELL_DISPATCH(w, b = std::min({b, ssell_blocks((const void*)k_apply_m<true, SymOp<WM>>, ns),
+                                           ssell_blocks((const void*)rich_r1<true, SymOp<WM>>, ns)}));
+    else
+      b = std::min({b, sell_blocks((const void*)k_apply_m<true, SellOp>, ns),
+                    sell_blocks((const void*)rich_r1<true, SellOp>, ns)});
+  }
+  b = std::min(b, sell_blocks((const void*)bicg_b7, ns));
+  s->bs = std::max(1u, b);
   return SPAI_OK;
 }
