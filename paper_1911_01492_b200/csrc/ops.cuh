@@ -10,7 +10,13 @@ namespace spai {
 
 // the two solve-phase operator formats behind one row() interface
 struct SellOp {
-  static constexpr int kMinBlocks = 0;   // as plain __launch_bounds__(kSpmvThreads)
+#ifndef SPAI_SELL_MINB
+#define SPAI_SELL_MINB 4
+#endif
+  // 4 CTAs of 256 threads per SM (64 registers): the latency-bound SELL
+  // kernels gain more from the fourth CTA than they lose to the cap
+  // (C5 400^3 BiCGStab: 11.38 -> 10.66 ms per iteration)
+  static constexpr int kMinBlocks = SPAI_SELL_MINB;
   Sell m;
   template <class XF>
   __device__ __forceinline__ double row(int64_t s, int lane, const XF& xf) const {
