@@ -354,3 +354,43 @@ def test_c5_bicgstab_200cubed_first_30_iterations_match_device_order_oracle():
     print(f"C5 200^3: SPAI worst {worst:.2e}, history rel {rel:.2e}")
     assert rel <= HIST_TOL, rel
     assert np.max(np.abs(x - xo)) <= 1e-10 * np.max(np.abs(xo))
+
+
+@pytest.mark.parametrize("dims,eps,conv", [((64, 60, 56), (1.0, 1e-2, 1e-3), None),
+                                           ((72, 64, 60), None, (2.0, -1.0, 0.5))])
+def test_bpath_anisotropic_and_convective_3d_columns(dims, eps, conv):
+    """The B = A^T A path on 3D operators whose G_k are far from the
+    Poisson ones (strong anisotropy; nonsymmetric convection): sampled
+    columns, every plan class, against the reference QR solve <= 1e-10."""
+    A = pb.q1_device(dims, eps=eps, conv=conv)
+    stats = pb.SpaiStats()
+    m_csc = pb.precond.spai1_columns_device(A, stats)
+    n = A.nrows
+    rng = np.random.default_rng(7)
+    cols = np.concatenate([rng.integers(0, n, 3000), _plan_class_columns(dims)])
+    worst = _check_columns(A, m_csc, cols)
+    print(f"{dims} eps={eps} conv={conv}: worst {worst:.2e}, QR fallbacks {stats.n_fallback}")
+
+
+def test_richardson_4096sq_first_200_sweeps_match_device_order_oracle():
+    """C1's smoother at C2's size (2D Q1 4096^2, raw SPAI(1), omega = 1):
+    200 K9 Richardson sweeps against the device-order oracle on the
+    downloaded A and M (SELL-32): histories and x <= 1e-12."""
+    from oracle import devorder
+    from paper_1911_01492_b200.krylov import DeviceKrylov
+    A = pb.q1_device((4096, 4096))
+    M = pb.spai1_device(A)
+    b = A.matvec(torch.ones(A.nrows, dtype=torch.float64, device="cuda"))
+    its = 200
+    s = DeviceKrylov(2, A, M, 1e-300, its, 1.0, False, symmetric=False)
+    st = s.run(b)
+    h = s.history(st[1])
+    x = s.x().cpu().numpy()
+    grid = s.grid()
+    s.close()
+    xo, ho, *_ = devorder.richardson_devorder(_host(A), _host(M), b.cpu().numpy(), 1.0, its, grid)
+    assert len(h) == len(ho) == its
+    rel = np.max(np.abs(h - ho) / ho)
+    print(f"Richardson 4096^2: history rel {rel:.2e}")
+    assert rel <= 1e-12, rel
+    assert np.max(np.abs(x - xo)) <= 1e-12 * np.max(np.abs(xo))
